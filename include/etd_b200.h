@@ -1,0 +1,154 @@
+/* etd_b200.h — C-ABI drop-in boundary for the B200-native ETD2RK-DS spectral
+ * time step (arXiv 2601.06849).  Plain pointers and sizes only; no torch or
+ * C++ types cross this boundary.
+ *
+ * The reference (`etdrd`, /root/reference/proj/core) exposes this path as a
+ * C++ value-semantics API (include/etdrd/stepper.hpp).  Each entry point below
+ * names the reference interface it replaces.  A C++ mirror of that interface
+ * built on these calls lives in include/etdrd_b200/stepper.hpp, and
+ * INTEGRATION.md shows the reference-side binding (a BackendKind::CudaSpectral
+ * dispatch in stepper.cpp:318-331).
+ *
+ * Layout conventions follow the reference Field (field.hpp:13-54): host arrays
+ * are dense FP64, x-fastest, index i + nx*(j + ny*k), interior points only.
+ * Error codes map 1:1 onto the reference exception types (errors.hpp:8-30).
+ */
+#ifndef ETD_B200_H
+#define ETD_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ETD_B200_ABI_VERSION 1
+
+/* Status codes (0 = OK).  errors.hpp:8-30; CLI mapping cli.cpp:204-217. */
+enum etd_status {
+    ETD_OK = 0,
+    ETD_ERR_CONFIG = 1,      /* etdrd::ConfigError      */
+    ETD_ERR_NUMERICS = 2,    /* etdrd::NumericsError    */
+    ETD_ERR_ABORT = 3,       /* etdrd::StepperAbort{t,step} */
+    ETD_ERR_MEMORY = 4,      /* etdrd::MemoryGuardError */
+    ETD_ERR_CUDA = 5,        /* device/driver failure (no reference equivalent) */
+    ETD_ERR_NODEVICE = 6     /* no CUDA device: there is no CPU fallback */
+};
+
+/* Pade family: rational.hpp:31 PadeFamily {P02, P04} */
+enum etd_family { ETD_P02 = 0, ETD_P04 = 1 };
+
+/* Device source descriptors.  The reference takes a std::function
+ * (SourceFunction / SystemSource, stepper.hpp:18-29) which cannot run on the
+ * device; the GPU backend takes a pointwise kind + parameters instead and
+ * rejects anything else with ETD_ERR_CONFIG. */
+enum etd_source_kind {
+    ETD_SRC_ZERO = 0,        /* f = 0                                             */
+    ETD_SRC_AC_CUBIC = 1,    /* f = u - u^3 (config 0-2; test_stepper.cpp:459-465) */
+    ETD_SRC_POLY3 = 2,       /* f = ((p3 u + p2) u + p1) u + p0                    */
+    ETD_SRC_NAN = 3,         /* f = NaN at grid point 0, else 0 (abort probe,
+                                test_stepper.cpp:304-321)                          */
+    ETD_SRC_FHN_CUBIC = 10,  /* fu = u(1-u)(u-p0) - v, fv = p1 (p2 u - v) (config 3-4) */
+    ETD_SRC_FHN_CLASSIC = 11,/* fu = u - u^3/3 - v, fv = p0 (u - p1 v) (problems.cpp:170-171) */
+    ETD_SRC_MIRROR_AC = 12,  /* fu = u - u^3, fv = v - v^3 (test_stepper.cpp:432-438) */
+    ETD_SRC_DECOUPLED = 13   /* fu = u - u^3, fv = p0 v + p1                     */
+};
+
+typedef struct etd_desc {
+    int dim;                 /* 2 or 3 (grid.hpp:17)                               */
+    int n[3];                /* interior points per axis = reference Grid::m[a]-1 */
+    double low[3], high[3];  /* box bounds (build_grid, grid.hpp:43-45)            */
+    double tau;              /* step size, > 0                                      */
+    int family;              /* etd_family                                          */
+    int nspecies;            /* 1: make_plan (stepper.hpp:59-61); 2: make_system_plan
+                                (stepper.hpp:107-108), 2D and 3D                     */
+    double kappa[2];         /* kappa (scalar) or kappa_u, kappa_v                  */
+    double q;                /* linear reaction, >= 0, split q/dim per axis         */
+    int src_kind;            /* etd_source_kind                                     */
+    double src_params[8];
+    int device;              /* CUDA device ordinal                                  */
+    /* z-slab sharding (3D): rank `rank` of `world_size` owns planes
+     * [etd_slab_range) ; world_size==1 -> whole grid on one GPU. */
+    int world_size, rank;
+    const void* nccl_unique_id; /* 128-byte ncclUniqueId (world_size > 1)            */
+} etd_desc;
+
+typedef struct etd_handle etd_handle;
+
+/* make_plan (stepper.cpp:118-177) / make_system_plan (system_stepper.cpp:31-70):
+ * host setup (closed-form eigensystems, Pade d-vectors) + one upload.  */
+int etd_create(const etd_desc* desc, etd_handle** out);
+/* Plan destruction (plans are immutable values in the reference). */
+int etd_destroy(etd_handle* h);
+
+/* This rank's z-slab [z0, z1) (3D) or [0,1) (2D). */
+int etd_slab_range(const etd_handle* h, int* z0, int* z1);
+
+/* StepperState/SystemState upload (stepper.hpp:63-67,110-114): species 0=U,
+ * 1=V; count = nx*ny*(z1-z0) values (this rank's slab), n,t = state.n,state.t. */
+int etd_set_state(etd_handle* h, int species, const double* host, size_t count, long n, double t);
+/* State download (materialises the reference Field). */
+int etd_get_state(etd_handle* h, int species, double* host, size_t count, long* n, double* t);
+
+/* advance (stepper.cpp:318-331) / etd2rkds_step_system (system_stepper.cpp:74-114)
+ * applied nsteps times on the device-resident state.  On a non-finite value the
+ * call returns ETD_ERR_ABORT, the state is left at the INPUT of the failing
+ * step and etd_last_error reports that step's t and n (stepper.cpp:18-23). */
+int etd_step(etd_handle* h, int nsteps);
+
+/* Value-semantics one-shot, the reference's advance(plan, state, f) shape:
+ * upload u (and v), step nsteps times, download into u_out (v_out).  Any of
+ * v/v_out may be NULL for scalar plans. */
+int etd_advance(etd_handle* h, const double* u, const double* v, long n, double t, int nsteps,
+                double* u_out, double* v_out, long* n_out, double* t_out);
+
+/* Replace the device source descriptor (the reference passes the source per
+ * advance() call, stepper.hpp:85-86; plans do not own it). */
+int etd_set_source(etd_handle* h, int src_kind, const double* src_params /* 8 values or NULL */);
+
+/* Last error of this handle: message, abort time and step (errors.hpp:22-28). */
+int etd_last_error(const etd_handle* h, char* msg, size_t len, double* t, long* step);
+
+/* ---- introspection / measurement (no reference equivalent) ---------------- */
+/* cudaStream_t the handle launches on (as an integer). */
+unsigned long long etd_stream(const etd_handle* h);
+/* Number of kernel launches one step issues (this rank). */
+int etd_launches_per_step(const etd_handle* h);
+/* Per-stage profiling: when enabled, etd_step records CUDA events around every
+ * launch (no CUDA graph) and accumulates device milliseconds per stage. */
+int etd_set_profiling(etd_handle* h, int on);
+/* stage names/times (ms summed since enable) and FLOPs per launch of stage i. */
+int etd_stage_count(const etd_handle* h);
+int etd_stage_info(const etd_handle* h, int i, char* name, size_t len, double* ms_total,
+                   long* launches, double* flops_per_launch, double* bytes_per_launch);
+
+/* Single eigenbasis transform on host data, for kernel-level parity tests:
+ * out = op(P_axis) contracted along `axis` (tensor_ops.cpp:107-119 contract_axis
+ * with M = P, transpose = !back), optionally followed by scaling with the
+ * d-vector d_ell (ell 1..3, 0 = none).  ell>0 && apply_q!=0 runs the full
+ * apply_Q_spectral (tensor_ops.cpp:164-172): 2 P (d_ell ⊙ P^T in). */
+int etd_debug_transform(etd_handle* h, int species, int axis, int back, int ell, int apply_q,
+                        const double* in, double* out);
+
+/* Seeded initial conditions for BASELINE configs 0-4;
+ * counter-based RNG, identical on every host, multithreaded.  Host only.
+ * Writes this rank's slab [z0,z1) of species `species` (x-fastest). */
+int etd_fill_config_ic(int config, unsigned long long seed, int species, int n, int z0, int z1,
+                       double* out);
+
+/* Host setup exported for parity tests of the one-time plan construction:
+ * operators.cpp:11-56 (P column-major n*n, ascending lambda) and
+ * rational.cpp:187-198 (d-vector for ell 1..3). */
+int etd_setup_axis(int n, double low, double high, int dim, double kappa, double q, double* P,
+                   double* lambda);
+int etd_setup_dvector(int n, const double* lambda, double tau, int family, int ell, double* d);
+/* rational.cpp:133-177: out[(ell-1)*nterms + t] = {pole.re, pole.im, res.re, res.im} */
+int etd_setup_scheme(int family, double* out, int* nterms);
+
+/* ABI version. */
+int etd_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ETD_B200_H */

@@ -1,0 +1,426 @@
+// etd_kernels.cuh — sm_100a device code for the ETD2RK-DS spectral step.
+//
+// One kernel template, `etd_contract`, performs every eigenbasis transform of
+// the step (reference tensor_ops.cpp:25-52 gemm_axis / cblas_dgemm sites K1-K3,
+// SURVEY.md §2.3) as a batched FP64 contraction on the DMMA tensor-core path
+// (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4; the only FP64 tensor instruction on
+// sm_100a, tcgen05 has no .kind::f64).  Operands are staged global->shared by
+// TMA (cp.async.bulk.tensor, 128B swizzle) through an mbarrier ring (full/empty
+// per stage); eight warps issue DMMA and lane 0 of warp 0 re-arms each slot as
+// soon as all warps have released it.  Pointwise stages of the
+// reference step are fused into the prologue (the source f(U), stepper.cpp:190)
+// and epilogues (Hadamard d-scaling tensor_ops.cpp:54-82, predictor mix
+// stepper.cpp:205-210, corrector bracket 214-217, update 218-219, non-finite
+// checks 18-23).
+//
+// Geometry.  Fields are x-fastest with a padded x pitch.  A transform along
+// axis a contracts index a of every "pencil":
+//   MODE 0 (a = x, unit stride):  C(r, i') = sum_i X(i, r) M(i', i)   r = pencil
+//   MODE 1 (a = y or z, strided): C(p, j') = sum_j X(p, j) M(j', j)   p = x index
+// The field is always the A operand (M-dim = pencils or x), the n x n transform
+// matrix is the B operand (L2-resident), the contracted axis is K and the
+// transformed axis is N, so every epilogue scales along N by d[n].
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace etd {
+
+// Device-resident step bookkeeping (reference StepperState n/t, and the
+// StepperAbort kind: 1 = source at t, 2 = source at t+tau, 3 = step update).
+struct StepStatus {
+    double t;
+    long long n;
+    int fail;
+    unsigned cta_done;
+    long long pad;
+};
+
+enum Epi : int {
+    EPI_STORE = 0,     // out_s = acc_s
+    EPI_SCALE = 1,     // out_s = dA[species(s)][n] * acc_s        (forward transform + Hadamard)
+    EPI_MIX = 2,       // S = 2ns: out_c = dA_c w1b + dB_c w2b ; out_{ns+c} = w2b
+    EPI_WHAT_SRC = 3,  // S = ns : out_c = What_c ; out_{ns+c} = f_c(What)  (+ check kind 2)
+    EPI_CORR = 4,      // S = ns : out_c = (acc_c - aux_c) * dA_c[n]
+    EPI_UPDATE = 5     // S = ns : out_c = aux_c + acc_c  (+ check kind 3, commit step)
+};
+
+struct ContractArgs {
+    int n_axis;             // contraction length = transformed extent (N and K)
+    int m_extent;           // MODE 0: pencils R ; MODE 1: nx
+    int zaxis;              // MODE 1: 0 = y (outer is z), 1 = z (outer is y)
+    int nspecies;
+    long long pitch, plane; // element strides of x-rows and z-planes
+    double* out;            // output operand 0
+    long long out_stride;   // elements between stacked outputs
+    const double* aux;      // EPI_CORR / EPI_UPDATE second input (operand 0)
+    long long aux_stride;
+    const double* dA;       // d-vector (species 0); species c at dA + c*dstride
+    const double* dB;
+    int dstride;
+    int src_kind;
+    double sp[8];
+    int ny_local;           // y extent of this buffer (for pencil -> (j,k) decoding)
+    int gj0, gz0;           // global (j,z) offset of this buffer (slabs / z-stage)
+    StepStatus* status;
+    double tau;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "ETD_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra ETD_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
+                                            int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
+                                            int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
+                                            int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+// D(8x8) += A(8x4) * B(4x8), FP64, one warp -> one DMMA.8x8x4
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// ------------------------------------------------------------- pointwise sources
+// Device forms of the source kinds of include/etd_b200.h (same expressions as
+// oracle/ref_driver.cpp so that rounding matches the checker).
+__device__ __forceinline__ double src_scalar(int kind, const double* p, double u) {
+    switch (kind) {
+    case 1: return u - u * u * u;
+    case 2: return ((p[3] * u + p[2]) * u + p[1]) * u + p[0];
+    default: return 0.0;
+    }
+}
+__device__ __forceinline__ void src_pair(int kind, const double* p, double u, double v, double& fu,
+                                         double& fv) {
+    switch (kind) {
+    case 10: fu = u * (1.0 - u) * (u - p[0]) - v; fv = p[1] * (p[2] * u - v); break;
+    case 11: fu = u - u * u * u / 3.0 - v; fv = p[0] * (u - p[1] * v); break;
+    case 12: fu = u - u * u * u; fv = v - v * v * v; break;
+    case 13: fu = u - u * u * u; fv = p[0] * v + p[1]; break;
+    default: fu = 0.0; fv = 0.0;
+    }
+}
+
+// ------------------------------------------------------------- tile geometry
+template <int MODE, int S, int EPI, bool PRO, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
+struct ContractCfg {
+    static constexpr int BK = 16;
+    static constexpr int NW = WARPS_M * WARPS_N;          // consumer warps
+    static constexpr int THREADS = 32 * NW;               // lane 0 of warp 0 also drives TMA
+    static constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
+    static constexpr int MF = WM / 8, NF = WN / 8;        // 8x8 DMMA fragments per warp
+    static constexpr int L = PRO ? S / 2 : S;             // operands fetched by TMA
+    static constexpr int A_DBL = S * BM * BK;
+    static constexpr int B_DBL = BN * BK;
+    static constexpr int STAGE_DBL = A_DBL + B_DBL;
+    static constexpr uint32_t TX_BYTES = (L * BM + BN) * BK * 8;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_DBL * 8 + 1024 + 2 * STAGES * 8 + 64;
+    static_assert(WM % 16 == 0 && WN % 8 == 0, "warp tile");
+    static_assert(BM % 16 == 0 && BN % 16 == 0, "cta tile");
+};
+
+// 128B-swizzled [rows][16 doubles] tile: element (row, col), TMA SWIZZLE_128B
+__device__ __forceinline__ int swz(int row, int col) {
+    return row * 16 + ((((col >> 1) ^ (row & 7)) << 1) | (col & 1));
+}
+
+// ------------------------------------------------------------- the kernel
+template <int MODE, int S, int EPI, bool PRO, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
+__global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
+    etd_contract(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const ContractArgs args) {
+    using C = ContractCfg<MODE, S, EPI, PRO, BM, BN, WARPS_M, WARPS_N, STAGES>;
+    constexpr int BK = C::BK;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment for the 128B swizzle atoms; pointer arithmetic on the
+    // __shared__ array keeps the address space visible (LDS, not generic LD)
+    double* smem = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_DBL);
+    uint64_t* empty = full + STAGES;
+    int* cta_flag = reinterpret_cast<int*>(empty + STAGES);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n0 = blockIdx.x * BN;
+    const int m0 = blockIdx.y * BM;
+    const int outer = blockIdx.z;
+    const int KT = (args.n_axis + BK - 1) / BK;
+
+    // A step aborted earlier in this launch sequence poisons every later kernel
+    // (stepper.cpp:18-23: the step throws, the input state survives).
+    if (tid == 0) {
+        cta_flag[0] = *reinterpret_cast<volatile int*>(&args.status->fail);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (cta_flag[0] != 0) return;
+
+    int bad = 0;  // non-finite seen (prologue or epilogue)
+
+    // TMA issue for k-tile kt into `stage` (thread 0 only)
+    auto issue = [&](int kt, int stage) {
+        double* sA = smem + stage * C::STAGE_DBL;
+        double* sB = sA + C::A_DBL;
+        mbar_expect_tx(&full[stage], C::TX_BYTES);
+        const int k0 = kt * BK;
+#pragma unroll
+        for (int c = 0; c < C::L; ++c) {
+            if constexpr (MODE == 0) {
+                tma_load_3d(sA + c * BM * BK, &tmA, &full[stage], k0, m0, c);
+            } else {
+#pragma unroll
+                for (int pb = 0; pb < BM / 16; ++pb) {
+                    double* dst = sA + (c * (BM / 16) + pb) * 256;
+                    if (args.zaxis)
+                        tma_load_4d(dst, &tmA, &full[stage], m0 + pb * 16, outer, k0, c);
+                    else
+                        tma_load_4d(dst, &tmA, &full[stage], m0 + pb * 16, k0, outer, c);
+                }
+            }
+        }
+        if constexpr (MODE == 0) {
+            tma_load_2d(sB, &tmB, &full[stage], k0, n0);
+        } else {
+#pragma unroll
+            for (int nb = 0; nb < BN / 16; ++nb) tma_load_2d(sB + nb * 256, &tmB, &full[stage], n0 + nb * 16, k0);
+        }
+    };
+    if (tid == 0) {
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+        for (int kt = 0; kt < KT && kt < STAGES; ++kt) issue(kt, kt);
+    }
+    {
+        // ===================== DMMA consumers =====================
+        const int g = lane >> 2, l = lane & 3;
+        const int wm0 = (warp / WARPS_N) * C::WM;
+        const int wn0 = (warp % WARPS_N) * C::WN;
+        double acc[S][C::MF][C::NF][2];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int i = 0; i < C::MF; ++i)
+#pragma unroll
+                for (int j = 0; j < C::NF; ++j) acc[s][i][j][0] = acc[s][i][j][1] = 0.0;
+
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kt = 0; kt < KT; ++kt) {
+            mbar_wait(&full[stage], phase);
+            double* sA = smem + stage * C::STAGE_DBL;
+            const double* sB = sA + C::A_DBL;
+            if constexpr (PRO) {
+                // fused source evaluation on the freshly landed state tile:
+                // slots [0,ns) hold U (,V); slots [ns,2ns) receive f(U(,V))
+                constexpr int ELEMS = BM * BK;
+                const int ns = S / 2;
+#pragma unroll
+                for (int q = 0; q < ELEMS / (32 * C::NW); ++q) {
+                    const int e = tid + q * 32 * C::NW;
+                    // decode the logical (p, k) of smem element e ([pb][kk][16] swizzled)
+                    const int pb = e >> 8, kk = (e >> 4) & 15;
+                    const int col = ((((e >> 1) & 7) ^ (kk & 7)) << 1) | (e & 1);
+                    const int p = m0 + pb * 16 + col, kc = kt * BK + kk;
+                    const bool valid = p < args.m_extent && kc < args.n_axis;
+                    const bool origin = args.src_kind == 3 && p == 0 &&
+                                        (args.zaxis ? (kc + args.gz0 == 0 && outer + args.gj0 == 0)
+                                                    : (kc + args.gj0 == 0 && outer + args.gz0 == 0));
+                    if (ns == 1) {
+                        double f = src_scalar(args.src_kind, args.sp, sA[e]);
+                        if (origin) f = __longlong_as_double(0x7ff8000000000000ll);
+                        sA[BM * BK + e] = f;
+                        bad |= valid && !isfinite(f);
+                    } else {
+                        double fu, fv;
+                        src_pair(args.src_kind, args.sp, sA[e], sA[BM * BK + e], fu, fv);
+                        sA[2 * BM * BK + e] = fu;
+                        sA[3 * BM * BK + e] = fv;
+                        bad |= valid && !(isfinite(fu) && isfinite(fv));
+                    }
+                }
+                named_bar_sync(1, 32 * C::NW);
+            }
+#pragma unroll
+            for (int st = 0; st < BK / 4; ++st) {
+                // k permutation inside the 16-wide stage keeps both fragment loads
+                // bank-conflict free under the 128B swizzle
+                const int kk = MODE == 0 ? (2 * st + (l & 1) + 8 * (l >> 1))
+                                         : (2 * l + (st & 1) + 8 * (st >> 1));
+                double a[S][C::MF], b[C::NF];
+#pragma unroll
+                for (int j = 0; j < C::NF; ++j) {
+                    const int nn = wn0 + j * 8 + g;
+                    b[j] = MODE == 0 ? sB[swz(nn, kk)] : sB[(nn >> 4) * 256 + swz(kk, nn & 15)];
+                }
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+#pragma unroll
+                    for (int i = 0; i < C::MF; ++i) {
+                        const int mm = wm0 + i * 8 + g;
+                        const double* base = sA + s * BM * BK;
+                        a[s][i] = MODE == 0 ? base[swz(mm, kk)] : base[(mm >> 4) * 256 + swz(kk, mm & 15)];
+                    }
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+#pragma unroll
+                    for (int i = 0; i < C::MF; ++i)
+#pragma unroll
+                        for (int j = 0; j < C::NF; ++j)
+                            dmma884(acc[s][i][j][0], acc[s][i][j][1], a[s][i], b[j]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (tid == 0 && kt + STAGES < KT) {
+                // refill this slot once every warp has released it
+                mbar_wait(&empty[stage], phase);
+                issue(kt + STAGES, stage);
+            }
+            __syncwarp();
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+
+        // ===================== fused epilogue =====================
+        const int ns = args.nspecies;
+#pragma unroll
+        for (int i = 0; i < C::MF; ++i) {
+            const int m = m0 + wm0 + i * 8 + g;
+            if (m >= args.m_extent) continue;
+#pragma unroll
+            for (int j = 0; j < C::NF; ++j) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int n = n0 + wn0 + j * 8 + 2 * l + e;
+                    if (n >= args.n_axis) continue;
+                    long long off;
+                    if constexpr (MODE == 0) off = (long long)m * args.pitch + n;
+                    else off = args.zaxis ? (long long)outer * args.pitch + (long long)n * args.plane + m
+                                          : (long long)outer * args.plane + (long long)n * args.pitch + m;
+                    if constexpr (EPI == EPI_STORE) {
+#pragma unroll
+                        for (int s = 0; s < S; ++s) args.out[s * args.out_stride + off] = acc[s][i][j][e];
+                    } else if constexpr (EPI == EPI_SCALE) {
+#pragma unroll
+                        for (int s = 0; s < S; ++s)
+                            args.out[s * args.out_stride + off] =
+                                acc[s][i][j][e] * __ldg(args.dA + (s % ns) * args.dstride + n);
+                    } else if constexpr (EPI == EPI_MIX) {
+#pragma unroll
+                        for (int c = 0; c < S / 2; ++c) {
+                            const double w1b = acc[c][i][j][e], w2b = acc[S / 2 + c][i][j][e];
+                            const double da = __ldg(args.dA + c * args.dstride + n);
+                            const double db = __ldg(args.dB + c * args.dstride + n);
+                            args.out[c * args.out_stride + off] = da * w1b + db * w2b;
+                            args.out[(S / 2 + c) * args.out_stride + off] = w2b;
+                        }
+                    } else if constexpr (EPI == EPI_WHAT_SRC) {
+                        double f0, f1 = 0.0;
+                        if constexpr (S == 1) {
+                            f0 = src_scalar(args.src_kind, args.sp, acc[0][i][j][e]);
+                            if (args.src_kind == 3 && n == 0 && m == 0 && args.gz0 == 0 && args.gj0 == 0)
+                                f0 = __longlong_as_double(0x7ff8000000000000ll);
+                            bad |= !isfinite(f0);
+                        } else {
+                            src_pair(args.src_kind, args.sp, acc[0][i][j][e], acc[1][i][j][e], f0, f1);
+                            bad |= !(isfinite(f0) && isfinite(f1));
+                        }
+#pragma unroll
+                        for (int c = 0; c < S; ++c) args.out[c * args.out_stride + off] = acc[c][i][j][e];
+                        args.out[S * args.out_stride + off] = f0;
+                        if constexpr (S == 2) args.out[3 * args.out_stride + off] = f1;
+                    } else if constexpr (EPI == EPI_CORR) {
+#pragma unroll
+                        for (int c = 0; c < S; ++c)
+                            args.out[c * args.out_stride + off] =
+                                (acc[c][i][j][e] - args.aux[c * args.aux_stride + off]) *
+                                __ldg(args.dA + c * args.dstride + n);
+                    } else if constexpr (EPI == EPI_UPDATE) {
+#pragma unroll
+                        for (int c = 0; c < S; ++c) {
+                            const double u1 = args.aux[c * args.aux_stride + off] + acc[c][i][j][e];
+                            bad |= !isfinite(u1);
+                            args.out[c * args.out_stride + off] = u1;
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    // ===================== status: abort flag and step commit =====================
+    const int any_bad = __syncthreads_or(bad);
+    if (tid == 0) {
+        if (any_bad) {
+            const int kind = EPI == EPI_WHAT_SRC ? 2 : EPI == EPI_UPDATE ? 3 : 1;
+            atomicCAS(&args.status->fail, 0, kind);
+        }
+        if constexpr (EPI == EPI_UPDATE) {
+            // last CTA of the final stage commits the step: n += 1, t = n tau
+            // (stepper.cpp:228).  An aborted step is never committed.
+            __threadfence();
+            const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+            const unsigned prev = atomicAdd(&args.status->cta_done, 1u);
+            if (prev == total - 1) {
+                __threadfence();
+                args.status->cta_done = 0;
+                if (*reinterpret_cast<volatile int*>(&args.status->fail) == 0) {
+                    const long long nn = args.status->n + 1;
+                    args.status->n = nn;
+                    args.status->t = (double)nn * args.tau;
+                }
+            }
+        }
+    }
+}
+
+}  // namespace etd

@@ -1,0 +1,44 @@
+// Host-side one-time setup for the ETD2RK-DS spectral step (may stay on the
+// host per BASELINE north_star): directional operators, closed-form Dirichlet
+// eigensystems, Pade pole/residue sets and the diagonal "d-vectors".
+#pragma once
+#include <array>
+#include <complex>
+#include <stdexcept>
+#include <cstddef>
+#include <string>
+#include <vector>
+
+namespace etd {
+
+struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct NumericsError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+// Toeplitz tridiagonal factor of kappa*(-Laplacian) + q along one axis
+// (reference operators.cpp:11-34): diag = (2k + (q/dim) h^2)/h^2, off = -k/h^2.
+struct AxisOperator {
+    int n = 0;
+    double h = 0.0, diag = 0.0, off = 0.0;
+};
+AxisOperator axis_operator(int n, double low, double high, int dim, double kappa, double q);
+
+// Closed-form eigensystem (reference operators.cpp:36-56):
+//   lambda_k = diag + 2 off cos(theta_k),  P(i,k) = sqrt(2/(n+1)) sin((i+1) theta_k),
+//   theta_k = (k+1) pi/(n+1).  P returned column-major (P[k*n+i] = P(i,k)).
+void eigensystem(const AxisOperator& op, std::vector<double>& P, std::vector<double>& lambda);
+
+// Pole/residue terms of the three rational weights (reference rational.cpp:133-177).
+struct PoleResidue { std::complex<double> pole, residue; };
+struct PadeScheme { int family = 0; std::array<std::vector<PoleResidue>, 3> terms; };
+PadeScheme pade_scheme(int family);
+
+// d_k = sum_l Re(r_l / (tau*lambda_k - s_l)) — half of Q_ell(tau lambda_k)
+// (reference rational.cpp:187-198).
+std::vector<double> dvector(const std::vector<double>& lambda, double tau, const PadeScheme& s,
+                            int ell);
+
+// Seeded initial conditions for BASELINE configs.
+void fill_config_ic(int config, unsigned long long seed, int species, int n, int z0, int z1,
+                    double* out);
+
+}  // namespace etd

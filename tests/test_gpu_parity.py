@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference itself
+(oracle/_ref, the unmodified etdrd core) and the C restatement (oracle/).
+
+Tolerances follow the reference's own tests: contraction vs naive <= 1e-13
+(test_tensor.cpp:45-71), apply_Q <= 1e-12 (test_tensor.cpp:105-125), steps
+normwise max|a-b|/max|a| <= 1e-11 (BASELINE north_star; rel_gap of
+test_stepper.cpp:50-57).
+"""
+import numpy as np
+import pytest
+
+import paper_2601_06849_b200 as etd
+from paper_2601_06849_b200 import configs
+from oracle import Oracle, Ref, rel_gap
+
+pytestmark = pytest.mark.gpu
+
+STEP_TOL = 1e-11
+
+
+def ref_or_oracle():
+    return Ref if Ref.available() else Oracle
+
+
+def sine_mode(g):
+    nx, ny, nz = g.interior_shape()
+    x = np.sin(np.pi * np.array([g.coord(0, i) for i in range(nx)]))
+    y = np.sin(np.pi * np.array([g.coord(1, j) for j in range(ny)]))
+    z = np.sin(np.pi * np.array([g.coord(2, k) for k in range(nz)])) if g.dim == 3 else np.ones(1)
+    return (z[:, None, None] * y[None, :, None] * x[None, None, :]).ravel()
+
+
+# ----------------------------------------------------------------- transforms
+@pytest.mark.parametrize("shape", [(45, 33, 1), (21, 17, 13), (127, 127, 1), (64, 48, 40), (7, 9, 5)])
+def test_transform_vs_reference_contract(shape):
+    nx, ny, nz = shape
+    dim = 3 if nz > 1 else 2
+    g = etd.build_grid(dim, [(0.0, 1.0)] * dim, [s + 1 for s in shape[:dim]])
+    plan = etd.make_plan(g, 0.01, 1.0, 1.0, source=etd.allen_cahn_cubic())
+    rng = np.random.default_rng(1)
+    x = rng.uniform(-1, 1, nx * ny * nz)
+    for axis in range(dim):
+        n = shape[axis]
+        P, _ = Oracle.spectral_factor(n, 2.0, -1.0)   # P is independent of diag/off
+        for back in (False, True):
+            got = plan.debug_transform(x, axis, back=back)
+            want = Ref.contract_axis(shape, P, n, x, axis, transpose=not back) if Ref.available() \
+                else Oracle.contract(shape, P, x, axis, transpose=not back)
+            assert np.max(np.abs(got - want)) <= 1e-13, (shape, axis, back)
+
+
+@pytest.mark.parametrize("dim,n", [(2, 31), (3, 15), (2, 100)])
+@pytest.mark.parametrize("family", [0, 1])
+def test_apply_q_vs_reference(dim, n, family):
+    tau, kappa, q = 0.02, 0.7, 1.0
+    g = etd.unit_box_grid(dim, n + 1)
+    plan = etd.make_plan(g, tau, kappa, q, scheme=family, source=etd.allen_cahn_cubic())
+    x = np.random.default_rng(2).uniform(-0.5, 0.5, n ** dim)
+    for axis in range(dim):
+        for ell in (1, 2, 3):
+            got = plan.debug_transform(x, axis, ell=ell, apply_q=True)
+            want = ref_or_oracle().apply_q(dim, n, tau, kappa, q, family, ell, axis, x)
+            assert np.max(np.abs(got - want)) <= 1e-12, (axis, ell)
+
+
+# ----------------------------------------------------------------- full steps
+@pytest.mark.parametrize("dim,n,steps", [(2, 63, 10), (3, 31, 5), (2, 9, 3), (3, 20, 4)])
+@pytest.mark.parametrize("family", [0, 1])
+def test_scalar_steps_vs_reference(dim, n, steps, family):
+    tau, kappa, q = 0.01, 1.0, 1.0
+    g = etd.unit_box_grid(dim, n + 1)
+    u0 = np.random.default_rng(3).uniform(-1, 1, n ** dim)
+    plan = etd.make_plan(g, tau, kappa, q, scheme=family)
+    got = etd.advance(plan, etd.StepperState(0, 0.0, u0), etd.allen_cahn_cubic(), nsteps=steps)
+    want, nn, tt = ref_or_oracle().scalar_run(dim, n, tau, kappa, q, u0, steps, src_kind=1, family=family)[:3]
+    assert got.n == nn == steps and got.t == pytest.approx(tt)
+    assert rel_gap(want, got.U) <= STEP_TOL
+
+
+@pytest.mark.parametrize("dim,n,steps", [(2, 63, 6), (3, 31, 4), (3, 17, 3)])
+@pytest.mark.parametrize("src", ["fhn_cubic", "fhn_classic"])
+def test_system_steps_vs_reference(dim, n, steps, src):
+    tau, ku, kv = 0.05, 1e-3, 5e-4
+    rng = np.random.default_rng(4)
+    u0, v0 = rng.uniform(-1, 1, n ** dim), rng.uniform(-1, 1, n ** dim)
+    if src == "fhn_cubic":
+        f, kind, params = etd.fhn_cubic(0.1, 0.01, 0.5), 10, (0.1, 0.01, 0.5)
+    else:
+        f, kind, params = etd.fhn_classic(1.0, 1.0), 11, (1.0, 1.0)
+    g = etd.unit_box_grid(dim, n + 1)
+    plan = etd.make_system_plan(g, tau, ku, kv, 0.0)
+    got = etd.etd2rkds_step_system(plan, etd.SystemState(0, 0.0, u0, v0), f, nsteps=steps)
+    wu, wv, nn, tt = ref_or_oracle().system_run(dim, n, tau, ku, kv, 0.0, u0, v0, steps, src_kind=kind,
+                                                 src_params=params)[:4]
+    assert got.n == nn
+    assert rel_gap(wu, got.U) <= STEP_TOL and rel_gap(wv, got.V) <= STEP_TOL
+
+
+@pytest.mark.parametrize("cfg_id,n,steps", [(0, 127, 100), (1, 255, 10), (2, 63, 10), (3, 47, 5), (4, 31, 5)])
+def test_config_shapes_vs_reference(cfg_id, n, steps):
+    """BASELINE configs with their own kappa/q/tau/source and seeded inputs, at
+    sizes the CPU reference finishes in seconds (config 0 at full size)."""
+    cfg = configs.CONFIGS[cfg_id]
+    ics = configs.initial_state(cfg, n)
+    plan = configs.make_plan(cfg, n)
+    R = ref_or_oracle()
+    if cfg.nspecies == 1:
+        got = etd.advance(plan, etd.StepperState(0, 0.0, ics[0]), cfg.source, nsteps=steps)
+        want = R.scalar_run(cfg.dim, n, cfg.tau, cfg.kappa[0], cfg.q, ics[0], steps, src_kind=1)[0]
+        assert rel_gap(want, got.U) <= STEP_TOL
+    else:
+        got = etd.etd2rkds_step_system(plan, etd.SystemState(0, 0.0, ics[0], ics[1]), cfg.source, nsteps=steps)
+        wu, wv = R.system_run(cfg.dim, n, cfg.tau, cfg.kappa[0], cfg.kappa[1], cfg.q, ics[0], ics[1], steps,
+                              src_kind=10, src_params=(0.1, 0.01, 0.5))[:2]
+        assert rel_gap(wu, got.U) <= STEP_TOL and rel_gap(wv, got.V) <= STEP_TOL
+
+
+# ----------------------------------------------------------------- semantics
+def test_zero_source_sine_mode_scalar_weights():
+    """test_stepper.cpp:109-126"""
+    g = etd.unit_box_grid(2, 10)
+    tau, kappa, q = 0.02, 1.3, 0.7
+    u0 = sine_mode(g)
+    for fam in (0, 1):
+        plan = etd.make_plan(g, tau, kappa, q, scheme=fam)
+        out = etd.advance(plan, etd.StepperState(0, 0.0, u0), etd.DeviceSource(etd.SourceKind.ZERO))
+        sch = etd.setup_scheme(fam)
+        lam = []
+        for a in range(2):
+            _, l = etd.setup_axis(9, kappa, q, 2)
+            lam.append(l[0])
+        w = 1.0
+        for lv in lam:
+            x = tau * lv
+            w *= 2.0 * sum(np.real(complex(t[2], t[3]) / (x - complex(t[0], t[1]))) for t in sch[0])
+        assert np.max(np.abs(out.U - w * u0)) <= 1e-12
+
+
+def test_nonfinite_source_aborts_with_input_state():
+    """test_stepper.cpp:304-321: StepperAbort carries the INPUT state's t and n."""
+    g = etd.unit_box_grid(2, 8)
+    plan = etd.make_plan(g, 0.01, 1.0, 1.0)
+    u0 = np.random.default_rng(7).uniform(-0.5, 0.5, 49)
+    with pytest.raises(etd.StepperAbort) as ei:
+        etd.advance(plan, etd.StepperState(4, 0.25, u0), etd.DeviceSource(etd.SourceKind.NAN_PROBE))
+    assert ei.value.t == pytest.approx(0.25) and ei.value.step == 4
+    # the device state is the input of the failing step (nothing committed)
+    u, n, t = plan.download(0)
+    assert n == 4 and np.array_equal(u, u0)
+
+
+def test_abort_mid_run_keeps_last_good_state():
+    """A run that blows up at step k reports step k and keeps the state after k steps."""
+    g = etd.unit_box_grid(2, 16)
+    plan = etd.make_plan(g, 0.5, 1e-3, 0.0)
+    u0 = np.full(15 * 15, 3.0)  # u - u^3 with a huge tau diverges within a few steps
+    st = etd.StepperState(0, 0.0, u0)
+    with pytest.raises(etd.StepperAbort) as ei:
+        etd.advance(plan, st, etd.poly3(0.0, 0.0, 0.0, 1e6), nsteps=50)
+    k = ei.value.step
+    assert 0 <= k < 50
+    u, n, t = plan.download(0)
+    assert n == k and np.all(np.isfinite(u))
+    # replaying k steps from the start reproduces that state bitwise
+    plan2 = etd.make_plan(g, 0.5, 1e-3, 0.0)
+    if k > 0:
+        again = etd.advance(plan2, st, etd.poly3(0.0, 0.0, 0.0, 1e6), nsteps=k)
+        assert np.array_equal(again.U, u)
+
+
+def test_bitwise_reproducible_and_batched_equals_single():
+    """test_stepper.cpp:323-332 plus advance(n) == n x advance(1)."""
+    g = etd.unit_box_grid(3, 24)
+    plan = etd.make_plan(g, 0.01, 0.5, 1.0, scheme=1)
+    u0 = np.random.default_rng(8).uniform(-1, 1, 23 ** 3)
+    st = etd.StepperState(0, 0.0, u0)
+    a = etd.advance(plan, st, etd.allen_cahn_cubic())
+    b = etd.advance(plan, st, etd.allen_cahn_cubic())
+    assert np.array_equal(a.U, b.U)
+    five = etd.advance(plan, st, etd.allen_cahn_cubic(), nsteps=5)
+    s = st
+    for _ in range(5):
+        s = etd.advance(plan, s, etd.allen_cahn_cubic())
+    assert np.array_equal(five.U, s.U) and five.n == s.n == 5
+
+
+def test_mirrored_system_keeps_v_equal_u():
+    """test_stepper.cpp:430-446"""
+    for dim, n in ((2, 9), (3, 11)):
+        g = etd.unit_box_grid(dim, n + 1)
+        u0 = np.random.default_rng(31).uniform(-0.5, 0.5, n ** dim)
+        plan = etd.make_system_plan(g, 0.02, 0.5, 0.5, 0.0, scheme=1)
+        st = etd.etd2rkds_step_system(plan, etd.SystemState(0, 0.0, u0, u0),
+                                      etd.DeviceSource(etd.SourceKind.MIRROR_AC), nsteps=10)
+        assert np.max(np.abs(st.U - st.V)) <= 1e-12
+
+
+def test_decoupled_system_equals_two_scalar_runs():
+    """test_stepper.cpp:448-488 (autonomous v source), in 2D and 3D."""
+    for dim, n in ((2, 9), (3, 9)):
+        g = etd.unit_box_grid(dim, n + 1)
+        tau, ku, kv = 0.01, 0.05, 2.0
+        rng = np.random.default_rng(11)
+        u0, v0 = rng.uniform(-0.5, 0.5, n ** dim), rng.uniform(-0.5, 0.5, n ** dim)
+        sp = etd.make_system_plan(g, tau, ku, kv, 0.0)
+        st = etd.etd2rkds_step_system(sp, etd.SystemState(0, 0.0, u0, v0),
+                                      etd.DeviceSource(etd.SourceKind.DECOUPLED, (-0.3, 0.1)), nsteps=8)
+        pu = etd.make_plan(g, tau, ku, 0.0)
+        pv = etd.make_plan(g, tau, kv, 0.0)
+        au = etd.advance(pu, etd.StepperState(0, 0.0, u0), etd.allen_cahn_cubic(), nsteps=8)
+        av = etd.advance(pv, etd.StepperState(0, 0.0, v0), etd.poly3(0.1, -0.3), nsteps=8)
+        assert np.max(np.abs(st.U - au.U)) <= 1e-12
+        assert np.max(np.abs(st.V - av.U)) <= 1e-12
+
+
+def test_shape_mismatch_and_host_source_rejected():
+    g = etd.unit_box_grid(2, 8)
+    plan = etd.make_plan(g, 0.01, 1.0, 1.0)
+    with pytest.raises(etd.ConfigError):
+        etd.advance(plan, etd.StepperState(0, 0.0, np.zeros(64)), etd.allen_cahn_cubic())
+    with pytest.raises(etd.ConfigError):
+        etd.advance(plan, etd.StepperState(0, 0.0, np.zeros(49)), lambda t, u, g: u)
+    with pytest.raises(etd.ConfigError):
+        etd.make_plan(g, 0.0, 1.0, 1.0)
