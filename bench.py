@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""bench.py — ETD2RK-DS spectral time stepping on B200 (driver contract).
+
+Default workload: BASELINE config 4 — 3D coupled FitzHugh–Nagumo, n=1023
+interior points per axis (1.07e9 points per species), tau=0.05, P02, seeded
+inputs.  A "step" is one ETD2RK-DS time step of both species (13 eigenbasis
+transforms each).  Metric: grid-point updates per second
+(one species value advanced one step), FP64.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--config C] [--n N] [--no-cpu]
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+the unmodified etdrd core + OpenBLAS) on this host's cores, as a bounded
+sample of the same workload (see oracle/ref_driver.cpp ref_sample_step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.19  # measured DMMA.8x8x4 peak, profiles/r01_fp64_peak.jsonl (MEASURED_PEAKS has no FP64)
+FP64_PEAK_NOTE = "measured: tools/fp64_peak.cu DMMA m8n8k4 sustained on this pool's B200 (profiles/r01_fp64_peak.jsonl)"
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        load = [s for s in sm if s > 300] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+# ------------------------------------------------------------------ CPU reference (bounded sample)
+def cpu_reference_sample(cfg, n, reps: int, warmup: int = 1):
+    """Reference etdrd step (oracle/_ref + OpenBLAS, all host cores) on a bounded
+    sample at full pencil length; returns (pt_upd_per_s list, cores, sample text)."""
+    from oracle import Ref
+    cores = os.cpu_count() or 1
+    Ref.set_threads(cores)
+    nsub = 16 if n >= 512 else max(4, n // 16)
+    src_kind, params = (1, None) if cfg.nspecies == 1 else (10, (0.1, 0.01, 0.5))
+    rates = []
+    for i in range(warmup + reps):
+        sec, pts, parts = Ref.sample_step(n, nsub, cfg.nspecies, cfg.tau, cfg.kappa, cfg.q, src_kind, params)
+        if i >= warmup:
+            rates.append(pts / sec)
+    sample = (f"reference etdrd step ({'make_plan+advance' if cfg.nspecies == 1 else 'composed 3D system step'}, "
+              f"OpenBLAS {cores} threads) on a {n}x{n}x{nsub} z-sub-box, z-applies re-timed on full-length "
+              f"(n={n}) z-pencils; rate = sample points / estimated step time")
+    return rates, cores, sample
+
+
+def reference_arm(args, cfg, n, rank, world):
+    if rank != 0:
+        return 0
+    steps, warmup = args.steps, args.warmup
+    from oracle import Ref
+    if not Ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libetdrd_ref.so not built"}))
+        return 0
+    if cfg.dim == 2:
+        # full reference steps fit: time make_plan+advance directly
+        from paper_2601_06849_b200 import configs
+        cores = os.cpu_count() or 1
+        Ref.set_threads(cores)
+        u0 = configs.initial_state(cfg, n)[0]
+        Ref.scalar_run(cfg.dim, n, cfg.tau, cfg.kappa[0], cfg.q, u0, warmup, src_kind=1)
+        _, _, _, sec = Ref.scalar_run(cfg.dim, n, cfg.tau, cfg.kappa[0], cfg.q, u0, steps, src_kind=1)
+        rate = n ** 2 * steps / sec
+        ms = sec / steps * 1e3
+        sample = f"reference make_plan+advance, full {n}x{n} grid, {steps} steps, OpenBLAS {cores} threads"
+    else:
+        rates, cores, sample = cpu_reference_sample(cfg, n, steps, warmup)
+        rate = statistics.median(rates)
+        ms = cfg.points(n) * cfg.nspecies / rate * 1e3
+    unit = "grid-point updates/s"
+    line = {"metric": "grid-point updates/sec (FP64)", "value": rate, "unit": unit, "impl": "reference",
+            "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+            "config": workload_config(cfg, n, world),
+            "cpu_baseline": {"value": rate, "unit": unit, "cores": cores, "kind": "reference", "sample": sample},
+            "e2e": {"value": rate, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(cfg, n, world):
+    return {"workload": f"BASELINE config {cfg.id}: " + cfg.describe().split(": ", 1)[1].replace(f"n={cfg.n}", f"n={n}"),
+            "grid": [n] * cfg.dim, "species": cfg.nspecies, "points_per_species": n ** cfg.dim,
+            "tau": cfg.tau, "pade": "P02", "parallelism": f"zslab{world}" if world > 1 else "single",
+            "l2": "inputs larger than L2" if n ** cfg.dim * 8 > 126e6 else "L2-resident working set (no flush)"}
+
+
+# ------------------------------------------------------------------ B200 arm
+def b200_arm(args, cfg, n, rank, world, local_rank):
+    import numpy as np
+    import torch
+    from paper_2601_06849_b200 import configs
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    kw = {}
+    if world > 1:
+        raise SystemExit("multi-GPU z-slab sharding is not available in this build")
+    plan = configs.make_plan(cfg, n, device=local_rank, **kw)
+    t0 = time.time()
+    ics = configs.initial_state(cfg, n, z0=plan.slab[0], z1=plan.slab[1] if cfg.dim == 3 else None)
+    t_ic = time.time() - t0
+    for s, a in enumerate(ics):
+        plan.upload(s, a)
+    stream = torch.cuda.ExternalStream(plan.stream, device=torch.device("cuda", local_rank))
+    local_pts = plan.local_count * cfg.nspecies
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (also builds the CUDA graphs)
+    plan.step(args.warmup)
+    barrier()
+
+    # ---- timed region: device-resident inputs, events on the launching stream ----
+    plan.set_profiling(True)  # per-launch events (eager launches; each launch >> launch latency at this size)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    plan.step(args.steps)
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    stats = plan.stage_stats()
+    plan.set_profiling(False)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_pts = cfg.points(n) * cfg.nspecies
+    value = total_pts / (ms * 1e-3)
+
+    # roofline of the dominant kernel (largest share of the step)
+    per = []
+    for s in stats:
+        avg = s["ms_total"] / max(1, s["launches"])
+        per.append((avg, s))
+    dom_ms, dom = max(per, key=lambda x: x[0])
+    achieved = dom["flops_per_launch"] / (dom_ms * 1e-3) * 1e-12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tr = json.load(open(tpath)).get(f"cfg{cfg.id}_n{n}", {})
+            traffic = tr.get(dom["name"])
+        except (OSError, ValueError):
+            traffic = None
+    transform_ms = sum(p[0] for p in per)
+    transform_flops = sum(s["flops_per_launch"] for _, s in per)
+    roofline = {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic, "kernel": dom["name"],
+                "peak_source": FP64_PEAK_NOTE,
+                "algorithmic_flops_per_launch": dom["flops_per_launch"],
+                "all_transforms": {"tflops": round(transform_flops / (transform_ms * 1e-3) * 1e-12, 3),
+                                   "frac": round(transform_flops / (transform_ms * 1e-3) * 1e-12 / FP64_PEAK_TFLOPS, 4),
+                                   "hbm_gbs": round(sum(s["bytes_per_launch"] for _, s in per) / (transform_ms * 1e-3) * 1e-9, 1),
+                                   "hbm_peak_gbs": 6552.0},
+                "stages": [{"name": s["name"], "ms": round(a, 3),
+                            "tflops": round(s["flops_per_launch"] / (a * 1e-3) * 1e-12, 2)} for a, s in per]}
+
+    # ---- e2e through the public API: pinned host in -> step -> pinned host out ----
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    hin = [torch.from_numpy(a).pin_memory() for a in ics]
+    hout = [torch.empty_like(h).pin_memory() for h in hin]
+    cnt = plan.local_count
+
+    def e2e_step():
+        for s in range(cfg.nspecies):
+            plan.upload_ptr(s, hin[s].data_ptr(), cnt, 0, 0.0)
+        plan.step(1)
+        for s in range(cfg.nspecies):
+            plan.download_ptr(s, hout[s].data_ptr(), cnt)
+
+    e2e_step()  # warm
+    barrier()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    f0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    f1.record(stream)
+    barrier()
+    e2e_wall = (time.perf_counter() - w0) / e2e_steps
+    e2e_ms = max(f0.elapsed_time(f1) / e2e_steps, e2e_wall * 1e3)
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    bytes_io = cnt * 8 * cfg.nspecies
+    e2e = {"value": total_pts / (e2e_ms * 1e-3), "unit": "grid-point updates/s", "h2d_bytes_per_step": bytes_io,
+           "d2h_bytes_per_step": bytes_io, "ms_per_step": e2e_ms,
+           "api": "etd_set_state -> etd_step(1) -> etd_get_state (pinned host buffers)"}
+    finite = bool(np.all(np.isfinite(hout[0].numpy())))
+
+    line = {"metric": "grid-point updates/sec (FP64)", "value": value, "unit": "grid-point updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-based RNG, DESIGN.md Inputs)",
+            "config": workload_config(cfg, n, world), "roofline": roofline, "e2e": e2e,
+            "gpu_launches": plan.launches_per_step * args.steps, "clocks": clk, "finite": finite,
+            "ic_seconds": round(t_ic, 2)}
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            rates, cores, sample = cpu_reference_sample(cfg, n, reps=2, warmup=1) if cfg.dim == 3 else (None, None, None)
+            if cfg.dim == 2:
+                from oracle import Ref
+                cores = os.cpu_count() or 1
+                Ref.set_threads(cores)
+                _, _, _, sec = Ref.scalar_run(cfg.dim, n, cfg.tau, cfg.kappa[0], cfg.q, ics[0], 3, src_kind=1)
+                rates = [n ** 2 * 3 / sec]
+                sample = f"reference make_plan+advance, full {n}x{n} grid, 3 steps"
+            line["cpu_baseline"] = {"value": statistics.median(rates), "unit": "grid-point updates/s",
+                                    "cores": cores, "kind": "reference", "sample": sample}
+        except Exception as e:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"value": None, "unit": "grid-point updates/s", "cores": os.cpu_count(),
+                                    "kind": "reference", "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=None)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--n", type=int, default=None, help="override the grid size (testing only)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.gpus is not None and args.gpus != world and world != 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    from paper_2601_06849_b200 import configs
+    cfg = configs.CONFIGS[args.config]
+    n = args.n or cfg.n
+    if args.impl == "reference":
+        return reference_arm(args, cfg, n, rank, world)
+    return b200_arm(args, cfg, n, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

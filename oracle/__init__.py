@@ -84,6 +84,8 @@ class Ref:
             L.ref_scheme.argtypes = [i, _dp, C.POINTER(i)]
             L.ref_contract_axis.argtypes = [i, i, i, i, _dp, i, _dp, i, i, _dp, C.c_char_p, i]
             L.ref_apply_q.argtypes = [i, i, d, d, d, i, i, i, _dp, _dp, C.c_char_p, i]
+            L.ref_sample_step.argtypes = [i, i, i, d, d, d, d, i, i, _dp, C.POINTER(d), C.POINTER(d), _dp,
+                                          C.c_char_p, i]
             L.ref_set_threads.argtypes = [i]
             L.ref_get_threads.restype = i
             L.ref_blas_config.restype = C.c_char_p
@@ -127,6 +129,19 @@ class Ref:
                                       C.byref(tab), C.byref(sab))
         _check(rc, err.value, tab.value, sab.value)
         return u, v, nn.value, tt.value, sec.value
+
+    @classmethod
+    def sample_step(cls, n, nsub, nspecies, tau, kappas, q, src_kind, src_params=None, family=0):
+        """Bounded reference-step sample at full pencil length n (see ref_driver.cpp).
+        Returns (seconds_for_sample_points, sample_points, parts)."""
+        sec, pts = C.c_double(), C.c_double()
+        parts = np.zeros(3)
+        err = C.create_string_buffer(512)
+        k1 = kappas[1] if len(kappas) > 1 else 0.0
+        rc = cls.lib().ref_sample_step(n, nsub, nspecies, tau, kappas[0], k1, q, family, src_kind,
+                                       _params(src_params), C.byref(sec), C.byref(pts), parts, err, 512)
+        _check(rc, err.value, 0, 0)
+        return sec.value, pts.value, parts
 
     @classmethod
     def operator(cls, dim, n, axis, kappa, q):

@@ -267,6 +267,81 @@ int ref_system_run(int dim, int n, double tau, double ku, double kv, double q, i
     }
 }
 
+// Bounded CPU sample of ONE reference step at full pencil length n (bench.py
+// cpu_baseline / --impl reference).  A full-size 3D step at n=1023 needs
+// ~140 GiB and minutes on the box's host, so the reference step is run on a
+// z-sub-box (n, n, nsub) — its x and y applies are exactly the full-grid
+// per-point work — and its z-direction applies (2 per species: Qz1 of U and of
+// f(U), stepper.cpp:244-247) are re-timed on an (n, nsub, n) block whose z
+// pencils have the full length n.  Estimated per-step time on the sample's
+// points:  t_step(sub) - nz_applies*t_z(sub) + nz_applies*t_z(full-length).
+// Scalar plans (nspecies=1) use make_plan+advance, systems the composed step.
+int ref_sample_step(int n, int nsub, int nspecies, double tau, double k0, double k1, double q, int family,
+                    int src_kind, const double* src_params, double* out_seconds, double* out_points,
+                    double* parts /* [t_sub, t_zsub, t_zfull] */, char* err, int errlen) {
+    try {
+        const auto scheme = scheme_by_family(family ? PadeFamily::P04 : PadeFamily::P02);
+        const std::array<std::pair<double, double>, 3> b{{{0.0, 1.0}, {0.0, 1.0}, {0.0, 1.0}}};
+        const std::array<int, 3> msub{n + 1, n + 1, nsub + 1}, mz{n + 1, nsub + 1, n + 1};
+        const Grid gs = build_grid(3, b, msub), gz = build_grid(3, b, mz);
+        auto fill = [](const Grid& g, unsigned seed) {
+            Field f = Field::zeros(g);
+            unsigned long long x = seed * 0x9E3779B97F4A7C15ull + 1;
+            for (std::size_t i = 0; i < f.size(); ++i) {
+                x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+                f[i] = 0.5 * static_cast<double>(x >> 11) * 0x1.0p-53;
+            }
+            return f;
+        };
+        using clk = std::chrono::steady_clock;
+        auto secs = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+        double t_sub, t_zs, t_zf;
+        int z_applies;
+        if (nspecies == 1) {
+            const auto plan = make_plan(gs, tau, k0, q, scheme, BackendKind::Spectral);
+            const auto src = make_scalar_source(src_kind, src_params);
+            StepperState st{0, 0.0, fill(gs, 1)};
+            auto t0 = clk::now();
+            st = advance(plan, st, src);
+            t_sub = secs(t0, clk::now());
+            const auto& pz = plan.spectral[2];
+            const Field a = fill(gs, 2);
+            t0 = clk::now();
+            (void)apply_Q_spectral(pz, 1, tau, a, Axis::Z);
+            t_zs = secs(t0, clk::now());
+            const auto planz = make_plan(gz, tau, k0, q, scheme, BackendKind::Spectral);
+            const Field c = fill(gz, 3);
+            t0 = clk::now();
+            (void)apply_Q_spectral(planz.spectral[2], 1, tau, c, Axis::Z);
+            t_zf = secs(t0, clk::now());
+            z_applies = 2;
+        } else {
+            const auto sp = make_sys3(gs, tau, k0, k1, q, scheme);
+            const auto src = make_system_source(src_kind, src_params);
+            SystemState st{0, 0.0, fill(gs, 1), fill(gs, 4)};
+            auto t0 = clk::now();
+            st = sys3_step(sp, st, src);
+            t_sub = secs(t0, clk::now());
+            const Field a = fill(gs, 2);
+            t0 = clk::now();
+            (void)apply_Q_spectral(sp.pu[2], 1, tau, a, Axis::Z);
+            t_zs = secs(t0, clk::now());
+            const auto spz = make_sys3(gz, tau, k0, k1, q, scheme);
+            const Field c = fill(gz, 3);
+            t0 = clk::now();
+            (void)apply_Q_spectral(spz.pu[2], 1, tau, c, Axis::Z);
+            t_zf = secs(t0, clk::now());
+            z_applies = 4;
+        }
+        *out_seconds = t_sub - z_applies * t_zs + z_applies * t_zf;
+        *out_points = static_cast<double>(n) * n * nsub * nspecies;
+        if (parts) { parts[0] = t_sub; parts[1] = t_zs; parts[2] = t_zf; }
+        return 0;
+    } catch (const std::exception& e) {
+        return map_exc(e, err, errlen, nullptr, nullptr);
+    }
+}
+
 // operators.cpp:11-34 on unit_box_grid(dim, n+1)
 int ref_operator(int dim, int n, int axis, double kappa, double q, double* diag, double* off,
                  char* err, int errlen) {
