@@ -118,6 +118,14 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uin
         "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
+                                            int c1, int c2, int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+        : "memory");
+}
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -158,12 +166,12 @@ struct ContractCfg {
     static constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
     static constexpr int MF = WM / 8, NF = WN / 8;        // 8x8 DMMA fragments per warp
     static constexpr int L = PRO ? S / 2 : S;             // operands fetched by TMA
-    static constexpr int A_DBL = S * BM * BK;
+    static constexpr int A_DBL = L * BM * BK;             // f(U) operands never touch smem
     static constexpr int B_DBL = BN * BK;
     static constexpr int STAGE_DBL = A_DBL + B_DBL;
     static constexpr uint32_t TX_BYTES = (L * BM + BN) * BK * 8;
     static constexpr int SMEM_BYTES = STAGES * STAGE_DBL * 8 + 1024 + 2 * STAGES * 8 + 64;
-    static_assert(WM % 16 == 0 && WN % 8 == 0, "warp tile");
+    static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile");
     static_assert(BM % 16 == 0 && BN % 16 == 0, "cta tile");
 };
 
@@ -208,32 +216,23 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
 
     int bad = 0;  // non-finite seen (prologue or epilogue)
 
-    // TMA issue for k-tile kt into `stage` (thread 0 only)
+    // TMA issue for k-tile kt into `stage` (thread 0 only): one box for all
+    // loaded operands (A) and one for the transform-matrix tile (B).
+    //   MODE 0  A: 3D {k, pencil, op}            box {16, BM, L}      -> [op][BM][16]
+    //   MODE 1  A: 5D {x%16, k, x/16, outer, op} box {16,16,BM/16,1,L} -> [op][pb][16][16]
+    //   MODE 0  B: 2D {k, n}                     box {16, BN}         -> [BN][16]
+    //   MODE 1  B: 3D {n%16, k, n/16}            box {16, 16, BN/16}  -> [nb][16][16]
     auto issue = [&](int kt, int stage) {
         double* sA = smem + stage * C::STAGE_DBL;
         double* sB = sA + C::A_DBL;
         mbar_expect_tx(&full[stage], C::TX_BYTES);
         const int k0 = kt * BK;
-#pragma unroll
-        for (int c = 0; c < C::L; ++c) {
-            if constexpr (MODE == 0) {
-                tma_load_3d(sA + c * BM * BK, &tmA, &full[stage], k0, m0, c);
-            } else {
-#pragma unroll
-                for (int pb = 0; pb < BM / 16; ++pb) {
-                    double* dst = sA + (c * (BM / 16) + pb) * 256;
-                    if (args.zaxis)
-                        tma_load_4d(dst, &tmA, &full[stage], m0 + pb * 16, outer, k0, c);
-                    else
-                        tma_load_4d(dst, &tmA, &full[stage], m0 + pb * 16, k0, outer, c);
-                }
-            }
-        }
         if constexpr (MODE == 0) {
+            tma_load_3d(sA, &tmA, &full[stage], k0, m0, 0);
             tma_load_2d(sB, &tmB, &full[stage], k0, n0);
         } else {
-#pragma unroll
-            for (int nb = 0; nb < BN / 16; ++nb) tma_load_2d(sB + nb * 256, &tmB, &full[stage], n0 + nb * 16, k0);
+            tma_load_5d(sA, &tmA, &full[stage], 0, k0, m0 >> 4, outer, 0);
+            tma_load_3d(sB, &tmB, &full[stage], 0, k0, n0 >> 4);
         }
     };
     if (tid == 0) {
@@ -260,37 +259,6 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
             mbar_wait(&full[stage], phase);
             double* sA = smem + stage * C::STAGE_DBL;
             const double* sB = sA + C::A_DBL;
-            if constexpr (PRO) {
-                // fused source evaluation on the freshly landed state tile:
-                // slots [0,ns) hold U (,V); slots [ns,2ns) receive f(U(,V))
-                constexpr int ELEMS = BM * BK;
-                const int ns = S / 2;
-#pragma unroll
-                for (int q = 0; q < ELEMS / (32 * C::NW); ++q) {
-                    const int e = tid + q * 32 * C::NW;
-                    // decode the logical (p, k) of smem element e ([pb][kk][16] swizzled)
-                    const int pb = e >> 8, kk = (e >> 4) & 15;
-                    const int col = ((((e >> 1) & 7) ^ (kk & 7)) << 1) | (e & 1);
-                    const int p = m0 + pb * 16 + col, kc = kt * BK + kk;
-                    const bool valid = p < args.m_extent && kc < args.n_axis;
-                    const bool origin = args.src_kind == 3 && p == 0 &&
-                                        (args.zaxis ? (kc + args.gz0 == 0 && outer + args.gj0 == 0)
-                                                    : (kc + args.gj0 == 0 && outer + args.gz0 == 0));
-                    if (ns == 1) {
-                        double f = src_scalar(args.src_kind, args.sp, sA[e]);
-                        if (origin) f = __longlong_as_double(0x7ff8000000000000ll);
-                        sA[BM * BK + e] = f;
-                        bad |= valid && !isfinite(f);
-                    } else {
-                        double fu, fv;
-                        src_pair(args.src_kind, args.sp, sA[e], sA[BM * BK + e], fu, fv);
-                        sA[2 * BM * BK + e] = fu;
-                        sA[3 * BM * BK + e] = fv;
-                        bad |= valid && !(isfinite(fu) && isfinite(fv));
-                    }
-                }
-                named_bar_sync(1, 32 * C::NW);
-            }
 #pragma unroll
             for (int st = 0; st < BK / 4; ++st) {
                 // k permutation inside the 16-wide stage keeps both fragment loads
@@ -304,13 +272,38 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
                     b[j] = MODE == 0 ? sB[swz(nn, kk)] : sB[(nn >> 4) * 256 + swz(kk, nn & 15)];
                 }
 #pragma unroll
-                for (int s = 0; s < S; ++s)
+                for (int s = 0; s < C::L; ++s)
 #pragma unroll
                     for (int i = 0; i < C::MF; ++i) {
                         const int mm = wm0 + i * 8 + g;
                         const double* base = sA + s * BM * BK;
                         a[s][i] = MODE == 0 ? base[swz(mm, kk)] : base[(mm >> 4) * 256 + swz(kk, mm & 15)];
                     }
+                if constexpr (PRO) {
+                    // fused source: the A fragment of f(U) at (m, k) is f of the U
+                    // fragment at (m, k) — evaluated in registers, no smem, no barrier
+                    const int kc = kt * BK + kk;
+#pragma unroll
+                    for (int i = 0; i < C::MF; ++i) {
+                        const int p = m0 + wm0 + i * 8 + g;
+                        const bool valid = p < args.m_extent && kc < args.n_axis;
+                        if constexpr (C::L == 1) {
+                            double f = src_scalar(args.src_kind, args.sp, a[0][i]);
+                            if (args.src_kind == 3 && p == 0 &&
+                                (args.zaxis ? (kc + args.gz0 == 0 && outer + args.gj0 == 0)
+                                            : (kc + args.gj0 == 0 && outer + args.gz0 == 0)))
+                                f = __longlong_as_double(0x7ff8000000000000ll);
+                            a[1][i] = f;
+                            bad |= valid && !isfinite(f);
+                        } else {
+                            double fu, fv;
+                            src_pair(args.src_kind, args.sp, a[0][i], a[1][i], fu, fv);
+                            a[2][i] = fu;
+                            a[3][i] = fv;
+                            bad |= valid && !(isfinite(fu) && isfinite(fv));
+                        }
+                    }
+                }
 #pragma unroll
                 for (int s = 0; s < S; ++s)
 #pragma unroll

@@ -90,22 +90,23 @@ struct KernelSpec {
     int threads, smem, bm, bn, S;
 };
 
+template <int MODE, int S, int EPI, bool PRO, int BM, int BN, int WMW, int WNW, int ST>
+static KernelSpec make_spec() {
+    using Cfg = ContractCfg<MODE, S, EPI, PRO, BM, BN, WMW, WNW, ST>;
+    auto k = etd_contract<MODE, S, EPI, PRO, BM, BN, WMW, WNW, ST>;
+    return {reinterpret_cast<const void*>(k), Cfg::THREADS, Cfg::SMEM_BYTES, BM, BN, S};
+}
+
 template <int MODE, int S, int EPI, bool PRO>
 static KernelSpec spec() {
-    // Tile shapes: every variant keeps 64 FP64 accumulators per consumer thread.
-    if constexpr (S == 1) {
-        using Cfg = ContractCfg<MODE, 1, EPI, PRO, 128, 128, 4, 2, 6>;
-        auto k = etd_contract<MODE, 1, EPI, PRO, 128, 128, 4, 2, 6>;
-        return {reinterpret_cast<const void*>(k), Cfg::THREADS, Cfg::SMEM_BYTES, 128, 128, 1};
-    } else if constexpr (S == 2) {
-        using Cfg = ContractCfg<MODE, 2, EPI, PRO, 64, 128, 2, 4, 6>;
-        auto k = etd_contract<MODE, 2, EPI, PRO, 64, 128, 2, 4, 6>;
-        return {reinterpret_cast<const void*>(k), Cfg::THREADS, Cfg::SMEM_BYTES, 64, 128, 2};
-    } else {
-        using Cfg = ContractCfg<MODE, 4, EPI, PRO, 64, 64, 2, 4, 5>;
-        auto k = etd_contract<MODE, 4, EPI, PRO, 64, 64, 2, 4, 5>;
-        return {reinterpret_cast<const void*>(k), Cfg::THREADS, Cfg::SMEM_BYTES, 64, 64, 4};
-    }
+    // Tile shapes: every variant keeps 64 FP64 accumulators per thread (8 warps).
+    // Source-prologue kernels use an 8x1 warp grid so that each A element's
+    // f(U) is evaluated by exactly one warp (it runs on the shared FP64/DMMA pipe).
+    if constexpr (S == 1) return make_spec<MODE, 1, EPI, PRO, 128, 128, 4, 2, 6>();
+    else if constexpr (S == 2 && PRO) return make_spec<MODE, 2, EPI, PRO, 64, 128, 8, 1, 8>();
+    else if constexpr (S == 2) return make_spec<MODE, 2, EPI, PRO, 64, 128, 2, 4, 6>();
+    else if constexpr (PRO) return make_spec<MODE, 4, EPI, PRO, 64, 64, 8, 1, 8>();
+    else return make_spec<MODE, 4, EPI, PRO, 64, 64, 2, 4, 5>();
 }
 
 static KernelSpec pick(int mode, int S, int epi, bool pro) {
@@ -194,31 +195,40 @@ struct Plan {
     }
     int n_axis(int a) const { return a == 0 ? nx : a == 1 ? ny : nz; }
 
-    // ---- maps over stacked fields ----
-    // MODE 0 view: dims {nx, R, count}, box {16, BM, 1}
+    // ---- maps over stacked fields (one TMA box per stage per operand set) ----
+    // MODE 0 view: dims {nx, R, count}, box {16, BM, count} -> smem [op][BM][16]
     CUtensorMap mapA_x(const double* base, int count, int bm) const {
         const unsigned long long dims[3] = {(unsigned long long)nx, (unsigned long long)ny * nz,
                                             (unsigned long long)count};
         const unsigned long long st[2] = {(unsigned long long)pitch, (unsigned long long)F};
-        const unsigned box[3] = {16, (unsigned)bm, 1};
+        const unsigned box[3] = {16, (unsigned)bm, (unsigned)count};
         return make_map(base, 3, dims, st, box);
     }
-    // MODE 1 view: dims {nx, ny, nz, count}, box {16, 16,1,1} (y) or {16,1,16,1} (z)
-    CUtensorMap mapA_yz(const double* base, int count, bool zaxis) const {
-        const unsigned long long dims[4] = {(unsigned long long)nx, (unsigned long long)ny,
-                                            (unsigned long long)nz, (unsigned long long)count};
-        const unsigned long long st[3] = {(unsigned long long)pitch, (unsigned long long)plane,
-                                          (unsigned long long)F};
-        const unsigned box[4] = {16, zaxis ? 1u : 16u, zaxis ? 16u : 1u, 1};
-        return make_map(base, 4, dims, st, box);
+    // MODE 1 view: dims {x%16, k, x/16, outer, count}, box {16, 16, BM/16, 1, count}
+    // -> smem [op][pb][k][16].  x columns past nx read the zero pad of the pitch.
+    CUtensorMap mapA_yz(const double* base, int count, bool zaxis, int bm) const {
+        const unsigned long long nk = zaxis ? nz : ny, no = zaxis ? ny : nz;
+        const unsigned long long sk = zaxis ? plane : pitch, so = zaxis ? pitch : plane;
+        const unsigned long long dims[5] = {16, nk, (unsigned long long)((nx + 15) / 16), no,
+                                            (unsigned long long)count};
+        const unsigned long long st[4] = {sk, 16, so, (unsigned long long)F};
+        const unsigned box[5] = {16, 16, (unsigned)(bm / 16), 1, (unsigned)count};
+        return make_map(base, 5, dims, st, box);
     }
-    // B: row-major n x n (padded rows), MODE 0 box {16, BN}, MODE 1 box {16, 16}
+    // B: row-major n x n (zero-padded to npad).  MODE 0: dims {k, n} box {16, BN};
+    // MODE 1: dims {n%16, k, n/16} box {16, 16, BN/16} -> smem [nb][k][16]
     CUtensorMap mapB(const double* M, int axis, int mode, int bn) const {
         const int n = n_axis(axis);
-        const unsigned long long dims[2] = {(unsigned long long)n, (unsigned long long)n};
-        const unsigned long long st[1] = {(unsigned long long)npad[axis]};
-        const unsigned box[2] = {16, mode == 0 ? (unsigned)bn : 16u};
-        return make_map(M, 2, dims, st, box);
+        if (mode == 0) {
+            const unsigned long long dims[2] = {(unsigned long long)n, (unsigned long long)n};
+            const unsigned long long st[1] = {(unsigned long long)npad[axis]};
+            const unsigned box[2] = {16, (unsigned)bn};
+            return make_map(M, 2, dims, st, box);
+        }
+        const unsigned long long dims[3] = {16, (unsigned long long)n, (unsigned long long)(npad[axis] / 16)};
+        const unsigned long long st[2] = {(unsigned long long)npad[axis], 16};
+        const unsigned box[3] = {16, 16, (unsigned)(bn / 16)};
+        return make_map(M, 3, dims, st, box);
     }
 
     ContractArgs base_args(int axis) const {
@@ -252,7 +262,7 @@ struct Plan {
         const int loaded = pro ? S / 2 : S;
         // fwd (M = P^T): mode 0 needs row-major P^T, mode 1 row-major P; back swaps
         const double* M = (mode == 0) != back ? PTR[axis] : PR[axis];
-        L.tmA = mode == 0 ? mapA_x(in, loaded, L.k.bm) : mapA_yz(in, loaded, axis == 2);
+        L.tmA = mode == 0 ? mapA_x(in, loaded, L.k.bm) : mapA_yz(in, loaded, axis == 2, L.k.bm);
         L.tmB = mapB(M, axis, mode, L.k.bn);
         L.args = base_args(axis);
         L.args.out = out;
