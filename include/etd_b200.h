@@ -70,7 +70,14 @@ typedef struct etd_desc {
     /* z-slab sharding (3D): rank `rank` of `world_size` owns planes
      * [etd_slab_range) ; world_size==1 -> whole grid on one GPU. */
     int world_size, rank;
-    const void* nccl_unique_id; /* 128-byte ncclUniqueId (world_size > 1)            */
+    const void* nccl_unique_id; /* The data movement of one sharded step for rank `rank` (host only): records of
+ * 12 int64 {kind(0 copy2d,1 send,2 recv), phase(0 pack,1 fwd,2 back,3 unpack),
+ * peer, dst_buf, dst_off, dst_pitch, src_buf, src_off, src_pitch, width, height,
+ * count}, element units; buffers 0 state,1 send,2 zin,3 wz,4 recv,5 w.
+ * out may be NULL to query *count. */
+int etd_sharded_schedule(int nx, int ny, int nz, int nspecies, int world_size, int rank, long long pitch,
+                         long long* out, int capacity, int* count);
+/* 128-byte ncclUniqueId (world_size > 1)            */
 } etd_desc;
 
 typedef struct etd_handle etd_handle;
@@ -83,6 +90,23 @@ int etd_destroy(etd_handle* h);
 
 /* This rank's z-slab [z0, z1) (3D) or [0,1) (2D). */
 int etd_slab_range(const etd_handle* h, int* z0, int* z1);
+/* The balanced partition every sharded plan uses for z planes (x/y stages) and
+ * y rows (z stage): rank r gets [lo, hi), sizes differ by at most one.  Host only. */
+int etd_zslab_partition(int n, int world_size, int rank, int* lo, int* hi);
+/* The data movement of one sharded step for rank `rank` (host only): records of
+ * 12 int64 {kind(0 copy2d,1 send,2 recv), phase(0 pack,1 fwd,2 back,3 unpack),
+ * peer, dst_buf, dst_off, dst_pitch, src_buf, src_off, src_pitch, width, height,
+ * count}, element units; buffers 0 state,1 send,2 zin,3 wz,4 recv,5 w.
+ * out may be NULL to query *count. */
+int etd_sharded_schedule(int nx, int ny, int nz, int nspecies, int world_size, int rank, long long pitch,
+                         long long* out, int capacity, int* count);
+/* 128-byte ncclUniqueId for etd_desc.nccl_unique_id (rank 0 creates, all ranks
+ * receive it out of band, e.g. over torch.distributed). */
+int etd_nccl_unique_id(void* out128);
+/* Virtual ranks: plans created with world_size = G and nccl_unique_id = NULL on
+ * one device form a group stepped here in lock-step (exchanges become device
+ * copies).  Same schedule and abort semantics as the NCCL path. */
+int etd_group_step(etd_handle** handles, int count, int nsteps);
 
 /* StepperState/SystemState upload (stepper.hpp:63-67,110-114): species 0=U,
  * 1=V; count = nx*ny*(z1-z0) values (this rank's slab), n,t = state.n,state.t. */

@@ -9,7 +9,7 @@ from .etd import (BackendKind, ConfigError, DeviceError, DeviceSource, Grid, Mem
                   PadeFamily, SourceKind, StepperAbort, StepperPlan, StepperState, SystemPlan, SystemState,
                   advance, allen_cahn_cubic, build_grid, etd2rkds_step_system, fhn_classic, fhn_cubic,
                   fill_config_ic, lib, make_plan, make_system_plan, poly3, setup_axis, setup_dvector,
-                  setup_scheme, unit_box_grid)
+                  setup_scheme, unit_box_grid, zslab_partition, nccl_unique_id, group_step)
 from . import configs
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -65,6 +65,8 @@ struct ContractArgs {
     int gj0, gz0;           // global (j,z) offset of this buffer (slabs / z-stage)
     StepStatus* status;
     double tau;
+    int commit;             // EPI_UPDATE: last CTA commits the step (single GPU); 0 under
+                            // z-slab sharding, where etd_commit runs after a global check
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
             const int kind = EPI == EPI_WHAT_SRC ? 2 : EPI == EPI_UPDATE ? 3 : 1;
             atomicCAS(&args.status->fail, 0, kind);
         }
-        if constexpr (EPI == EPI_UPDATE) {
+        if (EPI == EPI_UPDATE && args.commit) {
             // last CTA of the final stage commits the step: n += 1, t = n tau
             // (stepper.cpp:228).  An aborted step is never committed.
             __threadfence();
@@ -413,6 +415,28 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
                 }
             }
         }
+    }
+}
+
+// ------------------------------------------------------------- sharded-step bookkeeping
+// Under z-slab sharding every rank must agree on whether step n aborted (the
+// reference aborts the whole step).  Each rank publishes a code (its fail kind,
+// or 100 = ok), the codes are gathered over the exchange transport, and
+// etd_commit applies the first-in-program-order failure (min kind) everywhere or
+// commits n += 1, t = n tau on every rank (stepper.cpp:228).
+__global__ void etd_fail_code(const StepStatus* st, int* code) {
+    const int f = *reinterpret_cast<const volatile int*>(&st->fail);
+    *code = f ? f : 100;
+}
+__global__ void etd_commit(StepStatus* st, const int* codes, int ncodes, double tau) {
+    int g = 100;
+    for (int i = 0; i < ncodes; ++i) g = min(g, codes[i]);
+    if (g < 100) {
+        st->fail = g;
+    } else if (st->fail == 0) {
+        const long long nn = st->n + 1;
+        st->n = nn;
+        st->t = (double)nn * tau;
     }
 }
 

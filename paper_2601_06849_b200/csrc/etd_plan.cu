@@ -16,6 +16,8 @@
 // stepper.cpp:182-229).
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -134,6 +136,50 @@ static KernelSpec pick(int mode, int S, int epi, bool pro) {
     throw ConfigError("no kernel variant for this stage");
 }
 
+// ------------------------------------------------------------ NCCL (dlopen'd)
+// The extension does not link NCCL: single-GPU users and CPU tests never load
+// it.  Sharded plans resolve it at etd_create (torch's bundled libnccl.so.2
+// when torch is already loaded, else the system one).
+struct Nccl {
+    using ncclComm_t = void*;
+    int (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    int (*CommDestroy)(ncclComm_t) = nullptr;
+    int (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    int (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    int (*GroupStart)() = nullptr;
+    int (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+    bool ok = false;
+
+    static Nccl& get() {
+        static Nccl n;
+        if (!n.ok) {
+            void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+            if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+            if (!h) throw CudaError("libnccl.so.2 not found (needed for z-slab sharding)");
+            auto sym = [&](const char* s) {
+                void* f = dlsym(h, s);
+                if (!f) throw CudaError(std::string("NCCL symbol missing: ") + s);
+                return f;
+            };
+            n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(sym("ncclGetUniqueId"));
+            n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(sym("ncclCommInitRank"));
+            n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(sym("ncclCommDestroy"));
+            n.Send = reinterpret_cast<decltype(n.Send)>(sym("ncclSend"));
+            n.Recv = reinterpret_cast<decltype(n.Recv)>(sym("ncclRecv"));
+            n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(sym("ncclGroupStart"));
+            n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(sym("ncclGroupEnd"));
+            n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(sym("ncclGetErrorString"));
+            n.ok = true;
+        }
+        return n;
+    }
+    void check(int r, const char* what) const {
+        if (r != 0) throw CudaError(std::string(what) + ": " + (GetErrorString ? GetErrorString(r) : "nccl error"));
+    }
+};
+
 // ------------------------------------------------------------ the plan
 struct Launch {
     std::string name;
@@ -144,6 +190,23 @@ struct Launch {
     double flops = 0, bytes = 0;
 };
 
+// A piece of an exchange: `bytes` at `ptr` to (send) or from (recv) rank `peer`.
+struct Piece {
+    int peer;
+    void* ptr;
+    size_t bytes;
+};
+
+struct Op {
+    enum Kind { KERNEL, COPY2D, EXCHANGE, FAILCODE, COMMIT } kind = KERNEL;
+    Launch L;                                    // KERNEL
+    void* dst = nullptr;                         // COPY2D
+    const void* src = nullptr;
+    size_t dpitch = 0, spitch = 0, width = 0, height = 0;
+    std::vector<Piece> sends, recvs;             // EXCHANGE (matched by order per peer)
+    std::string name;
+};
+
 struct StageStat {
     std::string name;
     double ms = 0;
@@ -151,74 +214,165 @@ struct StageStat {
     double flops = 0, bytes = 0;
 };
 
+// Logical extents + strides of one buffer family (the slab, or the z-stage rows).
+struct View {
+    int nx = 1, ny = 1, nz = 1;
+    long long pitch = 0, plane = 0, F = 0;
+    int gj0 = 0, gz0 = 0;
+};
+
+static void partition(int n, int G, int r, int& lo, int& hi) {
+    const int base = n / G, rem = n % G;
+    lo = r * base + std::min(r, rem);
+    hi = lo + base + (r < rem ? 1 : 0);
+}
+
+// ------------------------------------------------------------ sharded schedule
+// Host-only description of the data movement of one sharded step (z-slab
+// layout for the x/y stages, y-row layout for the z stage).  Offsets and sizes
+// are in elements relative to the named buffers; build_plan turns the records
+// into device ops and etd_sharded_schedule exports them for the CPU
+// multi-process test (tests/test_dist_cpu.py), which runs the same schedule
+// over gloo.
+enum SchedBuf { SB_STATE = 0, SB_SEND = 1, SB_ZIN = 2, SB_WZ = 3, SB_RECV = 4, SB_W = 5 };
+enum SchedKind { SK_COPY = 0, SK_SEND = 1, SK_RECV = 2 };
+enum SchedPhase { SP_PACK = 0, SP_FWD = 1, SP_BACK = 2, SP_UNPACK = 3 };
+struct SchedRec {
+    long long kind, phase, peer;
+    long long dbuf, doff, dpitch;   // COPY: 2D copy, width/height in elements/rows
+    long long sbuf, soff, spitch;   // SEND/RECV: buffer in (sbuf|dbuf), offset, count
+    long long width, height, count;
+};
+
+static std::vector<SchedRec> sharded_schedule(int nx, int ny, int nz, int ns, int G, int r, long long pitch) {
+    (void)nx;
+    std::vector<int> zl(G), zh(G), jl(G), jh(G);
+    for (int s = 0; s < G; ++s) {
+        partition(nz, G, s, zl[s], zh[s]);
+        partition(ny, G, s, jl[s], jh[s]);
+    }
+    const long long nzr = zh[r] - zl[r], njr = jh[r] - jl[r];
+    const long long plane = pitch * ny, F = plane * nzr;            // slab field
+    const long long planez = pitch * njr, Fz = planez * nz;         // z-stage field
+    std::vector<long long> sblock(G), roff(G);
+    long long so = 0, ro = 0;
+    for (int s = 0; s < G; ++s) {
+        const long long njs = jh[s] - jl[s];
+        sblock[s] = so;
+        so += ns * nzr * njs * pitch;
+        roff[s] = ro;
+        ro += nzr * njs * pitch;
+    }
+    std::vector<SchedRec> out;
+    // pack: state[c][zl][j in rows(s)][:] -> send[s][c][zl][jj][:]
+    for (int s = 0; s < G; ++s) {
+        const long long njs = jh[s] - jl[s];
+        for (int c = 0; c < ns; ++c)
+            out.push_back({SK_COPY, SP_PACK, s, SB_SEND, sblock[s] + c * nzr * njs * pitch, njs * pitch, SB_STATE,
+                           c * F + jl[s] * pitch, plane, njs * pitch, nzr, njs * pitch * nzr});
+    }
+    // forward exchange: (s, c) blocks; receiver stores z in slab(s) contiguously
+    for (int s = 0; s < G; ++s) {
+        const long long njs = jh[s] - jl[s], nzs = zh[s] - zl[s];
+        for (int c = 0; c < ns; ++c) {
+            out.push_back({SK_SEND, SP_FWD, s, 0, 0, 0, SB_SEND, sblock[s] + c * nzr * njs * pitch, 0, 0, 0,
+                           nzr * njs * pitch});
+            out.push_back({SK_RECV, SP_FWD, s, SB_ZIN, c * Fz + zl[s] * planez, 0, 0, 0, 0, 0, 0, nzs * planez});
+        }
+    }
+    // backward exchange of the 2ns z-filtered fields
+    for (int c = 0; c < 2 * ns; ++c)
+        for (int s = 0; s < G; ++s) {
+            const long long njs = jh[s] - jl[s], nzs = zh[s] - zl[s];
+            out.push_back({SK_SEND, SP_BACK, s, 0, 0, 0, SB_WZ, c * Fz + zl[s] * planez, 0, 0, 0, nzs * planez});
+            out.push_back({SK_RECV, SP_BACK, s, SB_RECV, c * F + roff[s], 0, 0, 0, 0, 0, 0, nzr * njs * pitch});
+        }
+    // unpack: recv[c][s][zl][jj][:] -> W[c][zl][j in rows(s)][:]
+    for (int c = 0; c < 2 * ns; ++c)
+        for (int s = 0; s < G; ++s) {
+            const long long njs = jh[s] - jl[s];
+            out.push_back({SK_COPY, SP_UNPACK, s, SB_W, c * F + jl[s] * pitch, plane, SB_RECV, c * F + roff[s],
+                           njs * pitch, njs * pitch, nzr, njs * pitch * nzr});
+        }
+    return out;
+}
+
 struct Plan {
     etd_desc d{};
     int dim = 2, ns = 1;
-    int nx = 1, ny = 1, nz = 1;  // local extents
+    int G = 1, rank = 0;
+    bool sharded = false, local_group = false;
+    int nx = 1, ny = 1, nz = 1;      // global interior extents
     int npad[3] = {0, 0, 0};
-    long long pitch = 0, plane = 0, F = 0;
+    long long pitch = 0;
+    View slab, zst;                  // x/y-stage (z-slab) view, z-stage (y-rows) view
+    std::vector<int> zlo, zhi, jlo, jhi;
     double tau = 0;
     cudaStream_t stream = nullptr;
     double* state[2] = {nullptr, nullptr};
     double* Z = nullptr;
     double* W = nullptr;
+    double* sendbuf = nullptr;       // sharded: forward-exchange send blocks
+    double* zin = nullptr;           // sharded: z-stage input (U,V gathered along z)
+    double* Zz = nullptr;
+    double* Wz = nullptr;
+    double* recvb = nullptr;         // sharded: backward-exchange receive blocks
+    int* codes = nullptr;            // sharded: [G] gathered fail codes; codes[G] = own
     double* PR[3] = {nullptr, nullptr, nullptr};
     double* PTR[3] = {nullptr, nullptr, nullptr};
-    double* dvec = nullptr;  // [axis][slot 9][species 2][npadmax]
+    double* dvec = nullptr;          // [axis][slot 9][species 2][dmax]
     int dmax = 0;
     StepStatus* status = nullptr;
     StepStatus* status_host = nullptr;
     int cur = 0;
-    std::vector<Launch> steps[2];
+    std::vector<Op> steps[2];
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     bool profiling = false;
     std::vector<StageStat> stats;
-    std::string last_msg;
-    double last_t = 0;
-    long last_step = 0;
+    void* comm = nullptr;            // ncclComm_t
 
     ~Plan() {
         for (auto& g : graph)
             if (g) cudaGraphExecDestroy(g);
-        for (auto p : {state[0], state[1], Z, W, dvec}) if (p) cudaFree(p);
+        for (double* p : {state[0], state[1], Z, W, dvec, sendbuf, zin, Zz, Wz, recvb}) if (p) cudaFree(p);
+        if (codes) cudaFree(codes);
         for (int a = 0; a < 3; ++a) {
             if (PR[a]) cudaFree(PR[a]);
             if (PTR[a]) cudaFree(PTR[a]);
         }
         if (status) cudaFree(status);
         if (status_host) cudaFreeHost(status_host);
+        if (comm) Nccl::get().CommDestroy(comm);
         if (stream) cudaStreamDestroy(stream);
     }
 
-    const double* dv(int axis, int slot) const {
-        return dvec + ((size_t)axis * 9 + slot) * 2 * dmax;
-    }
-    int n_axis(int a) const { return a == 0 ? nx : a == 1 ? ny : nz; }
+    const double* dv(int axis, int slot) const { return dvec + ((size_t)axis * 9 + slot) * 2 * dmax; }
+    static int n_axis(const View& v, int a) { return a == 0 ? v.nx : a == 1 ? v.ny : v.nz; }
 
     // ---- maps over stacked fields (one TMA box per stage per operand set) ----
     // MODE 0 view: dims {nx, R, count}, box {16, BM, count} -> smem [op][BM][16]
-    CUtensorMap mapA_x(const double* base, int count, int bm) const {
-        const unsigned long long dims[3] = {(unsigned long long)nx, (unsigned long long)ny * nz,
+    static CUtensorMap mapA_x(const View& v, const double* base, int count, int bm) {
+        const unsigned long long dims[3] = {(unsigned long long)v.nx, (unsigned long long)v.ny * v.nz,
                                             (unsigned long long)count};
-        const unsigned long long st[2] = {(unsigned long long)pitch, (unsigned long long)F};
+        const unsigned long long st[2] = {(unsigned long long)v.pitch, (unsigned long long)v.F};
         const unsigned box[3] = {16, (unsigned)bm, (unsigned)count};
         return make_map(base, 3, dims, st, box);
     }
     // MODE 1 view: dims {x%16, k, x/16, outer, count}, box {16, 16, BM/16, 1, count}
     // -> smem [op][pb][k][16].  x columns past nx read the zero pad of the pitch.
-    CUtensorMap mapA_yz(const double* base, int count, bool zaxis, int bm) const {
-        const unsigned long long nk = zaxis ? nz : ny, no = zaxis ? ny : nz;
-        const unsigned long long sk = zaxis ? plane : pitch, so = zaxis ? pitch : plane;
-        const unsigned long long dims[5] = {16, nk, (unsigned long long)((nx + 15) / 16), no,
+    static CUtensorMap mapA_yz(const View& v, const double* base, int count, bool zaxis, int bm) {
+        const unsigned long long nk = zaxis ? v.nz : v.ny, no = zaxis ? v.ny : v.nz;
+        const unsigned long long sk = zaxis ? v.plane : v.pitch, so = zaxis ? v.pitch : v.plane;
+        const unsigned long long dims[5] = {16, nk, (unsigned long long)((v.nx + 15) / 16), no,
                                             (unsigned long long)count};
-        const unsigned long long st[4] = {sk, 16, so, (unsigned long long)F};
+        const unsigned long long st[4] = {sk, 16, so, (unsigned long long)v.F};
         const unsigned box[5] = {16, 16, (unsigned)(bm / 16), 1, (unsigned)count};
         return make_map(base, 5, dims, st, box);
     }
     // B: row-major n x n (zero-padded to npad).  MODE 0: dims {k, n} box {16, BN};
     // MODE 1: dims {n%16, k, n/16} box {16, 16, BN/16} -> smem [nb][k][16]
     CUtensorMap mapB(const double* M, int axis, int mode, int bn) const {
-        const int n = n_axis(axis);
+        const int n = d.n[axis];
         if (mode == 0) {
             const unsigned long long dims[2] = {(unsigned long long)n, (unsigned long long)n};
             const unsigned long long st[1] = {(unsigned long long)npad[axis]};
@@ -231,29 +385,30 @@ struct Plan {
         return make_map(M, 3, dims, st, box);
     }
 
-    ContractArgs base_args(int axis) const {
+    ContractArgs base_args(const View& v, int axis) const {
         ContractArgs a{};
-        a.n_axis = n_axis(axis);
-        a.m_extent = axis == 0 ? ny * nz : nx;
+        a.n_axis = n_axis(v, axis);
+        a.m_extent = axis == 0 ? v.ny * v.nz : v.nx;
         a.zaxis = axis == 2;
         a.nspecies = ns;
-        a.pitch = pitch;
-        a.plane = plane;
-        a.out_stride = F;
-        a.aux_stride = F;
+        a.pitch = v.pitch;
+        a.plane = v.plane;
+        a.out_stride = v.F;
+        a.aux_stride = v.F;
         a.dstride = dmax;
         a.src_kind = d.src_kind;
         for (int i = 0; i < 8; ++i) a.sp[i] = d.src_params[i];
-        a.ny_local = ny;
-        a.gj0 = 0;
-        a.gz0 = 0;
+        a.ny_local = v.ny;
+        a.gj0 = v.gj0;
+        a.gz0 = v.gz0;
         a.status = status;
         a.tau = tau;
+        a.commit = sharded ? 0 : 1;
         return a;
     }
 
     // A transform along `axis` of `S` stacked operands at `in` (L loaded), M = P^T (fwd) or P.
-    Launch transform(const std::string& name, int axis, bool back, int S, int epi, bool pro,
+    Launch transform(const View& v, const std::string& name, int axis, bool back, int S, int epi, bool pro,
                      const double* in, double* out) const {
         Launch L;
         L.name = name;
@@ -262,18 +417,22 @@ struct Plan {
         const int loaded = pro ? S / 2 : S;
         // fwd (M = P^T): mode 0 needs row-major P^T, mode 1 row-major P; back swaps
         const double* M = (mode == 0) != back ? PTR[axis] : PR[axis];
-        L.tmA = mode == 0 ? mapA_x(in, loaded, L.k.bm) : mapA_yz(in, loaded, axis == 2, L.k.bm);
+        L.tmA = mode == 0 ? mapA_x(v, in, loaded, L.k.bm) : mapA_yz(v, in, loaded, axis == 2, L.k.bm);
         L.tmB = mapB(M, axis, mode, L.k.bn);
-        L.args = base_args(axis);
+        L.args = base_args(v, axis);
         L.args.out = out;
-        const int nax = n_axis(axis);
+        const int nax = n_axis(v, axis);
         const long long mext = L.args.m_extent;
         const unsigned gx = (nax + L.k.bn - 1) / L.k.bn;
         const unsigned gy = (unsigned)((mext + L.k.bm - 1) / L.k.bm);
-        const unsigned gz = mode == 0 ? 1u : (axis == 1 ? (unsigned)nz : (unsigned)ny);
+        const unsigned gz = mode == 0 ? 1u : (axis == 1 ? (unsigned)v.nz : (unsigned)v.ny);
         L.grid = dim3(gx, gy, gz);
-        const double pts = (double)nx * ny * nz;
+        const double pts = (double)v.nx * v.ny * v.nz;
         L.flops = 2.0 * nax * pts * S;
+        int outs = S, aux = 0;
+        if (epi == EPI_WHAT_SRC) outs = 2 * S;
+        if (epi == EPI_CORR || epi == EPI_UPDATE) aux = S;
+        L.bytes = pts * 8.0 * (loaded + outs + aux);
         return L;
     }
 };
@@ -289,36 +448,81 @@ static void check_source(int nspecies, int k) {
         throw ConfigError("the CUDA backend needs a device source descriptor matching the plan (no CPU fallback)");
 }
 
+static void drop_graphs(Plan& p) {
+    for (auto& g : p.graph)
+        if (g) {
+            cudaGraphExecDestroy(g);
+            g = nullptr;
+        }
+}
+
 static void set_source(Plan& p, int kind, const double* params) {
     check_source(p.ns, kind);
     p.d.src_kind = kind;
     for (int i = 0; i < 8; ++i) p.d.src_params[i] = params ? params[i] : 0.0;
-    for (int par = 0; par < 2; ++par) {
-        for (auto& L : p.steps[par]) {
-            L.args.src_kind = kind;
-            for (int i = 0; i < 8; ++i) L.args.sp[i] = p.d.src_params[i];
-        }
-        if (p.graph[par]) {
-            cudaGraphExecDestroy(p.graph[par]);
-            p.graph[par] = nullptr;
-        }
-    }
+    for (int par = 0; par < 2; ++par)
+        for (auto& op : p.steps[par])
+            if (op.kind == Op::KERNEL) {
+                op.L.args.src_kind = kind;
+                for (int i = 0; i < 8; ++i) op.L.args.sp[i] = p.d.src_params[i];
+            }
+    drop_graphs(p);
 }
 
-static void build_plan(Plan& p, const etd_desc& d) {
-    p.d = d;
+static Op kernel_op(Launch L) {
+    Op o;
+    o.kind = Op::KERNEL;
+    o.name = L.name;
+    o.L = std::move(L);
+    return o;
+}
+
+static Op copy_op(const std::string& name, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                  size_t height) {
+    Op o;
+    o.kind = Op::COPY2D;
+    o.name = name;
+    o.dst = dst;
+    o.dpitch = dpitch;
+    o.src = src;
+    o.spitch = spitch;
+    o.width = width;
+    o.height = height;
+    return o;
+}
+
+static void validate(const etd_desc& d) {
     if (d.dim != 2 && d.dim != 3) throw ConfigError("grid dimension must be 2 or 3");
     if (!(d.tau > 0.0)) throw ConfigError("tau must be positive");
     if (d.nspecies != 1 && d.nspecies != 2) throw ConfigError("nspecies must be 1 or 2");
     if (d.family != 0 && d.family != 1) throw ConfigError("unknown Pade family");
-    const bool sys = d.nspecies == 2;
     check_source(d.nspecies, d.src_kind);
-    if (d.world_size > 1) throw ConfigError("multi-GPU z-slab plans: not available in this build");
-    if (sys && !(d.kappa[0] > 0.0 && d.kappa[1] > 0.0))
-        throw ConfigError("component diffusivities must be positive");
+    for (int a = 0; a < d.dim; ++a) {
+        if (d.n[a] < 1) throw ConfigError("need at least 2 subintervals for a nonempty interior");
+        if (!(d.high[a] > d.low[a])) throw ConfigError("upper bound must exceed lower");
+    }
+    if (!(d.kappa[0] > 0.0) || (d.nspecies == 2 && !(d.kappa[1] > 0.0)))
+        throw ConfigError(d.nspecies == 2 ? "component diffusivities must be positive" : "diffusivity must be positive");
+    if (d.q < 0.0) throw ConfigError("linear reaction coefficient must be nonnegative");
+    const int G = d.world_size < 1 ? 1 : d.world_size;
+    if (G > 1) {
+        if (d.dim != 3) throw ConfigError("z-slab sharding needs a 3D grid (2D configs run as replicas)");
+        if (d.rank < 0 || d.rank >= G) throw ConfigError("rank out of range");
+        if (G > d.n[2] || G > d.n[1]) throw ConfigError("more ranks than z planes / y rows");
+    }
+}
+
+static void build_plan(Plan& p, const etd_desc& d) {
+    validate(d);
+    p.d = d;
+    const bool sys = d.nspecies == 2;
     p.dim = d.dim;
     p.ns = d.nspecies;
     p.tau = d.tau;
+    p.G = d.world_size < 1 ? 1 : d.world_size;
+    p.rank = p.G > 1 ? d.rank : 0;
+    p.sharded = p.G > 1;
+    p.local_group = p.sharded && d.nccl_unique_id == nullptr;
     int dev_count = 0;
     if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
         throw NoDevice("no CUDA device visible: the ETD2RK-DS CUDA backend has no CPU fallback");
@@ -330,27 +534,45 @@ static void build_plan(Plan& p, const etd_desc& d) {
     p.nx = d.n[0];
     p.ny = d.n[1];
     p.nz = d.dim == 3 ? d.n[2] : 1;
-    for (int a = 0; a < d.dim; ++a)
-        if (d.n[a] < 1) throw ConfigError("need at least 2 subintervals for a nonempty interior");
     p.pitch = round_up(p.nx, 32);
-    p.plane = p.pitch * p.ny;
-    p.F = p.plane * p.nz;
     p.dmax = 0;
     for (int a = 0; a < d.dim; ++a) {
         p.npad[a] = round_up(d.n[a], 32);
         p.dmax = std::max(p.dmax, p.npad[a]);
     }
+    p.zlo.resize(p.G); p.zhi.resize(p.G); p.jlo.resize(p.G); p.jhi.resize(p.G);
+    for (int r = 0; r < p.G; ++r) {
+        partition(p.nz, p.G, r, p.zlo[r], p.zhi[r]);
+        partition(p.ny, p.G, r, p.jlo[r], p.jhi[r]);
+    }
+    const int R = p.rank;
+    p.slab = View{p.nx, p.ny, p.zhi[R] - p.zlo[R], p.pitch, p.pitch * p.ny, 0, 0, p.zlo[R]};
+    p.slab.F = p.slab.plane * p.slab.nz;
+    p.zst = p.slab;
+    if (p.sharded) {
+        p.zst = View{p.nx, p.jhi[R] - p.jlo[R], p.nz, p.pitch, p.pitch * (p.jhi[R] - p.jlo[R]), 0, p.jlo[R], 0};
+        p.zst.F = p.zst.plane * p.zst.nz;
+    }
 
     ETD_CK(cudaStreamCreateWithFlags(&p.stream, cudaStreamNonBlocking));
-    const size_t fb = (size_t)p.F * sizeof(double);
-    for (int s = 0; s < 2; ++s) {
-        ETD_CK(cudaMalloc(&p.state[s], fb * p.ns));
-        ETD_CK(cudaMemsetAsync(p.state[s], 0, fb * p.ns, p.stream));
+    auto alloc = [&](double*& ptr, size_t elems) {
+        ETD_CK(cudaMalloc(&ptr, elems * sizeof(double)));
+        ETD_CK(cudaMemsetAsync(ptr, 0, elems * sizeof(double), p.stream));  // pads stay +0.0 forever
+    };
+    const size_t F = (size_t)p.slab.F;
+    for (int s = 0; s < 2; ++s) alloc(p.state[s], F * p.ns);
+    alloc(p.Z, F * 2 * p.ns);
+    alloc(p.W, F * 2 * p.ns);
+    if (p.sharded) {
+        const size_t Fz = (size_t)p.zst.F;
+        alloc(p.sendbuf, F * p.ns);
+        alloc(p.zin, Fz * p.ns);
+        alloc(p.Zz, Fz * 2 * p.ns);
+        alloc(p.Wz, Fz * 2 * p.ns);
+        alloc(p.recvb, F * 2 * p.ns);
+        ETD_CK(cudaMalloc(&p.codes, sizeof(int) * (p.G + 1)));
+        ETD_CK(cudaMemsetAsync(p.codes, 0, sizeof(int) * (p.G + 1), p.stream));
     }
-    ETD_CK(cudaMalloc(&p.Z, fb * 2 * p.ns));
-    ETD_CK(cudaMalloc(&p.W, fb * 2 * p.ns));
-    ETD_CK(cudaMemsetAsync(p.Z, 0, fb * 2 * p.ns, p.stream));
-    ETD_CK(cudaMemsetAsync(p.W, 0, fb * 2 * p.ns, p.stream));
 
     // per-axis eigensystems and d-vectors (stepper.cpp:118-177; systems use the
     // unit-kappa operator and kappa_c * lambda, system_stepper.cpp:47-61)
@@ -413,54 +635,132 @@ static void build_plan(Plan& p, const etd_desc& d) {
         attr_done = true;
     }
 
+    if (p.sharded && !p.local_group) {
+        auto& nc = Nccl::get();
+        ncclUniqueId id;
+        std::memcpy(&id, d.nccl_unique_id, sizeof(id));
+        nc.check(nc.CommInitRank(&p.comm, p.G, id, p.rank), "ncclCommInitRank");
+    }
+
     // ---- step schedule per state parity ----
     const int ns = p.ns;
-    const long long F = p.F;
+    const View& V = p.slab;
+    const View& VZ = p.zst;
     for (int par = 0; par < 2; ++par) {
         auto& L = p.steps[par];
         L.clear();
         const double* in = p.state[par];
         double* out = p.state[1 - par];
-        if (p.dim == 3) {
-            L.push_back(p.transform("z_fwd_src", 2, false, 2 * ns, EPI_SCALE, true, in, p.Z));
-            L.back().args.dA = p.dv(2, 0);
-            L.push_back(p.transform("z_back", 2, true, 2 * ns, EPI_STORE, false, p.Z, p.W));
-            L.push_back(p.transform("y_fwd", 1, false, 2 * ns, EPI_SCALE, false, p.W, p.Z));
-            L.back().args.dA = p.dv(1, 0);
-        } else {
-            L.push_back(p.transform("y_fwd_src", 1, false, 2 * ns, EPI_SCALE, true, in, p.Z));
-            L.back().args.dA = p.dv(1, 0);
+        if (p.dim == 3 && !p.sharded) {
+            L.push_back(kernel_op(p.transform(V, "z_fwd_src", 2, false, 2 * ns, EPI_SCALE, true, in, p.Z)));
+            L.back().L.args.dA = p.dv(2, 0);
+            L.push_back(kernel_op(p.transform(V, "z_back", 2, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
+        } else if (p.dim == 3) {
+            // ---- z-stage on y-row partitions: pack, exchange, filter, exchange back, unpack ----
+            const auto sched = sharded_schedule(p.nx, p.ny, p.nz, ns, p.G, p.rank, p.pitch);
+            double* bufs[6] = {const_cast<double*>(in), p.sendbuf, p.zin, p.Wz, p.recvb, p.W};
+            auto add_phase = [&](int phase, const char* name) {
+                Op ex;
+                ex.kind = Op::EXCHANGE;
+                ex.name = name;
+                for (const auto& r : sched) {
+                    if (r.phase != phase) continue;
+                    if (r.kind == SK_COPY)
+                        L.push_back(copy_op(name, bufs[r.dbuf] + r.doff, r.dpitch * 8, bufs[r.sbuf] + r.soff,
+                                            r.spitch * 8, r.width * 8, r.height));
+                    else if (r.kind == SK_SEND)
+                        ex.sends.push_back({(int)r.peer, bufs[r.sbuf] + r.soff, (size_t)r.count * 8});
+                    else
+                        ex.recvs.push_back({(int)r.peer, bufs[r.dbuf] + r.doff, (size_t)r.count * 8});
+                }
+                if (!ex.sends.empty()) L.push_back(ex);
+            };
+            add_phase(SP_PACK, "pack");
+            add_phase(SP_FWD, "a2a_fwd");
+            L.push_back(kernel_op(p.transform(VZ, "z_fwd_src", 2, false, 2 * ns, EPI_SCALE, true, p.zin, p.Zz)));
+            L.back().L.args.dA = p.dv(2, 0);
+            L.push_back(kernel_op(p.transform(VZ, "z_back", 2, true, 2 * ns, EPI_STORE, false, p.Zz, p.Wz)));
+            add_phase(SP_BACK, "a2a_back");
+            add_phase(SP_UNPACK, "unpack");
         }
-        L.push_back(p.transform("y_back", 1, true, 2 * ns, EPI_STORE, false, p.Z, p.W));
-        L.push_back(p.transform("x_fwd_mix", 0, false, 2 * ns, EPI_MIX, false, p.W, p.Z));
-        L.back().args.dA = p.dv(0, 0);
-        L.back().args.dB = p.dv(0, 1);
-        L.push_back(p.transform("x_back_src", 0, true, ns, EPI_WHAT_SRC, false, p.Z, p.W));
-        L.push_back(p.transform("x_fwd_corr", 0, false, ns, EPI_CORR, false, p.W + ns * F, p.Z));
-        L.back().args.aux = p.Z + ns * F;
-        L.back().args.dA = p.dv(0, 2);
-        L.push_back(p.transform("x_back_upd", 0, true, ns, EPI_UPDATE, false, p.Z, out));
-        L.back().args.aux = p.W;
-        // algorithmic HBM bytes: operands read + outputs written + aux read
-        const double pts = (double)p.nx * p.ny * p.nz * 8.0;
-        for (auto& x : L) {
-            const int S = x.k.S;
-            int loaded = S, outs = S, aux = 0;
-            if (x.name.find("_src") != std::string::npos && x.name.rfind("x_", 0) != 0) loaded = S / 2;
-            if (x.name == "x_back_src") outs = 2 * S;
-            if (x.name == "x_fwd_corr" || x.name == "x_back_upd") aux = S;
-            x.bytes = pts * (loaded + outs + aux);
+        if (p.dim == 3) {
+            L.push_back(kernel_op(p.transform(V, "y_fwd", 1, false, 2 * ns, EPI_SCALE, false, p.W, p.Z)));
+            L.back().L.args.dA = p.dv(1, 0);
+        } else {
+            L.push_back(kernel_op(p.transform(V, "y_fwd_src", 1, false, 2 * ns, EPI_SCALE, true, in, p.Z)));
+            L.back().L.args.dA = p.dv(1, 0);
+        }
+        L.push_back(kernel_op(p.transform(V, "y_back", 1, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
+        L.push_back(kernel_op(p.transform(V, "x_fwd_mix", 0, false, 2 * ns, EPI_MIX, false, p.W, p.Z)));
+        L.back().L.args.dA = p.dv(0, 0);
+        L.back().L.args.dB = p.dv(0, 1);
+        L.push_back(kernel_op(p.transform(V, "x_back_src", 0, true, ns, EPI_WHAT_SRC, false, p.Z, p.W)));
+        L.push_back(kernel_op(p.transform(V, "x_fwd_corr", 0, false, ns, EPI_CORR, false, p.W + ns * V.F, p.Z)));
+        L.back().L.args.aux = p.Z + ns * V.F;
+        L.back().L.args.dA = p.dv(0, 2);
+        L.push_back(kernel_op(p.transform(V, "x_back_upd", 0, true, ns, EPI_UPDATE, false, p.Z, out)));
+        L.back().L.args.aux = p.W;
+        if (p.sharded) {
+            // global abort agreement, then commit on every rank
+            Op fc;
+            fc.kind = Op::FAILCODE;
+            fc.name = "fail_code";
+            L.push_back(fc);
+            Op gx;
+            gx.kind = Op::EXCHANGE;
+            gx.name = "gather_codes";
+            for (int s = 0; s < p.G; ++s) {
+                gx.sends.push_back({s, p.codes + p.G, sizeof(int)});
+                gx.recvs.push_back({s, p.codes + s, sizeof(int)});
+            }
+            L.push_back(gx);
+            Op cm;
+            cm.kind = Op::COMMIT;
+            cm.name = "commit";
+            L.push_back(cm);
         }
     }
     p.stats.clear();
-    for (auto& x : p.steps[0]) p.stats.push_back({x.name, 0, 0, x.flops, x.bytes});
+    for (auto& op : p.steps[0])
+        if (op.kind == Op::KERNEL) p.stats.push_back({op.L.name, 0, 0, op.L.flops, op.L.bytes});
     ETD_CK(cudaStreamSynchronize(p.stream));
 }
 
-static void launch(const Plan& p, const Launch& L, cudaStream_t s) {
+static void launch(const Launch& L, cudaStream_t s) {
     void* args[3] = {const_cast<CUtensorMap*>(&L.tmA), const_cast<CUtensorMap*>(&L.tmB),
                      const_cast<ContractArgs*>(&L.args)};
     ETD_CK(cudaLaunchKernel(L.k.fn, L.grid, dim3(L.k.threads), args, L.k.smem, s));
+}
+
+// One op of one rank.  EXCHANGE over NCCL here; virtual-rank groups route
+// exchanges through run_group_exchange instead.
+static void run_op(Plan& p, const Op& op, cudaStream_t s) {
+    switch (op.kind) {
+    case Op::KERNEL: launch(op.L, s); break;
+    case Op::COPY2D:
+        ETD_CK(cudaMemcpy2DAsync(op.dst, op.dpitch, op.src, op.spitch, op.width, op.height,
+                                 cudaMemcpyDeviceToDevice, s));
+        break;
+    case Op::FAILCODE: etd_fail_code<<<1, 1, 0, s>>>(p.status, p.codes + p.G); break;
+    case Op::COMMIT: etd_commit<<<1, 1, 0, s>>>(p.status, p.codes, p.G, p.tau); break;
+    case Op::EXCHANGE: {
+        if (p.local_group) throw ConfigError("virtual-rank plans step through etd_group_step");
+        auto& nc = Nccl::get();
+        // self pieces are device copies; peer pieces one grouped send/recv set
+        std::vector<const Piece*> self_s, self_r;
+        for (auto& x : op.sends) if (x.peer == p.rank) self_s.push_back(&x);
+        for (auto& x : op.recvs) if (x.peer == p.rank) self_r.push_back(&x);
+        for (size_t i = 0; i < self_s.size(); ++i)
+            ETD_CK(cudaMemcpyAsync(self_r[i]->ptr, self_s[i]->ptr, self_s[i]->bytes, cudaMemcpyDeviceToDevice, s));
+        nc.check(nc.GroupStart(), "ncclGroupStart");
+        for (auto& x : op.sends)
+            if (x.peer != p.rank) nc.check(nc.Send(x.ptr, x.bytes, /*ncclChar*/ 0, x.peer, p.comm, s), "ncclSend");
+        for (auto& x : op.recvs)
+            if (x.peer != p.rank) nc.check(nc.Recv(x.ptr, x.bytes, /*ncclChar*/ 0, x.peer, p.comm, s), "ncclRecv");
+        nc.check(nc.GroupEnd(), "ncclGroupEnd");
+        break;
+    }
+    }
 }
 
 static void ensure_graphs(Plan& p) {
@@ -468,7 +768,7 @@ static void ensure_graphs(Plan& p) {
         if (p.graph[par]) continue;
         cudaGraph_t g;
         ETD_CK(cudaStreamBeginCapture(p.stream, cudaStreamCaptureModeThreadLocal));
-        for (auto& L : p.steps[par]) launch(p, L, p.stream);
+        for (auto& op : p.steps[par]) run_op(p, op, p.stream);
         ETD_CK(cudaStreamEndCapture(p.stream, &g));
         ETD_CK(cudaGraphInstantiate(&p.graph[par], g, 0));
         cudaGraphDestroy(g);
@@ -480,40 +780,13 @@ static void copy_status_from_device(Plan& p) {
     ETD_CK(cudaStreamSynchronize(p.stream));
 }
 
-static void do_steps(Plan& p, int nsteps) {
-    if (nsteps < 0) throw ConfigError("nsteps must be >= 0");
-    if (nsteps == 0) return;
-    copy_status_from_device(p);
-    const long long n_before = p.status_host->n;
+static void reset_status(Plan& p, cudaStream_t s) {
     p.status_host->fail = 0;
     p.status_host->cta_done = 0;
-    ETD_CK(cudaMemcpyAsync(p.status, p.status_host, sizeof(StepStatus), cudaMemcpyHostToDevice, p.stream));
-    if (p.profiling) {
-        const size_t nl = p.steps[0].size();
-        std::vector<cudaEvent_t> ev((size_t)nsteps * nl + 1);
-        for (auto& e : ev) ETD_CK(cudaEventCreate(&e));
-        ETD_CK(cudaEventRecord(ev[0], p.stream));
-        for (int s = 0; s < nsteps; ++s) {
-            const auto& L = p.steps[(p.cur + s) & 1];
-            for (size_t i = 0; i < nl; ++i) {
-                launch(p, L[i], p.stream);
-                ETD_CK(cudaEventRecord(ev[(size_t)s * nl + i + 1], p.stream));
-            }
-        }
-        ETD_CK(cudaStreamSynchronize(p.stream));
-        for (int s = 0; s < nsteps; ++s)
-            for (size_t i = 0; i < nl; ++i) {
-                float ms = 0;
-                ETD_CK(cudaEventElapsedTime(&ms, ev[(size_t)s * nl + i], ev[(size_t)s * nl + i + 1]));
-                p.stats[i].ms += ms;
-                p.stats[i].launches += 1;
-            }
-        for (auto& e : ev) cudaEventDestroy(e);
-    } else {
-        ensure_graphs(p);
-        for (int s = 0; s < nsteps; ++s) ETD_CK(cudaGraphLaunch(p.graph[(p.cur + s) & 1], p.stream));
-    }
-    ETD_CK(cudaGetLastError());
+    ETD_CK(cudaMemcpyAsync(p.status, p.status_host, sizeof(StepStatus), cudaMemcpyHostToDevice, s));
+}
+
+static void finish_steps(Plan& p, long long n_before) {
     copy_status_from_device(p);
     const long long committed = p.status_host->n - n_before;
     p.cur = (int)((p.cur + committed) & 1);
@@ -526,12 +799,125 @@ static void do_steps(Plan& p, int nsteps) {
     }
 }
 
+static void do_steps(Plan& p, int nsteps) {
+    if (nsteps < 0) throw ConfigError("nsteps must be >= 0");
+    if (p.local_group) throw ConfigError("virtual-rank plans step through etd_group_step");
+    if (nsteps == 0) return;
+    copy_status_from_device(p);
+    const long long n_before = p.status_host->n;
+    reset_status(p, p.stream);
+    const bool eager = p.profiling || p.sharded;
+    if (eager) {
+        // per-kernel device intervals: [event before op, event after op] for KERNEL ops
+        std::vector<cudaEvent_t> ev;
+        std::vector<std::pair<size_t, size_t>> spans;  // (start ev, stat index)
+        auto rec = [&] {
+            cudaEvent_t e;
+            ETD_CK(cudaEventCreate(&e));
+            ETD_CK(cudaEventRecord(e, p.stream));
+            ev.push_back(e);
+            return ev.size() - 1;
+        };
+        size_t prev = p.profiling ? rec() : 0;
+        for (int s = 0; s < nsteps; ++s) {
+            size_t kidx = 0;
+            for (const auto& op : p.steps[(p.cur + s) & 1]) {
+                run_op(p, op, p.stream);
+                if (!p.profiling) continue;
+                const size_t e = rec();
+                if (op.kind == Op::KERNEL) spans.push_back({prev, kidx++});
+                prev = e;
+            }
+        }
+        ETD_CK(cudaStreamSynchronize(p.stream));
+        for (auto& sp : spans) {
+            float ms = 0;
+            ETD_CK(cudaEventElapsedTime(&ms, ev[sp.first], ev[sp.first + 1]));
+            p.stats[sp.second].ms += ms;
+            p.stats[sp.second].launches += 1;
+        }
+        for (auto e : ev) cudaEventDestroy(e);
+    } else {
+        ensure_graphs(p);
+        for (int s = 0; s < nsteps; ++s) ETD_CK(cudaGraphLaunch(p.graph[(p.cur + s) & 1], p.stream));
+    }
+    ETD_CK(cudaGetLastError());
+    finish_steps(p, n_before);
+}
+
+// Virtual ranks: G plans of one sharded grid on ONE device, stepped op by op in
+// lock-step on the first plan's stream.  No kernel ever waits on another rank;
+// an exchange is a set of device copies issued once every rank has finished the
+// preceding op.  Exercises the sharded schedule (partition, pack, exchange,
+// unpack, global abort agreement) without NCCL or a second GPU.
+static void group_steps(std::vector<Plan*>& ps, int nsteps) {
+    const int G = (int)ps.size();
+    if (G < 1) throw ConfigError("empty group");
+    for (int r = 0; r < G; ++r) {
+        if (!ps[r]->local_group || ps[r]->G != G || ps[r]->rank != r)
+            throw ConfigError("group handles must be virtual ranks 0..G-1 of one sharded plan");
+        if (ps[r]->d.device != ps[0]->d.device) throw ConfigError("virtual ranks must share a device");
+    }
+    if (nsteps < 0) throw ConfigError("nsteps must be >= 0");
+    if (nsteps == 0) return;
+    cudaStream_t s = ps[0]->stream;
+    for (auto* p : ps) ETD_CK(cudaStreamSynchronize(p->stream));
+    std::vector<long long> before(G);
+    for (int r = 0; r < G; ++r) {
+        copy_status_from_device(*ps[r]);
+        before[r] = ps[r]->status_host->n;
+        reset_status(*ps[r], s);
+    }
+    for (int st = 0; st < nsteps; ++st) {
+        const size_t nops = ps[0]->steps[0].size();
+        for (size_t k = 0; k < nops; ++k) {
+            for (int r = 0; r < G; ++r) {
+                Plan& p = *ps[r];
+                const Op& op = p.steps[(p.cur + st) & 1][k];
+                if (op.kind != Op::EXCHANGE) {
+                    run_op(p, op, s);
+                    continue;
+                }
+                // push this rank's sends into the peers' receive pieces (matched in order)
+                std::vector<int> seen(G, 0);
+                for (const auto& x : op.sends) {
+                    Plan& q = *ps[x.peer];
+                    const Op& qo = q.steps[(q.cur + st) & 1][k];
+                    int idx = -1, cnt = 0;
+                    for (size_t i = 0; i < qo.recvs.size(); ++i)
+                        if (qo.recvs[i].peer == r && cnt++ == seen[x.peer]) { idx = (int)i; break; }
+                    if (idx < 0 || qo.recvs[idx].bytes != x.bytes)
+                        throw CudaError("exchange plan mismatch between virtual ranks");
+                    ++seen[x.peer];
+                    ETD_CK(cudaMemcpyAsync(qo.recvs[idx].ptr, x.ptr, x.bytes, cudaMemcpyDeviceToDevice, s));
+                }
+            }
+        }
+    }
+    ETD_CK(cudaGetLastError());
+    ETD_CK(cudaStreamSynchronize(s));
+    std::string err;
+    double et = 0;
+    long es = 0;
+    for (int r = 0; r < G; ++r) {
+        try {
+            finish_steps(*ps[r], before[r]);
+        } catch (const AbortError& e) {
+            err = e.what();
+            et = e.t;
+            es = e.step;
+        }
+    }
+    if (!err.empty()) throw AbortError(err, et, es);
+}
+
 static void set_state(Plan& p, int species, const double* host, size_t count, long n, double t) {
     if (species < 0 || species >= p.ns) throw ConfigError("species index out of range");
-    if (count != (size_t)p.nx * p.ny * p.nz) throw ConfigError("state shape does not match plan grid");
-    double* dst = p.state[p.cur] + (size_t)species * p.F;
-    ETD_CK(cudaMemcpy2DAsync(dst, p.pitch * 8, host, (size_t)p.nx * 8, (size_t)p.nx * 8,
-                             (size_t)p.ny * p.nz, cudaMemcpyHostToDevice, p.stream));
+    const View& v = p.slab;
+    if (count != (size_t)v.nx * v.ny * v.nz) throw ConfigError("state shape does not match plan grid");
+    double* dst = p.state[p.cur] + (size_t)species * v.F;
+    ETD_CK(cudaMemcpy2DAsync(dst, v.pitch * 8, host, (size_t)v.nx * 8, (size_t)v.nx * 8, (size_t)v.ny * v.nz,
+                             cudaMemcpyHostToDevice, p.stream));
     p.status_host->n = n;
     p.status_host->t = t;
     p.status_host->fail = 0;
@@ -542,10 +928,11 @@ static void set_state(Plan& p, int species, const double* host, size_t count, lo
 
 static void get_state(Plan& p, int species, double* host, size_t count, long* n, double* t) {
     if (species < 0 || species >= p.ns) throw ConfigError("species index out of range");
-    if (count != (size_t)p.nx * p.ny * p.nz) throw ConfigError("output shape does not match plan grid");
-    const double* src = p.state[p.cur] + (size_t)species * p.F;
-    ETD_CK(cudaMemcpy2DAsync(host, (size_t)p.nx * 8, src, p.pitch * 8, (size_t)p.nx * 8,
-                             (size_t)p.ny * p.nz, cudaMemcpyDeviceToHost, p.stream));
+    const View& v = p.slab;
+    if (count != (size_t)v.nx * v.ny * v.nz) throw ConfigError("output shape does not match plan grid");
+    const double* src = p.state[p.cur] + (size_t)species * v.F;
+    ETD_CK(cudaMemcpy2DAsync(host, (size_t)v.nx * 8, src, v.pitch * 8, (size_t)v.nx * 8, (size_t)v.ny * v.nz,
+                             cudaMemcpyDeviceToHost, p.stream));
     copy_status_from_device(p);
     if (n) *n = (long)p.status_host->n;
     if (t) *t = p.status_host->t;
@@ -554,33 +941,32 @@ static void get_state(Plan& p, int species, double* host, size_t count, long* n,
 static void debug_transform(Plan& p, int species, int axis, int back, int ell, int apply_q,
                             const double* in, double* out) {
     if (axis < 0 || axis >= p.dim) throw ConfigError("axis out of range for field dimension");
+    if (p.sharded) throw ConfigError("debug transforms run on unsharded plans");
     if (species < 0 || species >= p.ns) throw ConfigError("species index out of range");
     if (ell < 0 || ell > 3) throw ConfigError("ell must be 1, 2, or 3");
-    const size_t cnt = (size_t)p.nx * p.ny * p.nz;
-    ETD_CK(cudaMemcpy2DAsync(p.W, p.pitch * 8, in, (size_t)p.nx * 8, (size_t)p.nx * 8, (size_t)p.ny * p.nz,
+    const View& v = p.slab;
+    ETD_CK(cudaMemcpy2DAsync(p.W, v.pitch * 8, in, (size_t)v.nx * 8, (size_t)v.nx * 8, (size_t)v.ny * v.nz,
                              cudaMemcpyHostToDevice, p.stream));
-    p.status_host->fail = 0;
-    ETD_CK(cudaMemcpyAsync(p.status, p.status_host, sizeof(StepStatus), cudaMemcpyHostToDevice, p.stream));
+    reset_status(p, p.stream);
     const double* result = nullptr;
     if (apply_q) {
         if (ell < 1) throw ConfigError("apply_q needs ell in 1..3");
-        Launch f = p.transform("dbg_fwd", axis, false, 1, EPI_SCALE, false, p.W, p.Z);
+        Launch f = p.transform(v, "dbg_fwd", axis, false, 1, EPI_SCALE, false, p.W, p.Z);
         f.args.dA = p.dv(axis, 6 + ell - 1) + species * p.dmax;
-        Launch b = p.transform("dbg_back", axis, true, 1, EPI_STORE, false, p.Z, p.W + p.F);
-        launch(p, f, p.stream);
-        launch(p, b, p.stream);
-        result = p.W + p.F;
+        Launch b = p.transform(v, "dbg_back", axis, true, 1, EPI_STORE, false, p.Z, p.W + v.F);
+        launch(f, p.stream);
+        launch(b, p.stream);
+        result = p.W + v.F;
     } else {
-        Launch f = p.transform("dbg", axis, back != 0, 1, ell ? EPI_SCALE : EPI_STORE, false, p.W, p.Z);
+        Launch f = p.transform(v, "dbg", axis, back != 0, 1, ell ? EPI_SCALE : EPI_STORE, false, p.W, p.Z);
         if (ell) f.args.dA = p.dv(axis, 3 + ell - 1) + species * p.dmax;
-        launch(p, f, p.stream);
+        launch(f, p.stream);
         result = p.Z;
     }
     ETD_CK(cudaGetLastError());
-    ETD_CK(cudaMemcpy2DAsync(out, (size_t)p.nx * 8, result, p.pitch * 8, (size_t)p.nx * 8, (size_t)p.ny * p.nz,
+    ETD_CK(cudaMemcpy2DAsync(out, (size_t)v.nx * 8, result, v.pitch * 8, (size_t)v.nx * 8, (size_t)v.ny * v.nz,
                              cudaMemcpyDeviceToHost, p.stream));
     ETD_CK(cudaStreamSynchronize(p.stream));
-    (void)cnt;
 }
 
 }  // namespace etd
@@ -650,9 +1036,51 @@ int etd_destroy(etd_handle* h) {
 
 int etd_slab_range(const etd_handle* h, int* z0, int* z1) {
     if (!h) return ETD_ERR_CONFIG;
-    if (z0) *z0 = 0;
-    if (z1) *z1 = h->plan->nz;
+    const auto& p = *h->plan;
+    if (z0) *z0 = p.dim == 3 ? p.zlo[p.rank] : 0;
+    if (z1) *z1 = p.dim == 3 ? p.zhi[p.rank] : 1;
     return ETD_OK;
+}
+
+int etd_zslab_partition(int n, int world_size, int rank, int* lo, int* hi) {
+    if (n < 1 || world_size < 1 || rank < 0 || rank >= world_size || world_size > n || !lo || !hi)
+        return ETD_ERR_CONFIG;
+    etd::partition(n, world_size, rank, *lo, *hi);
+    return ETD_OK;
+}
+
+int etd_sharded_schedule(int nx, int ny, int nz, int nspecies, int world_size, int rank, long long pitch,
+                         long long* out, int capacity, int* count) {
+    if (!count || world_size < 1 || rank < 0 || rank >= world_size || world_size > nz || world_size > ny ||
+        nspecies < 1 || nspecies > 2 || pitch < nx)
+        return ETD_ERR_CONFIG;
+    const auto recs = etd::sharded_schedule(nx, ny, nz, nspecies, world_size, rank, pitch);
+    *count = (int)recs.size();
+    if (out) {
+        if (capacity < (int)recs.size()) return ETD_ERR_CONFIG;
+        std::memcpy(out, recs.data(), recs.size() * sizeof(etd::SchedRec));
+    }
+    return ETD_OK;
+}
+
+int etd_nccl_unique_id(void* out) {
+    if (!out) return ETD_ERR_CONFIG;
+    return guarded(nullptr, [&] {
+        auto& nc = etd::Nccl::get();
+        ncclUniqueId id;
+        nc.check(nc.GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out, &id, sizeof(id));
+    });
+}
+
+int etd_group_step(etd_handle** hs, int count, int nsteps) {
+    if (!hs || count < 1) return ETD_ERR_CONFIG;
+    std::vector<etd::Plan*> ps;
+    for (int i = 0; i < count; ++i) {
+        if (!hs[i]) return ETD_ERR_CONFIG;
+        ps.push_back(hs[i]->plan.get());
+    }
+    return guarded(hs[0], [&] { etd::group_steps(ps, nsteps); });
 }
 
 int etd_set_state(etd_handle* h, int species, const double* host, size_t count, long n, double t) {
@@ -675,7 +1103,7 @@ int etd_advance(etd_handle* h, const double* u, const double* v, long n, double 
     if (!h || !u || !u_out) return ETD_ERR_CONFIG;
     auto& p = *h->plan;
     if (p.ns == 2 && (!v || !v_out)) return ETD_ERR_CONFIG;
-    const size_t cnt = (size_t)p.nx * p.ny * p.nz;
+    const size_t cnt = (size_t)p.slab.nx * p.slab.ny * p.slab.nz;
     int rc = guarded(h, [&] {
         etd::set_state(p, 0, u, cnt, n, t);
         if (p.ns == 2) etd::set_state(p, 1, v, cnt, n, t);
@@ -708,7 +1136,12 @@ unsigned long long etd_stream(const etd_handle* h) {
     return h ? reinterpret_cast<unsigned long long>(h->plan->stream) : 0ull;
 }
 
-int etd_launches_per_step(const etd_handle* h) { return h ? (int)h->plan->steps[0].size() : 0; }
+int etd_launches_per_step(const etd_handle* h) {
+    if (!h) return 0;
+    int k = 0;
+    for (const auto& op : h->plan->steps[0]) k += op.kind != etd::Op::COPY2D && op.kind != etd::Op::EXCHANGE;
+    return k;
+}
 
 int etd_set_profiling(etd_handle* h, int on) {
     if (!h) return ETD_ERR_CONFIG;

@@ -211,6 +211,9 @@ def lib():
         L.etd_setup_axis.argtypes = [i, d, d, i, d, d, vp, vp]
         L.etd_setup_dvector.argtypes = [i, vp, d, i, i, vp]
         L.etd_setup_scheme.argtypes = [i, vp, C.POINTER(i)]
+        L.etd_zslab_partition.argtypes = [i, i, i, C.POINTER(i), C.POINTER(i)]
+        L.etd_nccl_unique_id.argtypes = [vp]
+        L.etd_group_step.argtypes = [C.POINTER(vp), i, i]
         _lib = L
     return _lib
 
@@ -279,7 +282,10 @@ def _make_desc(grid: Grid, tau, family, nspecies, kappas, q, source: DeviceSourc
     d.device = device
     d.world_size = world_size
     d.rank = rank
-    d.nccl_unique_id = nccl_id
+    d.nccl_unique_id = None
+    if nccl_id is not None:
+        d._id_buf = C.create_string_buffer(bytes(nccl_id), 128)  # kept alive with the desc
+        d.nccl_unique_id = C.cast(d._id_buf, C.c_void_p)
     return d
 
 
@@ -501,6 +507,27 @@ def setup_scheme(family: int) -> np.ndarray:
     nt = C.c_int()
     _raise(lib().etd_setup_scheme(int(family), _ptr(out), C.byref(nt)), None)
     return out[: 12 * nt.value].reshape(3, nt.value, 4)
+
+
+def zslab_partition(n: int, world_size: int, rank: int):
+    """Balanced [lo, hi) split used for z planes (x/y stages) and y rows (z stage)."""
+    lo, hi = C.c_int(), C.c_int()
+    _raise(lib().etd_zslab_partition(n, world_size, rank, C.byref(lo), C.byref(hi)), None)
+    return lo.value, hi.value
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it, the others receive it out of band)."""
+    buf = C.create_string_buffer(128)
+    _raise(lib().etd_nccl_unique_id(C.cast(buf, C.c_void_p)), None)
+    return buf.raw
+
+
+def group_step(plans, nsteps: int = 1) -> None:
+    """Step virtual ranks (plans created with world_size=G, rank=r, no NCCL id, one
+    device) in lock-step: the sharded schedule with exchanges as device copies."""
+    arr = (C.c_void_p * len(plans))(*[p.handle for p in plans])
+    _raise(lib().etd_group_step(arr, len(plans), int(nsteps)), plans[0].handle)
 
 
 def fill_config_ic(config: int, seed: int, species: int, n: int, z0: int = 0, z1: Optional[int] = None,
