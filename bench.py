@@ -173,7 +173,12 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     kw = {}
     if world > 1:
-        raise SystemExit("multi-GPU z-slab sharding is not available in this build")
+        if cfg.dim != 3:
+            raise SystemExit("2D configs are not sharded (replicas only); use a 3D config for N>1")
+        from paper_2601_06849_b200 import nccl_unique_id
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        kw = {"world_size": world, "rank": rank, "nccl_id": obj[0]}
     plan = configs.make_plan(cfg, n, device=local_rank, **kw)
     t0 = time.time()
     ics = configs.initial_state(cfg, n, z0=plan.slab[0], z1=plan.slab[1] if cfg.dim == 3 else None)
@@ -181,7 +186,6 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
     for s, a in enumerate(ics):
         plan.upload(s, a)
     stream = torch.cuda.ExternalStream(plan.stream, device=torch.device("cuda", local_rank))
-    local_pts = plan.local_count * cfg.nspecies
 
     def barrier():
         if dist is not None:
@@ -219,6 +223,10 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
     for s in stats:
         avg = s["ms_total"] / max(1, s["launches"])
         per.append((avg, s))
+    if dist is not None:  # slowest rank's per-stage times
+        t = torch.tensor([p[0] for p in per], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        per = [(float(a), s) for a, (_, s) in zip(t.tolist(), per)]
     dom_ms, dom = max(per, key=lambda x: x[0])
     achieved = dom["flops_per_launch"] / (dom_ms * 1e-3) * 1e-12
     traffic = None
@@ -231,6 +239,7 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
             traffic = None
     transform_ms = sum(p[0] for p in per)
     transform_flops = sum(s["flops_per_launch"] for _, s in per)
+    comm_ms = ms - transform_ms  # exchange + pack/unpack + commit (sharded), launch gaps
     roofline = {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic, "kernel": dom["name"],
                 "peak_source": FP64_PEAK_NOTE,
@@ -240,7 +249,8 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
                                    "hbm_gbs": round(sum(s["bytes_per_launch"] for _, s in per) / (transform_ms * 1e-3) * 1e-9, 1),
                                    "hbm_peak_gbs": 6552.0},
                 "stages": [{"name": s["name"], "ms": round(a, 3),
-                            "tflops": round(s["flops_per_launch"] / (a * 1e-3) * 1e-12, 2)} for a, s in per]}
+                            "tflops": round(s["flops_per_launch"] / (a * 1e-3) * 1e-12, 2)} for a, s in per],
+                "non_transform_ms_per_step": round(comm_ms, 3)}
 
     # ---- e2e through the public API: pinned host in -> step -> pinned host out ----
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
