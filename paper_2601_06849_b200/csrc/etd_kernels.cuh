@@ -326,66 +326,110 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
         }
 
         // ===================== fused epilogue =====================
+        // Thread owns C(m, n..n+1) for each (i, j): adjacent n.  Aux inputs of a
+        // row are loaded up front (independent of this kernel's stores, so the
+        // loads overlap instead of serialising behind possible aliasing);
+        // MODE 0 stores the (n, n+1) pair as one 16-byte STG.
         const int ns = args.nspecies;
+        double* __restrict__ outp = args.out;
+        const double* __restrict__ auxp = args.aux;
+        auto offset = [&](int m, int n) -> long long {
+            if constexpr (MODE == 0) return (long long)m * args.pitch + n;
+            else return args.zaxis ? (long long)outer * args.pitch + (long long)n * args.plane + m
+                                   : (long long)outer * args.plane + (long long)n * args.pitch + m;
+        };
+        auto store = [&](int o, int m, int n, double v0, double v1, bool two) {
+            double* base = outp + (long long)o * args.out_stride;
+            if constexpr (MODE == 0) {
+                if (two) *reinterpret_cast<double2*>(base + offset(m, n)) = make_double2(v0, v1);
+                else base[offset(m, n)] = v0;
+            } else {
+                base[offset(m, n)] = v0;
+                if (two) base[offset(m, n + 1)] = v1;
+            }
+        };
+        auto dpair = [&](const double* d, int c, int n) {
+            return __ldg(reinterpret_cast<const double2*>(d + c * args.dstride + n));
+        };
 #pragma unroll
         for (int i = 0; i < C::MF; ++i) {
             const int m = m0 + wm0 + i * 8 + g;
             if (m >= args.m_extent) continue;
+            constexpr bool HAS_AUX = EPI == EPI_CORR || EPI == EPI_UPDATE;
+            double av[HAS_AUX ? S : 1][C::NF][2];
+            if constexpr (HAS_AUX) {
+#pragma unroll
+                for (int j = 0; j < C::NF; ++j) {
+                    const int nb = n0 + wn0 + j * 8 + 2 * l;
+#pragma unroll
+                    for (int c = 0; c < S; ++c) {
+                        const double* a = auxp + (long long)c * args.aux_stride;
+                        if (MODE == 0 && nb + 1 < args.n_axis) {
+                            const double2 t = __ldg(reinterpret_cast<const double2*>(a + offset(m, nb)));
+                            av[c][j][0] = t.x;
+                            av[c][j][1] = t.y;
+                        } else {
+                            av[c][j][0] = nb < args.n_axis ? __ldg(a + offset(m, nb)) : 0.0;
+                            av[c][j][1] = nb + 1 < args.n_axis ? __ldg(a + offset(m, nb + 1)) : 0.0;
+                        }
+                    }
+                }
+            }
 #pragma unroll
             for (int j = 0; j < C::NF; ++j) {
+                const int nb = n0 + wn0 + j * 8 + 2 * l;
+                if (nb >= args.n_axis) continue;
+                const bool two = nb + 1 < args.n_axis;
+                if constexpr (EPI == EPI_STORE) {
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int n = n0 + wn0 + j * 8 + 2 * l + e;
-                    if (n >= args.n_axis) continue;
-                    long long off;
-                    if constexpr (MODE == 0) off = (long long)m * args.pitch + n;
-                    else off = args.zaxis ? (long long)outer * args.pitch + (long long)n * args.plane + m
-                                          : (long long)outer * args.plane + (long long)n * args.pitch + m;
-                    if constexpr (EPI == EPI_STORE) {
+                    for (int s = 0; s < S; ++s) store(s, m, nb, acc[s][i][j][0], acc[s][i][j][1], two);
+                } else if constexpr (EPI == EPI_SCALE) {
 #pragma unroll
-                        for (int s = 0; s < S; ++s) args.out[s * args.out_stride + off] = acc[s][i][j][e];
-                    } else if constexpr (EPI == EPI_SCALE) {
+                    for (int s = 0; s < S; ++s) {
+                        const double2 d = dpair(args.dA, s % ns, nb);
+                        store(s, m, nb, acc[s][i][j][0] * d.x, acc[s][i][j][1] * d.y, two);
+                    }
+                } else if constexpr (EPI == EPI_MIX) {
 #pragma unroll
-                        for (int s = 0; s < S; ++s)
-                            args.out[s * args.out_stride + off] =
-                                acc[s][i][j][e] * __ldg(args.dA + (s % ns) * args.dstride + n);
-                    } else if constexpr (EPI == EPI_MIX) {
+                    for (int c = 0; c < S / 2; ++c) {
+                        const double2 da = dpair(args.dA, c, nb), db = dpair(args.dB, c, nb);
+                        const double* w1 = acc[c][i][j];
+                        const double* w2 = acc[S / 2 + c][i][j];
+                        store(c, m, nb, da.x * w1[0] + db.x * w2[0], da.y * w1[1] + db.y * w2[1], two);
+                        store(S / 2 + c, m, nb, w2[0], w2[1], two);
+                    }
+                } else if constexpr (EPI == EPI_WHAT_SRC) {
+                    double f0[2], f1[2] = {0.0, 0.0};
 #pragma unroll
-                        for (int c = 0; c < S / 2; ++c) {
-                            const double w1b = acc[c][i][j][e], w2b = acc[S / 2 + c][i][j][e];
-                            const double da = __ldg(args.dA + c * args.dstride + n);
-                            const double db = __ldg(args.dB + c * args.dstride + n);
-                            args.out[c * args.out_stride + off] = da * w1b + db * w2b;
-                            args.out[(S / 2 + c) * args.out_stride + off] = w2b;
-                        }
-                    } else if constexpr (EPI == EPI_WHAT_SRC) {
-                        double f0, f1 = 0.0;
+                    for (int e = 0; e < 2; ++e) {
+                        const bool in = e == 0 || two;
                         if constexpr (S == 1) {
-                            f0 = src_scalar(args.src_kind, args.sp, acc[0][i][j][e]);
-                            if (args.src_kind == 3 && n == 0 && m == 0 && args.gz0 == 0 && args.gj0 == 0)
-                                f0 = __longlong_as_double(0x7ff8000000000000ll);
-                            bad |= !isfinite(f0);
+                            f0[e] = src_scalar(args.src_kind, args.sp, acc[0][i][j][e]);
+                            if (args.src_kind == 3 && nb + e == 0 && m == 0 && args.gz0 == 0 && args.gj0 == 0)
+                                f0[e] = __longlong_as_double(0x7ff8000000000000ll);
+                            bad |= in && !isfinite(f0[e]);
                         } else {
-                            src_pair(args.src_kind, args.sp, acc[0][i][j][e], acc[1][i][j][e], f0, f1);
-                            bad |= !(isfinite(f0) && isfinite(f1));
+                            src_pair(args.src_kind, args.sp, acc[0][i][j][e], acc[1][i][j][e], f0[e], f1[e]);
+                            bad |= in && !(isfinite(f0[e]) && isfinite(f1[e]));
                         }
+                    }
 #pragma unroll
-                        for (int c = 0; c < S; ++c) args.out[c * args.out_stride + off] = acc[c][i][j][e];
-                        args.out[S * args.out_stride + off] = f0;
-                        if constexpr (S == 2) args.out[3 * args.out_stride + off] = f1;
-                    } else if constexpr (EPI == EPI_CORR) {
+                    for (int c = 0; c < S; ++c) store(c, m, nb, acc[c][i][j][0], acc[c][i][j][1], two);
+                    store(S, m, nb, f0[0], f0[1], two);
+                    if constexpr (S == 2) store(3, m, nb, f1[0], f1[1], two);
+                } else if constexpr (EPI == EPI_CORR) {
 #pragma unroll
-                        for (int c = 0; c < S; ++c)
-                            args.out[c * args.out_stride + off] =
-                                (acc[c][i][j][e] - args.aux[c * args.aux_stride + off]) *
-                                __ldg(args.dA + c * args.dstride + n);
-                    } else if constexpr (EPI == EPI_UPDATE) {
+                    for (int c = 0; c < S; ++c) {
+                        const double2 d = dpair(args.dA, c, nb);
+                        store(c, m, nb, (acc[c][i][j][0] - av[c][j][0]) * d.x, (acc[c][i][j][1] - av[c][j][1]) * d.y,
+                              two);
+                    }
+                } else if constexpr (EPI == EPI_UPDATE) {
 #pragma unroll
-                        for (int c = 0; c < S; ++c) {
-                            const double u1 = args.aux[c * args.aux_stride + off] + acc[c][i][j][e];
-                            bad |= !isfinite(u1);
-                            args.out[c * args.out_stride + off] = u1;
-                        }
+                    for (int c = 0; c < S; ++c) {
+                        const double u0 = av[c][j][0] + acc[c][i][j][0], u1 = av[c][j][1] + acc[c][i][j][1];
+                        bad |= !isfinite(u0) || (two && !isfinite(u1));
+                        store(c, m, nb, u0, u1, two);
                     }
                 }
             }
