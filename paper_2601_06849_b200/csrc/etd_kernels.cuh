@@ -138,25 +138,21 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                  : "d"(a), "d"(b));
 }
 
-// ------------------------------------------------------------- pointwise sources
-// Device forms of the source kinds of include/etd_b200.h (same expressions as
-// oracle/ref_driver.cpp so that rounding matches the checker).
-__device__ __forceinline__ double src_scalar(int kind, const double* p, double u) {
-    switch (kind) {
-    case 1: return u - u * u * u;
-    case 2: return ((p[3] * u + p[2]) * u + p[1]) * u + p[0];
-    default: return 0.0;
-    }
+// Compile-time source kind for the hot kernels: straight-line code lets the
+// scheduler interleave the FP64 source math with DMMA issue.
+template <int SK>
+__device__ __forceinline__ double src1(const double* p, double u) {
+    if constexpr (SK == 1) return u - u * u * u;
+    else if constexpr (SK == 2) return ((p[3] * u + p[2]) * u + p[1]) * u + p[0];
+    else return 0.0;
 }
-__device__ __forceinline__ void src_pair(int kind, const double* p, double u, double v, double& fu,
-                                         double& fv) {
-    switch (kind) {
-    case 10: fu = u * (1.0 - u) * (u - p[0]) - v; fv = p[1] * (p[2] * u - v); break;
-    case 11: fu = u - u * u * u / 3.0 - v; fv = p[0] * (u - p[1] * v); break;
-    case 12: fu = u - u * u * u; fv = v - v * v * v; break;
-    case 13: fu = u - u * u * u; fv = p[0] * v + p[1]; break;
-    default: fu = 0.0; fv = 0.0;
-    }
+template <int SK>
+__device__ __forceinline__ void src2(const double* p, double u, double v, double& fu, double& fv) {
+    if constexpr (SK == 10) { fu = u * (1.0 - u) * (u - p[0]) - v; fv = p[1] * (p[2] * u - v); }
+    else if constexpr (SK == 11) { fu = u - u * u * u / 3.0 - v; fv = p[0] * (u - p[1] * v); }
+    else if constexpr (SK == 12) { fu = u - u * u * u; fv = v - v * v * v; }
+    else if constexpr (SK == 13) { fu = u - u * u * u; fv = p[0] * v + p[1]; }
+    else { fu = 0.0; fv = 0.0; }
 }
 
 // ------------------------------------------------------------- tile geometry
@@ -183,7 +179,7 @@ __device__ __forceinline__ int swz(int row, int col) {
 }
 
 // ------------------------------------------------------------- the kernel
-template <int MODE, int S, int EPI, bool PRO, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
+template <int MODE, int S, int EPI, bool PRO, int SK, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
 __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
     etd_contract(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const ContractArgs args) {
@@ -255,74 +251,106 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
 #pragma unroll
                 for (int j = 0; j < C::NF; ++j) acc[s][i][j][0] = acc[s][i][j][1] = 0.0;
 
+        // k permutation inside the 16-wide stage keeps both fragment loads
+        // bank-conflict free under the 128B swizzle
+        auto kperm = [&](int st) {
+            return MODE == 0 ? (2 * st + (l & 1) + 8 * (l >> 1)) : (2 * l + (st & 1) + 8 * (st >> 1));
+        };
+        auto load_frags = [&](int stg, int st, double (&a)[S][C::MF], double (&b)[C::NF]) {
+            const double* sA = smem + stg * C::STAGE_DBL;
+            const double* sB = sA + C::A_DBL;
+            const int kk = kperm(st);
+#pragma unroll
+            for (int j = 0; j < C::NF; ++j) {
+                const int nn = wn0 + j * 8 + g;
+                b[j] = MODE == 0 ? sB[swz(nn, kk)] : sB[(nn >> 4) * 256 + swz(kk, nn & 15)];
+            }
+#pragma unroll
+            for (int s = 0; s < C::L; ++s)
+#pragma unroll
+                for (int i = 0; i < C::MF; ++i) {
+                    const int mm = wm0 + i * 8 + g;
+                    const double* base = sA + s * BM * BK;
+                    a[s][i] = MODE == 0 ? base[swz(mm, kk)] : base[(mm >> 4) * 256 + swz(kk, mm & 15)];
+                }
+        };
+        // non-finite test without branches (keeps the DMMA stream one basic block)
+        auto nonfinite = [](double x) { return (__double2hiint(x) & 0x7ff00000) == 0x7ff00000; };
+        // fused source: the A fragment of f(U) at (m, k) is f of the U fragment at
+        // (m, k) — evaluated in registers, no smem round trip, no barrier
+        auto apply_src = [&](int kt, int st, double (&a)[S][C::MF]) {
+            if constexpr (PRO) {
+                const int kc = kt * BK + kperm(st);
+#pragma unroll
+                for (int i = 0; i < C::MF; ++i) {
+                    const int p = m0 + wm0 + i * 8 + g;
+                    const int valid = (p < args.m_extent) & (kc < args.n_axis);
+                    if constexpr (C::L == 1) {
+                        double f = src1<SK>(args.sp, a[0][i]);
+                        if constexpr (SK == 3)
+                            if (p == 0 && (args.zaxis ? (kc + args.gz0 == 0 && outer + args.gj0 == 0)
+                                                      : (kc + args.gj0 == 0 && outer + args.gz0 == 0)))
+                                f = __longlong_as_double(0x7ff8000000000000ll);
+                        a[1][i] = f;
+                        bad |= valid & nonfinite(f);
+                    } else {
+                        double fu, fv;
+                        src2<SK>(args.sp, a[0][i], a[1][i], fu, fv);
+                        a[2][i] = fu;
+                        a[3][i] = fv;
+                        bad |= valid & (nonfinite(fu) | nonfinite(fv));
+                    }
+                }
+            }
+        };
+        auto mma = [&](const double (&a)[S][C::MF], const double (&b)[C::NF]) {
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int i = 0; i < C::MF; ++i)
+#pragma unroll
+                    for (int j = 0; j < C::NF; ++j) dmma884(acc[s][i][j][0], acc[s][i][j][1], a[s][i], b[j]);
+        };
+
+        // Flat (k-tile, step) stream with a one-step lookahead that also crosses
+        // stage boundaries: fragments (and source math) of the next step are in
+        // flight while the DMMAs of the current step issue.
+        double fa[2][S][C::MF], fb[2][C::NF];
         int stage = 0;
         uint32_t phase = 0;
+        mbar_wait(&full[0], 0);
+        load_frags(0, 0, fa[0], fb[0]);
+        apply_src(0, 0, fa[0]);
         for (int kt = 0; kt < KT; ++kt) {
-            mbar_wait(&full[stage], phase);
-            double* sA = smem + stage * C::STAGE_DBL;
-            const double* sB = sA + C::A_DBL;
+            const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
+            const uint32_t nphase = stage + 1 == STAGES ? phase ^ 1 : phase;
 #pragma unroll
             for (int st = 0; st < BK / 4; ++st) {
-                // k permutation inside the 16-wide stage keeps both fragment loads
-                // bank-conflict free under the 128B swizzle
-                const int kk = MODE == 0 ? (2 * st + (l & 1) + 8 * (l >> 1))
-                                         : (2 * l + (st & 1) + 8 * (st >> 1));
-                double a[S][C::MF], b[C::NF];
-#pragma unroll
-                for (int j = 0; j < C::NF; ++j) {
-                    const int nn = wn0 + j * 8 + g;
-                    b[j] = MODE == 0 ? sB[swz(nn, kk)] : sB[(nn >> 4) * 256 + swz(kk, nn & 15)];
-                }
-#pragma unroll
-                for (int s = 0; s < C::L; ++s)
-#pragma unroll
-                    for (int i = 0; i < C::MF; ++i) {
-                        const int mm = wm0 + i * 8 + g;
-                        const double* base = sA + s * BM * BK;
-                        a[s][i] = MODE == 0 ? base[swz(mm, kk)] : base[(mm >> 4) * 256 + swz(kk, mm & 15)];
-                    }
-                if constexpr (PRO) {
-                    // fused source: the A fragment of f(U) at (m, k) is f of the U
-                    // fragment at (m, k) — evaluated in registers, no smem, no barrier
-                    const int kc = kt * BK + kk;
-#pragma unroll
-                    for (int i = 0; i < C::MF; ++i) {
-                        const int p = m0 + wm0 + i * 8 + g;
-                        const bool valid = p < args.m_extent && kc < args.n_axis;
-                        if constexpr (C::L == 1) {
-                            double f = src_scalar(args.src_kind, args.sp, a[0][i]);
-                            if (args.src_kind == 3 && p == 0 &&
-                                (args.zaxis ? (kc + args.gz0 == 0 && outer + args.gj0 == 0)
-                                            : (kc + args.gj0 == 0 && outer + args.gz0 == 0)))
-                                f = __longlong_as_double(0x7ff8000000000000ll);
-                            a[1][i] = f;
-                            bad |= valid && !isfinite(f);
-                        } else {
-                            double fu, fv;
-                            src_pair(args.src_kind, args.sp, a[0][i], a[1][i], fu, fv);
-                            a[2][i] = fu;
-                            a[3][i] = fv;
-                            bad |= valid && !(isfinite(fu) && isfinite(fv));
-                        }
+                const int cur = st & 1, nxt = cur ^ 1;
+                if (st < BK / 4 - 1) {
+                    load_frags(stage, st + 1, fa[nxt], fb[nxt]);
+                } else {
+                    // every read of this stage has been issued: release it, then
+                    // look ahead into the next stage
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[stage]);
+                    if (kt + 1 < KT) {
+                        mbar_wait(&full[nstage], nphase);
+                        load_frags(nstage, 0, fa[nxt], fb[nxt]);
                     }
                 }
-#pragma unroll
-                for (int s = 0; s < S; ++s)
-#pragma unroll
-                    for (int i = 0; i < C::MF; ++i)
-#pragma unroll
-                        for (int j = 0; j < C::NF; ++j)
-                            dmma884(acc[s][i][j][0], acc[s][i][j][1], a[s][i], b[j]);
+                mma(fa[cur], fb[cur]);
+                if (st < BK / 4 - 1) apply_src(kt, st + 1, fa[nxt]);
+                else if (kt + 1 < KT) apply_src(kt + 1, 0, fa[nxt]);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
             if (tid == 0 && kt + STAGES < KT) {
                 // refill this slot once every warp has released it
                 mbar_wait(&empty[stage], phase);
                 issue(kt + STAGES, stage);
             }
             __syncwarp();
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            stage = nstage;
+            phase = nphase;
         }
 
         // ===================== fused epilogue =====================
@@ -404,13 +432,14 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
                     for (int e = 0; e < 2; ++e) {
                         const bool in = e == 0 || two;
                         if constexpr (S == 1) {
-                            f0[e] = src_scalar(args.src_kind, args.sp, acc[0][i][j][e]);
-                            if (args.src_kind == 3 && nb + e == 0 && m == 0 && args.gz0 == 0 && args.gj0 == 0)
-                                f0[e] = __longlong_as_double(0x7ff8000000000000ll);
-                            bad |= in && !isfinite(f0[e]);
+                            f0[e] = src1<SK>(args.sp, acc[0][i][j][e]);
+                            if constexpr (SK == 3)
+                                if (nb + e == 0 && m == 0 && args.gz0 == 0 && args.gj0 == 0)
+                                    f0[e] = __longlong_as_double(0x7ff8000000000000ll);
+                            bad |= (int)in & (int)!isfinite(f0[e]);
                         } else {
-                            src_pair(args.src_kind, args.sp, acc[0][i][j][e], acc[1][i][j][e], f0[e], f1[e]);
-                            bad |= in && !(isfinite(f0[e]) && isfinite(f1[e]));
+                            src2<SK>(args.sp, acc[0][i][j][e], acc[1][i][j][e], f0[e], f1[e]);
+                            bad |= (int)in & (int)!(isfinite(f0[e]) && isfinite(f1[e]));
                         }
                     }
 #pragma unroll

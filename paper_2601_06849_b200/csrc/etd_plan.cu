@@ -92,48 +92,58 @@ struct KernelSpec {
     int threads, smem, bm, bn, S;
 };
 
-template <int MODE, int S, int EPI, bool PRO, int BM, int BN, int WMW, int WNW, int ST>
+template <int MODE, int S, int EPI, bool PRO, int SK, int BM, int BN, int WMW, int WNW, int ST>
 static KernelSpec make_spec() {
     using Cfg = ContractCfg<MODE, S, EPI, PRO, BM, BN, WMW, WNW, ST>;
-    auto k = etd_contract<MODE, S, EPI, PRO, BM, BN, WMW, WNW, ST>;
+    auto k = etd_contract<MODE, S, EPI, PRO, SK, BM, BN, WMW, WNW, ST>;
     return {reinterpret_cast<const void*>(k), Cfg::THREADS, Cfg::SMEM_BYTES, BM, BN, S};
 }
 
-template <int MODE, int S, int EPI, bool PRO>
+template <int MODE, int S, int EPI, bool PRO, int SK>
 static KernelSpec spec() {
     // Tile shapes: every variant keeps 64 FP64 accumulators per thread (8 warps).
     // Source-prologue kernels use an 8x1 warp grid so that each A element's
     // f(U) is evaluated by exactly one warp (it runs on the shared FP64/DMMA pipe).
-    if constexpr (S == 1) return make_spec<MODE, 1, EPI, PRO, 128, 128, 4, 2, 6>();
-    else if constexpr (S == 2 && PRO) return make_spec<MODE, 2, EPI, PRO, 64, 128, 8, 1, 8>();
-    else if constexpr (S == 2) return make_spec<MODE, 2, EPI, PRO, 64, 128, 2, 4, 6>();
-    else if constexpr (PRO) return make_spec<MODE, 4, EPI, PRO, 64, 64, 8, 1, 8>();
-    else return make_spec<MODE, 4, EPI, PRO, 64, 64, 2, 4, 5>();
+    if constexpr (S == 1) return make_spec<MODE, 1, EPI, PRO, SK, 128, 128, 4, 2, 6>();
+    else if constexpr (S == 2 && PRO) return make_spec<MODE, 2, EPI, PRO, SK, 64, 128, 8, 1, 8>();
+    else if constexpr (S == 2) return make_spec<MODE, 2, EPI, PRO, SK, 64, 128, 2, 4, 6>();
+    else if constexpr (PRO) return make_spec<MODE, 4, EPI, PRO, SK, 64, 64, 8, 1, 8>();
+    else return make_spec<MODE, 4, EPI, PRO, SK, 64, 64, 2, 4, 5>();
 }
 
-static KernelSpec pick(int mode, int S, int epi, bool pro) {
-#define ETD_SPEC(M, SS, E, P) \
-    if (mode == M && S == SS && epi == E && pro == P) return spec<M, SS, E, P>();
-    ETD_SPEC(1, 2, EPI_SCALE, true)
-    ETD_SPEC(1, 4, EPI_SCALE, true)
-    ETD_SPEC(1, 2, EPI_SCALE, false)
-    ETD_SPEC(1, 4, EPI_SCALE, false)
-    ETD_SPEC(1, 2, EPI_STORE, false)
-    ETD_SPEC(1, 4, EPI_STORE, false)
-    ETD_SPEC(1, 1, EPI_SCALE, false)
-    ETD_SPEC(1, 1, EPI_STORE, false)
-    ETD_SPEC(0, 2, EPI_MIX, false)
-    ETD_SPEC(0, 4, EPI_MIX, false)
-    ETD_SPEC(0, 1, EPI_WHAT_SRC, false)
-    ETD_SPEC(0, 2, EPI_WHAT_SRC, false)
-    ETD_SPEC(0, 1, EPI_CORR, false)
-    ETD_SPEC(0, 2, EPI_CORR, false)
-    ETD_SPEC(0, 1, EPI_UPDATE, false)
-    ETD_SPEC(0, 2, EPI_UPDATE, false)
-    ETD_SPEC(0, 1, EPI_SCALE, false)
-    ETD_SPEC(0, 1, EPI_STORE, false)
+// Kernels that evaluate the source are instantiated per source kind; every
+// other kernel ignores sk.
+static KernelSpec pick(int mode, int S, int epi, bool pro, int sk = 0) {
+    const bool uses_src = pro || epi == EPI_WHAT_SRC;
+    if (!uses_src) sk = 0;
+#define ETD_SPEC(M, SS, E, P, K) \
+    if (mode == M && S == SS && epi == E && pro == P && sk == K) return spec<M, SS, E, P, K>();
+#define ETD_SCALAR_KINDS(M, SS, E, P) ETD_SPEC(M, SS, E, P, 0) ETD_SPEC(M, SS, E, P, 1) ETD_SPEC(M, SS, E, P, 2) \
+    ETD_SPEC(M, SS, E, P, 3)
+#define ETD_PAIR_KINDS(M, SS, E, P) ETD_SPEC(M, SS, E, P, 0) ETD_SPEC(M, SS, E, P, 10) ETD_SPEC(M, SS, E, P, 11) \
+    ETD_SPEC(M, SS, E, P, 12) ETD_SPEC(M, SS, E, P, 13)
+    ETD_SCALAR_KINDS(1, 2, EPI_SCALE, true)
+    ETD_PAIR_KINDS(1, 4, EPI_SCALE, true)
+    ETD_SCALAR_KINDS(0, 1, EPI_WHAT_SRC, false)
+    ETD_PAIR_KINDS(0, 2, EPI_WHAT_SRC, false)
+    ETD_SPEC(1, 2, EPI_SCALE, false, 0)
+    ETD_SPEC(1, 4, EPI_SCALE, false, 0)
+    ETD_SPEC(1, 2, EPI_STORE, false, 0)
+    ETD_SPEC(1, 4, EPI_STORE, false, 0)
+    ETD_SPEC(1, 1, EPI_SCALE, false, 0)
+    ETD_SPEC(1, 1, EPI_STORE, false, 0)
+    ETD_SPEC(0, 2, EPI_MIX, false, 0)
+    ETD_SPEC(0, 4, EPI_MIX, false, 0)
+    ETD_SPEC(0, 1, EPI_CORR, false, 0)
+    ETD_SPEC(0, 2, EPI_CORR, false, 0)
+    ETD_SPEC(0, 1, EPI_UPDATE, false, 0)
+    ETD_SPEC(0, 2, EPI_UPDATE, false, 0)
+    ETD_SPEC(0, 1, EPI_SCALE, false, 0)
+    ETD_SPEC(0, 1, EPI_STORE, false, 0)
+#undef ETD_PAIR_KINDS
+#undef ETD_SCALAR_KINDS
 #undef ETD_SPEC
-    throw ConfigError("no kernel variant for this stage");
+    throw ConfigError("no kernel variant for this stage / source kind");
 }
 
 // ------------------------------------------------------------ NCCL (dlopen'd)
@@ -183,6 +193,8 @@ struct Nccl {
 // ------------------------------------------------------------ the plan
 struct Launch {
     std::string name;
+    int mode = 0, S = 1, epi = 0;
+    bool pro = false;
     KernelSpec k;
     dim3 grid;
     CUtensorMap tmA, tmB;
@@ -413,7 +425,11 @@ struct Plan {
         Launch L;
         L.name = name;
         const int mode = axis == 0 ? 0 : 1;
-        L.k = pick(mode, S, epi, pro);
+        L.mode = mode;
+        L.S = S;
+        L.epi = epi;
+        L.pro = pro;
+        L.k = pick(mode, S, epi, pro, d.src_kind);
         const int loaded = pro ? S / 2 : S;
         // fwd (M = P^T): mode 0 needs row-major P^T, mode 1 row-major P; back swaps
         const double* M = (mode == 0) != back ? PTR[axis] : PR[axis];
@@ -465,6 +481,7 @@ static void set_source(Plan& p, int kind, const double* params) {
             if (op.kind == Op::KERNEL) {
                 op.L.args.src_kind = kind;
                 for (int i = 0; i < 8; ++i) op.L.args.sp[i] = p.d.src_params[i];
+                op.L.k = pick(op.L.mode, op.L.S, op.L.epi, op.L.pro, kind);
             }
     drop_graphs(p);
 }
@@ -625,13 +642,15 @@ static void build_plan(Plan& p, const etd_desc& d) {
         for (int mode = 0; mode < 2; ++mode)
             for (int S : {1, 2, 4})
                 for (int e = 0; e < 6; ++e)
-                    for (int pro = 0; pro < 2; ++pro) {
-                        try {
-                            KernelSpec ks = pick(mode, S, e, pro != 0);
-                            ETD_CK(cudaFuncSetAttribute(ks.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ks.smem));
-                        } catch (const ConfigError&) {
+                    for (int pro = 0; pro < 2; ++pro)
+                        for (int sk : {0, 1, 2, 3, 10, 11, 12, 13}) {
+                            try {
+                                KernelSpec ks = pick(mode, S, e, pro != 0, sk);
+                                ETD_CK(cudaFuncSetAttribute(ks.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                            ks.smem));
+                            } catch (const ConfigError&) {
+                            }
                         }
-                    }
         attr_done = true;
     }
 
