@@ -258,12 +258,12 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
     hout = [torch.empty_like(h).pin_memory() for h in hin]
     cnt = plan.local_count
 
+    ptr = lambda lst, i: lst[i].data_ptr() if i < len(lst) else 0
+
     def e2e_step():
-        for s in range(cfg.nspecies):
-            plan.upload_ptr(s, hin[s].data_ptr(), cnt, 0, 0.0)
-        plan.step(1)
-        for s in range(cfg.nspecies):
-            plan.download_ptr(s, hout[s].data_ptr(), cnt)
+        # public API call: etd_advance(host in -> 1 step -> host out), copies
+        # pipelined against the first/last kernels inside the library
+        plan.advance_ptr(ptr(hin, 0), ptr(hin, 1), ptr(hout, 0), ptr(hout, 1), 0, 0.0, 1)
 
     e2e_step()  # warm
     barrier()
@@ -281,10 +281,10 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    bytes_io = cnt * 8 * cfg.nspecies
+    bytes_io = cnt * 8 * cfg.nspecies * world
     e2e = {"value": total_pts / (e2e_ms * 1e-3), "unit": "grid-point updates/s", "h2d_bytes_per_step": bytes_io,
            "d2h_bytes_per_step": bytes_io, "ms_per_step": e2e_ms,
-           "api": "etd_set_state -> etd_step(1) -> etd_get_state (pinned host buffers)"}
+           "api": "etd_advance(pinned host U,V in -> 1 step -> pinned host U,V out)"}
     finite = bool(np.all(np.isfinite(hout[0].numpy())))
 
     line = {"metric": "grid-point updates/sec (FP64)", "value": value, "unit": "grid-point updates/s",

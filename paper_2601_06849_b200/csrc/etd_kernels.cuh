@@ -66,7 +66,9 @@ struct ContractArgs {
     StepStatus* status;
     double tau;
     int commit;             // EPI_UPDATE: last CTA commits the step (single GPU); 0 under
-                            // z-slab sharding, where etd_commit runs after a global check
+                            // z-slab sharding / chunked launches, where etd_commit runs after
+    int outer0;             // first outer index (MODE 1) of a chunked launch
+    int mtile0;             // first M tile of a chunked launch
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -195,8 +197,8 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int n0 = blockIdx.x * BN;
-    const int m0 = blockIdx.y * BM;
-    const int outer = blockIdx.z;
+    const int m0 = (blockIdx.y + args.mtile0) * BM;
+    const int outer = blockIdx.z + args.outer0;
     const int KT = (args.n_axis + BK - 1) / BK;
 
     // A step aborted earlier in this launch sequence poisons every later kernel

@@ -342,6 +342,8 @@ struct Plan {
     bool profiling = false;
     std::vector<StageStat> stats;
     void* comm = nullptr;            // ncclComm_t
+    cudaStream_t cstream = nullptr;  // host<->device copy stream of the pipelined advance
+    std::vector<cudaEvent_t> xev;    // its chunk events
 
     ~Plan() {
         for (auto& g : graph)
@@ -355,6 +357,8 @@ struct Plan {
         if (status) cudaFree(status);
         if (status_host) cudaFreeHost(status_host);
         if (comm) Nccl::get().CommDestroy(comm);
+        for (auto e : xev) cudaEventDestroy(e);
+        if (cstream) cudaStreamDestroy(cstream);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -930,6 +934,125 @@ static void group_steps(std::vector<Plan*>& ps, int nsteps) {
     if (!err.empty()) throw AbortError(err, et, es);
 }
 
+// Host-buffer advance (the reference's value-semantics call shape) with the
+// host<->device copies pipelined against compute.
+//  * upload: y-row chunks on a copy stream; the z stage (z_fwd_src, z_back —
+//    independent per (x, y) pencil) of the first step runs per y-row chunk as
+//    soon as its rows land.
+//  * download: the y and x stages of the last step (independent per z plane /
+//    per x pencil) run per z-plane chunk; each chunk's rows of U' are copied
+//    back while the next chunk computes.  x-stage tiles of chunk c cover pencil
+//    rows [B_{c-1}, B_c) with B_c = 128*floor(k1*ny/128) <= k1*ny, so a chunk
+//    only reads rows whose y stage has finished and never rows of a later chunk.
+//  * the step commit moves to one etd_commit after the chunks.
+// 3D, unsharded plans; everything else takes set_state / etd_step / get_state.
+static constexpr int kXferChunks = 8;
+
+static bool overlap_eligible(const Plan& p, int nsteps) {
+    if (p.dim != 3 || p.sharded || p.profiling || nsteps < 1) return false;
+    const auto& ops = p.steps[0];
+    if (ops.size() != 8) return false;
+    for (const auto& op : ops)
+        if (op.kind != Op::KERNEL) return false;
+    return ops[0].L.name == "z_fwd_src" && ops[1].L.name == "z_back" && ops[2].L.name == "y_fwd" &&
+           ops.back().L.name == "x_back_upd";
+}
+
+static void advance_overlapped(Plan& p, const double* const* hin, double* const* hout, long n, double t,
+                               int nsteps) {
+    const View& V = p.slab;
+    const int C = std::max(1, std::min(kXferChunks, std::min(V.ny, V.nz)));
+    if (!p.cstream) {
+        ETD_CK(cudaStreamCreateWithFlags(&p.cstream, cudaStreamNonBlocking));
+        p.xev.resize(2 * kXferChunks + 1);
+        for (auto& e : p.xev) ETD_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaEvent_t* ev_in = p.xev.data();
+    cudaEvent_t* ev_out = p.xev.data() + kXferChunks;
+    cudaEvent_t ev_start = p.xev[2 * kXferChunks];
+    p.status_host->n = n;
+    p.status_host->t = t;
+    p.status_host->fail = 0;
+    p.status_host->cta_done = 0;
+    ETD_CK(cudaMemcpyAsync(p.status, p.status_host, sizeof(StepStatus), cudaMemcpyHostToDevice, p.stream));
+    ETD_CK(cudaEventRecord(ev_start, p.stream));
+    ETD_CK(cudaStreamWaitEvent(p.cstream, ev_start, 0));
+    auto jlo = [&](int c) { return (int)((long long)c * V.ny / C); };
+    auto zlo = [&](int c) { return (int)((long long)c * V.nz / C); };
+    const long long R = (long long)V.ny * V.nz;
+    auto rowb = [&](int c) {  // x-stage row boundary after chunk c-1 (c = 0..C)
+        if (c >= C) return R;
+        return (long long)zlo(c) * V.ny / 128 * 128;
+    };
+    double* st_in = p.state[p.cur];
+    for (int c = 0; c < C; ++c) {
+        const int j0 = jlo(c), j1 = jlo(c + 1);
+        for (int sp = 0; sp < p.ns; ++sp) {
+            cudaMemcpy3DParms m{};
+            m.srcPtr = make_cudaPitchedPtr(const_cast<double*>(hin[sp]), (size_t)V.nx * 8, V.nx, V.ny);
+            m.dstPtr = make_cudaPitchedPtr(st_in + (size_t)sp * V.F, (size_t)V.pitch * 8, V.nx, V.ny);
+            m.srcPos = make_cudaPos(0, j0, 0);
+            m.dstPos = make_cudaPos(0, j0, 0);
+            m.extent = make_cudaExtent((size_t)V.nx * 8, j1 - j0, V.nz);
+            m.kind = cudaMemcpyHostToDevice;
+            ETD_CK(cudaMemcpy3DAsync(&m, p.cstream));
+        }
+        ETD_CK(cudaEventRecord(ev_in[c], p.cstream));
+    }
+    for (int s = 0; s < nsteps; ++s) {
+        const auto& ops = p.steps[(p.cur + s) & 1];
+        const bool first = s == 0, last = s == nsteps - 1;
+        // z stage
+        if (first) {
+            for (int c = 0; c < C; ++c) {
+                ETD_CK(cudaStreamWaitEvent(p.stream, ev_in[c], 0));
+                for (int k = 0; k < 2; ++k) {
+                    Launch L = ops[k].L;
+                    L.args.outer0 = jlo(c);
+                    L.grid.z = jlo(c + 1) - jlo(c);
+                    if (L.grid.z) launch(L, p.stream);
+                }
+            }
+        } else {
+            run_op(p, ops[0], p.stream);
+            run_op(p, ops[1], p.stream);
+        }
+        // y and x stages
+        if (!last) {
+            for (size_t k = 2; k < ops.size(); ++k) run_op(p, ops[k], p.stream);
+            continue;
+        }
+        const Op& upd = ops.back();
+        for (int c = 0; c < C; ++c) {
+            for (size_t k = 2; k < ops.size(); ++k) {
+                Launch L = ops[k].L;
+                if (L.mode == 1) {  // y stage: outer index is z
+                    L.args.outer0 = zlo(c);
+                    L.grid.z = zlo(c + 1) - zlo(c);
+                } else {            // x stage: pencil-row tiles
+                    const long long r0 = rowb(c), r1 = rowb(c + 1);
+                    L.args.mtile0 = (int)(r0 / L.k.bm);
+                    L.grid.y = (unsigned)((r1 + L.k.bm - 1) / L.k.bm - r0 / L.k.bm);
+                    L.args.commit = 0;
+                }
+                if (L.grid.y && L.grid.z) launch(L, p.stream);
+            }
+            ETD_CK(cudaEventRecord(ev_out[c], p.stream));
+            ETD_CK(cudaStreamWaitEvent(p.cstream, ev_out[c], 0));
+            const long long r0 = rowb(c), r1 = rowb(c + 1);
+            if (r1 > r0)
+                for (int sp = 0; sp < p.ns; ++sp)
+                    ETD_CK(cudaMemcpy2DAsync(hout[sp] + r0 * V.nx, (size_t)V.nx * 8,
+                                             upd.L.args.out + (size_t)sp * V.F + r0 * V.pitch, (size_t)V.pitch * 8,
+                                             (size_t)V.nx * 8, (size_t)(r1 - r0), cudaMemcpyDeviceToHost, p.cstream));
+        }
+        etd_commit<<<1, 1, 0, p.stream>>>(p.status, nullptr, 0, p.tau);
+    }
+    ETD_CK(cudaGetLastError());
+    ETD_CK(cudaStreamSynchronize(p.cstream));
+    finish_steps(p, n);
+}
+
 static void set_state(Plan& p, int species, const double* host, size_t count, long n, double t) {
     if (species < 0 || species >= p.ns) throw ConfigError("species index out of range");
     const View& v = p.slab;
@@ -1123,6 +1246,27 @@ int etd_advance(etd_handle* h, const double* u, const double* v, long n, double 
     auto& p = *h->plan;
     if (p.ns == 2 && (!v || !v_out)) return ETD_ERR_CONFIG;
     const size_t cnt = (size_t)p.slab.nx * p.slab.ny * p.slab.nz;
+    if (etd::overlap_eligible(p, nsteps)) {
+        const double* hin[2] = {u, v};
+        double* hout[2] = {u_out, v_out};
+        int rs = guarded(h, [&] { etd::advance_overlapped(p, hin, hout, n, t, nsteps); });
+        if (rs == ETD_OK) {
+            if (n_out) *n_out = (long)p.status_host->n;
+            if (t_out) *t_out = p.status_host->t;
+            return ETD_OK;
+        }
+        if (rs != ETD_ERR_ABORT) return rs;
+        // abort: hand back the last good state (the input of the failing step)
+        std::string keep = h->msg;
+        double kt = h->t;
+        long ks = h->step;
+        guarded(h, [&] {
+            etd::get_state(p, 0, u_out, cnt, n_out, t_out);
+            if (p.ns == 2) etd::get_state(p, 1, v_out, cnt, n_out, t_out);
+        });
+        h->msg = keep; h->t = kt; h->step = ks;
+        return rs;
+    }
     int rc = guarded(h, [&] {
         etd::set_state(p, 0, u, cnt, n, t);
         if (p.ns == 2) etd::set_state(p, 1, v, cnt, n, t);

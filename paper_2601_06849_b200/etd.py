@@ -361,6 +361,16 @@ class _PlanBase:
                self.handle)
         return n.value, t.value
 
+    def advance_ptr(self, u_in: int, v_in: int, u_out: int, v_out: int, n: int = 0, t: float = 0.0,
+                    nsteps: int = 1):
+        """etd_advance on raw host pointers (pinned buffers overlap the copies with
+        compute): upload, nsteps steps, download.  Returns (n, t)."""
+        no, to = C.c_long(), C.c_double()
+        rc = lib().etd_advance(self.handle, C.c_void_p(u_in), C.c_void_p(v_in or None), int(n), float(t),
+                               int(nsteps), C.c_void_p(u_out), C.c_void_p(v_out or None), C.byref(no), C.byref(to))
+        _raise(rc, self.handle)
+        return no.value, to.value
+
     def step(self, nsteps: int = 1):
         """Advance the device-resident state nsteps times (StepperAbort on non-finite)."""
         _raise(lib().etd_step(self.handle, int(nsteps)), self.handle)
@@ -464,10 +474,12 @@ def advance(plan: StepperPlan, state: StepperState, f: DeviceSource, nsteps: int
         raise ConfigError("advance needs a scalar plan")
     plan.set_source(f)
     shape = np.shape(state.U)
-    plan.upload(0, state.U, state.n, state.t)
-    plan.step(nsteps)
-    u, n, t = plan.download(0)
-    return StepperState(n, t, u.reshape(shape))
+    u_in = np.ascontiguousarray(state.U, dtype=np.float64).reshape(-1)
+    if u_in.size != plan.local_count:
+        raise ConfigError("state shape does not match plan grid")
+    u_out = np.empty_like(u_in)
+    n, t = plan.advance_ptr(u_in.ctypes.data, 0, u_out.ctypes.data, 0, state.n, state.t, nsteps)
+    return StepperState(n, t, u_out.reshape(shape))
 
 
 def etd2rkds_step_system(plan: SystemPlan, state: SystemState, f: DeviceSource, nsteps: int = 1) -> SystemState:
@@ -478,12 +490,14 @@ def etd2rkds_step_system(plan: SystemPlan, state: SystemState, f: DeviceSource, 
         raise ConfigError("system state shape does not match plan grid")
     plan.set_source(f)
     shape = np.shape(state.U)
-    plan.upload(0, state.U, state.n, state.t)
-    plan.upload(1, state.V, state.n, state.t)
-    plan.step(nsteps)
-    u, n, t = plan.download(0)
-    v, _, _ = plan.download(1)
-    return SystemState(n, t, u.reshape(shape), v.reshape(shape))
+    u_in = np.ascontiguousarray(state.U, dtype=np.float64).reshape(-1)
+    v_in = np.ascontiguousarray(state.V, dtype=np.float64).reshape(-1)
+    if u_in.size != plan.local_count:
+        raise ConfigError("system state shape does not match plan grid")
+    u_out, v_out = np.empty_like(u_in), np.empty_like(v_in)
+    n, t = plan.advance_ptr(u_in.ctypes.data, v_in.ctypes.data, u_out.ctypes.data, v_out.ctypes.data, state.n,
+                            state.t, nsteps)
+    return SystemState(n, t, u_out.reshape(shape), v_out.reshape(shape))
 
 
 # ----------------------------------------------------------------- host setup exports

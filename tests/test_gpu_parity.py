@@ -222,3 +222,35 @@ def test_shape_mismatch_and_host_source_rejected():
         etd.advance(plan, etd.StepperState(0, 0.0, np.zeros(49)), lambda t, u, g: u)
     with pytest.raises(etd.ConfigError):
         etd.make_plan(g, 0.0, 1.0, 1.0)
+
+
+def test_pipelined_advance_equals_device_resident_steps():
+    """etd_advance (H2D/D2H pipelined against the first/last kernels, chunked
+    launches, deferred commit) is bitwise equal to upload + etd_step + download."""
+    grid = etd.build_grid(3, [(0, 1)] * 3, [30, 26, 40])
+    nx, ny, nz = grid.interior_shape()
+    rng = np.random.default_rng(12)
+    u0, v0 = rng.uniform(-1, 1, nx * ny * nz), rng.uniform(-0.5, 0.5, nx * ny * nz)
+    f = etd.fhn_cubic()
+    for steps in (1, 3):
+        plan = etd.make_system_plan(grid, 0.05, 1e-3, 5e-4, 0.0)
+        a = etd.etd2rkds_step_system(plan, etd.SystemState(2, 0.1, u0, v0), f, nsteps=steps)
+        plan2 = etd.make_system_plan(grid, 0.05, 1e-3, 5e-4, 0.0, source=f)
+        plan2.upload(0, u0, 2, 0.1)
+        plan2.upload(1, v0, 2, 0.1)
+        plan2.step(steps)
+        bu, n, t = plan2.download(0)
+        bv, _, _ = plan2.download(1)
+        assert np.array_equal(a.U, bu) and np.array_equal(a.V, bv)
+        assert a.n == n == 2 + steps and a.t == pytest.approx(t)
+
+
+def test_pipelined_advance_abort_3d():
+    g = etd.unit_box_grid(3, 14)
+    plan = etd.make_plan(g, 0.01, 1.0, 1.0)
+    u0 = np.random.default_rng(3).uniform(-0.5, 0.5, 13 ** 3)
+    with pytest.raises(etd.StepperAbort) as ei:
+        etd.advance(plan, etd.StepperState(9, 0.09, u0), etd.DeviceSource(etd.SourceKind.NAN_PROBE), nsteps=3)
+    assert ei.value.step == 9 and ei.value.t == pytest.approx(0.09)
+    u, n, t = plan.download(0)
+    assert n == 9 and np.array_equal(u, u0)
