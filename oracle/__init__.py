@@ -119,9 +119,14 @@ class Ref:
 
     @classmethod
     def system_run(cls, dim, n, tau, ku, kv, q, u, v, nsteps, src_kind=10, src_params=(0.1, 0.01, 0.5),
-                   family=0, n0=0, t0=0.0, composed=False):
-        u = np.ascontiguousarray(u, dtype=np.float64).copy()
-        v = np.ascontiguousarray(v, dtype=np.float64).copy()
+                   family=0, n0=0, t0=0.0, composed=False, lean=False, inplace=False):
+        """lean: memory-lean composition (same reference calls, explicit lifetimes);
+        inplace: update the given float64 arrays instead of copying them."""
+        if not inplace:
+            u = np.ascontiguousarray(u, dtype=np.float64).copy()
+            v = np.ascontiguousarray(v, dtype=np.float64).copy()
+        if lean:
+            composed = 2
         nn, tt, sec, tab, sab = C.c_long(n0), C.c_double(t0), C.c_double(0), C.c_double(0), C.c_long(0)
         err = C.create_string_buffer(512)
         rc = cls.lib().ref_system_run(dim, n, tau, ku, kv, q, family, src_kind, _params(src_params), u, v,
