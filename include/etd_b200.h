@@ -48,6 +48,10 @@ enum etd_source_kind {
     ETD_SRC_POLY3 = 2,       /* f = ((p3 u + p2) u + p1) u + p0                    */
     ETD_SRC_NAN = 3,         /* f = NaN at grid point 0, else 0 (abort probe,
                                 test_stepper.cpp:304-321)                          */
+    ETD_SRC_AC_MANUFACTURED = 4, /* u(1-u^2) + p1 u* - u*(1-u*^2), u* = e^{-p0 t} prod sin(pi x_a):
+                                the catalogue Allen-Cahn source (problems.cpp:93-104);
+                                p0 = lambda, p1 = -lambda + kappa dim pi^2, p2 = kappa */
+    ETD_SRC_SINGULAR = 5,    /* p0 u/(1-u), abort (step -1) if any u >= 1 (problems.cpp:122-133) */
     ETD_SRC_FHN_CUBIC = 10,  /* fu = u(1-u)(u-p0) - v, fv = p1 (p2 u - v) (config 3-4) */
     ETD_SRC_FHN_CLASSIC = 11,/* fu = u - u^3/3 - v, fv = p0 (u - p1 v) (problems.cpp:170-171) */
     ETD_SRC_MIRROR_AC = 12,  /* fu = u - u^3, fv = v - v^3 (test_stepper.cpp:432-438) */

@@ -235,16 +235,40 @@ int etd_o_apply_q(int dim, int n, double tau, double kappa, double q, int family
 
 /* ---- sources (kinds as include/etd_b200.h ETD_SRC_*) ------------------- */
 
-static void scalar_src(int kind, const double* p, const double* u, double* f, size_t N) {
-    for (size_t i = 0; i < N; ++i) {
-        const double x = u[i];
+/* Returns 4 on a source domain violation (problems.cpp:126-129), else 0.
+ * kind 4: problems.cpp:88-104 (manufactured Allen-Cahn forcing; p0 = lambda,
+ * p1 = -lambda + kappa dim pi^2); kind 5: problems.cpp:122-133 (rho u/(1-u)). */
+static int scalar_src(int kind, const double* p, const double* u, double* f, size_t N, int n, int dim, double t) {
+    if (kind == 5)
+        for (size_t i = 0; i < N; ++i)
+            if (u[i] >= 1.0) return 4;
+    double* s = NULL;
+    if (kind == 4) {  /* sine_product(g, 1.0): sin(pi coord), coord = (i+1) h (problems.cpp:17-33) */
+        s = (double*)malloc(sizeof(double) * n);
+        const double h = 1.0 / (n + 1);
+        for (int i = 0; i < n; ++i) s[i] = sin(ETD_PI * ((i + 1) * h));
+    }
+    const double a = kind == 4 ? exp(-p[0] * t) : 0.0;
+    for (size_t idx = 0; idx < N; ++idx) {
+        const double x = u[idx];
         switch (kind) {
-        case 1: f[i] = x - x * x * x; break;                                  /* u - u^3 */
-        case 2: f[i] = ((p[3] * x + p[2]) * x + p[1]) * x + p[0]; break;      /* cubic poly */
-        case 3: f[i] = i == 0 ? NAN : 0.0; break;                             /* NaN probe */
-        default: f[i] = 0.0;
+        case 1: f[idx] = x - x * x * x; break;                                  /* u - u^3 */
+        case 2: f[idx] = ((p[3] * x + p[2]) * x + p[1]) * x + p[0]; break;      /* cubic poly */
+        case 3: f[idx] = idx == 0 ? NAN : 0.0; break;                           /* NaN probe */
+        case 4: {
+            const size_t i = idx % n, j = (idx / n) % n, k = idx / ((size_t)n * n);
+            double v = 1.0 * s[i] * s[j];
+            if (dim == 3) v *= s[k];
+            const double us = a * v;
+            f[idx] = x * (1.0 - x * x) + p[1] * us - us * (1.0 - us * us);
+            break;
+        }
+        case 5: f[idx] = p[0] * x / (1.0 - x); break;
+        default: f[idx] = 0.0;
         }
     }
+    free(s);
+    return 0;
 }
 
 static void system_src(int kind, const double* p, const double* U, const double* V, double* fu,
@@ -279,7 +303,7 @@ static int scalar_step(plan_t* pl, int kind, const double* sp, double* U, long n
     double* fn = malloc(N * 8), *w1 = malloc(N * 8), *w2 = malloc(N * 8), *a = malloc(N * 8),
           *b = malloc(N * 8), *What = malloc(N * 8), *fw = malloc(N * 8);
     int rc = 0;
-    scalar_src(kind, sp, U, fn, N);
+    if (scalar_src(kind, sp, U, fn, N, pl->n, pl->dim, t)) { *t_abort = t; *step_abort = -1; rc = 3; goto done; }
     if (!all_finite(fn, N)) { *t_abort = t; *step_abort = n; rc = 3; goto done; }
     if (pl->dim == 2) {
         apply_q(pl, 0, 1, 1, U, w1);                          /* 193 */
@@ -295,7 +319,9 @@ static int scalar_step(plan_t* pl, int kind, const double* sp, double* U, long n
                                           tau * w2b[i + (size_t)nx * j] * d2[i]; /* 205-208 */
         etd_o_contract(nx, ny, nz, pl->P[0], 0, 0, mix, What);           /* 209 */
         for (size_t i = 0; i < N; ++i) What[i] *= 2.0;                    /* 210 */
-        scalar_src(kind, sp, What, fw, N);                                /* 212 */
+        if (scalar_src(kind, sp, What, fw, N, pl->n, pl->dim, t + tau)) {   /* 212 */
+            *t_abort = t + tau; *step_abort = -1; rc = 3; goto done;
+        }
         if (!all_finite(fw, N)) { *t_abort = t + tau; *step_abort = n; rc = 3; goto done; }
         double* gb = w2;
         etd_o_contract(nx, ny, nz, pl->P[0], 0, 1, fw, gb);               /* 214 */
@@ -311,7 +337,9 @@ static int scalar_step(plan_t* pl, int kind, const double* sp, double* U, long n
         apply_q(pl, 0, 1, 0, w1, What);                                  /* 249 */
         apply_q(pl, 0, 2, 0, w2, b);
         for (size_t i = 0; i < N; ++i) What[i] += tau * b[i];
-        scalar_src(kind, sp, What, fw, N);                               /* 250 */
+        if (scalar_src(kind, sp, What, fw, N, pl->n, pl->dim, t + tau)) {  /* 250 */
+            *t_abort = t + tau; *step_abort = -1; rc = 3; goto done;
+        }
         if (!all_finite(fw, N)) { *t_abort = t + tau; *step_abort = n; rc = 3; goto done; }
         for (size_t i = 0; i < N; ++i) fw[i] -= w2[i];                   /* 252 */
         apply_q(pl, 0, 3, 0, fw, b);                                     /* 253 */

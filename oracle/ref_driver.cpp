@@ -23,6 +23,7 @@
 #include "etdrd/errors.hpp"
 #include "etdrd/grid.hpp"
 #include "etdrd/operators.hpp"
+#include "etdrd/problems.hpp"
 #include "etdrd/rational.hpp"
 #include "etdrd/stepper.hpp"
 #include "etdrd/tensor_ops.hpp"
@@ -39,7 +40,7 @@ namespace {
 
 // source kinds shared with paper_2601_06849_b200 (include/etd_b200.h ETD_SRC_*)
 enum {
-    SRC_ZERO = 0, SRC_AC_CUBIC = 1, SRC_POLY3 = 2, SRC_NAN = 3,
+    SRC_ZERO = 0, SRC_AC_CUBIC = 1, SRC_POLY3 = 2, SRC_NAN = 3, SRC_AC_MANUFACTURED = 4, SRC_SINGULAR = 5,
     SRC_FHN_CUBIC = 10, SRC_FHN_CLASSIC = 11, SRC_MIRROR_AC = 12, SRC_DECOUPLED = 13
 };
 
@@ -52,9 +53,21 @@ double scalar_f(int kind, const double* p, double u) {
     }
 }
 
-SourceFunction make_scalar_source(int kind, const double* params) {
+SourceFunction make_scalar_source(int kind, const double* params, int dim = 2) {
     double p[8] = {0};
     if (params) std::memcpy(p, params, sizeof p);
+    // catalogue sources: the reference's own functors (problems.cpp:68-136)
+    if (kind == SRC_AC_MANUFACTURED) {
+        ProblemParams pp;
+        pp.lambda = p[0];
+        pp.kappa = p[2];
+        return allen_cahn(dim, pp).source;
+    }
+    if (kind == SRC_SINGULAR) {
+        ProblemParams pp;
+        pp.rho = p[0];
+        return singular_source(dim, pp).source;
+    }
     return {[kind, p](double, const Field& u, const Grid&) {
                 Field f(u.dim(), u.shape());
                 for (std::size_t i = 0; i < f.size(); ++i) f[i] = scalar_f(kind, p, u[i]);
@@ -256,7 +269,7 @@ int ref_scalar_run(int dim, int n, double tau, double kappa, double q, int famil
         const auto plan = make_plan(g, tau, kappa, q,
                                     scheme_by_family(family ? PadeFamily::P04 : PadeFamily::P02),
                                     static_cast<BackendKind>(backend));
-        const auto src = make_scalar_source(src_kind, src_params);
+        const auto src = make_scalar_source(src_kind, src_params, dim);
         StepperState st{*n_io, *t_io, field_from(g, u)};
         const auto t0 = std::chrono::steady_clock::now();
         for (int s = 0; s < nsteps; ++s) st = advance(plan, st, src);

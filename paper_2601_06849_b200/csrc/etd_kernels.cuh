@@ -67,6 +67,9 @@ struct ContractArgs {
     double tau;
     int commit;             // EPI_UPDATE: last CTA commits the step (single GPU); 0 under
                             // z-slab sharding / chunked launches, where etd_commit runs after
+    const double* sinx;     // sin(pi x_i), sin(pi y_j), sin(pi z_k) tables of the grid
+    const double* siny;     //   (manufactured-solution source, problems.cpp:17-33)
+    const double* sinz;
     int outer0;             // first outer index (MODE 1) of a chunked launch
     int mtile0;             // first M tile of a chunked launch
 };
@@ -142,11 +145,23 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 
 // Compile-time source kind for the hot kernels: straight-line code lets the
 // scheduler interleave the FP64 source math with DMMA issue.
+//  SK 4: Allen-Cahn with the manufactured forcing of problems.cpp:93-104,
+//        u(1-u^2) + lin u* - u*(1-u*^2), u* = e^{-lambda t} prod sin(pi x_a);
+//        p0 = lambda, p1 = lin = -lambda + kappa dim pi^2 (ustar supplied by caller)
+//  SK 5: singular source rho u/(1-u) (problems.cpp:122-133), p0 = rho; the
+//        domain guard u >= 1 is checked by the caller (src_domain)
 template <int SK>
-__device__ __forceinline__ double src1(const double* p, double u) {
+__device__ __forceinline__ double src1(const double* p, double u, double ustar = 0.0) {
     if constexpr (SK == 1) return u - u * u * u;
     else if constexpr (SK == 2) return ((p[3] * u + p[2]) * u + p[1]) * u + p[0];
+    else if constexpr (SK == 4) return u * (1.0 - u * u) + p[1] * ustar - ustar * (1.0 - ustar * ustar);
+    else if constexpr (SK == 5) return p[0] * u / (1.0 - u);
     else return 0.0;
+}
+template <int SK>
+__device__ __forceinline__ int src_domain_violation(double u) {
+    if constexpr (SK == 5) return u >= 1.0;
+    else return 0;
 }
 template <int SK>
 __device__ __forceinline__ void src2(const double* p, double u, double v, double& fu, double& fv) {
@@ -215,6 +230,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
     if (cta_flag[0] != 0) return;
 
     int bad = 0;  // non-finite seen (prologue or epilogue)
+    int dom = 0;  // source domain violated (singular source: u >= 1)
 
     // TMA issue for k-tile kt into `stage` (thread 0 only): one box for all
     // loaded operands (A) and one for the transform-matrix tile (B).
@@ -276,6 +292,10 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
                     a[s][i] = MODE == 0 ? base[swz(mm, kk)] : base[(mm >> 4) * 256 + swz(kk, mm & 15)];
                 }
         };
+        // e^{-lambda t} for the manufactured source: t of the input state (prologue)
+        // or t + tau (the x_back_src epilogue), from the device step status
+        const double src_a = SK == 4 ? exp(-args.sp[0] * (args.status->t + (EPI == EPI_WHAT_SRC ? args.tau : 0.0)))
+                                     : 0.0;
         // non-finite test without branches (keeps the DMMA stream one basic block)
         auto nonfinite = [](double x) { return (__double2hiint(x) & 0x7ff00000) == 0x7ff00000; };
         // fused source: the A fragment of f(U) at (m, k) is f of the U fragment at
@@ -288,13 +308,24 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
                     const int p = m0 + wm0 + i * 8 + g;
                     const int valid = (p < args.m_extent) & (kc < args.n_axis);
                     if constexpr (C::L == 1) {
-                        double f = src1<SK>(args.sp, a[0][i]);
+                        double ustar = 0.0;
+                        if constexpr (SK == 4) {
+                            // (x, y, z) of this element; out-of-grid lanes get u* = 0
+                            const int jj = (args.zaxis ? outer : kc) + args.gj0, kz = (args.zaxis ? kc : outer) + args.gz0;
+                            ustar = valid ? src_a * (args.sinx[p] * args.siny[jj] *
+                                                     (args.sinz ? args.sinz[kz] : 1.0))
+                                          : 0.0;
+                        }
+                        double f = src1<SK>(args.sp, a[0][i], ustar);
                         if constexpr (SK == 3)
                             if (p == 0 && (args.zaxis ? (kc + args.gz0 == 0 && outer + args.gj0 == 0)
                                                       : (kc + args.gj0 == 0 && outer + args.gz0 == 0)))
                                 f = __longlong_as_double(0x7ff8000000000000ll);
+                        if constexpr (SK == 4 || SK == 5)
+                            if (!valid) f = 0.0;  // outside the grid: keep the padded A operand zero
                         a[1][i] = f;
                         bad |= valid & nonfinite(f);
+                        dom |= valid & src_domain_violation<SK>(a[0][i]);
                     } else {
                         double fu, fv;
                         src2<SK>(args.sp, a[0][i], a[1][i], fu, fv);
@@ -434,11 +465,19 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
                     for (int e = 0; e < 2; ++e) {
                         const bool in = e == 0 || two;
                         if constexpr (S == 1) {
-                            f0[e] = src1<SK>(args.sp, acc[0][i][j][e]);
+                            double ustar = 0.0;
+                            if constexpr (SK == 4) {
+                                const int jj = m % args.ny_local + args.gj0, kz = m / args.ny_local + args.gz0;
+                                ustar = in ? src_a * (args.sinx[nb + e] * args.siny[jj] *
+                                                      (args.sinz ? args.sinz[kz] : 1.0))
+                                           : 0.0;
+                            }
+                            f0[e] = src1<SK>(args.sp, acc[0][i][j][e], ustar);
                             if constexpr (SK == 3)
                                 if (nb + e == 0 && m == 0 && args.gz0 == 0 && args.gj0 == 0)
                                     f0[e] = __longlong_as_double(0x7ff8000000000000ll);
                             bad |= (int)in & (int)!isfinite(f0[e]);
+                            dom |= (int)in & src_domain_violation<SK>(acc[0][i][j][e]);
                         } else {
                             src2<SK>(args.sp, acc[0][i][j][e], acc[1][i][j][e], f0[e], f1[e]);
                             bad |= (int)in & (int)!(isfinite(f0[e]) && isfinite(f1[e]));
@@ -468,10 +507,15 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
     }
 
     // ===================== status: abort flag and step commit =====================
+    // fail kinds: 1/2 non-finite source at t / t+tau, 3 non-finite update,
+    // 4/5 source domain violation at t / t+tau (problems.cpp:126-129, thrown
+    // before the finiteness check, so it takes precedence)
+    const int any_dom = __syncthreads_or(dom);
     const int any_bad = __syncthreads_or(bad);
     if (tid == 0) {
-        if (any_bad) {
-            const int kind = EPI == EPI_WHAT_SRC ? 2 : EPI == EPI_UPDATE ? 3 : 1;
+        if (any_dom || any_bad) {
+            int kind = EPI == EPI_WHAT_SRC ? 2 : EPI == EPI_UPDATE ? 3 : 1;
+            if (any_dom) kind = EPI == EPI_WHAT_SRC ? 5 : 4;
             atomicCAS(&args.status->fail, 0, kind);
         }
         if (EPI == EPI_UPDATE && args.commit) {
@@ -495,19 +539,30 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
 
 // ------------------------------------------------------------- sharded-step bookkeeping
 // Under z-slab sharding every rank must agree on whether step n aborted (the
-// reference aborts the whole step).  Each rank publishes a code (its fail kind,
-// or 100 = ok), the codes are gathered over the exchange transport, and
-// etd_commit applies the first-in-program-order failure (min kind) everywhere or
-// commits n += 1, t = n tau on every rank (stepper.cpp:228).
+// reference aborts the whole step).  Each rank publishes a code for its fail
+// kind, the codes are gathered over the exchange transport, and etd_commit
+// applies the first failure in program order everywhere or commits n += 1,
+// t = n tau on every rank (stepper.cpp:228).
+// Code = 10 * (program-order position: source at t, source at t+tau, update)
+//        + (0 for a domain violation, which the reference raises before the
+//           finiteness check, 1 otherwise); 1000 = ok.
+__host__ __device__ inline int fail_code(int kind) {
+    if (kind == 0) return 1000;
+    const int order = (kind == 1 || kind == 4) ? 1 : (kind == 2 || kind == 5) ? 2 : 3;
+    return order * 10 + (kind >= 4 ? 0 : 1);
+}
+__host__ __device__ inline int fail_kind(int code) {
+    const int order = code / 10, domain = code % 10 == 0;
+    return domain ? (order == 1 ? 4 : 5) : order;
+}
 __global__ void etd_fail_code(const StepStatus* st, int* code) {
-    const int f = *reinterpret_cast<const volatile int*>(&st->fail);
-    *code = f ? f : 100;
+    *code = fail_code(*reinterpret_cast<const volatile int*>(&st->fail));
 }
 __global__ void etd_commit(StepStatus* st, const int* codes, int ncodes, double tau) {
-    int g = 100;
+    int g = 1000;
     for (int i = 0; i < ncodes; ++i) g = min(g, codes[i]);
-    if (g < 100) {
-        st->fail = g;
+    if (g < 1000) {
+        st->fail = fail_kind(g);
     } else if (st->fail == 0) {
         const long long nn = st->n + 1;
         st->n = nn;

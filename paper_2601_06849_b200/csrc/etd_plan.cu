@@ -24,6 +24,7 @@
 #include <cstring>
 #include <functional>
 #include <memory>
+#include <numbers>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -119,7 +120,7 @@ static KernelSpec pick(int mode, int S, int epi, bool pro, int sk = 0) {
 #define ETD_SPEC(M, SS, E, P, K) \
     if (mode == M && S == SS && epi == E && pro == P && sk == K) return spec<M, SS, E, P, K>();
 #define ETD_SCALAR_KINDS(M, SS, E, P) ETD_SPEC(M, SS, E, P, 0) ETD_SPEC(M, SS, E, P, 1) ETD_SPEC(M, SS, E, P, 2) \
-    ETD_SPEC(M, SS, E, P, 3)
+    ETD_SPEC(M, SS, E, P, 3) ETD_SPEC(M, SS, E, P, 4) ETD_SPEC(M, SS, E, P, 5)
 #define ETD_PAIR_KINDS(M, SS, E, P) ETD_SPEC(M, SS, E, P, 0) ETD_SPEC(M, SS, E, P, 10) ETD_SPEC(M, SS, E, P, 11) \
     ETD_SPEC(M, SS, E, P, 12) ETD_SPEC(M, SS, E, P, 13)
     ETD_SCALAR_KINDS(1, 2, EPI_SCALE, true)
@@ -333,6 +334,7 @@ struct Plan {
     double* PR[3] = {nullptr, nullptr, nullptr};
     double* PTR[3] = {nullptr, nullptr, nullptr};
     double* dvec = nullptr;          // [axis][slot 9][species 2][dmax]
+    double* sintab[3] = {nullptr, nullptr, nullptr};  // sin(pi * coord) per axis (global extents)
     int dmax = 0;
     StepStatus* status = nullptr;
     StepStatus* status_host = nullptr;
@@ -350,6 +352,7 @@ struct Plan {
             if (g) cudaGraphExecDestroy(g);
         for (double* p : {state[0], state[1], Z, W, dvec, sendbuf, zin, Zz, Wz, recvb}) if (p) cudaFree(p);
         if (codes) cudaFree(codes);
+        for (double* t : sintab) if (t) cudaFree(t);
         for (int a = 0; a < 3; ++a) {
             if (PR[a]) cudaFree(PR[a]);
             if (PTR[a]) cudaFree(PTR[a]);
@@ -420,6 +423,9 @@ struct Plan {
         a.status = status;
         a.tau = tau;
         a.commit = sharded ? 0 : 1;
+        a.sinx = sintab[0];
+        a.siny = sintab[1];
+        a.sinz = dim == 3 ? sintab[2] : nullptr;
         return a;
     }
 
@@ -461,7 +467,8 @@ struct Plan {
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 static void check_source(int nspecies, int k) {
-    const bool scalar_src = k == ETD_SRC_ZERO || k == ETD_SRC_AC_CUBIC || k == ETD_SRC_POLY3 || k == ETD_SRC_NAN;
+    const bool scalar_src = k == ETD_SRC_ZERO || k == ETD_SRC_AC_CUBIC || k == ETD_SRC_POLY3 || k == ETD_SRC_NAN ||
+                            k == ETD_SRC_AC_MANUFACTURED || k == ETD_SRC_SINGULAR;
     const bool pair_src = k == ETD_SRC_FHN_CUBIC || k == ETD_SRC_FHN_CLASSIC || k == ETD_SRC_MIRROR_AC ||
                           k == ETD_SRC_DECOUPLED || k == ETD_SRC_ZERO;
     if (nspecies == 2 ? !pair_src : !scalar_src)
@@ -633,6 +640,15 @@ static void build_plan(Plan& p, const etd_desc& d) {
             put(6, d1, 2.0); put(7, d2, 2.0); put(8, d3, 2.0);
         }
     }
+    // sin(pi x_i) tables, reference expression std::sin(pi * coord(a, i)) with
+    // coord = low + (i+1) h (grid.hpp:36, problems.cpp:22-23)
+    for (int a = 0; a < d.dim; ++a) {
+        const double h = (d.high[a] - d.low[a]) / (d.n[a] + 1);
+        std::vector<double> st(d.n[a]);
+        for (int i = 0; i < d.n[a]; ++i) st[i] = std::sin(std::numbers::pi * (d.low[a] + (i + 1) * h));
+        ETD_CK(cudaMalloc(&p.sintab[a], st.size() * 8));
+        ETD_CK(cudaMemcpy(p.sintab[a], st.data(), st.size() * 8, cudaMemcpyHostToDevice));
+    }
     ETD_CK(cudaMalloc(&p.dvec, hd.size() * 8));
     ETD_CK(cudaMemcpy(p.dvec, hd.data(), hd.size() * 8, cudaMemcpyHostToDevice));
     ETD_CK(cudaMalloc(&p.status, sizeof(StepStatus)));
@@ -647,7 +663,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
             for (int S : {1, 2, 4})
                 for (int e = 0; e < 6; ++e)
                     for (int pro = 0; pro < 2; ++pro)
-                        for (int sk : {0, 1, 2, 3, 10, 11, 12, 13}) {
+                        for (int sk : {0, 1, 2, 3, 4, 5, 10, 11, 12, 13}) {
                             try {
                                 KernelSpec ks = pick(mode, S, e, pro != 0, sk);
                                 ETD_CK(cudaFuncSetAttribute(ks.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -815,7 +831,9 @@ static void finish_steps(Plan& p, long long n_before) {
     p.cur = (int)((p.cur + committed) & 1);
     if (p.status_host->fail) {
         const int kind = p.status_host->fail;
-        const double t = p.status_host->t + (kind >= 2 ? p.tau : 0.0);
+        const double t = p.status_host->t + ((kind == 2 || kind == 3 || kind == 5) ? p.tau : 0.0);
+        if (kind >= 4)  // problems.cpp:126-129: the source throws StepperAbort(t, -1)
+            throw AbortError("source domain violation: u >= 1 at t=" + std::to_string(t), t, -1);
         const char* what = kind == 3 ? "step update" : "source";
         throw AbortError(std::string(what) + " produced non-finite values at t=" + std::to_string(t), t,
                          (long)p.status_host->n);

@@ -78,6 +78,8 @@ class SourceKind(enum.IntEnum):
     AC_CUBIC = 1
     POLY3 = 2
     NAN_PROBE = 3
+    AC_MANUFACTURED = 4
+    SINGULAR = 5
     FHN_CUBIC = 10
     FHN_CLASSIC = 11
     MIRROR_AC = 12
@@ -113,6 +115,20 @@ def fhn_cubic(a: float = 0.1, eps: float = 0.01, beta: float = 0.5) -> DeviceSou
 def fhn_classic(eps: float = 1.0, alpha: float = 1.0) -> DeviceSource:
     """fu = u - u^3/3 - v ; fv = eps(u - alpha v) (reference problems.cpp:170-171)."""
     return DeviceSource(SourceKind.FHN_CLASSIC, (eps, alpha))
+
+
+def allen_cahn_manufactured(dim: int, lam: float = 1.0, kappa: float = 1.0) -> DeviceSource:
+    """Catalogue Allen-Cahn source with the manufactured forcing that pins the
+    decaying sine-product solution u* = e^{-lam t} prod sin(pi x_a)
+    (reference problems.cpp:68-106; non-autonomous)."""
+    import math
+    lin = -lam + kappa * dim * math.pi * math.pi  # problems.cpp:91
+    return DeviceSource(SourceKind.AC_MANUFACTURED, (lam, lin, kappa, float(dim)), autonomous=False)
+
+
+def singular(rho: float = 0.1) -> DeviceSource:
+    """rho u/(1-u) with the domain guard u >= 1 -> StepperAbort(t, -1) (problems.cpp:108-136)."""
+    return DeviceSource(SourceKind.SINGULAR, (rho,))
 
 
 def poly3(p0=0.0, p1=0.0, p2=0.0, p3=0.0) -> DeviceSource:

@@ -35,9 +35,15 @@ def main():
         ("scalar2d_poly", 2, 10, 0.01, 1.0, 1.0, 0, 2, (0.05, -0.3, 0.2, -1.0), 6),
         ("cfg0_physics_n31", 2, 31, 1e-3, 1.0, 1.0, 0, 1, None, 10),
         ("cfg2_physics_n15", 3, 15, 1e-3, 0.1, 1.0, 0, 1, None, 5),
+        # catalogue sources (problems.cpp): manufactured Allen-Cahn (p0 lambda, p1 lin, p2 kappa), singular
+        ("ac_manufactured2d_p02", 2, 20, 0.02, 1.0, 0.0, 0, 4, (1.0, -1.0 + 2 * np.pi ** 2, 1.0), 5),
+        ("ac_manufactured3d_p04", 3, 10, 0.02, 1.0, 0.0, 1, 4, (1.0, -1.0 + 3 * np.pi ** 2, 1.0), 4),
+        ("singular2d_p02", 2, 16, 0.01, 1.0, 1.0, 0, 5, (0.1,), 5),
     ]
     for name, dim, n, tau, kappa, q, fam, kind, params, steps in scalar:
         u0 = rng_field(zlib.crc32(name.encode()), n ** dim)
+        if kind in (4, 5):
+            u0 = 0.4 * (u0 + 1.0)  # inside the singular source's domain (u < 1)
         u1, nn, tt, _ = Ref.scalar_run(dim, n, tau, kappa, q, u0, steps, src_kind=kind, src_params=params,
                                        family=fam)
         cases[name] = dict(kind="scalar", dim=dim, n=n, tau=tau, kappa=kappa, q=q, family=fam, src_kind=kind,

@@ -14,6 +14,8 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 CASES = sorted(p for p in glob.glob(os.path.join(GOLD, "*.npz")) if not p.endswith("setup.npz"))
 SRC = {1: lambda p: etd.allen_cahn_cubic(), 2: lambda p: etd.poly3(*p[:4]),
+       4: lambda p: etd.DeviceSource(etd.SourceKind.AC_MANUFACTURED, tuple(p[:4]), False),
+       5: lambda p: etd.singular(p[0]),
        10: lambda p: etd.fhn_cubic(*p[:3]), 11: lambda p: etd.fhn_classic(*p[:2])}
 
 

@@ -254,3 +254,39 @@ def test_pipelined_advance_abort_3d():
     assert ei.value.step == 9 and ei.value.t == pytest.approx(0.09)
     u, n, t = plan.download(0)
     assert n == 9 and np.array_equal(u, u0)
+
+
+@pytest.mark.parametrize("dim,n,steps", [(2, 47, 6), (3, 21, 4)])
+def test_manufactured_allen_cahn_vs_reference(dim, n, steps):
+    """Catalogue Allen-Cahn source (non-autonomous, position dependent) against
+    the reference's own allen_cahn().source (problems.cpp:68-106)."""
+    g = etd.unit_box_grid(dim, n + 1)
+    src = etd.allen_cahn_manufactured(dim, 1.0, 1.0)
+    u0 = np.random.default_rng(21).uniform(0.0, 0.8, n ** dim)
+    for fam in (0, 1):
+        plan = etd.make_plan(g, 0.01, 1.0, 0.0, scheme=fam)
+        got = etd.advance(plan, etd.StepperState(3, 0.03, u0), src, nsteps=steps)
+        want = ref_or_oracle().scalar_run(dim, n, 0.01, 1.0, 0.0, u0, steps, src_kind=4,
+                                          src_params=src.params8(), family=fam, n0=3, t0=0.03)[0]
+        assert rel_gap(want, got.U) <= STEP_TOL
+
+
+def test_singular_source_vs_reference_and_domain_abort():
+    """rho u/(1-u) (problems.cpp:108-136) and its domain guard: u >= 1 aborts
+    with StepperAbort(t, step = -1) and the input state kept."""
+    n = 31
+    for dim in (2, 3):
+        nn = n if dim == 2 else 15
+        g = etd.unit_box_grid(dim, nn + 1)
+        u0 = 0.5 * np.random.default_rng(5).uniform(0.0, 1.0, nn ** dim)
+        plan = etd.make_plan(g, 0.01, 1.0, 1.0)
+        got = etd.advance(plan, etd.StepperState(0, 0.0, u0), etd.singular(0.1), nsteps=5)
+        want = ref_or_oracle().scalar_run(dim, nn, 0.01, 1.0, 1.0, u0, 5, src_kind=5, src_params=(0.1,))[0]
+        assert rel_gap(want, got.U) <= STEP_TOL
+        bad = u0.copy()
+        bad[7] = 1.0
+        with pytest.raises(etd.StepperAbort) as ei:
+            etd.advance(plan, etd.StepperState(2, 0.02, bad), etd.singular(0.1), nsteps=3)
+        assert ei.value.step == -1 and ei.value.t == pytest.approx(0.02)
+        u, n_, t = plan.download(0)
+        assert n_ == 2 and np.array_equal(u, bad)
