@@ -153,6 +153,13 @@ struct DeviceSource {
     static DeviceSource poly3(double p0, double p1, double p2, double p3) {
         return {ETD_SRC_POLY3, {p0, p1, p2, p3}, true};
     }
+    // catalogue Allen-Cahn with manufactured forcing (problems.cpp:68-106)
+    static DeviceSource allen_cahn_manufactured(int dim, double lambda = 1.0, double kappa = 1.0) {
+        const double pi = 3.14159265358979323846;
+        return {ETD_SRC_AC_MANUFACTURED, {lambda, -lambda + kappa * dim * pi * pi, kappa, double(dim)}, false};
+    }
+    // rho u/(1-u) with the u >= 1 domain guard (problems.cpp:108-136)
+    static DeviceSource singular(double rho = 0.1) { return {ETD_SRC_SINGULAR, {rho}, true}; }
 };
 using SourceFunction = DeviceSource;
 using SystemSource = DeviceSource;

@@ -196,8 +196,9 @@ __device__ __forceinline__ int swz(int row, int col) {
 }
 
 // ------------------------------------------------------------- the kernel
-template <int MODE, int S, int EPI, bool PRO, int SK, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
-__global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, 1)
+template <int MODE, int S, int EPI, bool PRO, int SK, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES,
+          int MINB = 1>
+__global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     etd_contract(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const ContractArgs args) {
     using C = ContractCfg<MODE, S, EPI, PRO, BM, BN, WARPS_M, WARPS_N, STAGES>;

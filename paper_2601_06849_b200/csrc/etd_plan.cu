@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -93,32 +94,49 @@ struct KernelSpec {
     int threads, smem, bm, bn, S;
 };
 
-template <int MODE, int S, int EPI, bool PRO, int SK, int BM, int BN, int WMW, int WNW, int ST>
+template <int MODE, int S, int EPI, bool PRO, int SK, int BM, int BN, int WMW, int WNW, int ST, int MINB = 1>
 static KernelSpec make_spec() {
     using Cfg = ContractCfg<MODE, S, EPI, PRO, BM, BN, WMW, WNW, ST>;
-    auto k = etd_contract<MODE, S, EPI, PRO, SK, BM, BN, WMW, WNW, ST>;
+    auto k = etd_contract<MODE, S, EPI, PRO, SK, BM, BN, WMW, WNW, ST, MINB>;
     return {reinterpret_cast<const void*>(k), Cfg::THREADS, Cfg::SMEM_BYTES, BM, BN, S};
 }
 
-template <int MODE, int S, int EPI, bool PRO, int SK>
+// Tile classes.  T=0 (large grids): 8 warps, 64 FP64 accumulators per thread.
+// T=1 (mid, e.g. 2D n~1000) and T=2 (tiny, n~128): 4-warp CTAs with smaller
+// tiles so that a launch still spreads over the 148 SMs (the step of a 2D
+// 1023^2 grid has only ~1e6 outputs per transform; of a 127^2 grid ~16k).
+// Source-prologue kernels use an Mx1 warp grid so that each A element's f(U) is
+// evaluated by exactly one warp (it runs on the shared FP64/DMMA pipe).
+template <int MODE, int S, int EPI, bool PRO, int SK, int T>
 static KernelSpec spec() {
-    // Tile shapes: every variant keeps 64 FP64 accumulators per thread (8 warps).
-    // Source-prologue kernels use an 8x1 warp grid so that each A element's
-    // f(U) is evaluated by exactly one warp (it runs on the shared FP64/DMMA pipe).
-    if constexpr (S == 1) return make_spec<MODE, 1, EPI, PRO, SK, 128, 128, 4, 2, 6>();
-    else if constexpr (S == 2 && PRO) return make_spec<MODE, 2, EPI, PRO, SK, 64, 128, 8, 1, 8>();
-    else if constexpr (S == 2) return make_spec<MODE, 2, EPI, PRO, SK, 64, 128, 2, 4, 6>();
-    else if constexpr (PRO) return make_spec<MODE, 4, EPI, PRO, SK, 64, 64, 8, 1, 8>();
-    else return make_spec<MODE, 4, EPI, PRO, SK, 64, 64, 2, 4, 5>();
+    if constexpr (T == 3 && !PRO) {  // experimental: 2 CTAs per SM, 32 accumulators per thread
+        if constexpr (S == 4) return make_spec<MODE, 4, EPI, PRO, SK, 32, 64, 2, 4, 4, 2>();
+        else if constexpr (S == 2) return make_spec<MODE, 2, EPI, PRO, SK, 32, 128, 2, 4, 4, 2>();
+        else return make_spec<MODE, 1, EPI, PRO, SK, 64, 128, 2, 4, 4, 2>();
+    } else if constexpr (T == 2) {
+        if constexpr (PRO) return make_spec<MODE, S, EPI, PRO, SK, 32, 32, 4, 1, 4>();
+        else return make_spec<MODE, S, EPI, PRO, SK, 32, 32, 2, 2, 4>();
+    } else if constexpr (T == 1 && S <= 2) {
+        if constexpr (PRO) return make_spec<MODE, S, EPI, PRO, SK, 64, 64, 4, 1, 6>();
+        else return make_spec<MODE, S, EPI, PRO, SK, 64, 64, 2, 2, 6>();
+    } else {
+        if constexpr (S == 1) return make_spec<MODE, 1, EPI, PRO, SK, 128, 128, 4, 2, 6>();
+        else if constexpr (S == 2 && PRO) return make_spec<MODE, 2, EPI, PRO, SK, 64, 128, 8, 1, 8>();
+        else if constexpr (S == 2) return make_spec<MODE, 2, EPI, PRO, SK, 64, 128, 2, 4, 6>();
+        else if constexpr (PRO) return make_spec<MODE, 4, EPI, PRO, SK, 64, 64, 8, 1, 8>();
+        else return make_spec<MODE, 4, EPI, PRO, SK, 64, 64, 2, 4, 5>();
+    }
 }
 
 // Kernels that evaluate the source are instantiated per source kind; every
 // other kernel ignores sk.
-static KernelSpec pick(int mode, int S, int epi, bool pro, int sk = 0) {
+static KernelSpec pick(int mode, int S, int epi, bool pro, int sk = 0, int tile = 0) {
     const bool uses_src = pro || epi == EPI_WHAT_SRC;
     if (!uses_src) sk = 0;
-#define ETD_SPEC(M, SS, E, P, K) \
-    if (mode == M && S == SS && epi == E && pro == P && sk == K) return spec<M, SS, E, P, K>();
+#define ETD_SPEC(M, SS, E, P, K)                                                                \
+    if (mode == M && S == SS && epi == E && pro == P && sk == K)                                \
+        return tile == 3 ? spec<M, SS, E, P, K, 3>() : tile == 2 ? spec<M, SS, E, P, K, 2>()   \
+               : tile == 1 ? spec<M, SS, E, P, K, 1>() : spec<M, SS, E, P, K, 0>();
 #define ETD_SCALAR_KINDS(M, SS, E, P) ETD_SPEC(M, SS, E, P, 0) ETD_SPEC(M, SS, E, P, 1) ETD_SPEC(M, SS, E, P, 2) \
     ETD_SPEC(M, SS, E, P, 3) ETD_SPEC(M, SS, E, P, 4) ETD_SPEC(M, SS, E, P, 5)
 #define ETD_PAIR_KINDS(M, SS, E, P) ETD_SPEC(M, SS, E, P, 0) ETD_SPEC(M, SS, E, P, 10) ETD_SPEC(M, SS, E, P, 11) \
@@ -194,7 +212,7 @@ struct Nccl {
 // ------------------------------------------------------------ the plan
 struct Launch {
     std::string name;
-    int mode = 0, S = 1, epi = 0;
+    int mode = 0, S = 1, epi = 0, tile = 0;
     bool pro = false;
     KernelSpec k;
     dim3 grid;
@@ -492,7 +510,7 @@ static void set_source(Plan& p, int kind, const double* params) {
             if (op.kind == Op::KERNEL) {
                 op.L.args.src_kind = kind;
                 for (int i = 0; i < 8; ++i) op.L.args.sp[i] = p.d.src_params[i];
-                op.L.k = pick(op.L.mode, op.L.S, op.L.epi, op.L.pro, kind);
+                op.L.k = pick(op.L.mode, op.L.S, op.L.epi, op.L.pro, kind, op.L.tile);
             }
     drop_graphs(p);
 }
@@ -663,14 +681,15 @@ static void build_plan(Plan& p, const etd_desc& d) {
             for (int S : {1, 2, 4})
                 for (int e = 0; e < 6; ++e)
                     for (int pro = 0; pro < 2; ++pro)
-                        for (int sk : {0, 1, 2, 3, 4, 5, 10, 11, 12, 13}) {
-                            try {
-                                KernelSpec ks = pick(mode, S, e, pro != 0, sk);
-                                ETD_CK(cudaFuncSetAttribute(ks.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                            ks.smem));
-                            } catch (const ConfigError&) {
+                        for (int sk : {0, 1, 2, 3, 4, 5, 10, 11, 12, 13})
+                            for (int tile = 0; tile < 4; ++tile) {
+                                try {
+                                    KernelSpec ks = pick(mode, S, e, pro != 0, sk, tile);
+                                    ETD_CK(cudaFuncSetAttribute(ks.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                                ks.smem));
+                                } catch (const ConfigError&) {
+                                }
                             }
-                        }
         attr_done = true;
     }
 

@@ -290,3 +290,30 @@ def test_singular_source_vs_reference_and_domain_abort():
         assert ei.value.step == -1 and ei.value.t == pytest.approx(0.02)
         u, n_, t = plan.download(0)
         assert n_ == 2 and np.array_equal(u, bad)
+
+
+@pytest.mark.parametrize("tile", ["0", "1", "2"])
+def test_every_tile_class_vs_reference(tile, monkeypatch):
+    """Large (8-warp), mid and tiny (4-warp) tile variants of every stage kernel,
+    forced on the same small problems, all match the reference."""
+    monkeypatch.setenv("ETD_FORCE_TILE", tile)
+    R = ref_or_oracle()
+    rng = np.random.default_rng(int(tile) + 40)
+    g = etd.unit_box_grid(3, 26)
+    c0, c1 = rng.uniform(-1, 1, 25 ** 3), rng.uniform(-1, 1, 25 ** 3)
+    sp = etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0)
+    got = etd.etd2rkds_step_system(sp, etd.SystemState(0, 0.0, c0, c1), etd.fhn_cubic(), nsteps=3)
+    wu, wv = R.system_run(3, 25, 0.05, 1e-3, 5e-4, 0.0, c0, c1, 3)[:2]
+    assert rel_gap(wu, got.U) <= STEP_TOL and rel_gap(wv, got.V) <= STEP_TOL
+    for dim, n in ((2, 57), (3, 19)):
+        g = etd.unit_box_grid(dim, n + 1)
+        x = rng.uniform(-1, 1, n ** dim)
+        p = etd.make_plan(g, 0.01, 0.7, 1.0, scheme=1)
+        got = etd.advance(p, etd.StepperState(0, 0.0, x), etd.allen_cahn_cubic(), nsteps=3)
+        want = R.scalar_run(dim, n, 0.01, 0.7, 1.0, x, 3, src_kind=1, family=1)[0]
+        assert rel_gap(want, got.U) <= STEP_TOL
+        for axis in range(dim):
+            P, _ = Oracle.spectral_factor(n, 2.0, -1.0)
+            t = p.debug_transform(x, axis)
+            w = Oracle.contract((n, n, n if dim == 3 else 1), P, x, axis, True)
+            assert np.max(np.abs(t - w)) <= 1e-13

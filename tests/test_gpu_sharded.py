@@ -77,3 +77,18 @@ def test_sharded_abort_is_global():
         u, n, t = p.download(0)
         z0, z1 = p.slab
         assert n == 7 and np.array_equal(u, u0.reshape(11, 11, 11)[z0:z1].reshape(-1))
+
+
+def test_sharded_position_dependent_source_equals_single_gpu():
+    """The manufactured Allen-Cahn source reads sin(pi x) tables at GLOBAL (y, z)
+    indices: on y-row blocks (z stage) and z-slabs (x/y stages) the offsets must
+    line up exactly with the unsharded plan."""
+    grid = etd.build_grid(3, [(0, 1)] * 3, [30, 27, 25])
+    nx, ny, nz = grid.interior_shape()
+    u0 = np.random.default_rng(4).uniform(0.0, 0.8, nx * ny * nz)
+    f = etd.allen_cahn_manufactured(3)
+    make = lambda **kw: etd.StepperPlan(grid, 0.01, 1.0, 0.0, source=f, **kw)
+    single = etd.advance(make(), etd.StepperState(0, 0.0, u0), f, nsteps=3)
+    for G in (2, 3):
+        (u,), n, t = run_sharded(make, G, [u0], 3, grid, f)
+        assert np.array_equal(u, single.U)
