@@ -109,7 +109,7 @@ static KernelSpec make_spec() {
 // evaluated by exactly one warp (it runs on the shared FP64/DMMA pipe).
 template <int MODE, int S, int EPI, bool PRO, int SK, int T>
 static KernelSpec spec() {
-    if constexpr (T == 3 && !PRO) {  // experimental: 2 CTAs per SM, 32 accumulators per thread
+    if constexpr (T == 3 && !PRO) {  // large grids, unit-stride kernels: 2 CTAs/SM, 32 accumulators/thread
         if constexpr (S == 4) return make_spec<MODE, 4, EPI, PRO, SK, 32, 64, 2, 4, 4, 2>();
         else if constexpr (S == 2) return make_spec<MODE, 2, EPI, PRO, SK, 32, 128, 2, 4, 4, 2>();
         else return make_spec<MODE, 1, EPI, PRO, SK, 64, 128, 2, 4, 4, 2>();
@@ -457,7 +457,26 @@ struct Plan {
         L.S = S;
         L.epi = epi;
         L.pro = pro;
-        L.k = pick(mode, S, epi, pro, d.src_kind);
+        const int nax = n_axis(v, axis);
+        const long long mext = axis == 0 ? (long long)v.ny * v.nz : v.nx;
+        const unsigned gz = mode == 0 ? 1u : (axis == 1 ? (unsigned)v.nz : (unsigned)v.ny);
+        // Tile class (measured):
+        //  * unit-stride (x) kernels on large grids: 2 CTAs/SM, 32 accumulators (T=3)
+        //  * otherwise the 8-warp tile (T=0) while it fills >= 3/4 of a wave
+        //  * else 4-warp 64x64 (T=1, S <= 2) if that fills a wave, else 32x32 (T=2)
+        auto ctas = [&](int t) {
+            const KernelSpec k = pick(mode, S, epi, pro, d.src_kind, t);
+            return (long long)((nax + k.bn - 1) / k.bn) * ((mext + k.bm - 1) / k.bm) * gz;
+        };
+        int tile;
+        if (mode == 0 && ctas(3) >= 2 * 148) tile = 3;
+        else if (ctas(0) >= 111) tile = 0;
+        else if (S <= 2 && ctas(1) >= 148) tile = 1;
+        else tile = 2;
+        if (const char* f = std::getenv("ETD_FORCE_TILE"))  // tests: exercise every tile class
+            if (f[0] >= '0' && f[0] <= '3' && f[1] == 0) tile = f[0] - '0';
+        L.tile = tile;
+        L.k = pick(mode, S, epi, pro, d.src_kind, tile);
         const int loaded = pro ? S / 2 : S;
         // fwd (M = P^T): mode 0 needs row-major P^T, mode 1 row-major P; back swaps
         const double* M = (mode == 0) != back ? PTR[axis] : PR[axis];
@@ -465,11 +484,8 @@ struct Plan {
         L.tmB = mapB(M, axis, mode, L.k.bn);
         L.args = base_args(v, axis);
         L.args.out = out;
-        const int nax = n_axis(v, axis);
-        const long long mext = L.args.m_extent;
         const unsigned gx = (nax + L.k.bn - 1) / L.k.bn;
         const unsigned gy = (unsigned)((mext + L.k.bm - 1) / L.k.bm);
-        const unsigned gz = mode == 0 ? 1u : (axis == 1 ? (unsigned)v.nz : (unsigned)v.ny);
         L.grid = dim3(gx, gy, gz);
         const double pts = (double)v.nx * v.ny * v.nz;
         L.flops = 2.0 * nax * pts * S;

@@ -292,7 +292,7 @@ def test_singular_source_vs_reference_and_domain_abort():
         assert n_ == 2 and np.array_equal(u, bad)
 
 
-@pytest.mark.parametrize("tile", ["0", "1", "2"])
+@pytest.mark.parametrize("tile", ["0", "1", "2", "3"])
 def test_every_tile_class_vs_reference(tile, monkeypatch):
     """Large (8-warp), mid and tiny (4-warp) tile variants of every stage kernel,
     forced on the same small problems, all match the reference."""

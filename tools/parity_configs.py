@@ -4,7 +4,7 @@ number of steps).  Runs on the GPU box: the GPU result first, then the reference
 (oracle/_ref: the unmodified etdrd core + OpenBLAS on all host cores) on the
 same seeded inputs.  Appends one JSON line per config to the output file.
 
-python tools/parity_configs.py OUT.jsonl [cfg ids]   (default 0 1 2 3 4)
+python tools/parity_configs.py OUT.jsonl [cfg ids]   (default 0 1 2 3 4; "4:2" = config 4, 2 steps)
 """
 import json
 import os
@@ -23,12 +23,13 @@ from oracle import Ref, rel_gap  # noqa: E402
 
 def main():
     out = sys.argv[1]
-    ids = [int(a) for a in sys.argv[2:]] or [0, 1, 2, 3, 4]
+    ids = sys.argv[2:] or ["0", "1", "2", "3", "4"]
     cores = os.cpu_count() or 1
     Ref.set_threads(cores)
-    for cid in ids:
+    for spec in ids:
+        cid = int(spec.split(":")[0])
         cfg = configs.CONFIGS[cid]
-        n, steps = cfg.n, cfg.steps
+        n, steps = cfg.n, (int(spec.split(":")[1]) if ":" in spec else cfg.steps)
         ics = configs.initial_state(cfg, n)
         plan = configs.make_plan(cfg, n)
         t0 = time.time()
@@ -49,7 +50,8 @@ def main():
                                src_kind=10, src_params=(0.1, 0.01, 0.5), lean=True, inplace=True)
             ref = [r[0], r[1]]
         t_ref = time.time() - t0
-        rec = {"config": cid, "dim": cfg.dim, "n": n, "steps": steps, "species": cfg.nspecies,
+        rec = {"config": cid, "dim": cfg.dim, "n": n, "steps": steps, "config_steps": cfg.steps,
+               "species": cfg.nspecies,
                "rel_gap": [rel_gap(a, b) for a, b in zip(ref, gpu)],
                "max_abs_diff": [float(np.max(np.abs(a - b))) for a, b in zip(ref, gpu)],
                "max_abs_ref": [float(np.max(np.abs(a))) for a in ref],
