@@ -35,8 +35,11 @@ enum etd_status {
     ETD_ERR_NODEVICE = 6     /* no CUDA device: there is no CPU fallback */
 };
 
-/* Pade family: rational.hpp:31 PadeFamily {P02, P04} */
-enum etd_family { ETD_P02 = 0, ETD_P04 = 1 };
+/* Pade family: rational.hpp:31 PadeFamily {P02, P04}.  ETD_EXACT selects the
+ * reference's BackendKind::ExactExpReference step (stepper.cpp:259-295: exact
+ * e^{-tau A}, phi_1, phi_2 multipliers on the same transforms), without its
+ * 64-points-per-axis cap. */
+enum etd_family { ETD_P02 = 0, ETD_P04 = 1, ETD_EXACT = 2 };
 
 /* Device source descriptors.  The reference takes a std::function
  * (SourceFunction / SystemSource, stepper.hpp:18-29) which cannot run on the
@@ -129,6 +132,13 @@ int etd_step(etd_handle* h, int nsteps);
  * v/v_out may be NULL for scalar plans. */
 int etd_advance(etd_handle* h, const double* u, const double* v, long n, double t, int nsteps,
                 double* u_out, double* v_out, long* n_out, double* t_out);
+
+/* ETRD field snapshot of the device state (reference save_field / load_field,
+ * field.cpp:46-81: "ETRD", u32 1, u32 dim, u32 shape[3], f64 t, f64 data), streamed
+ * through pinned staging.  Non-finite data is refused (ETD_ERR_NUMERICS).  load
+ * restores state t and n (n < 0: n = round(t / tau)).  Sharded plans use their slab. */
+int etd_save_snapshot(etd_handle* h, int species, const char* path);
+int etd_load_snapshot(etd_handle* h, int species, const char* path, long n);
 
 /* Replace the device source descriptor (the reference passes the source per
  * advance() call, stepper.hpp:85-86; plans do not own it). */

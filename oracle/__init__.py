@@ -86,6 +86,9 @@ class Ref:
             L.ref_apply_q.argtypes = [i, i, d, d, d, i, i, i, _dp, _dp, C.c_char_p, i]
             L.ref_sample_step.argtypes = [i, i, i, d, d, d, d, i, i, _dp, C.POINTER(d), C.POINTER(d), _dp,
                                           C.c_char_p, i]
+            L.ref_save_field.argtypes = [i, i, i, i, _dp, d, C.c_char_p, C.c_char_p, i]
+            L.ref_load_field.argtypes = [C.c_char_p, _dp, C.c_longlong, C.POINTER(C.c_int * 4), C.POINTER(d),
+                                         C.c_char_p, i]
             L.ref_set_threads.argtypes = [i]
             L.ref_get_threads.restype = i
             L.ref_blas_config.restype = C.c_char_p
@@ -147,6 +150,25 @@ class Ref:
                                        _params(src_params), C.byref(sec), C.byref(pts), parts, err, 512)
         _check(rc, err.value, 0, 0)
         return sec.value, pts.value, parts
+
+    @classmethod
+    def save_field(cls, shape, data, t, path):
+        nx, ny, nz = shape
+        err = C.create_string_buffer(256)
+        rc = cls.lib().ref_save_field(3 if nz > 1 else 2, nx, ny, nz, np.ascontiguousarray(data, dtype=np.float64),
+                                      t, path.encode(), err, 256)
+        _check(rc, err.value, 0, 0)
+
+    @classmethod
+    def load_field(cls, path, cap):
+        out = np.zeros(cap)
+        shape = (C.c_int * 4)()
+        t = C.c_double()
+        err = C.create_string_buffer(256)
+        rc = cls.lib().ref_load_field(path.encode(), out, cap, C.byref(shape), C.byref(t), err, 256)
+        _check(rc, err.value, 0, 0)
+        n = shape[1] * shape[2] * shape[3]
+        return out[:n], tuple(shape), t.value
 
     @classmethod
     def operator(cls, dim, n, axis, kappa, q):

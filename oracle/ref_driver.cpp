@@ -404,6 +404,32 @@ int ref_sample_step(int n, int nsub, int nspecies, double tau, double k0, double
     }
 }
 
+// field.cpp:46-81 (format cross-check of device snapshots)
+int ref_save_field(int dim, int nx, int ny, int nz, const double* data, double t, const char* path, char* err,
+                   int errlen) {
+    try {
+        Field f(dim, {nx, ny, nz});
+        std::memcpy(f.data(), data, f.size() * sizeof(double));
+        save_field(f, t, path);
+        return 0;
+    } catch (const std::exception& e) {
+        return map_exc(e, err, errlen, nullptr, nullptr);
+    }
+}
+
+int ref_load_field(const char* path, double* data, long long cap, int* shape, double* t, char* err, int errlen) {
+    try {
+        auto [f, tt] = load_field(path);
+        if ((long long)f.size() > cap) throw ConfigError("buffer too small");
+        std::memcpy(data, f.data(), f.size() * sizeof(double));
+        shape[0] = f.dim(); shape[1] = f.nx(); shape[2] = f.ny(); shape[3] = f.nz();
+        *t = tt;
+        return 0;
+    } catch (const std::exception& e) {
+        return map_exc(e, err, errlen, nullptr, nullptr);
+    }
+}
+
 // operators.cpp:11-34 on unit_box_grid(dim, n+1)
 int ref_operator(int dim, int n, int axis, double kappa, double q, double* diag, double* off,
                  char* err, int errlen) {

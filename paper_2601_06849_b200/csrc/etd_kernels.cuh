@@ -571,4 +571,13 @@ __global__ void etd_commit(StepStatus* st, const int* codes, int ncodes, double 
     }
 }
 
+// Finiteness scan of one padded field (snapshot save/load refuse non-finite
+// data, field.cpp:46-49, 79).  Pads are +0.0, so the whole allocation is scanned.
+__global__ void etd_nonfinite_scan(const double* __restrict__ f, long long n, int* flag) {
+    int bad = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        bad |= (__double2hiint(f[i]) & 0x7ff00000) == 0x7ff00000;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 }  // namespace etd

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -557,7 +558,8 @@ static void validate(const etd_desc& d) {
     if (d.dim != 2 && d.dim != 3) throw ConfigError("grid dimension must be 2 or 3");
     if (!(d.tau > 0.0)) throw ConfigError("tau must be positive");
     if (d.nspecies != 1 && d.nspecies != 2) throw ConfigError("nspecies must be 1 or 2");
-    if (d.family != 0 && d.family != 1) throw ConfigError("unknown Pade family");
+    if (d.family != ETD_P02 && d.family != ETD_P04 && d.family != ETD_EXACT)
+        throw ConfigError("unknown Pade family / backend");
     check_source(d.nspecies, d.src_kind);
     for (int a = 0; a < d.dim; ++a) {
         if (d.n[a] < 1) throw ConfigError("need at least 2 subintervals for a nonempty interior");
@@ -638,7 +640,8 @@ static void build_plan(Plan& p, const etd_desc& d) {
 
     // per-axis eigensystems and d-vectors (stepper.cpp:118-177; systems use the
     // unit-kappa operator and kappa_c * lambda, system_stepper.cpp:47-61)
-    const PadeScheme scheme = pade_scheme(d.family);
+    const bool exact = d.family == ETD_EXACT;
+    const PadeScheme scheme = pade_scheme(exact ? 0 : d.family);
     std::vector<double> hd((size_t)3 * 9 * 2 * p.dmax, 0.0);
     for (int a = 0; a < d.dim; ++a) {
         const int n = d.n[a], np = p.npad[a];
@@ -659,12 +662,25 @@ static void build_plan(Plan& p, const etd_desc& d) {
             std::vector<double> lc(lam);
             if (sys)
                 for (auto& x : lc) x *= d.kappa[c];
-            const auto d1 = dvector(lc, d.tau, scheme, 1), d2 = dvector(lc, d.tau, scheme, 2),
-                       d3 = dvector(lc, d.tau, scheme, 3);
             auto put = [&](int slot, const std::vector<double>& v, double sc) {
                 double* o = hd.data() + (((size_t)a * 9 + slot) * 2 + c) * p.dmax;
                 for (int i = 0; i < n; ++i) o[i] = sc * v[i];
             };
+            if (exact) {
+                // BackendKind::ExactExpReference (stepper.cpp:145-170, 259-295): the same
+                // step structure with exact exponential multipliers e^{-tau lambda}
+                // (every axis), tau phi1(tau lambda) and tau phi2(tau lambda) (x axis).
+                // The reference caps this dense path at 64 points per axis; the
+                // transform engine has no such limit.
+                const auto ev = exp_multipliers(lc, d.tau);
+                const auto g1 = phi_multipliers(lc, d.tau, 1), hh = phi_multipliers(lc, d.tau, 2);
+                put(0, ev, 1.0); put(1, g1, 1.0); put(2, hh, 1.0);
+                put(3, ev, 1.0); put(4, g1, 1.0); put(5, hh, 1.0);
+                put(6, ev, 2.0); put(7, g1, 2.0); put(8, hh, 2.0);
+                continue;
+            }
+            const auto d1 = dvector(lc, d.tau, scheme, 1), d2 = dvector(lc, d.tau, scheme, 2),
+                       d3 = dvector(lc, d.tau, scheme, 3);
             // production slots (power-of-two 2 folds exactly; tau folds once)
             put(0, d1, 2.0);
             put(1, d2, 2.0 * d.tau);
@@ -1133,6 +1149,94 @@ static void get_state(Plan& p, int species, double* host, size_t count, long* n,
     if (t) *t = p.status_host->t;
 }
 
+// ---- ETRD snapshots (reference field.cpp:32-81): "ETRD", u32 version 1, u32 dim,
+// u32 shape[3], f64 time, nx*ny*nz f64 (x-fastest).  Streamed through a pinned
+// staging buffer so a multi-GB field never needs a full host copy.  Sharded plans
+// write/read their own z-slab (shape nx, ny, z1-z0).
+static bool field_finite(Plan& p, const double* f) {
+    int* flag = p.codes ? p.codes : nullptr;
+    int* tmp = nullptr;
+    if (!flag) {
+        ETD_CK(cudaMalloc(&tmp, sizeof(int)));
+        flag = tmp;
+    }
+    ETD_CK(cudaMemsetAsync(flag, 0, sizeof(int), p.stream));
+    etd_nonfinite_scan<<<148 * 8, 256, 0, p.stream>>>(f, p.slab.F, flag);
+    int h = 0;
+    ETD_CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, p.stream));
+    ETD_CK(cudaStreamSynchronize(p.stream));
+    if (tmp) cudaFree(tmp);
+    return h == 0;
+}
+
+struct PinnedBuf {
+    double* ptr = nullptr;
+    size_t elems = 0;
+    explicit PinnedBuf(size_t n) : elems(n) { ETD_CK(cudaMallocHost(&ptr, n * sizeof(double))); }
+    ~PinnedBuf() { if (ptr) cudaFreeHost(ptr); }
+};
+
+static void save_snapshot(Plan& p, int species, const char* path) {
+    if (species < 0 || species >= p.ns) throw ConfigError("species index out of range");
+    const View& v = p.slab;
+    const double* src = p.state[p.cur] + (size_t)species * v.F;
+    if (!field_finite(p, src)) throw NumericsError("refusing to save field with non-finite entries");
+    copy_status_from_device(p);
+    FILE* fp = std::fopen(path, "wb");
+    if (!fp) throw ConfigError(std::string("cannot open ") + path + " for writing");
+    std::unique_ptr<FILE, int (*)(FILE*)> guard(fp, &std::fclose);
+    const uint32_t hdr[5] = {1u, (uint32_t)p.dim, (uint32_t)v.nx, (uint32_t)v.ny, (uint32_t)(p.dim == 3 ? v.nz : 1)};
+    const double t = p.status_host->t;
+    bool ok = std::fwrite("ETRD", 1, 4, fp) == 4 && std::fwrite(hdr, 4, 5, fp) == 5 && std::fwrite(&t, 8, 1, fp) == 1;
+    const size_t rows = (size_t)v.ny * v.nz, per = std::max<size_t>(1, (32u << 20) / v.nx);
+    PinnedBuf buf(per * v.nx);
+    for (size_t r0 = 0; ok && r0 < rows; r0 += per) {
+        const size_t nr = std::min(per, rows - r0);
+        ETD_CK(cudaMemcpy2DAsync(buf.ptr, (size_t)v.nx * 8, src + r0 * v.pitch, v.pitch * 8, (size_t)v.nx * 8, nr,
+                                 cudaMemcpyDeviceToHost, p.stream));
+        ETD_CK(cudaStreamSynchronize(p.stream));
+        ok = std::fwrite(buf.ptr, 8, nr * v.nx, fp) == nr * v.nx;
+    }
+    if (!ok) throw ConfigError(std::string("short write to ") + path);
+}
+
+static void load_snapshot(Plan& p, int species, const char* path, long n) {
+    if (species < 0 || species >= p.ns) throw ConfigError("species index out of range");
+    const View& v = p.slab;
+    FILE* fp = std::fopen(path, "rb");
+    if (!fp) throw ConfigError(std::string("cannot open ") + path);
+    std::unique_ptr<FILE, int (*)(FILE*)> guard(fp, &std::fclose);
+    char magic[4];
+    uint32_t hdr[5];
+    double t = 0.0;
+    if (std::fread(magic, 1, 4, fp) != 4 || std::memcmp(magic, "ETRD", 4) != 0)
+        throw ConfigError(std::string(path) + ": not a field snapshot");
+    if (std::fread(hdr, 4, 5, fp) != 5 || hdr[0] != 1u) throw ConfigError(std::string(path) + ": unsupported version");
+    if ((int)hdr[1] != p.dim || (int)hdr[2] != v.nx || (int)hdr[3] != v.ny ||
+        (int)hdr[4] != (p.dim == 3 ? v.nz : 1))
+        throw ConfigError(std::string(path) + ": snapshot shape does not match plan grid");
+    if (std::fread(&t, 8, 1, fp) != 1) throw ConfigError(std::string(path) + ": truncated snapshot");
+    double* dst = p.state[p.cur] + (size_t)species * v.F;
+    const size_t rows = (size_t)v.ny * v.nz, per = std::max<size_t>(1, (32u << 20) / v.nx);
+    PinnedBuf buf(per * v.nx);
+    for (size_t r0 = 0; r0 < rows; r0 += per) {
+        const size_t nr = std::min(per, rows - r0);
+        if (std::fread(buf.ptr, 8, nr * v.nx, fp) != nr * v.nx)
+            throw ConfigError(std::string(path) + ": truncated snapshot");
+        ETD_CK(cudaMemcpy2DAsync(dst + r0 * v.pitch, v.pitch * 8, buf.ptr, (size_t)v.nx * 8, (size_t)v.nx * 8, nr,
+                                 cudaMemcpyHostToDevice, p.stream));
+        ETD_CK(cudaStreamSynchronize(p.stream));
+    }
+    if (!field_finite(p, dst)) throw NumericsError(std::string(path) + ": snapshot has non-finite entries");
+    // a snapshot carries t only; restart at n = round(t / tau) unless given
+    p.status_host->n = n >= 0 ? n : (long long)std::llround(t / p.tau);
+    p.status_host->t = t;
+    p.status_host->fail = 0;
+    p.status_host->cta_done = 0;
+    ETD_CK(cudaMemcpyAsync(p.status, p.status_host, sizeof(StepStatus), cudaMemcpyHostToDevice, p.stream));
+    ETD_CK(cudaStreamSynchronize(p.stream));
+}
+
 static void debug_transform(Plan& p, int species, int axis, int back, int ell, int apply_q,
                             const double* in, double* out) {
     if (axis < 0 || axis >= p.dim) throw ConfigError("axis out of range for field dimension");
@@ -1387,6 +1491,16 @@ int etd_debug_transform(etd_handle* h, int species, int axis, int back, int ell,
                         double* out) {
     if (!h || !in || !out) return ETD_ERR_CONFIG;
     return guarded(h, [&] { etd::debug_transform(*h->plan, species, axis, back, ell, apply_q, in, out); });
+}
+
+int etd_save_snapshot(etd_handle* h, int species, const char* path) {
+    if (!h || !path) return ETD_ERR_CONFIG;
+    return guarded(h, [&] { etd::save_snapshot(*h->plan, species, path); });
+}
+
+int etd_load_snapshot(etd_handle* h, int species, const char* path, long n) {
+    if (!h || !path) return ETD_ERR_CONFIG;
+    return guarded(h, [&] { etd::load_snapshot(*h->plan, species, path, n); });
 }
 
 int etd_set_source(etd_handle* h, int src_kind, const double* src_params) {

@@ -131,6 +131,29 @@ std::vector<double> dvector(const std::vector<double>& lambda, double tau, const
     return d;
 }
 
+// stepper.cpp:162-170: series branch below 1e-4 (branches agree to 1e-12 there)
+double phi1(double x) {
+    if (x < 1e-4) return 1.0 - x / 2.0 + x * x / 6.0 - x * x * x / 24.0;
+    return (1.0 - std::exp(-x)) / x;
+}
+double phi2(double x) {
+    if (x < 1e-4) return 0.5 - x / 6.0 + x * x / 24.0 - x * x * x / 120.0;
+    return (x - 1.0 + std::exp(-x)) / (x * x);
+}
+std::vector<double> exp_multipliers(const std::vector<double>& lambda, double tau) {
+    std::vector<double> v(lambda.size());
+    for (std::size_t k = 0; k < lambda.size(); ++k) v[k] = std::exp(-tau * lambda[k]);  // stepper.cpp:279
+    return v;
+}
+std::vector<double> phi_multipliers(const std::vector<double>& lambda, double tau, int which) {
+    std::vector<double> v(lambda.size());
+    for (std::size_t k = 0; k < lambda.size(); ++k) {
+        const double x = tau * lambda[k];
+        v[k] = tau * (which == 1 ? phi1(x) : phi2(x));                               // stepper.cpp:289-291
+    }
+    return v;
+}
+
 // ---- seeded inputs ---------------------------------------------------------
 namespace {
 

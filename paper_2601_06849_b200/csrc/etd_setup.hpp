@@ -37,6 +37,14 @@ PadeScheme pade_scheme(int family);
 std::vector<double> dvector(const std::vector<double>& lambda, double tau, const PadeScheme& s,
                             int ell);
 
+// Exact-exponential multipliers (reference stepper.cpp:162-170, 276-292):
+// e^{-tau lambda_k}; tau phi_1(tau lambda_k) (which = 1) or tau phi_2 (which = 2),
+// phi with the reference's series branch below x = 1e-4.
+double phi1(double x);
+double phi2(double x);
+std::vector<double> exp_multipliers(const std::vector<double>& lambda, double tau);
+std::vector<double> phi_multipliers(const std::vector<double>& lambda, double tau, int which);
+
 // Seeded initial conditions for BASELINE configs.
 void fill_config_ic(int config, unsigned long long seed, int species, int n, int z0, int z1,
                     double* out);

@@ -63,6 +63,9 @@ class PadeFamily(enum.IntEnum):
     P04 = 1
 
 
+EXACT_FAMILY = 2  # etd_family ETD_EXACT
+
+
 class BackendKind(enum.IntEnum):
     """tensor_ops.hpp:31 plus the B200 backend this package adds."""
     Spectral = 0
@@ -227,6 +230,8 @@ def lib():
         L.etd_setup_axis.argtypes = [i, d, d, i, d, d, vp, vp]
         L.etd_setup_dvector.argtypes = [i, vp, d, i, i, vp]
         L.etd_setup_scheme.argtypes = [i, vp, C.POINTER(i)]
+        L.etd_save_snapshot.argtypes = [vp, i, C.c_char_p]
+        L.etd_load_snapshot.argtypes = [vp, i, C.c_char_p, l]
         L.etd_zslab_partition.argtypes = [i, i, i, C.POINTER(i), C.POINTER(i)]
         L.etd_nccl_unique_id.argtypes = [vp]
         L.etd_group_step.argtypes = [C.POINTER(vp), i, i]
@@ -308,6 +313,8 @@ def _make_desc(grid: Grid, tau, family, nspecies, kappas, q, source: DeviceSourc
 def _family(scheme) -> int:
     if isinstance(scheme, (int, PadeFamily)):
         return int(scheme)
+    if isinstance(scheme, str) and scheme.lower() == "exact":
+        return EXACT_FAMILY
     if isinstance(scheme, str):
         return {"p02": 0, "p04": 1}[scheme.lower()]
     raise ConfigError("scheme must be a PadeFamily")
@@ -329,7 +336,8 @@ class _PlanBase:
             raise ConfigError("tau must be positive")
         self.grid = grid
         self.tau = float(tau)
-        self.family = PadeFamily(_family(family))
+        fam = _family(family)
+        self.family = PadeFamily(fam) if fam in (0, 1) else fam
         self.q = float(q)
         self.backend = BackendKind.CudaSpectral
         self._source = source or (allen_cahn_cubic() if self.nspecies == 1 else fhn_cubic())
@@ -386,6 +394,14 @@ class _PlanBase:
                                int(nsteps), C.c_void_p(u_out), C.c_void_p(v_out or None), C.byref(no), C.byref(to))
         _raise(rc, self.handle)
         return no.value, to.value
+
+    def save_snapshot(self, species: int, path: str):
+        """ETRD snapshot of the device state (reference save_field, field.cpp:46-58)."""
+        _raise(lib().etd_save_snapshot(self.handle, species, os.fsencode(path)), self.handle)
+
+    def load_snapshot(self, species: int, path: str, n: int = -1):
+        """Restore a species from an ETRD snapshot (reference load_field, field.cpp:60-81)."""
+        _raise(lib().etd_load_snapshot(self.handle, species, os.fsencode(path), int(n)), self.handle)
 
     def step(self, nsteps: int = 1):
         """Advance the device-resident state nsteps times (StepperAbort on non-finite)."""
@@ -451,9 +467,13 @@ class SystemPlan(_PlanBase):
 def make_plan(grid: Grid, tau: float, kappa: float, q: float, scheme=PadeFamily.P02,
               backend: BackendKind = BackendKind.CudaSpectral, memory_cap_bytes: int = 0,
               source: Optional[DeviceSource] = None, device: int = 0) -> StepperPlan:
-    """stepper.hpp:59-61.  Only BackendKind.CudaSpectral is served here."""
+    """stepper.hpp:59-61.  BackendKind.CudaSpectral runs the Pade scheme `scheme`;
+    BackendKind.ExactExpReference runs the reference's exact-exponential step
+    (stepper.cpp:259-295) on the same device transforms."""
+    if backend == BackendKind.ExactExpReference:
+        return StepperPlan(grid, tau, kappa, q, EXACT_FAMILY, source, device)
     if backend != BackendKind.CudaSpectral:
-        raise ConfigError("this package implements BackendKind.CudaSpectral only")
+        raise ConfigError("this package implements BackendKind.CudaSpectral and ExactExpReference")
     return StepperPlan(grid, tau, kappa, q, scheme, source, device)
 
 

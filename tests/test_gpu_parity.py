@@ -317,3 +317,35 @@ def test_every_tile_class_vs_reference(tile, monkeypatch):
             t = p.debug_transform(x, axis)
             w = Oracle.contract((n, n, n if dim == 3 else 1), P, x, axis, True)
             assert np.max(np.abs(t - w)) <= 1e-13
+
+
+@pytest.mark.parametrize("dim,n,steps", [(2, 48, 5), (3, 20, 4), (2, 12, 3)])
+def test_exact_exponential_backend_vs_reference(dim, n, steps):
+    """BackendKind.ExactExpReference on the device transforms against the
+    reference's etd2rkds_reference_step (stepper.cpp:259-295; the reference caps
+    it at 64 points per axis, so parity is checked there)."""
+    g = etd.unit_box_grid(dim, n + 1)
+    u0 = np.random.default_rng(dim + n).uniform(-0.8, 0.8, n ** dim)
+    plan = etd.make_plan(g, 0.02, 0.9, 1.0, backend=etd.BackendKind.ExactExpReference)
+    got = etd.advance(plan, etd.StepperState(0, 0.0, u0), etd.allen_cahn_cubic(), nsteps=steps)
+    if Ref.available():
+        want = Ref.scalar_run(dim, n, 0.02, 0.9, 1.0, u0, steps, src_kind=1, backend=3)[0]
+        assert rel_gap(want, got.U) <= STEP_TOL
+    # exact decay of a sine mode under a zero source (test_stepper.cpp:96-112)
+    s = sine_mode(g)
+    out = etd.advance(plan, etd.StepperState(0, 0.0, s), etd.DeviceSource(etd.SourceKind.ZERO))
+    mu = sum(etd.setup_axis(n, 0.9, 1.0, dim)[1][0] for _ in range(dim))
+    assert np.max(np.abs(out.U - np.exp(-0.02 * mu) * s)) <= 1e-12
+
+
+def test_exact_exponential_backend_beyond_reference_cap():
+    """No 64-point cap on the device: a 200^2 exact-exponential run stays consistent
+    with the P04 Pade run to the Pade approximation error."""
+    n = 200
+    g = etd.unit_box_grid(2, n + 1)
+    u0 = np.random.default_rng(2).uniform(-0.5, 0.5, n * n)
+    ex = etd.advance(etd.make_plan(g, 1e-4, 1.0, 0.0, backend=etd.BackendKind.ExactExpReference),
+                     etd.StepperState(0, 0.0, u0), etd.allen_cahn_cubic(), nsteps=5)
+    p4 = etd.advance(etd.make_plan(g, 1e-4, 1.0, 0.0, scheme=1), etd.StepperState(0, 0.0, u0),
+                     etd.allen_cahn_cubic(), nsteps=5)
+    assert np.all(np.isfinite(ex.U)) and rel_gap(ex.U, p4.U) < 1e-2
