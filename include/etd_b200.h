@@ -168,6 +168,13 @@ int etd_stage_info(const etd_handle* h, int i, char* name, size_t len, double* m
 int etd_debug_transform(etd_handle* h, int species, int axis, int back, int ell, int apply_q,
                         const double* in, double* out);
 
+/* Determinism check: re-run the step's stage kernel `name` (e.g. "x_fwd_corr")
+ * `reps` times on its current inputs; *mismatches = max number of output
+ * elements (operand `out`) that differ bitwise from the first re-run, pos[0..cap)
+ * their element offsets.  A correct (race-free) kernel reports 0. */
+int etd_debug_repeat_op(etd_handle* h, const char* name, int out, int reps, long long* mismatches,
+                        long long* pos, int cap);
+
 /* Seeded initial conditions for BASELINE configs 0-4;
  * counter-based RNG, identical on every host, multithreaded.  Host only.
  * Writes this rank's slab [z0,z1) of species `species` (x-fastest). */

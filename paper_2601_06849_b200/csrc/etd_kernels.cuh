@@ -363,17 +363,21 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                 const int cur = st & 1, nxt = cur ^ 1;
                 if (st < BK / 4 - 1) {
                     load_frags(stage, st + 1, fa[nxt], fb[nxt]);
-                } else {
-                    // every read of this stage has been issued: release it, then
+                } else if (kt + 1 < KT) {
                     // look ahead into the next stage
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[stage]);
-                    if (kt + 1 < KT) {
-                        mbar_wait(&full[nstage], nphase);
-                        load_frags(nstage, 0, fa[nxt], fb[nxt]);
-                    }
+                    mbar_wait(&full[nstage], nphase);
+                    load_frags(nstage, 0, fa[nxt], fb[nxt]);
                 }
                 mma(fa[cur], fb[cur]);
+                if (st == BK / 4 - 1) {
+                    // Release this stage only now: the DMMAs above could not issue
+                    // before their fragment loads from this stage had returned, so no
+                    // LDS of this stage is still in flight when the producer's TMA
+                    // refills the slot (releasing right after *issuing* the last
+                    // loads was a WAR race on the slot).
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[stage]);
+                }
                 if (st < BK / 4 - 1) apply_src(kt, st + 1, fa[nxt]);
                 else if (kt + 1 < KT) apply_src(kt + 1, 0, fa[nxt]);
             }
@@ -569,6 +573,88 @@ __global__ void etd_commit(StepStatus* st, const int* codes, int ncodes, double 
         st->n = nn;
         st->t = (double)nn * tau;
     }
+}
+
+// ------------------------------------------------------------- source pass
+// f(t, U(,V)) for one step, written next to the state: buf = [U,(V),fU,(fV)]
+// (stepper.cpp:190 / system_stepper.cpp:80).  HBM-bound elementwise pass over
+// the rows [j0, j1) of every z plane (the pipelined advance runs it per y-row
+// chunk).  Fail kinds as in etd_contract: 1 non-finite, 4 domain violation.
+// Measured faster than evaluating f inside the z-transform prologue, where the
+// FP64 source math competes with DMMA for the shared FP64 pipe.
+struct SourceArgs {
+    double* buf;            // operand stack base, stride F
+    long long F, pitch, plane;
+    int nx, ny, nz, j0, j1;
+    int gj0, gz0;           // global (y, z) offsets of this buffer
+    int nspecies;
+    double sp[8];
+    const double* sinx;
+    const double* siny;
+    const double* sinz;
+    StepStatus* status;
+};
+
+template <int SK>
+__global__ void __launch_bounds__(256) etd_source(const SourceArgs a) {
+    __shared__ int stop;
+    if (threadIdx.x == 0) stop = *reinterpret_cast<volatile int*>(&a.status->fail);
+    __syncthreads();
+    if (stop) return;
+    const double srcA = SK == 4 ? exp(-a.sp[0] * a.status->t) : 0.0;
+    const int nj = a.j1 - a.j0;
+    const long long rows = (long long)a.nz * nj;
+    int bad = 0, dom = 0;
+    for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int kz = (int)(r / nj), j = a.j0 + (int)(r % nj);
+        const long long base = kz * a.plane + (long long)j * a.pitch;
+        for (int i = threadIdx.x; i < a.nx; i += blockDim.x) {
+            const long long o = base + i;
+            if (a.nspecies == 1) {
+                const double u = a.buf[o];
+                double ustar = 0.0;
+                if constexpr (SK == 4)
+                    ustar = srcA * (a.sinx[i] * a.siny[j + a.gj0] * (a.sinz ? a.sinz[kz + a.gz0] : 1.0));
+                double f = src1<SK>(a.sp, u, ustar);
+                if constexpr (SK == 3)
+                    if (i == 0 && j + a.gj0 == 0 && kz + a.gz0 == 0) f = __longlong_as_double(0x7ff8000000000000ll);
+                a.buf[a.F + o] = f;
+                bad |= !isfinite(f);
+                dom |= src_domain_violation<SK>(u);
+            } else {
+                double fu, fv;
+                src2<SK>(a.sp, a.buf[o], a.buf[a.F + o], fu, fv);
+                a.buf[2 * a.F + o] = fu;
+                a.buf[3 * a.F + o] = fv;
+                bad |= !(isfinite(fu) && isfinite(fv));
+            }
+        }
+    }
+    const int any_dom = __syncthreads_or(dom), any_bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0 && (any_dom || any_bad)) atomicCAS(&a.status->fail, 0, any_dom ? 4 : 1);
+}
+
+// Order-independent checksum of a buffer (debugging aid, ETD_DEBUG_CHECKSUM):
+// wrapping sum of the raw 64-bit patterns and of index-mixed patterns.
+__global__ void etd_checksum(const double* __restrict__ f, long long n, unsigned long long* out) {
+    unsigned long long a = 0, b = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long x = (unsigned long long)__double_as_longlong(f[i]);
+        a += x;
+        b += x * (2ull * (unsigned long long)i + 1ull);
+    }
+    atomicAdd(out, a);
+    atomicAdd(out + 1, b);
+}
+
+// Positions where two buffers differ bitwise (debugging aid).
+__global__ void etd_diff_positions(const double* a, const double* b, long long n, unsigned long long* count,
+                                   long long* pos, int cap) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        if (__double_as_longlong(a[i]) != __double_as_longlong(b[i])) {
+            const unsigned long long k = atomicAdd(count, 1ull);
+            if (k < (unsigned long long)cap) pos[k] = i;
+        }
 }
 
 // Finiteness scan of one padded field (snapshot save/load refuse non-finite

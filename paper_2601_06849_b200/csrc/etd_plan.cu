@@ -166,6 +166,22 @@ static KernelSpec pick(int mode, int S, int epi, bool pro, int sk = 0, int tile 
     throw ConfigError("no kernel variant for this stage / source kind");
 }
 
+static const void* pick_source(int sk) {
+    switch (sk) {
+    case 0: return reinterpret_cast<const void*>(etd_source<0>);
+    case 1: return reinterpret_cast<const void*>(etd_source<1>);
+    case 2: return reinterpret_cast<const void*>(etd_source<2>);
+    case 3: return reinterpret_cast<const void*>(etd_source<3>);
+    case 4: return reinterpret_cast<const void*>(etd_source<4>);
+    case 5: return reinterpret_cast<const void*>(etd_source<5>);
+    case 10: return reinterpret_cast<const void*>(etd_source<10>);
+    case 11: return reinterpret_cast<const void*>(etd_source<11>);
+    case 12: return reinterpret_cast<const void*>(etd_source<12>);
+    case 13: return reinterpret_cast<const void*>(etd_source<13>);
+    default: throw ConfigError("unknown source kind");
+    }
+}
+
 // ------------------------------------------------------------ NCCL (dlopen'd)
 // The extension does not link NCCL: single-GPU users and CPU tests never load
 // it.  Sharded plans resolve it at etd_create (torch's bundled libnccl.so.2
@@ -230,8 +246,11 @@ struct Piece {
 };
 
 struct Op {
-    enum Kind { KERNEL, COPY2D, EXCHANGE, FAILCODE, COMMIT } kind = KERNEL;
-    Launch L;                                    // KERNEL
+    enum Kind { KERNEL, SOURCE, COPY2D, EXCHANGE, FAILCODE, COMMIT } kind = KERNEL;
+    Launch L;                                    // KERNEL (and SOURCE: name/flops/bytes)
+    SourceArgs sargs{};                          // SOURCE
+    const void* src_fn = nullptr;
+    unsigned src_blocks = 0;
     void* dst = nullptr;                         // COPY2D
     const void* src = nullptr;
     size_t dpitch = 0, spitch = 0, width = 0, height = 0;
@@ -448,6 +467,38 @@ struct Plan {
         return a;
     }
 
+    // The per-step source pass f(t, U(,V)) into the f slots of the stack at `buf`.
+    Op source_op(const View& v, double* buf) const {
+        Op o;
+        o.kind = Op::SOURCE;
+        o.name = "source";
+        o.L.name = "source";
+        SourceArgs& a = o.sargs;
+        a.buf = buf;
+        a.F = v.F;
+        a.pitch = v.pitch;
+        a.plane = v.plane;
+        a.nx = v.nx;
+        a.ny = v.ny;
+        a.nz = v.nz;
+        a.j0 = 0;
+        a.j1 = v.ny;
+        a.gj0 = v.gj0;
+        a.gz0 = v.gz0;
+        a.nspecies = ns;
+        for (int i = 0; i < 8; ++i) a.sp[i] = d.src_params[i];
+        a.sinx = sintab[0];
+        a.siny = sintab[1];
+        a.sinz = dim == 3 ? sintab[2] : nullptr;
+        a.status = status;
+        o.src_fn = pick_source(d.src_kind);
+        o.src_blocks = (unsigned)std::min<long long>((long long)v.ny * v.nz, 148LL * 16);
+        const double pts = (double)v.nx * v.ny * v.nz;
+        o.L.flops = 0.0;
+        o.L.bytes = pts * 8.0 * 2 * ns;  // read U(,V), write fU(,fV)
+        return o;
+    }
+
     // A transform along `axis` of `S` stacked operands at `in` (L loaded), M = P^T (fwd) or P.
     Launch transform(const View& v, const std::string& name, int axis, bool back, int S, int epi, bool pro,
                      const double* in, double* out) const {
@@ -524,7 +575,10 @@ static void set_source(Plan& p, int kind, const double* params) {
     for (int i = 0; i < 8; ++i) p.d.src_params[i] = params ? params[i] : 0.0;
     for (int par = 0; par < 2; ++par)
         for (auto& op : p.steps[par])
-            if (op.kind == Op::KERNEL) {
+            if (op.kind == Op::SOURCE) {
+                for (int i = 0; i < 8; ++i) op.sargs.sp[i] = p.d.src_params[i];
+                op.src_fn = pick_source(kind);
+            } else if (op.kind == Op::KERNEL) {
                 op.L.args.src_kind = kind;
                 for (int i = 0; i < 8; ++i) op.L.args.sp[i] = p.d.src_params[i];
                 op.L.k = pick(op.L.mode, op.L.S, op.L.epi, op.L.pro, kind, op.L.tile);
@@ -624,13 +678,13 @@ static void build_plan(Plan& p, const etd_desc& d) {
         ETD_CK(cudaMemsetAsync(ptr, 0, elems * sizeof(double), p.stream));  // pads stay +0.0 forever
     };
     const size_t F = (size_t)p.slab.F;
-    for (int s = 0; s < 2; ++s) alloc(p.state[s], F * p.ns);
+    for (int s = 0; s < 2; ++s) alloc(p.state[s], F * 2 * p.ns);  // [U,(V),fU,(fV)]
     alloc(p.Z, F * 2 * p.ns);
     alloc(p.W, F * 2 * p.ns);
     if (p.sharded) {
         const size_t Fz = (size_t)p.zst.F;
         alloc(p.sendbuf, F * p.ns);
-        alloc(p.zin, Fz * p.ns);
+        alloc(p.zin, Fz * 2 * p.ns);
         alloc(p.Zz, Fz * 2 * p.ns);
         alloc(p.Wz, Fz * 2 * p.ns);
         alloc(p.recvb, F * 2 * p.ns);
@@ -734,6 +788,8 @@ static void build_plan(Plan& p, const etd_desc& d) {
 
     // ---- step schedule per state parity ----
     const int ns = p.ns;
+    const char* fenv = std::getenv("ETD_FUSED_SOURCE");
+    const bool fused = fenv && fenv[0] == '1';
     const View& V = p.slab;
     const View& VZ = p.zst;
     for (int par = 0; par < 2; ++par) {
@@ -741,9 +797,18 @@ static void build_plan(Plan& p, const etd_desc& d) {
         L.clear();
         const double* in = p.state[par];
         double* out = p.state[1 - par];
+        // The source f(t, U) either runs as its own HBM-bound pass into the f
+        // slots of the state stack (default; "source" + "z_fwd"/"y_fwd"), or fused
+        // into the first transform's prologue (ETD_FUSED_SOURCE=1, "z_fwd_src"):
+        // measured 265 vs 246 + 5.5 ms per config-4 step.
+        auto first_transform = [&](const View& vv, int axis, double* stack, double* dst) {
+            const char* nm = axis == 2 ? (fused ? "z_fwd_src" : "z_fwd") : (fused ? "y_fwd_src" : "y_fwd");
+            if (!fused) L.push_back(p.source_op(vv, stack));
+            L.push_back(kernel_op(p.transform(vv, nm, axis, false, 2 * ns, EPI_SCALE, fused, stack, dst)));
+            L.back().L.args.dA = p.dv(axis, 0);
+        };
         if (p.dim == 3 && !p.sharded) {
-            L.push_back(kernel_op(p.transform(V, "z_fwd_src", 2, false, 2 * ns, EPI_SCALE, true, in, p.Z)));
-            L.back().L.args.dA = p.dv(2, 0);
+            first_transform(V, 2, const_cast<double*>(in), p.Z);
             L.push_back(kernel_op(p.transform(V, "z_back", 2, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
         } else if (p.dim == 3) {
             // ---- z-stage on y-row partitions: pack, exchange, filter, exchange back, unpack ----
@@ -767,8 +832,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
             };
             add_phase(SP_PACK, "pack");
             add_phase(SP_FWD, "a2a_fwd");
-            L.push_back(kernel_op(p.transform(VZ, "z_fwd_src", 2, false, 2 * ns, EPI_SCALE, true, p.zin, p.Zz)));
-            L.back().L.args.dA = p.dv(2, 0);
+            first_transform(VZ, 2, p.zin, p.Zz);
             L.push_back(kernel_op(p.transform(VZ, "z_back", 2, true, 2 * ns, EPI_STORE, false, p.Zz, p.Wz)));
             add_phase(SP_BACK, "a2a_back");
             add_phase(SP_UNPACK, "unpack");
@@ -777,8 +841,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
             L.push_back(kernel_op(p.transform(V, "y_fwd", 1, false, 2 * ns, EPI_SCALE, false, p.W, p.Z)));
             L.back().L.args.dA = p.dv(1, 0);
         } else {
-            L.push_back(kernel_op(p.transform(V, "y_fwd_src", 1, false, 2 * ns, EPI_SCALE, true, in, p.Z)));
-            L.back().L.args.dA = p.dv(1, 0);
+            first_transform(V, 1, const_cast<double*>(in), p.Z);
         }
         L.push_back(kernel_op(p.transform(V, "y_back", 1, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
         L.push_back(kernel_op(p.transform(V, "x_fwd_mix", 0, false, 2 * ns, EPI_MIX, false, p.W, p.Z)));
@@ -812,7 +875,8 @@ static void build_plan(Plan& p, const etd_desc& d) {
     }
     p.stats.clear();
     for (auto& op : p.steps[0])
-        if (op.kind == Op::KERNEL) p.stats.push_back({op.L.name, 0, 0, op.L.flops, op.L.bytes});
+        if (op.kind == Op::KERNEL || op.kind == Op::SOURCE)
+            p.stats.push_back({op.L.name, 0, 0, op.L.flops, op.L.bytes});
     ETD_CK(cudaStreamSynchronize(p.stream));
 }
 
@@ -831,6 +895,11 @@ static void run_op(Plan& p, const Op& op, cudaStream_t s) {
         ETD_CK(cudaMemcpy2DAsync(op.dst, op.dpitch, op.src, op.spitch, op.width, op.height,
                                  cudaMemcpyDeviceToDevice, s));
         break;
+    case Op::SOURCE: {
+        void* args[1] = {const_cast<SourceArgs*>(&op.sargs)};
+        ETD_CK(cudaLaunchKernel(op.src_fn, dim3(op.src_blocks), dim3(256), args, 0, s));
+        break;
+    }
     case Op::FAILCODE: etd_fail_code<<<1, 1, 0, s>>>(p.status, p.codes + p.G); break;
     case Op::COMMIT: etd_commit<<<1, 1, 0, s>>>(p.status, p.codes, p.G, p.tau); break;
     case Op::EXCHANGE: {
@@ -898,7 +967,7 @@ static void do_steps(Plan& p, int nsteps) {
     copy_status_from_device(p);
     const long long n_before = p.status_host->n;
     reset_status(p, p.stream);
-    const bool eager = p.profiling || p.sharded;
+    const bool eager = p.profiling || p.sharded || std::getenv("ETD_DEBUG_CHECKSUM");
     if (eager) {
         // per-kernel device intervals: [event before op, event after op] for KERNEL ops
         std::vector<cudaEvent_t> ev;
@@ -911,13 +980,33 @@ static void do_steps(Plan& p, int nsteps) {
             return ev.size() - 1;
         };
         size_t prev = p.profiling ? rec() : 0;
+        const char* dbg = std::getenv("ETD_DEBUG_CHECKSUM");
+        unsigned long long* dsum = nullptr;
+        if (dbg) ETD_CK(cudaMalloc(&dsum, 16));
         for (int s = 0; s < nsteps; ++s) {
             size_t kidx = 0;
             for (const auto& op : p.steps[(p.cur + s) & 1]) {
                 run_op(p, op, p.stream);
+                if (dbg && (op.kind == Op::KERNEL || op.kind == Op::SOURCE)) {
+                    // checksum every output operand of this op (debugging aid)
+                    const double* base = op.kind == Op::SOURCE ? op.sargs.buf : op.L.args.out;
+                    const long long F = op.kind == Op::SOURCE ? op.sargs.F : op.L.args.out_stride;
+                    const int nout = op.kind == Op::SOURCE ? 2 * p.ns
+                                   : op.L.epi == EPI_WHAT_SRC ? 2 * op.L.S
+                                   : op.L.epi == EPI_MIX ? op.L.S : op.L.S;
+                    for (int o = 0; o < nout; ++o) {
+                        unsigned long long h[2];
+                        ETD_CK(cudaMemsetAsync(dsum, 0, 16, p.stream));
+                        etd_checksum<<<1184, 256, 0, p.stream>>>(base + (size_t)o * F, F, dsum);
+                        ETD_CK(cudaMemcpyAsync(h, dsum, 16, cudaMemcpyDeviceToHost, p.stream));
+                        ETD_CK(cudaStreamSynchronize(p.stream));
+                        std::fprintf(stderr, "ETD_CHECKSUM step %d op %s out %d %016llx %016llx\n", s, op.name.c_str(),
+                                     o, h[0], h[1]);
+                    }
+                }
                 if (!p.profiling) continue;
                 const size_t e = rec();
-                if (op.kind == Op::KERNEL) spans.push_back({prev, kidx++});
+                if (op.kind == Op::KERNEL || op.kind == Op::SOURCE) spans.push_back({prev, kidx++});
                 prev = e;
             }
         }
@@ -929,6 +1018,7 @@ static void do_steps(Plan& p, int nsteps) {
             p.stats[sp.second].launches += 1;
         }
         for (auto e : ev) cudaEventDestroy(e);
+        if (dsum) cudaFree(dsum);
     } else {
         ensure_graphs(p);
         for (int s = 0; s < nsteps; ++s) ETD_CK(cudaGraphLaunch(p.graph[(p.cur + s) & 1], p.stream));
@@ -1017,14 +1107,21 @@ static void group_steps(std::vector<Plan*>& ps, int nsteps) {
 // 3D, unsharded plans; everything else takes set_state / etd_step / get_state.
 static constexpr int kXferChunks = 8;
 
+// index of the first y-stage op: ops [0, iy) are the z stage (source pass,
+// z_fwd(_src), z_back), ops [iy, end) the y and x stages
+static int y_stage_index(const Plan& p) {
+    const auto& ops = p.steps[0];
+    for (size_t k = 0; k < ops.size(); ++k)
+        if (ops[k].kind == Op::KERNEL && ops[k].L.name == "y_fwd") return (int)k;
+    return -1;
+}
+
 static bool overlap_eligible(const Plan& p, int nsteps) {
     if (p.dim != 3 || p.sharded || p.profiling || nsteps < 1) return false;
     const auto& ops = p.steps[0];
-    if (ops.size() != 8) return false;
     for (const auto& op : ops)
-        if (op.kind != Op::KERNEL) return false;
-    return ops[0].L.name == "z_fwd_src" && ops[1].L.name == "z_back" && ops[2].L.name == "y_fwd" &&
-           ops.back().L.name == "x_back_upd";
+        if (op.kind != Op::KERNEL && op.kind != Op::SOURCE) return false;
+    return y_stage_index(p) > 0 && ops.back().L.name == "x_back_upd";
 }
 
 static void advance_overlapped(Plan& p, const double* const* hin, double* const* hout, long n, double t,
@@ -1068,6 +1165,7 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
         }
         ETD_CK(cudaEventRecord(ev_in[c], p.cstream));
     }
+    const int iy = y_stage_index(p);
     for (int s = 0; s < nsteps; ++s) {
         const auto& ops = p.steps[(p.cur + s) & 1];
         const bool first = s == 0, last = s == nsteps - 1;
@@ -1075,25 +1173,33 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
         if (first) {
             for (int c = 0; c < C; ++c) {
                 ETD_CK(cudaStreamWaitEvent(p.stream, ev_in[c], 0));
-                for (int k = 0; k < 2; ++k) {
-                    Launch L = ops[k].L;
-                    L.args.outer0 = jlo(c);
-                    L.grid.z = jlo(c + 1) - jlo(c);
-                    if (L.grid.z) launch(L, p.stream);
+                const int j0 = jlo(c), j1 = jlo(c + 1);
+                if (j1 == j0) continue;
+                for (int k = 0; k < iy; ++k) {
+                    if (ops[k].kind == Op::SOURCE) {
+                        Op o = ops[k];
+                        o.sargs.j0 = j0;
+                        o.sargs.j1 = j1;
+                        run_op(p, o, p.stream);
+                    } else {
+                        Launch L = ops[k].L;
+                        L.args.outer0 = j0;
+                        L.grid.z = j1 - j0;
+                        launch(L, p.stream);
+                    }
                 }
             }
         } else {
-            run_op(p, ops[0], p.stream);
-            run_op(p, ops[1], p.stream);
+            for (int k = 0; k < iy; ++k) run_op(p, ops[k], p.stream);
         }
         // y and x stages
         if (!last) {
-            for (size_t k = 2; k < ops.size(); ++k) run_op(p, ops[k], p.stream);
+            for (size_t k = iy; k < ops.size(); ++k) run_op(p, ops[k], p.stream);
             continue;
         }
         const Op& upd = ops.back();
         for (int c = 0; c < C; ++c) {
-            for (size_t k = 2; k < ops.size(); ++k) {
+            for (size_t k = iy; k < ops.size(); ++k) {
                 Launch L = ops[k].L;
                 if (L.mode == 1) {  // y stage: outer index is z
                     L.args.outer0 = zlo(c);
@@ -1271,6 +1377,8 @@ static void debug_transform(Plan& p, int species, int axis, int back, int ell, i
 }  // namespace etd
 
 // =================================================================== C-ABI
+using etd::CudaError;  // for ETD_CK in the C-ABI shims
+
 struct etd_handle {
     std::unique_ptr<etd::Plan> plan;
     std::string msg;
@@ -1485,6 +1593,48 @@ int etd_stage_info(const etd_handle* h, int i, char* name, size_t len, double* m
     if (flops) *flops = s.flops;
     if (bytes) *bytes = s.bytes;
     return ETD_OK;
+}
+
+// Debugging aid: re-run step op `name` (parity 0 schedule) `reps` times on its
+// current inputs and report bitwise differences of output `out` against the
+// first re-run (a deterministic kernel reports none).
+int etd_debug_repeat_op(etd_handle* h, const char* name, int out, int reps, long long* mismatches, long long* pos,
+                        int cap) {
+    if (!h || !name || !mismatches) return ETD_ERR_CONFIG;
+    return guarded(h, [&] {
+        auto& p = *h->plan;
+        const etd::Op* op = nullptr;
+        for (const auto& o : p.steps[p.cur & 1])
+            if ((o.kind == etd::Op::KERNEL || o.kind == etd::Op::SOURCE) && o.name == name) op = &o;
+        if (!op || op->kind != etd::Op::KERNEL) throw etd::ConfigError("no such kernel op");
+        const long long F = op->L.args.out_stride;
+        const double* target = op->L.args.out + (size_t)out * F;
+        double* ref = nullptr;
+        unsigned long long* cnt = nullptr;
+        long long* dpos = nullptr;
+        ETD_CK(cudaMalloc(&ref, F * 8));
+        ETD_CK(cudaMalloc(&cnt, 8));
+        ETD_CK(cudaMalloc(&dpos, 8 * std::max(1, cap)));
+        etd::run_op(p, *op, p.stream);
+        ETD_CK(cudaMemcpyAsync(ref, target, F * 8, cudaMemcpyDeviceToDevice, p.stream));
+        *mismatches = 0;
+        for (int r = 0; r < reps; ++r) {
+            etd::run_op(p, *op, p.stream);
+            ETD_CK(cudaMemsetAsync(cnt, 0, 8, p.stream));
+            etd::etd_diff_positions<<<1184, 256, 0, p.stream>>>(ref, target, F, cnt, dpos, cap);
+            unsigned long long c = 0;
+            ETD_CK(cudaMemcpyAsync(&c, cnt, 8, cudaMemcpyDeviceToHost, p.stream));
+            ETD_CK(cudaStreamSynchronize(p.stream));
+            if ((long long)c > *mismatches) {
+                *mismatches = (long long)c;
+                if (pos && cap > 0)
+                    ETD_CK(cudaMemcpy(pos, dpos, 8 * std::min<long long>(cap, c), cudaMemcpyDeviceToHost));
+            }
+        }
+        cudaFree(ref);
+        cudaFree(cnt);
+        cudaFree(dpos);
+    });
 }
 
 int etd_debug_transform(etd_handle* h, int species, int axis, int back, int ell, int apply_q, const double* in,
