@@ -10,6 +10,6 @@ from .etd import (BackendKind, ConfigError, DeviceError, DeviceSource, Grid, Mem
                   advance, allen_cahn_cubic, allen_cahn_manufactured, singular, build_grid, etd2rkds_step_system, fhn_classic, fhn_cubic,
                   fill_config_ic, lib, make_plan, make_system_plan, poly3, setup_axis, setup_dvector,
                   setup_scheme, unit_box_grid, zslab_partition, nccl_unique_id, group_step)
-from . import configs
+from . import configs, harness
 
 __all__ = [n for n in dir() if not n.startswith("_")]

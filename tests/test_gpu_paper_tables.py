@@ -11,30 +11,16 @@ import numpy as np
 import pytest
 
 import paper_2601_06849_b200 as etd
+from paper_2601_06849_b200 import harness
 
 pytestmark = pytest.mark.gpu
 
 
-def sine_product(n, dim):
-    s = np.sin(np.pi * (np.arange(1, n + 1) / (n + 1)))
-    if dim == 2:
-        return (s[None, :] * s[:, None]).ravel()          # index j*n + i -> s_i s_j
-    return (s[:, None, None] * s[None, :, None] * s[None, None, :]).ravel()
-
-
 def error_E(dim, n, N, family, coarse):
-    g = etd.unit_box_grid(dim, n + 1)
-    src = etd.allen_cahn_manufactured(dim, 1.0, 1.0)
-    plan = etd.make_plan(g, 1.0 / N, 1.0, 0.0, scheme=family, source=src)
-    S = sine_product(n, dim)
-    plan.upload(0, S, 0, 0.0)
-    E = 0.0
-    for _ in range(coarse):
-        plan.step(N // coarse)
-        u, nn, t = plan.download(0)
-        E = max(E, float(np.max(np.abs(u - math.exp(-t) * S))))
-    plan.close()
-    return E
+    """E(N) through the device harness (harness.cpp:305-362 semantics)."""
+    spec = harness.allen_cahn(dim)
+    rows = harness.run_convergence(spec, n + 1, [N], scheme=family, coarse=coarse)
+    return rows[0].E
 
 
 def eoc(E):
@@ -64,3 +50,14 @@ def test_table2_3d_p02_gate3():
     golden = [2.96e-1, 1.04e-1, 3.01e-2, 8.05e-3, 2.14e-3]
     for e, g in zip(E, golden):
         assert abs(e - g) / g <= 0.10, (E, golden)
+
+
+def test_run_convergence_eoc_and_guards():
+    """run_convergence reports EOC under step halving and rejects N not a multiple
+    of the coarse count (harness.cpp:307-312)."""
+    spec = harness.allen_cahn(2)
+    rows = harness.run_convergence(spec, 64, [32, 64, 128], coarse=16)
+    assert rows[0].eoc is None and all(r.eoc is not None for r in rows[1:])
+    assert all(1.5 < r.eoc < 2.5 for r in rows[1:])
+    with pytest.raises(etd.ConfigError):
+        harness.run_convergence(spec, 64, [24], coarse=16)
