@@ -227,7 +227,7 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
         t = torch.tensor([p[0] for p in per], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         per = [(float(a), s) for a, (_, s) in zip(t.tolist(), per)]
-    dom_ms, dom = max(per, key=lambda x: x[0])
+    dom_ms, dom = max((x for x in per if x[1]["flops_per_launch"] > 0), key=lambda x: x[0])
     achieved = dom["flops_per_launch"] / (dom_ms * 1e-3) * 1e-12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -237,20 +237,29 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
             traffic = tr.get(dom["name"])
         except (OSError, ValueError):
             traffic = None
-    transform_ms = sum(p[0] for p in per)
-    transform_flops = sum(s["flops_per_launch"] for _, s in per)
-    comm_ms = ms - transform_ms  # exchange + pack/unpack + commit (sharded), launch gaps
+    transform_ms = sum(a for a, st in per if st["flops_per_launch"] > 0)
+    transform_flops = sum(st["flops_per_launch"] for _, st in per)
+    comm_ms = ms - sum(a for a, _ in per)  # exchange + pack/unpack + commit (sharded), launch gaps
+
+    def stage_line(a, st):
+        if st["flops_per_launch"] > 0:
+            return {"name": st["name"], "ms": round(a, 3), "bound": "tensor",
+                    "tflops": round(st["flops_per_launch"] / (a * 1e-3) * 1e-12, 2),
+                    "frac": round(st["flops_per_launch"] / (a * 1e-3) * 1e-12 / FP64_PEAK_TFLOPS, 4)}
+        gbs = st["bytes_per_launch"] / (a * 1e-3) * 1e-9
+        return {"name": st["name"], "ms": round(a, 3), "bound": "hbm", "gbs": round(gbs, 1),
+                "frac": round(gbs / 6552.0, 4)}
+
     roofline = {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic, "kernel": dom["name"],
                 "peak_source": FP64_PEAK_NOTE,
                 "algorithmic_flops_per_launch": dom["flops_per_launch"],
                 "all_transforms": {"tflops": round(transform_flops / (transform_ms * 1e-3) * 1e-12, 3),
                                    "frac": round(transform_flops / (transform_ms * 1e-3) * 1e-12 / FP64_PEAK_TFLOPS, 4),
-                                   "hbm_gbs": round(sum(s["bytes_per_launch"] for _, s in per) / (transform_ms * 1e-3) * 1e-9, 1),
-                                   "hbm_peak_gbs": 6552.0},
-                "stages": [{"name": s["name"], "ms": round(a, 3),
-                            "tflops": round(s["flops_per_launch"] / (a * 1e-3) * 1e-12, 2)} for a, s in per],
-                "non_transform_ms_per_step": round(comm_ms, 3)}
+                                   "ms_per_step": round(transform_ms, 3)},
+                "stages": [stage_line(a, st) for a, st in per],
+                "non_kernel_ms_per_step": round(comm_ms, 3),
+                "hbm_peak_gbs": 6552.0}
 
     # ---- e2e through the public API: pinned host in -> step -> pinned host out ----
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
