@@ -1105,7 +1105,7 @@ static void group_steps(std::vector<Plan*>& ps, int nsteps) {
 //    only reads rows whose y stage has finished and never rows of a later chunk.
 //  * the step commit moves to one etd_commit after the chunks.
 // 3D, unsharded plans; everything else takes set_state / etd_step / get_state.
-static constexpr int kXferChunks = 8;
+static constexpr int kXferChunks = 16;
 
 // index of the first y-stage op: ops [0, iy) are the z stage (source pass,
 // z_fwd(_src), z_back), ops [iy, end) the y and x stages
