@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define ETD_B200_ABI_VERSION 1
+#define ETD_B200_ABI_VERSION 2
 
 /* Status codes (0 = OK).  errors.hpp:8-30; CLI mapping cli.cpp:204-217. */
 enum etd_status {
@@ -40,6 +40,13 @@ enum etd_status {
  * e^{-tau A}, phi_1, phi_2 multipliers on the same transforms), without its
  * 64-points-per-axis cap. */
 enum etd_family { ETD_P02 = 0, ETD_P04 = 1, ETD_EXACT = 2 };
+
+/* Directional rational applies: tensor_ops.hpp:31 BackendKind.  ETD_SPECTRAL is
+ * the eigenbasis-transform step (BackendKind::Spectral, DMMA tensor cores);
+ * ETD_THOMAS the per-pole complex tridiagonal solves (BackendKind::Thomas,
+ * thomas.cpp:14-160) with the same step structure (stepper.cpp:231-240,
+ * 243-266, system_stepper.cpp:74-114).  Thomas plans run on one GPU. */
+enum etd_backend { ETD_SPECTRAL = 0, ETD_THOMAS = 1 };
 
 /* Device source descriptors.  The reference takes a std::function
  * (SourceFunction / SystemSource, stepper.hpp:18-29) which cannot run on the
@@ -77,14 +84,8 @@ typedef struct etd_desc {
     /* z-slab sharding (3D): rank `rank` of `world_size` owns planes
      * [etd_slab_range) ; world_size==1 -> whole grid on one GPU. */
     int world_size, rank;
-    const void* nccl_unique_id; /* The data movement of one sharded step for rank `rank` (host only): records of
- * 12 int64 {kind(0 copy2d,1 send,2 recv), phase(0 pack,1 fwd,2 back,3 unpack),
- * peer, dst_buf, dst_off, dst_pitch, src_buf, src_off, src_pitch, width, height,
- * count}, element units; buffers 0 state,1 send,2 zin,3 wz,4 recv,5 w.
- * out may be NULL to query *count. */
-int etd_sharded_schedule(int nx, int ny, int nz, int nspecies, int world_size, int rank, long long pitch,
-                         long long* out, int capacity, int* count);
-/* 128-byte ncclUniqueId (world_size > 1)            */
+    const void* nccl_unique_id; /* 128-byte ncclUniqueId (world_size > 1)          */
+    int backend;             /* etd_backend (0 = spectral transforms)               */
 } etd_desc;
 
 typedef struct etd_handle etd_handle;

@@ -135,7 +135,7 @@ private:
 
 // ---------------------------------------------------------------- rational / backend
 enum class PadeFamily { P02 = ETD_P02, P04 = ETD_P04 };
-enum class BackendKind { Spectral, Thomas, NonSplitBanded, ExactExpReference, CudaSpectral = 100 };
+enum class BackendKind { Spectral, Thomas, NonSplitBanded, ExactExpReference, CudaSpectral = 100, CudaThomas = 101 };
 
 // Device stand-in for SourceFunction / SystemSource (stepper.hpp:18-29).
 struct DeviceSource {
@@ -204,7 +204,14 @@ inline etd_desc make_desc(const Grid& g, double tau, PadeFamily fam, int ns, dou
     d.world_size = 1;
     d.rank = 0;
     d.nccl_unique_id = nullptr;
+    d.backend = ETD_SPECTRAL;
     return d;
+}
+// Spectral / CudaSpectral -> transforms, Thomas / CudaThomas -> tridiagonal solves
+inline int device_backend(BackendKind b) {
+    if (b == BackendKind::Spectral || b == BackendKind::CudaSpectral) return ETD_SPECTRAL;
+    if (b == BackendKind::Thomas || b == BackendKind::CudaThomas) return ETD_THOMAS;
+    throw ConfigError("etdrd_b200 implements the Spectral and Thomas backends");
 }
 inline void set_source(etd_handle* h, const DeviceSource& s) {
     check(etd_set_source(h, s.kind, s.params.data()), h);
@@ -225,20 +232,22 @@ struct StepperState {
     Field U;
 };
 
-// stepper.hpp:59-61.  Only BackendKind::CudaSpectral is served by this backend.
+// stepper.hpp:59-61.  Spectral and Thomas backends on the device.
 inline StepperPlan make_plan(const Grid& grid, double tau, double kappa, double q, PadeFamily scheme,
                              BackendKind backend = BackendKind::CudaSpectral, std::size_t memory_cap_bytes = 0,
                              int device = 0) {
     (void)memory_cap_bytes;
-    if (backend != BackendKind::CudaSpectral) throw ConfigError("etdrd_b200 implements BackendKind::CudaSpectral");
+    const int bk = detail::device_backend(backend);
     StepperPlan p;
+    p.backend = backend;
     p.grid = grid;
     p.tau = tau;
     p.kappa = kappa;
     p.q = q;
     p.scheme = scheme;
-    p.handle = PlanHandle(detail::make_desc(grid, tau, scheme, 1, kappa, 0.0, q, DeviceSource::allen_cahn_cubic(),
-                                            device));
+    etd_desc d = detail::make_desc(grid, tau, scheme, 1, kappa, 0.0, q, DeviceSource::allen_cahn_cubic(), device);
+    d.backend = bk;
+    p.handle = PlanHandle(d);
     return p;
 }
 
@@ -274,16 +283,18 @@ struct SystemState {
 inline SystemPlan make_system_plan(const Grid& grid, double tau, double kappa_u, double kappa_v, double q,
                                    PadeFamily scheme, BackendKind backend = BackendKind::CudaSpectral,
                                    int device = 0) {
-    if (backend != BackendKind::CudaSpectral) throw ConfigError("etdrd_b200 implements BackendKind::CudaSpectral");
+    const int bk = detail::device_backend(backend);
     SystemPlan p;
+    p.backend = backend;
     p.grid = grid;
     p.tau = tau;
     p.kappa_u = kappa_u;
     p.kappa_v = kappa_v;
     p.q = q;
     p.scheme = scheme;
-    p.handle = PlanHandle(detail::make_desc(grid, tau, scheme, 2, kappa_u, kappa_v, q, DeviceSource::fhn_cubic(),
-                                            device));
+    etd_desc d = detail::make_desc(grid, tau, scheme, 2, kappa_u, kappa_v, q, DeviceSource::fhn_cubic(), device);
+    d.backend = bk;
+    p.handle = PlanHandle(d);
     return p;
 }
 

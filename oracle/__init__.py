@@ -76,7 +76,7 @@ class Ref:
             i, d, l = C.c_int, C.c_double, C.c_long
             L.ref_scalar_run.argtypes = [i, i, d, d, d, i, i, i, _dp, _dp, C.POINTER(l), C.POINTER(d), i,
                                          C.POINTER(d), C.c_char_p, i, C.POINTER(d), C.POINTER(l)]
-            L.ref_system_run.argtypes = [i, i, d, d, d, d, i, i, _dp, _dp, _dp, C.POINTER(l), C.POINTER(d), i, i,
+            L.ref_system_run.argtypes = [i, i, d, d, d, d, i, i, i, _dp, _dp, _dp, C.POINTER(l), C.POINTER(d), i, i,
                                          C.POINTER(d), C.c_char_p, i, C.POINTER(d), C.POINTER(l)]
             L.ref_spectral_factor.argtypes = [i, d, d, _dp, _dp]
             L.ref_operator.argtypes = [i, i, i, d, d, C.POINTER(d), C.POINTER(d), C.c_char_p, i]
@@ -84,6 +84,7 @@ class Ref:
             L.ref_scheme.argtypes = [i, _dp, C.POINTER(i)]
             L.ref_contract_axis.argtypes = [i, i, i, i, _dp, i, _dp, i, i, _dp, C.c_char_p, i]
             L.ref_apply_q.argtypes = [i, i, d, d, d, i, i, i, _dp, _dp, C.c_char_p, i]
+            L.ref_apply_q_thomas.argtypes = [i, i, d, d, d, i, i, i, _dp, _dp, C.c_char_p, i]
             L.ref_sample_step.argtypes = [i, i, i, d, d, d, d, i, i, _dp, C.POINTER(d), C.POINTER(d), _dp,
                                           C.c_char_p, i]
             L.ref_save_field.argtypes = [i, i, i, i, _dp, d, C.c_char_p, C.c_char_p, i]
@@ -122,9 +123,10 @@ class Ref:
 
     @classmethod
     def system_run(cls, dim, n, tau, ku, kv, q, u, v, nsteps, src_kind=10, src_params=(0.1, 0.01, 0.5),
-                   family=0, n0=0, t0=0.0, composed=False, lean=False, inplace=False):
+                   family=0, n0=0, t0=0.0, composed=False, lean=False, inplace=False, backend=0):
         """lean: memory-lean composition (same reference calls, explicit lifetimes);
-        inplace: update the given float64 arrays instead of copying them."""
+        inplace: update the given float64 arrays instead of copying them;
+        backend: BackendKind (0 Spectral, 1 Thomas)."""
         if not inplace:
             u = np.ascontiguousarray(u, dtype=np.float64).copy()
             v = np.ascontiguousarray(v, dtype=np.float64).copy()
@@ -132,7 +134,7 @@ class Ref:
             composed = 2
         nn, tt, sec, tab, sab = C.c_long(n0), C.c_double(t0), C.c_double(0), C.c_double(0), C.c_long(0)
         err = C.create_string_buffer(512)
-        rc = cls.lib().ref_system_run(dim, n, tau, ku, kv, q, family, src_kind, _params(src_params), u, v,
+        rc = cls.lib().ref_system_run(dim, n, tau, ku, kv, q, family, backend, src_kind, _params(src_params), u, v,
                                       C.byref(nn), C.byref(tt), nsteps, int(composed), C.byref(sec), err, 512,
                                       C.byref(tab), C.byref(sab))
         _check(rc, err.value, tab.value, sab.value)
@@ -217,6 +219,16 @@ class Ref:
         err = C.create_string_buffer(256)
         rc = cls.lib().ref_apply_q(dim, n, tau, kappa, q, family, ell, axis,
                                    np.ascontiguousarray(x, dtype=np.float64), out, err, 256)
+        _check(rc, err.value, 0, 0)
+        return out
+
+    @classmethod
+    def apply_q_thomas(cls, dim, n, tau, kappa, q, family, ell, axis, x):
+        """apply_Q_thomas (thomas.cpp:128-160)."""
+        out = np.zeros(n ** dim)
+        err = C.create_string_buffer(256)
+        rc = cls.lib().ref_apply_q_thomas(dim, n, tau, kappa, q, family, ell, axis,
+                                          np.ascontiguousarray(x, dtype=np.float64), out, err, 256)
         _check(rc, err.value, 0, 0)
         return out
 

@@ -131,15 +131,29 @@ struct SysPlan3 {
     double tau;
     std::array<std::shared_ptr<const SpectralFactor>, 3> fac;
     std::array<SpectralAxisPayload, 3> pu, pv;
+    bool thomas = false;  // BackendKind::Thomas payloads (system_stepper.cpp:62-64)
+    std::array<ThomasAxisPayload, 3> tu, tv;
+
+    Field Q(int c, int ell, const Field& g, Axis ax) const {
+        const int a = axis_index(ax);
+        if (thomas) return apply_Q_thomas(c == 0 ? tu[a] : tv[a], ell, tau, g, ax);
+        return apply_Q_spectral(c == 0 ? pu[a] : pv[a], ell, tau, g, ax);
+    }
 };
 
 SysPlan3 make_sys3(const Grid& g, double tau, double ku, double kv, double q,
-                   const RationalScheme& scheme) {
+                   const RationalScheme& scheme, BackendKind backend = BackendKind::Spectral) {
     SysPlan3 sp;
     sp.grid = g;
     sp.tau = tau;
+    sp.thomas = backend == BackendKind::Thomas;
     for (int a = 0; a < g.dim; ++a) {
         auto op = build_operator(g, static_cast<Axis>(a), 1.0, q);
+        if (sp.thomas) {
+            sp.tu[a] = build_thomas_payload(op, tau, scheme, ku);
+            sp.tv[a] = build_thomas_payload(op, tau, scheme, kv);
+            continue;
+        }
         sp.fac[a] = std::make_shared<const SpectralFactor>(spectral_factor(op));
         const auto& lam = sp.fac[a]->eigvals;
         std::vector<double> lu(lam.size()), lv(lam.size());
@@ -156,10 +170,7 @@ SysPlan3 make_sys3(const Grid& g, double tau, double ku, double kv, double q,
 // system_stepper.cpp:74-114 with the 3D z->y stage-input filter of stepper.cpp:244-247
 SystemState sys3_step(const SysPlan3& sp, const SystemState& st, const SystemSource& f) {
     const double t = st.t, tau = sp.tau;
-    auto Q = [&](int c, int ell, const Field& g, Axis ax) {
-        const auto& p = c == 0 ? sp.pu[axis_index(ax)] : sp.pv[axis_index(ax)];
-        return apply_Q_spectral(p, ell, tau, g, ax);
-    };
+    auto Q = [&](int c, int ell, const Field& g, Axis ax) { return sp.Q(c, ell, g, ax); };
     auto chk = [&](const Field& a, const Field& b, const char* what, double tt) {
         if (!a.all_finite() || !b.all_finite())
             throw StepperAbort(std::string(what) + " produced non-finite values", tt, st.n);
@@ -197,10 +208,7 @@ SystemState sys3_step(const SysPlan3& sp, const SystemState& st, const SystemSou
 // reference step would no longer read them.
 SystemState sys3_step_lean(const SysPlan3& sp, SystemState st, const SystemSource& f) {
     const double t = st.t, tau = sp.tau;
-    auto Q = [&](int c, int ell, const Field& g, Axis ax) {
-        const auto& p = c == 0 ? sp.pu[axis_index(ax)] : sp.pv[axis_index(ax)];
-        return apply_Q_spectral(p, ell, tau, g, ax);
-    };
+    auto Q = [&](int c, int ell, const Field& g, Axis ax) { return sp.Q(c, ell, g, ax); };
     auto chk = [&](const Field& a, const Field& b, const char* what, double tt) {
         if (!a.all_finite() || !b.all_finite())
             throw StepperAbort(std::string(what) + " produced non-finite values", tt, st.n);
@@ -287,7 +295,7 @@ int ref_scalar_run(int dim, int n, double tau, double kappa, double q, int famil
 // Two-species run.  dim==2 uses the reference make_system_plan/etd2rkds_step_system
 // unchanged; dim==3 uses the composition above (use_composed=1 forces it in 2D too).
 int ref_system_run(int dim, int n, double tau, double ku, double kv, double q, int family,
-                   int src_kind, const double* src_params, double* u, double* v, long* n_io,
+                   int backend, int src_kind, const double* src_params, double* u, double* v, long* n_io,
                    double* t_io, int nsteps, int use_composed, double* seconds, char* err,
                    int errlen, double* t_abort, long* step_abort) {
     try {
@@ -296,20 +304,21 @@ int ref_system_run(int dim, int n, double tau, double ku, double kv, double q, i
         const auto src = make_system_source(src_kind, src_params);
         SystemState st{*n_io, *t_io, field_from(g, u), field_from(g, v)};
         std::chrono::steady_clock::time_point t0, t1;
+        const auto bk = static_cast<BackendKind>(backend);
         if (dim == 2 && !use_composed) {
-            const auto plan = make_system_plan(g, tau, ku, kv, q, scheme, BackendKind::Spectral);
+            const auto plan = make_system_plan(g, tau, ku, kv, q, scheme, bk);
             t0 = std::chrono::steady_clock::now();
             for (int s = 0; s < nsteps; ++s) st = etd2rkds_step_system(plan, st, src);
             t1 = std::chrono::steady_clock::now();
         } else {
             if (dim == 2) {
                 // 2D composed variant: identical to etd2rkds_step_system without the z filter
-                const auto plan = make_system_plan(g, tau, ku, kv, q, scheme, BackendKind::Spectral);
+                const auto plan = make_system_plan(g, tau, ku, kv, q, scheme, bk);
                 t0 = std::chrono::steady_clock::now();
                 for (int s = 0; s < nsteps; ++s) st = etd2rkds_step_system(plan, st, src);
                 t1 = std::chrono::steady_clock::now();
             } else {
-                const auto sp = make_sys3(g, tau, ku, kv, q, scheme);
+                const auto sp = make_sys3(g, tau, ku, kv, q, scheme, bk);
                 t0 = std::chrono::steady_clock::now();
                 if (use_composed == 2)
                     for (int s = 0; s < nsteps; ++s) st = sys3_step_lean(sp, std::move(st), src);
@@ -504,6 +513,21 @@ int ref_apply_q(int dim, int n, double tau, double kappa, double q, int family, 
         const auto pay = build_spectral_payload(
             fac, tau, scheme_by_family(family ? PadeFamily::P04 : PadeFamily::P02));
         const Field r = apply_Q_spectral(pay, ell, tau, field_from(g, in), static_cast<Axis>(axis));
+        std::memcpy(out, r.data(), r.size() * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        return map_exc(e, err, errlen, nullptr, nullptr);
+    }
+}
+
+// apply_Q_thomas (thomas.cpp:128-160) of one field along `axis`.
+int ref_apply_q_thomas(int dim, int n, double tau, double kappa, double q, int family, int ell,
+                       int axis, const double* in, double* out, char* err, int errlen) {
+    try {
+        const Grid g = unit_box_grid(dim, n + 1);
+        const auto op = build_operator(g, static_cast<Axis>(axis), kappa, q);
+        const auto pay = build_thomas_payload(op, tau, scheme_by_family(family ? PadeFamily::P04 : PadeFamily::P02));
+        const Field r = apply_Q_thomas(pay, ell, tau, field_from(g, in), static_cast<Axis>(axis));
         std::memcpy(out, r.data(), r.size() * sizeof(double));
         return 0;
     } catch (const std::exception& e) {

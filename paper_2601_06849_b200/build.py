@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libetd_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["etd_setup.cpp", "etd_plan.cu"]
-HEADERS = ["etd_setup.hpp", "etd_kernels.cuh"]
+HEADERS = ["etd_setup.hpp", "etd_kernels.cuh", "etd_thomas.cuh"]
 
 
 def _nvcc() -> str:

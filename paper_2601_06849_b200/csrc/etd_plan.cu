@@ -33,6 +33,7 @@
 
 #include "../../include/etd_b200.h"
 #include "etd_kernels.cuh"
+#include "etd_thomas.cuh"
 #include "etd_setup.hpp"
 
 namespace etd {
@@ -182,6 +183,36 @@ static const void* pick_source(int sk) {
     }
 }
 
+template <int EPI, int NS>
+static const void* thomas_fn(int sk) {
+    if constexpr (EPI != TH_WHAT) {
+        return reinterpret_cast<const void*>(etd_thomas<EPI, NS, 0>);
+    } else if constexpr (NS == 1) {
+        switch (sk) {
+        case 0: return reinterpret_cast<const void*>(etd_thomas<EPI, 1, 0>);
+        case 1: return reinterpret_cast<const void*>(etd_thomas<EPI, 1, 1>);
+        case 2: return reinterpret_cast<const void*>(etd_thomas<EPI, 1, 2>);
+        case 3: return reinterpret_cast<const void*>(etd_thomas<EPI, 1, 3>);
+        case 4: return reinterpret_cast<const void*>(etd_thomas<EPI, 1, 4>);
+        case 5: return reinterpret_cast<const void*>(etd_thomas<EPI, 1, 5>);
+        }
+    } else {
+        switch (sk) {
+        case 0: return reinterpret_cast<const void*>(etd_thomas<EPI, 2, 0>);
+        case 10: return reinterpret_cast<const void*>(etd_thomas<EPI, 2, 10>);
+        case 11: return reinterpret_cast<const void*>(etd_thomas<EPI, 2, 11>);
+        case 12: return reinterpret_cast<const void*>(etd_thomas<EPI, 2, 12>);
+        case 13: return reinterpret_cast<const void*>(etd_thomas<EPI, 2, 13>);
+        }
+    }
+    throw ConfigError("unknown source kind");
+}
+static const void* pick_thomas(int epi, int ns, int sk) {
+    if (epi == TH_STORE) return ns == 1 ? thomas_fn<TH_STORE, 1>(sk) : thomas_fn<TH_STORE, 2>(sk);
+    if (epi == TH_WHAT) return ns == 1 ? thomas_fn<TH_WHAT, 1>(sk) : thomas_fn<TH_WHAT, 2>(sk);
+    return ns == 1 ? thomas_fn<TH_UPDATE, 1>(sk) : thomas_fn<TH_UPDATE, 2>(sk);
+}
+
 // ------------------------------------------------------------ NCCL (dlopen'd)
 // The extension does not link NCCL: single-GPU users and CPU tests never load
 // it.  Sharded plans resolve it at etd_create (torch's bundled libnccl.so.2
@@ -246,10 +277,12 @@ struct Piece {
 };
 
 struct Op {
-    enum Kind { KERNEL, SOURCE, COPY2D, EXCHANGE, FAILCODE, COMMIT } kind = KERNEL;
-    Launch L;                                    // KERNEL (and SOURCE: name/flops/bytes)
+    enum Kind { KERNEL, SOURCE, COPY2D, EXCHANGE, FAILCODE, COMMIT, THOMAS } kind = KERNEL;
+    Launch L;                                    // KERNEL (and SOURCE/THOMAS: name/flops/bytes)
     SourceArgs sargs{};                          // SOURCE
-    const void* src_fn = nullptr;
+    ThomasArgs targs{};                          // THOMAS
+    int th_epi = 0;
+    const void* src_fn = nullptr;                // SOURCE / THOMAS kernel
     unsigned src_blocks = 0;
     void* dst = nullptr;                         // COPY2D
     const void* src = nullptr;
@@ -384,6 +417,14 @@ struct Plan {
     void* comm = nullptr;            // ncclComm_t
     cudaStream_t cstream = nullptr;  // host<->device copy stream of the pipelined advance
     std::vector<cudaEvent_t> xev;    // its chunk events
+    // BackendKind::Thomas: per-axis factors [species][pole][mul, piv, 1/piv][n],
+    // per-axis launch templates, forward-sweep scratch and pole partial sums
+    bool thomas = false;
+    double2* thfac[3] = {nullptr, nullptr, nullptr};
+    ThomasArgs thbase[3] = {};
+    double2* thscr = nullptr;
+    double* thacc = nullptr;
+    long long th_T = 0;
 
     ~Plan() {
         for (auto& g : graph)
@@ -391,6 +432,9 @@ struct Plan {
         for (double* p : {state[0], state[1], Z, W, dvec, sendbuf, zin, Zz, Wz, recvb}) if (p) cudaFree(p);
         if (codes) cudaFree(codes);
         for (double* t : sintab) if (t) cudaFree(t);
+        for (double2* t : thfac) if (t) cudaFree(t);
+        if (thscr) cudaFree(thscr);
+        if (thacc) cudaFree(thacc);
         for (int a = 0; a < 3; ++a) {
             if (PR[a]) cudaFree(PR[a]);
             if (PTR[a]) cudaFree(PTR[a]);
@@ -547,6 +591,66 @@ struct Plan {
         L.bytes = pts * 8.0 * (loaded + outs + aux);
         return L;
     }
+
+    // Threads of one Thomas launch: one pencil (x: one row) per thread and
+    // pass, at most 4 CTAs of 256 per SM (the scratch is sized by it).
+    static long long thomas_threads(long long items) {
+        const long long cap = 148LL * 4 * 256;
+        return std::min(cap, (items + 255) / 256 * 256);
+    }
+    // One Thomas pass along `axis` (apply_Q_thomas, thomas.cpp:128-160, with the
+    // stage epilogue `epi`): TH_STORE Q_ell of `nfields` stacked fields,
+    // TH_WHAT the predictor + f(t + tau) of every species, TH_UPDATE the corrector.
+    Op thomas_op(const std::string& name, int axis, int epi, const double* in, double* out, const double* aux,
+                 int nfields, int ell) const {
+        const View& v = slab;
+        Op o;
+        o.kind = Op::THOMAS;
+        o.name = name;
+        o.L.name = name;
+        o.th_epi = epi;
+        ThomasArgs a = thbase[axis];
+        a.in = in;
+        a.out = out;
+        a.aux = aux;
+        a.nfields = epi == TH_WHAT ? 2 * ns : nfields;
+        a.ell = ell;
+        if (axis == 0) {
+            a.npencil = (long long)v.ny * v.nz;
+            a.es = 1;
+            a.pin = a.npencil;
+            a.sa = v.pitch;
+            a.sb = 0;
+        } else if (axis == 1) {
+            a.npencil = (long long)v.nx * v.nz;
+            a.es = v.pitch;
+            a.pin = v.nx;
+            a.sa = 1;
+            a.sb = v.plane;
+        } else {
+            a.npencil = (long long)v.nx * v.ny;
+            a.es = v.plane;
+            a.pin = v.nx;
+            a.sa = 1;
+            a.sb = v.pitch;
+        }
+        a.xdiv = axis == 0;
+        a.commit = epi == TH_UPDATE;
+        const long long items = epi == TH_WHAT ? a.npencil : a.npencil * a.nfields;
+        a.T = thomas_threads(items);
+        a.scratch = thscr;
+        a.acc = thacc;
+        o.targs = a;
+        o.src_fn = pick_thomas(epi, ns, d.src_kind);
+        o.src_blocks = (unsigned)(a.T / 256);
+        const double pts = (double)v.nx * v.ny * v.nz;
+        const int rhs = epi == TH_WHAT ? 2 * ns : nfields;
+        const int outs = epi == TH_WHAT ? 2 * ns : nfields;
+        // per pole: forward (mul w, 6 flops) + back (e w, 1/piv w, 2 Re(r w): ~16 flops)
+        o.L.flops = pts * rhs * a.npoles * 22.0;
+        o.L.bytes = pts * 8.0 * (rhs + outs + (epi == TH_UPDATE ? nfields : epi == TH_WHAT ? ns : 0));
+        return o;
+    }
 };
 
 // ------------------------------------------------------------ setup
@@ -578,6 +682,9 @@ static void set_source(Plan& p, int kind, const double* params) {
             if (op.kind == Op::SOURCE) {
                 for (int i = 0; i < 8; ++i) op.sargs.sp[i] = p.d.src_params[i];
                 op.src_fn = pick_source(kind);
+            } else if (op.kind == Op::THOMAS) {
+                for (int i = 0; i < 8; ++i) op.targs.sp[i] = p.d.src_params[i];
+                op.src_fn = pick_thomas(op.th_epi, p.ns, kind);
             } else if (op.kind == Op::KERNEL) {
                 op.L.args.src_kind = kind;
                 for (int i = 0; i < 8; ++i) op.L.args.sp[i] = p.d.src_params[i];
@@ -614,6 +721,11 @@ static void validate(const etd_desc& d) {
     if (d.nspecies != 1 && d.nspecies != 2) throw ConfigError("nspecies must be 1 or 2");
     if (d.family != ETD_P02 && d.family != ETD_P04 && d.family != ETD_EXACT)
         throw ConfigError("unknown Pade family / backend");
+    if (d.backend != ETD_SPECTRAL && d.backend != ETD_THOMAS) throw ConfigError("unknown backend");
+    if (d.backend == ETD_THOMAS && d.family == ETD_EXACT)
+        throw ConfigError("the exact-exponential reference runs on the spectral backend");
+    if (d.backend == ETD_THOMAS && d.world_size > 1)
+        throw ConfigError("the Thomas backend runs on one GPU (no z-slab sharding)");
     check_source(d.nspecies, d.src_kind);
     for (int a = 0; a < d.dim; ++a) {
         if (d.n[a] < 1) throw ConfigError("need at least 2 subintervals for a nonempty interior");
@@ -696,8 +808,55 @@ static void build_plan(Plan& p, const etd_desc& d) {
     // unit-kappa operator and kappa_c * lambda, system_stepper.cpp:47-61)
     const bool exact = d.family == ETD_EXACT;
     const PadeScheme scheme = pade_scheme(exact ? 0 : d.family);
+    p.thomas = d.backend == ETD_THOMAS;
     std::vector<double> hd((size_t)3 * 9 * 2 * p.dmax, 0.0);
-    for (int a = 0; a < d.dim; ++a) {
+    for (int a = 0; a < d.dim && p.thomas; ++a) {
+        // build_thomas_payload (thomas.cpp:88-126) per species: c = tau diag k - s_l,
+        // e = tau off k; systems scale the unit-kappa operator by kappa_c
+        // (system_stepper.cpp:62-64)
+        const int n = d.n[a];
+        const AxisOperator op = axis_operator(n, d.low[a], d.high[a], d.dim, sys ? 1.0 : d.kappa[0], d.q);
+        const auto& poles = scheme.terms[0];
+        const int np = (int)poles.size();
+        if (np > 2) throw ConfigError("Thomas backend: at most 2 poles");
+        std::vector<double2> hf((size_t)p.ns * np * 3 * n);
+        ThomasArgs& tb = p.thbase[a];
+        tb = ThomasArgs{};
+        tb.F = p.slab.F;
+        tb.n = n;
+        tb.ns = p.ns;
+        tb.npoles = np;
+        tb.tau = d.tau;
+        tb.ny = p.slab.ny;
+        tb.gj0 = p.slab.gj0;
+        tb.gz0 = p.slab.gz0;
+        for (int i = 0; i < 8; ++i) tb.sp[i] = d.src_params[i];
+        for (int c = 0; c < p.ns; ++c) {
+            const double ks = sys ? d.kappa[c] : 1.0;
+            const std::complex<double> e(d.tau * op.off * ks, 0.0);
+            tb.e[c] = make_double2(e.real(), e.imag());
+            for (int l = 0; l < np; ++l) {
+                const std::complex<double> cc = d.tau * op.diag * ks - poles[l].pole;
+                const ThomasPole f = thomas_factor(n, cc, e);
+                double2* o = hf.data() + ((size_t)c * np + l) * 3 * n;
+                for (int i = 0; i < n; ++i) {
+                    o[i] = make_double2(f.mul[i].real(), f.mul[i].imag());
+                    o[n + i] = make_double2(f.piv[i].real(), f.piv[i].imag());
+                    o[2 * n + i] = make_double2(f.inv[i].real(), f.inv[i].imag());
+                }
+                for (int ell = 1; ell <= 3; ++ell) {
+                    const auto& t = scheme.terms[ell - 1];
+                    if ((int)t.size() != np || t[l].pole != poles[l].pole)
+                        throw NumericsError("pole ordering differs across weight functions");
+                    tb.res[c][ell - 1][l] = make_double2(t[l].residue.real(), t[l].residue.imag());
+                }
+            }
+        }
+        ETD_CK(cudaMalloc(&p.thfac[a], hf.size() * sizeof(double2)));
+        ETD_CK(cudaMemcpy(p.thfac[a], hf.data(), hf.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        tb.fac = p.thfac[a];
+    }
+    for (int a = 0; a < d.dim && !p.thomas; ++a) {
         const int n = d.n[a], np = p.npad[a];
         const AxisOperator op = axis_operator(n, d.low[a], d.high[a], d.dim, sys ? 1.0 : d.kappa[0], d.q);
         std::vector<double> Pc, lam;
@@ -759,6 +918,22 @@ static void build_plan(Plan& p, const etd_desc& d) {
     ETD_CK(cudaMallocHost(&p.status_host, sizeof(StepStatus)));
     std::memset(p.status_host, 0, sizeof(StepStatus));
     ETD_CK(cudaMemcpy(p.status, p.status_host, sizeof(StepStatus), cudaMemcpyHostToDevice));
+    if (p.thomas) {
+        for (int a = 0; a < d.dim; ++a) {
+            p.thbase[a].sinx = p.sintab[0];
+            p.thbase[a].siny = p.sintab[1];
+            p.thbase[a].sinz = d.dim == 3 ? p.sintab[2] : nullptr;
+            p.thbase[a].status = p.status;
+        }
+        // scratch for the largest pass: rhs x extent x launched threads
+        const long long nx = p.slab.nx, ny = p.slab.ny, nz = p.slab.nz, ns2 = 2LL * p.ns;
+        long long need = std::max(ns2 * nx * Plan::thomas_threads(ny * nz),            // x, TH_WHAT
+                                  nx * Plan::thomas_threads(ny * nz * p.ns));          // x, TH_UPDATE
+        need = std::max(need, ny * Plan::thomas_threads(nx * nz * ns2));              // y
+        if (d.dim == 3) need = std::max(need, nz * Plan::thomas_threads(nx * ny * ns2));  // z
+        ETD_CK(cudaMalloc(&p.thscr, (size_t)need * sizeof(double2)));
+        if (p.thbase[0].npoles > 1) ETD_CK(cudaMalloc(&p.thacc, (size_t)need * sizeof(double)));
+    }
 
     // opt every variant into large dynamic shared memory
     static bool attr_done = false;
@@ -797,6 +972,22 @@ static void build_plan(Plan& p, const etd_desc& d) {
         L.clear();
         const double* in = p.state[par];
         double* out = p.state[1 - par];
+        if (p.thomas) {
+            // BackendKind::Thomas (stepper.cpp:231-240, 243-253; system_stepper.cpp:74-114):
+            // fn = f(t, U); w = Q1_y(Q1_z(.)) of [U, fn]; What = Q1_x(w1) + tau Q2_x(w2);
+            // fw = f(t + tau, What) - w2; U1 = What + tau Q3_x(fw)
+            const long long F = V.F;
+            L.push_back(p.source_op(V, const_cast<double*>(in)));
+            const double* yin = in;
+            if (p.dim == 3) {
+                L.push_back(p.thomas_op("thomas_z", 2, TH_STORE, in, p.Z, nullptr, 2 * ns, 1));
+                yin = p.Z;
+            }
+            L.push_back(p.thomas_op("thomas_y", 1, TH_STORE, yin, p.W, nullptr, 2 * ns, 1));
+            L.push_back(p.thomas_op("thomas_x_what", 0, TH_WHAT, p.W, p.Z, nullptr, 2 * ns, 1));
+            L.push_back(p.thomas_op("thomas_x_upd", 0, TH_UPDATE, p.Z + ns * F, out, p.Z, ns, 3));
+            continue;
+        }
         // The source f(t, U) either runs as its own HBM-bound pass into the f
         // slots of the state stack (default; "source" + "z_fwd"/"y_fwd"), or fused
         // into the first transform's prologue (ETD_FUSED_SOURCE=1, "z_fwd_src"):
@@ -875,7 +1066,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
     }
     p.stats.clear();
     for (auto& op : p.steps[0])
-        if (op.kind == Op::KERNEL || op.kind == Op::SOURCE)
+        if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS)
             p.stats.push_back({op.L.name, 0, 0, op.L.flops, op.L.bytes});
     ETD_CK(cudaStreamSynchronize(p.stream));
 }
@@ -897,6 +1088,11 @@ static void run_op(Plan& p, const Op& op, cudaStream_t s) {
         break;
     case Op::SOURCE: {
         void* args[1] = {const_cast<SourceArgs*>(&op.sargs)};
+        ETD_CK(cudaLaunchKernel(op.src_fn, dim3(op.src_blocks), dim3(256), args, 0, s));
+        break;
+    }
+    case Op::THOMAS: {
+        void* args[1] = {const_cast<ThomasArgs*>(&op.targs)};
         ETD_CK(cudaLaunchKernel(op.src_fn, dim3(op.src_blocks), dim3(256), args, 0, s));
         break;
     }
@@ -1006,7 +1202,8 @@ static void do_steps(Plan& p, int nsteps) {
                 }
                 if (!p.profiling) continue;
                 const size_t e = rec();
-                if (op.kind == Op::KERNEL || op.kind == Op::SOURCE) spans.push_back({prev, kidx++});
+                if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS)
+                    spans.push_back({prev, kidx++});
                 prev = e;
             }
         }
@@ -1354,7 +1551,16 @@ static void debug_transform(Plan& p, int species, int axis, int back, int ell, i
                              cudaMemcpyHostToDevice, p.stream));
     reset_status(p, p.stream);
     const double* result = nullptr;
-    if (apply_q) {
+    if (p.thomas) {
+        // apply_Q_thomas (thomas.cpp:128-160) of field `species`
+        if (!apply_q || ell < 1) throw ConfigError("Thomas plans support only apply_q with ell in 1..3");
+        ETD_CK(cudaMemcpyAsync(p.W + (size_t)species * v.F, p.W, (size_t)v.F * 8, cudaMemcpyDeviceToDevice,
+                               p.stream));
+        Op o = p.thomas_op("dbg_thomas", axis, TH_STORE, p.W, p.Z, nullptr, 1, ell);
+        o.targs.f_first = species;
+        run_op(p, o, p.stream);
+        result = p.Z + (size_t)species * v.F;
+    } else if (apply_q) {
         if (ell < 1) throw ConfigError("apply_q needs ell in 1..3");
         Launch f = p.transform(v, "dbg_fwd", axis, false, 1, EPI_SCALE, false, p.W, p.Z);
         f.args.dA = p.dv(axis, 6 + ell - 1) + species * p.dmax;

@@ -132,6 +132,23 @@ std::vector<double> dvector(const std::vector<double>& lambda, double tau, const
 }
 
 // stepper.cpp:162-170: series branch below 1e-4 (branches agree to 1e-12 there)
+ThomasPole thomas_factor(int n, std::complex<double> c, std::complex<double> e) {
+    ThomasPole f;
+    f.mul.assign(n, 0.0);
+    f.piv.assign(n, 0.0);
+    f.inv.assign(n, 0.0);
+    f.piv[0] = c;
+    for (int i = 1; i < n; ++i) {
+        if (std::abs(f.piv[i - 1]) < 1e-30)
+            throw NumericsError("Thomas pivot underflow at row " + std::to_string(i - 1));
+        f.mul[i] = e / f.piv[i - 1];
+        f.piv[i] = c - f.mul[i] * e;
+    }
+    if (std::abs(f.piv[n - 1]) < 1e-30) throw NumericsError("Thomas pivot underflow at last row");
+    for (int i = 0; i < n; ++i) f.inv[i] = 1.0 / f.piv[i];
+    return f;
+}
+
 double phi1(double x) {
     if (x < 1e-4) return 1.0 - x / 2.0 + x * x / 6.0 - x * x * x / 24.0;
     return (1.0 - std::exp(-x)) / x;

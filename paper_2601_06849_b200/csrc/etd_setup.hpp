@@ -37,6 +37,13 @@ PadeScheme pade_scheme(int family);
 std::vector<double> dvector(const std::vector<double>& lambda, double tau, const PadeScheme& s,
                             int ell);
 
+// Thomas factors of one pole (reference thomas.cpp:14-29 factor_pole): LU of the
+// Toeplitz tridiagonal with diagonal c and off-diagonals e, no pivoting,
+// mul_i = e / piv_{i-1}, piv_i = c - mul_i e; inv_i = 1 / piv_i (thomas.cpp:70,76).
+// NumericsError on a pivot below 1e-30 in magnitude.
+struct ThomasPole { std::vector<std::complex<double>> mul, piv, inv; };
+ThomasPole thomas_factor(int n, std::complex<double> c, std::complex<double> e);
+
 // Exact-exponential multipliers (reference stepper.cpp:162-170, 276-292):
 // e^{-tau lambda_k}; tau phi_1(tau lambda_k) (which = 1) or tau phi_2 (which = 2),
 // phi with the reference's series branch below x = 1e-4.

@@ -67,12 +67,19 @@ EXACT_FAMILY = 2  # etd_family ETD_EXACT
 
 
 class BackendKind(enum.IntEnum):
-    """tensor_ops.hpp:31 plus the B200 backend this package adds."""
+    """tensor_ops.hpp:31 plus the B200 backends this package adds.  Spectral and
+    Thomas select the device implementations of the same backends (CudaSpectral,
+    CudaThomas); NonSplitBanded is not implemented (out of scope)."""
     Spectral = 0
     Thomas = 1
     NonSplitBanded = 2
     ExactExpReference = 3
     CudaSpectral = 100
+    CudaThomas = 101
+
+
+_DEVICE_BACKEND = {BackendKind.Spectral: 0, BackendKind.CudaSpectral: 0,
+                   BackendKind.Thomas: 1, BackendKind.CudaThomas: 1}
 
 
 class SourceKind(enum.IntEnum):
@@ -194,7 +201,7 @@ class _Desc(C.Structure):
         ("dim", C.c_int), ("n", C.c_int * 3), ("low", C.c_double * 3), ("high", C.c_double * 3),
         ("tau", C.c_double), ("family", C.c_int), ("nspecies", C.c_int), ("kappa", C.c_double * 2),
         ("q", C.c_double), ("src_kind", C.c_int), ("src_params", C.c_double * 8), ("device", C.c_int),
-        ("world_size", C.c_int), ("rank", C.c_int), ("nccl_unique_id", C.c_void_p),
+        ("world_size", C.c_int), ("rank", C.c_int), ("nccl_unique_id", C.c_void_p), ("backend", C.c_int),
     ]
 
 
@@ -283,7 +290,7 @@ class _Handle:
 
 
 def _make_desc(grid: Grid, tau, family, nspecies, kappas, q, source: DeviceSource, device=0,
-               world_size=1, rank=0, nccl_id=None) -> _Desc:
+               world_size=1, rank=0, nccl_id=None, backend=0) -> _Desc:
     d = _Desc()
     d.dim = grid.dim
     sh = grid.interior_shape()
@@ -303,6 +310,7 @@ def _make_desc(grid: Grid, tau, family, nspecies, kappas, q, source: DeviceSourc
     d.device = device
     d.world_size = world_size
     d.rank = rank
+    d.backend = int(backend)
     d.nccl_unique_id = None
     if nccl_id is not None:
         d._id_buf = C.create_string_buffer(bytes(nccl_id), 128)  # kept alive with the desc
@@ -331,7 +339,7 @@ class _PlanBase:
     nspecies = 1
 
     def __init__(self, grid: Grid, tau: float, family, kappas, q, source: Optional[DeviceSource], device=0,
-                 world_size=1, rank=0, nccl_id=None):
+                 world_size=1, rank=0, nccl_id=None, backend=BackendKind.CudaSpectral):
         if not tau > 0.0:
             raise ConfigError("tau must be positive")
         self.grid = grid
@@ -339,10 +347,12 @@ class _PlanBase:
         fam = _family(family)
         self.family = PadeFamily(fam) if fam in (0, 1) else fam
         self.q = float(q)
-        self.backend = BackendKind.CudaSpectral
+        if backend not in _DEVICE_BACKEND:
+            raise ConfigError(f"backend {BackendKind(backend).name} is not implemented on the device")
+        self.backend = BackendKind.CudaThomas if _DEVICE_BACKEND[backend] == 1 else BackendKind.CudaSpectral
         self._source = source or (allen_cahn_cubic() if self.nspecies == 1 else fhn_cubic())
         self._h = _Handle(_make_desc(grid, tau, self.family, self.nspecies, kappas, q, self._source, device,
-                                     world_size, rank, nccl_id))
+                                     world_size, rank, nccl_id, _DEVICE_BACKEND[backend]))
         z0, z1 = C.c_int(), C.c_int()
         lib().etd_slab_range(self._h.h, C.byref(z0), C.byref(z1))
         self.slab = (z0.value, z1.value)
@@ -445,11 +455,11 @@ class StepperPlan(_PlanBase):
     nspecies = 1
 
     def __init__(self, grid, tau, kappa, q, family=PadeFamily.P02, source=None, device=0, world_size=1, rank=0,
-                 nccl_id=None):
+                 nccl_id=None, backend=BackendKind.CudaSpectral):
         if not kappa > 0.0:
             raise ConfigError("diffusivity must be positive")
         self.kappa = float(kappa)
-        super().__init__(grid, tau, family, (kappa,), q, source, device, world_size, rank, nccl_id)
+        super().__init__(grid, tau, family, (kappa,), q, source, device, world_size, rank, nccl_id, backend)
 
 
 class SystemPlan(_PlanBase):
@@ -457,33 +467,36 @@ class SystemPlan(_PlanBase):
     nspecies = 2
 
     def __init__(self, grid, tau, kappa_u, kappa_v, q, family=PadeFamily.P02, source=None, device=0,
-                 world_size=1, rank=0, nccl_id=None):
+                 world_size=1, rank=0, nccl_id=None, backend=BackendKind.CudaSpectral):
         if not (kappa_u > 0.0 and kappa_v > 0.0):
             raise ConfigError("component diffusivities must be positive")
         self.kappa_u, self.kappa_v = float(kappa_u), float(kappa_v)
-        super().__init__(grid, tau, family, (kappa_u, kappa_v), q, source, device, world_size, rank, nccl_id)
+        super().__init__(grid, tau, family, (kappa_u, kappa_v), q, source, device, world_size, rank, nccl_id,
+                         backend)
 
 
 def make_plan(grid: Grid, tau: float, kappa: float, q: float, scheme=PadeFamily.P02,
               backend: BackendKind = BackendKind.CudaSpectral, memory_cap_bytes: int = 0,
               source: Optional[DeviceSource] = None, device: int = 0) -> StepperPlan:
-    """stepper.hpp:59-61.  BackendKind.CudaSpectral runs the Pade scheme `scheme`;
-    BackendKind.ExactExpReference runs the reference's exact-exponential step
-    (stepper.cpp:259-295) on the same device transforms."""
+    """stepper.hpp:59-61.  Spectral / CudaSpectral: eigenbasis transforms on the
+    tensor cores; Thomas / CudaThomas: per-pole complex tridiagonal solves
+    (thomas.cpp); ExactExpReference: the reference's exact-exponential step
+    (stepper.cpp:259-295) on the spectral transforms."""
     if backend == BackendKind.ExactExpReference:
         return StepperPlan(grid, tau, kappa, q, EXACT_FAMILY, source, device)
-    if backend != BackendKind.CudaSpectral:
-        raise ConfigError("this package implements BackendKind.CudaSpectral and ExactExpReference")
-    return StepperPlan(grid, tau, kappa, q, scheme, source, device)
+    if backend not in _DEVICE_BACKEND:
+        raise ConfigError("this package implements the Spectral, Thomas and ExactExpReference backends")
+    return StepperPlan(grid, tau, kappa, q, scheme, source, device, backend=backend)
 
 
 def make_system_plan(grid: Grid, tau: float, kappa_u: float, kappa_v: float, q: float, scheme=PadeFamily.P02,
                      backend: BackendKind = BackendKind.CudaSpectral, source: Optional[DeviceSource] = None,
                      device: int = 0) -> SystemPlan:
-    """stepper.hpp:107-108, extended to 3D (the reference throws for dim != 2)."""
-    if backend != BackendKind.CudaSpectral:
-        raise ConfigError("this package implements BackendKind.CudaSpectral only")
-    return SystemPlan(grid, tau, kappa_u, kappa_v, q, scheme, source, device)
+    """stepper.hpp:107-108, extended to 3D (the reference throws for dim != 2).
+    Spectral and Thomas backends (system_stepper.cpp:47-68)."""
+    if backend not in _DEVICE_BACKEND:
+        raise ConfigError("system plans support the spectral and thomas backends only")
+    return SystemPlan(grid, tau, kappa_u, kappa_v, q, scheme, source, device, backend=backend)
 
 
 @dataclass

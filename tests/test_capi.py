@@ -26,7 +26,33 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 20
     for s in syms:
         assert hasattr(L, s), s
-    assert L.etd_abi_version() == 1
+    assert L.etd_abi_version() == 2
+
+
+def test_header_is_plain_c_and_matches_ctypes_layout():
+    """include/etd_b200.h compiles as C99 (a C/cgo/FFI client can include it) and
+    sizeof/offsetof(etd_desc) agree with the ctypes mirror in etd.py."""
+    import shutil
+    import subprocess
+    import tempfile
+    import ctypes
+    cc = shutil.which("gcc")
+    if not cc:
+        pytest.skip("gcc unavailable")
+    d = etd.etd._Desc
+    fields = [f[0] for f in d._fields_]
+    prog = '#include <stdio.h>\n#include <stddef.h>\n#include "etd_b200.h"\nint main(void){printf("%zu", sizeof(etd_desc));'
+    for f in fields:
+        prog += 'printf(" %zu", offsetof(etd_desc, ' + f + '));'
+    prog += 'return 0;}\n'
+    with tempfile.TemporaryDirectory() as td:
+        src, exe = os.path.join(td, "h.c"), os.path.join(td, "h")
+        open(src, "w").write(prog)
+        subprocess.run([cc, "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), src, "-o", exe],
+                       check=True)
+        got = [int(x) for x in subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()]
+    assert got[0] == ctypes.sizeof(d)
+    assert got[1:] == [getattr(d, f).offset for f in fields]
 
 
 def test_sass_targets_sm100a():
@@ -52,7 +78,9 @@ def test_config_errors_before_device():
     with pytest.raises(etd.ConfigError):
         etd.make_plan(g, 0.01, 1.0, 1.0, source=etd.fhn_cubic())  # pair source on a scalar plan
     with pytest.raises(etd.ConfigError):
-        etd.make_plan(g, 0.01, 1.0, 1.0, backend=etd.BackendKind.Spectral)
+        etd.make_plan(g, 0.01, 1.0, 1.0, backend=etd.BackendKind.NonSplitBanded)
+    with pytest.raises(etd.ConfigError):
+        etd.make_system_plan(g, 0.01, 1.0, 1.0, 0.0, backend=etd.BackendKind.ExactExpReference)
     with pytest.raises(etd.ConfigError):
         etd.build_grid(2, [(0, 1), (1, 1)], [4, 4])
     with pytest.raises(etd.ConfigError):
