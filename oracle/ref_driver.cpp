@@ -27,6 +27,9 @@
 #include "etdrd/rational.hpp"
 #include "etdrd/stepper.hpp"
 #include "etdrd/tensor_ops.hpp"
+#ifdef REF_HAS_HARNESS
+#include "etdrd/harness.hpp"
+#endif
 
 using namespace etdrd;
 
@@ -534,5 +537,31 @@ int ref_apply_q_thomas(int dim, int n, double tau, double kappa, double q, int f
         return map_exc(e, err, errlen, nullptr, nullptr);
     }
 }
+
+#ifdef REF_HAS_HARNESS
+// The reference study harness (harness.cpp:305-362): run_convergence writes
+// <out>/convergence_*.csv, a manifest and, for problems without a closed form,
+// the ETRJ reference-trajectory cache <out>/references/*.traj.  Used to make
+// golden trajectory/CSV fixtures (tests/golden/make_golden_harness.py).
+int ref_run_convergence(const char* problem, int m, const int* Ns, int nN, int family, int backend,
+                        int coarse, double T, const char* out, double* E, char* err, int errlen) {
+    try {
+        RunConfig cfg;
+        cfg.problem = problem;
+        cfg.m = m;
+        cfg.Ns.assign(Ns, Ns + nN);
+        cfg.scheme = family ? PadeFamily::P04 : PadeFamily::P02;
+        cfg.backend = static_cast<BackendKind>(backend);
+        cfg.coarse = coarse;
+        cfg.T = T;
+        cfg.out = out;
+        const auto rep = run_convergence(cfg);
+        for (std::size_t i = 0; i < rep.rows.size(); ++i) E[i] = rep.rows[i].E;
+        return 0;
+    } catch (const std::exception& e) {
+        return map_exc(e, err, errlen, nullptr, nullptr);
+    }
+}
+#endif
 
 }  // extern "C"

@@ -1,6 +1,6 @@
 """Per-stage device timing of the CUDA step on the BASELINE configs (dev tool).
 
-python tools/quick_perf.py [cfg ids...] [--steps K]
+python tools/quick_perf.py [cfg ids...] [--steps K] [--thomas]
 Prints one JSON line per config with per-stage ms, TFLOP/s and pt-updates/s.
 """
 import json
@@ -14,13 +14,13 @@ import numpy as np  # noqa: E402
 from paper_2601_06849_b200 import configs  # noqa: E402
 
 
-def run(cfg_id: int, steps: int, n=None):
+def run(cfg_id: int, steps: int, n=None, **kw):
     cfg = configs.CONFIGS[cfg_id]
     n = cfg.n if n is None else n
     t0 = time.time()
     ics = configs.initial_state(cfg, n)
     t_ic = time.time() - t0
-    plan = configs.make_plan(cfg, n)
+    plan = configs.make_plan(cfg, n, **kw)
     for s, a in enumerate(ics):
         plan.upload(s, a)
     plan.step(1)  # warm-up (graph build, L2)
@@ -29,7 +29,7 @@ def run(cfg_id: int, steps: int, n=None):
     st = plan.stage_stats()
     tot = sum(x["ms_total"] for x in st) / steps
     pts = cfg.points(n) * cfg.nspecies
-    out = {"cfg": cfg_id, "n": n, "steps": steps, "ms_per_step": tot, "pt_upd_per_s": pts / (tot * 1e-3),
+    out = {"cfg": cfg_id, "backend": plan.backend.name, "n": n, "steps": steps, "ms_per_step": tot, "pt_upd_per_s": pts / (tot * 1e-3),
            "tflops": cfg.flops_per_step(n) / (tot * 1e-3) * 1e-12, "ic_s": round(t_ic, 2), "stages": []}
     for x in st:
         ms = x["ms_total"] / max(1, x["launches"])
@@ -55,6 +55,11 @@ if __name__ == "__main__":
         i = args.index("--steps")
         steps = int(args[i + 1])
         del args[i:i + 2]
+    kw = {}
+    if "--thomas" in args:
+        args.remove("--thomas")
+        from paper_2601_06849_b200 import etd
+        kw["backend"] = etd.BackendKind.Thomas
     ids = [int(a) for a in args] or [0, 1, 2, 3, 4]
     for c in ids:
-        run(c, steps if c < 3 else min(steps, 2))
+        run(c, steps if c < 3 else min(steps, 2), **kw)
