@@ -319,12 +319,51 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "unit": "grid-point updates/s", "cores": os.cpu_count(),
                                     "kind": "reference", "sample": f"unavailable: {e}"}
+    plan.close()
+    if world == 1 and not args.no_alt:
+        line["alt_backends"] = {"thomas": thomas_backend(args, cfg, n, ics, local_rank)}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    plan.close()
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def thomas_backend(args, cfg, n, ics, local_rank):
+    """The same step with BackendKind::Thomas (per-pole complex tridiagonal
+    sweeps, thomas.cpp) on the same inputs: device-resident, CUDA events on the
+    plan's stream.  Reported next to the headline, which stays the eigenbasis
+    transform path the north star names."""
+    import torch
+    from paper_2601_06849_b200 import configs, etd
+    try:
+        tp = configs.make_plan(cfg, n, device=local_rank, backend=etd.BackendKind.Thomas)
+    except Exception as e:  # e.g. out of memory on a smaller device
+        return {"value": None, "note": f"unavailable: {e}"}
+    try:
+        for s_, a in enumerate(ics):
+            tp.upload(s_, a)
+        tp.step(max(1, args.warmup))
+        stream = torch.cuda.ExternalStream(tp.stream, device=torch.device("cuda", local_rank))
+        tp.set_profiling(True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        tp.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        stages = []
+        for st in tp.stage_stats():
+            a = st["ms_total"] / max(1, st["launches"])
+            gbs = st["bytes_per_launch"] / (a * 1e-3) * 1e-9
+            stages.append({"name": st["name"], "ms": round(a, 3), "bound": "hbm", "gbs": round(gbs, 1),
+                           "frac": round(gbs / 6552.0, 4)})
+        return {"value": cfg.points(n) * cfg.nspecies / (ms * 1e-3), "unit": "grid-point updates/s",
+                "ms_per_step": ms, "stages": stages,
+                "note": "BackendKind::Thomas on the device; algorithmic bytes = stage inputs + outputs"}
+    finally:
+        tp.close()
 
 
 def main():
@@ -337,6 +376,7 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override the grid size (testing only)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip the Thomas-backend line")
     args = ap.parse_args()
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)

@@ -73,7 +73,8 @@ static EncodeTiledFn encode_fn() {
 
 // FP64 tiled map, 128B swizzle, OOB elements read as +0.0 (never touch pads).
 static CUtensorMap make_map(const double* base, int rank, const unsigned long long* dims,
-                            const unsigned long long* strides_elems, const unsigned* box) {
+                            const unsigned long long* strides_elems, const unsigned* box,
+                            CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
     CUtensorMap m;
     cuuint64_t gd[5], gs[4];
     cuuint32_t bx[5], es[5];
@@ -84,7 +85,7 @@ static CUtensorMap make_map(const double* base, int rank, const unsigned long lo
     }
     for (int i = 0; i < rank - 1; ++i) gs[i] = strides_elems[i] * sizeof(double);
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(base), gd, gs,
-                             bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
     return m;
@@ -183,34 +184,68 @@ static const void* pick_source(int sk) {
     }
 }
 
-template <int EPI, int NS>
-static const void* thomas_fn(int sk) {
+// Thomas kernels: MODE 1 (y/z) only stores (the z/y filters); MODE 0 (x) runs
+// every epilogue, and only TH_WHAT evaluates a source.
+struct ThomasSpec {
+    const void* fn = nullptr;
+    int smem = 0;
+    int occ = 0;  // resident CTAs per SM (set once the smem attribute is applied)
+};
+template <int MODE, int EPI, int NS, int SK>
+static ThomasSpec thomas_spec(int np) {
+    const void* fn = np == 1 ? reinterpret_cast<const void*>(etd_thomas<MODE, EPI, NS, SK, 1>)
+                             : reinterpret_cast<const void*>(etd_thomas<MODE, EPI, NS, SK, 2>);
+    return {fn, ThomasCfg<MODE, EPI, NS>::SMEM_BYTES, 0};
+}
+template <int MODE, int EPI, int NS>
+static ThomasSpec thomas_sk(int sk, int np) {
     if constexpr (EPI != TH_WHAT) {
-        return reinterpret_cast<const void*>(etd_thomas<EPI, NS, 0>);
+        return thomas_spec<MODE, EPI, NS, 0>(np);
     } else if constexpr (NS == 1) {
         switch (sk) {
-        case 0: return reinterpret_cast<const void*>(etd_thomas<EPI, 1, 0>);
-        case 1: return reinterpret_cast<const void*>(etd_thomas<EPI, 1, 1>);
-        case 2: return reinterpret_cast<const void*>(etd_thomas<EPI, 1, 2>);
-        case 3: return reinterpret_cast<const void*>(etd_thomas<EPI, 1, 3>);
-        case 4: return reinterpret_cast<const void*>(etd_thomas<EPI, 1, 4>);
-        case 5: return reinterpret_cast<const void*>(etd_thomas<EPI, 1, 5>);
+        case 0: return thomas_spec<MODE, EPI, 1, 0>(np);
+        case 1: return thomas_spec<MODE, EPI, 1, 1>(np);
+        case 2: return thomas_spec<MODE, EPI, 1, 2>(np);
+        case 3: return thomas_spec<MODE, EPI, 1, 3>(np);
+        case 4: return thomas_spec<MODE, EPI, 1, 4>(np);
+        case 5: return thomas_spec<MODE, EPI, 1, 5>(np);
         }
     } else {
         switch (sk) {
-        case 0: return reinterpret_cast<const void*>(etd_thomas<EPI, 2, 0>);
-        case 10: return reinterpret_cast<const void*>(etd_thomas<EPI, 2, 10>);
-        case 11: return reinterpret_cast<const void*>(etd_thomas<EPI, 2, 11>);
-        case 12: return reinterpret_cast<const void*>(etd_thomas<EPI, 2, 12>);
-        case 13: return reinterpret_cast<const void*>(etd_thomas<EPI, 2, 13>);
+        case 0: return thomas_spec<MODE, EPI, 2, 0>(np);
+        case 10: return thomas_spec<MODE, EPI, 2, 10>(np);
+        case 11: return thomas_spec<MODE, EPI, 2, 11>(np);
+        case 12: return thomas_spec<MODE, EPI, 2, 12>(np);
+        case 13: return thomas_spec<MODE, EPI, 2, 13>(np);
         }
     }
     throw ConfigError("unknown source kind");
 }
-static const void* pick_thomas(int epi, int ns, int sk) {
-    if (epi == TH_STORE) return ns == 1 ? thomas_fn<TH_STORE, 1>(sk) : thomas_fn<TH_STORE, 2>(sk);
-    if (epi == TH_WHAT) return ns == 1 ? thomas_fn<TH_WHAT, 1>(sk) : thomas_fn<TH_WHAT, 2>(sk);
-    return ns == 1 ? thomas_fn<TH_UPDATE, 1>(sk) : thomas_fn<TH_UPDATE, 2>(sk);
+static ThomasSpec pick_thomas(int mode, int epi, int ns, int sk, int np) {
+    if (np != 1 && np != 2) throw ConfigError("Thomas backend: 1 or 2 poles");
+    ThomasSpec k;
+    if (mode == 1) {
+        if (epi != TH_STORE) throw ConfigError("Thomas y/z passes only store");
+        k = ns == 1 ? thomas_sk<1, TH_STORE, 1>(sk, np) : thomas_sk<1, TH_STORE, 2>(sk, np);
+    } else if (epi == TH_STORE) {
+        k = ns == 1 ? thomas_sk<0, TH_STORE, 1>(sk, np) : thomas_sk<0, TH_STORE, 2>(sk, np);
+    } else if (epi == TH_WHAT) {
+        k = ns == 1 ? thomas_sk<0, TH_WHAT, 1>(sk, np) : thomas_sk<0, TH_WHAT, 2>(sk, np);
+    } else {
+        k = ns == 1 ? thomas_sk<0, TH_UPDATE, 1>(sk, np) : thomas_sk<0, TH_UPDATE, 2>(sk, np);
+    }
+    // large dynamic shared memory + occupancy, once per kernel
+    static std::vector<std::pair<const void*, int>> done;
+    for (auto& dn : done)
+        if (dn.first == k.fn) {
+            k.occ = dn.second;
+            return k;
+        }
+    ETD_CK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem));
+    ETD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k.occ, k.fn, 128, k.smem));
+    if (k.occ < 1) throw CudaError("Thomas kernel does not fit on an SM");
+    done.push_back({k.fn, k.occ});
+    return k;
 }
 
 // ------------------------------------------------------------ NCCL (dlopen'd)
@@ -423,7 +458,9 @@ struct Plan {
     double2* thfac[3] = {nullptr, nullptr, nullptr};
     ThomasArgs thbase[3] = {};
     double2* thscr = nullptr;
-    double* thacc = nullptr;
+    long long th_cap = 0;            // thscr capacity in double2
+    long long th_need = 0;           // largest checkpoint scratch of the built passes
+    int nsm = 148;
     long long th_T = 0;
 
     ~Plan() {
@@ -434,7 +471,6 @@ struct Plan {
         for (double* t : sintab) if (t) cudaFree(t);
         for (double2* t : thfac) if (t) cudaFree(t);
         if (thscr) cudaFree(thscr);
-        if (thacc) cudaFree(thacc);
         for (int a = 0; a < 3; ++a) {
             if (PR[a]) cudaFree(PR[a]);
             if (PTR[a]) cudaFree(PTR[a]);
@@ -592,63 +628,72 @@ struct Plan {
         return L;
     }
 
-    // Threads of one Thomas launch: one pencil (x: one row) per thread and
-    // pass, at most 4 CTAs of 256 per SM (the scratch is sized by it).
-    static long long thomas_threads(long long items) {
-        const long long cap = 148LL * 4 * 256;
-        return std::min(cap, (items + 255) / 256 * 256);
-    }
     // One Thomas pass along `axis` (apply_Q_thomas, thomas.cpp:128-160, with the
-    // stage epilogue `epi`): TH_STORE Q_ell of `nfields` stacked fields,
-    // TH_WHAT the predictor + f(t + tau) of every species, TH_UPDATE the corrector.
-    Op thomas_op(const std::string& name, int axis, int epi, const double* in, double* out, const double* aux,
-                 int nfields, int ell) const {
+    // stage epilogue `epi`) over the operand stack `stack` (2 ns fields, stride F):
+    //   TH_STORE   Q_ell of fields [f0, f0 + nfields) -> out (same field index)
+    //   TH_WHAT    (x) the predictor + f(t + tau) of every species: W stack -> out
+    //   TH_UPDATE  (x) the corrector U1 = What + tau Q3(fw): fw at stack[fin_off + c],
+    //              What at stack[c] -> out[c], c < nfields; commits the step
+    // Scratch (checkpoints) is sized after the schedule is built (th_need).
+    Op thomas_op(const std::string& name, int axis, int epi, const double* stack, double* out, int nfields,
+                 int ell, int f0 = 0, int fin_off = 0) {
         const View& v = slab;
+        const int mode = axis == 0 ? 0 : 1;
         Op o;
         o.kind = Op::THOMAS;
         o.name = name;
         o.L.name = name;
+        o.L.mode = mode;
         o.th_epi = epi;
         ThomasArgs a = thbase[axis];
-        a.in = in;
         a.out = out;
-        a.aux = aux;
-        a.nfields = epi == TH_WHAT ? 2 * ns : nfields;
         a.ell = ell;
-        if (axis == 0) {
-            a.npencil = (long long)v.ny * v.nz;
-            a.es = 1;
-            a.pin = a.npencil;
-            a.sa = v.pitch;
-            a.sb = 0;
-        } else if (axis == 1) {
-            a.npencil = (long long)v.nx * v.nz;
-            a.es = v.pitch;
-            a.pin = v.nx;
-            a.sa = 1;
-            a.sb = v.plane;
-        } else {
-            a.npencil = (long long)v.nx * v.ny;
-            a.es = v.plane;
-            a.pin = v.nx;
-            a.sa = 1;
-            a.sb = v.pitch;
-        }
-        a.xdiv = axis == 0;
+        a.f_first = f0;
+        a.fin_off = fin_off;
         a.commit = epi == TH_UPDATE;
-        const long long items = epi == TH_WHAT ? a.npencil : a.npencil * a.nfields;
-        a.T = thomas_threads(items);
-        a.scratch = thscr;
-        a.acc = thacc;
+        const int nfl = epi == TH_WHAT ? 1 : nfields;
+        const unsigned long long nst = 2ull * ns;
+        if (mode == 1) {
+            const bool z = axis == 2;
+            a.es = z ? v.plane : v.pitch;
+            a.so = z ? v.pitch : v.plane;
+            a.npen = v.nx;
+            a.nouter = z ? v.ny : v.nz;
+            a.ptiles = (v.nx + 127) / 128;
+            // {x%16, axis, x/16, outer, field}, box {16, 16, 8, 1, 1} -> [x-block][16][16]
+            const unsigned long long dims[5] = {16, (unsigned long long)a.n, (unsigned long long)((v.nx + 15) / 16),
+                                                (unsigned long long)a.nouter, nst};
+            const unsigned long long st[4] = {(unsigned long long)a.es, 16, (unsigned long long)a.so,
+                                              (unsigned long long)v.F};
+            const unsigned box[5] = {16, 16, 8, 1, 1};
+            o.L.tmA = make_map(stack, 5, dims, st, box);
+        } else {
+            a.pitch = v.pitch;
+            a.npen = v.ny * v.nz;
+            a.nouter = 1;
+            a.ptiles = (a.npen + 127) / 128;
+            // {x, row, field}, box {8, 128, 1}, 64B swizzle -> [row][8]
+            const unsigned long long dims[3] = {(unsigned long long)v.nx, (unsigned long long)a.npen, nst};
+            const unsigned long long st[2] = {(unsigned long long)v.pitch, (unsigned long long)v.F};
+            const unsigned box[3] = {8, 128, 1};
+            o.L.tmA = make_map(stack, 3, dims, st, box, CU_TENSOR_MAP_SWIZZLE_64B);
+        }
+        a.ntiles = (long long)a.ptiles * a.nouter * nfl;
+        const ThomasSpec k = pick_thomas(mode, epi, ns, d.src_kind, a.npoles);
+        const long long G = std::max<long long>(1, std::min<long long>(a.ntiles, (long long)nsm * k.occ));
+        const long long R = thomas_rhs(epi, ns), K = thomas_chunk((int)R);
+        th_need = std::max(th_need, R * a.npoles * ((a.n + K - 1) / K) * G * 128);
         o.targs = a;
-        o.src_fn = pick_thomas(epi, ns, d.src_kind);
-        o.src_blocks = (unsigned)(a.T / 256);
+        o.src_fn = k.fn;
+        o.src_blocks = (unsigned)G;
+        o.L.k.smem = k.smem;
         const double pts = (double)v.nx * v.ny * v.nz;
         const int rhs = epi == TH_WHAT ? 2 * ns : nfields;
         const int outs = epi == TH_WHAT ? 2 * ns : nfields;
         // per pole: forward (mul w, 6 flops) + back (e w, 1/piv w, 2 Re(r w): ~16 flops)
         o.L.flops = pts * rhs * a.npoles * 22.0;
-        o.L.bytes = pts * 8.0 * (rhs + outs + (epi == TH_UPDATE ? nfields : epi == TH_WHAT ? ns : 0));
+        // algorithmic bytes: operands in, results out (TH_UPDATE also reads What)
+        o.L.bytes = pts * 8.0 * (rhs + outs + (epi == TH_UPDATE ? nfields : 0));
         return o;
     }
 };
@@ -684,7 +729,7 @@ static void set_source(Plan& p, int kind, const double* params) {
                 op.src_fn = pick_source(kind);
             } else if (op.kind == Op::THOMAS) {
                 for (int i = 0; i < 8; ++i) op.targs.sp[i] = p.d.src_params[i];
-                op.src_fn = pick_thomas(op.th_epi, p.ns, kind);
+                op.src_fn = pick_thomas(op.L.mode, op.th_epi, p.ns, kind, op.targs.npoles).fn;
             } else if (op.kind == Op::KERNEL) {
                 op.L.args.src_kind = kind;
                 for (int i = 0; i < 8; ++i) op.L.args.sp[i] = p.d.src_params[i];
@@ -742,6 +787,21 @@ static void validate(const etd_desc& d) {
     }
 }
 
+// (Re)allocate the Thomas checkpoint scratch to hold `need` entries and point
+// every Thomas op of the step schedule at it.
+static void ensure_thomas_scratch(Plan& p, long long need) {
+    if (need > p.th_cap) {
+        if (p.thscr) ETD_CK(cudaFree(p.thscr));
+        p.thscr = nullptr;
+        ETD_CK(cudaMalloc(&p.thscr, (size_t)need * sizeof(double2)));
+        p.th_cap = need;
+        drop_graphs(p);
+    }
+    for (auto& steps : p.steps)
+        for (auto& op : steps)
+            if (op.kind == Op::THOMAS) op.targs.scratch = p.thscr;
+}
+
 static void build_plan(Plan& p, const etd_desc& d) {
     validate(d);
     p.d = d;
@@ -760,6 +820,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
     int major = 0;
     ETD_CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d.device));
     if (major != 10) throw NoDevice("this build targets sm_100a (B200)");
+    ETD_CK(cudaDeviceGetAttribute(&p.nsm, cudaDevAttrMultiProcessorCount, d.device));
 
     p.nx = d.n[0];
     p.ny = d.n[1];
@@ -925,14 +986,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
             p.thbase[a].sinz = d.dim == 3 ? p.sintab[2] : nullptr;
             p.thbase[a].status = p.status;
         }
-        // scratch for the largest pass: rhs x extent x launched threads
-        const long long nx = p.slab.nx, ny = p.slab.ny, nz = p.slab.nz, ns2 = 2LL * p.ns;
-        long long need = std::max(ns2 * nx * Plan::thomas_threads(ny * nz),            // x, TH_WHAT
-                                  nx * Plan::thomas_threads(ny * nz * p.ns));          // x, TH_UPDATE
-        need = std::max(need, ny * Plan::thomas_threads(nx * nz * ns2));              // y
-        if (d.dim == 3) need = std::max(need, nz * Plan::thomas_threads(nx * ny * ns2));  // z
-        ETD_CK(cudaMalloc(&p.thscr, (size_t)need * sizeof(double2)));
-        if (p.thbase[0].npoles > 1) ETD_CK(cudaMalloc(&p.thacc, (size_t)need * sizeof(double)));
+
     }
 
     // opt every variant into large dynamic shared memory
@@ -977,15 +1031,16 @@ static void build_plan(Plan& p, const etd_desc& d) {
             // fn = f(t, U); w = Q1_y(Q1_z(.)) of [U, fn]; What = Q1_x(w1) + tau Q2_x(w2);
             // fw = f(t + tau, What) - w2; U1 = What + tau Q3_x(fw)
             const long long F = V.F;
+            (void)F;
             L.push_back(p.source_op(V, const_cast<double*>(in)));
             const double* yin = in;
             if (p.dim == 3) {
-                L.push_back(p.thomas_op("thomas_z", 2, TH_STORE, in, p.Z, nullptr, 2 * ns, 1));
+                L.push_back(p.thomas_op("thomas_z", 2, TH_STORE, in, p.Z, 2 * ns, 1));
                 yin = p.Z;
             }
-            L.push_back(p.thomas_op("thomas_y", 1, TH_STORE, yin, p.W, nullptr, 2 * ns, 1));
-            L.push_back(p.thomas_op("thomas_x_what", 0, TH_WHAT, p.W, p.Z, nullptr, 2 * ns, 1));
-            L.push_back(p.thomas_op("thomas_x_upd", 0, TH_UPDATE, p.Z + ns * F, out, p.Z, ns, 3));
+            L.push_back(p.thomas_op("thomas_y", 1, TH_STORE, yin, p.W, 2 * ns, 1));
+            L.push_back(p.thomas_op("thomas_x_what", 0, TH_WHAT, p.W, p.Z, 2 * ns, 1));
+            L.push_back(p.thomas_op("thomas_x_upd", 0, TH_UPDATE, p.Z, out, ns, 3, 0, ns));
             continue;
         }
         // The source f(t, U) either runs as its own HBM-bound pass into the f
@@ -1064,6 +1119,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
             L.push_back(cm);
         }
     }
+    if (p.thomas) ensure_thomas_scratch(p, p.th_need);
     p.stats.clear();
     for (auto& op : p.steps[0])
         if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS)
@@ -1092,8 +1148,8 @@ static void run_op(Plan& p, const Op& op, cudaStream_t s) {
         break;
     }
     case Op::THOMAS: {
-        void* args[1] = {const_cast<ThomasArgs*>(&op.targs)};
-        ETD_CK(cudaLaunchKernel(op.src_fn, dim3(op.src_blocks), dim3(256), args, 0, s));
+        void* args[2] = {const_cast<CUtensorMap*>(&op.L.tmA), const_cast<ThomasArgs*>(&op.targs)};
+        ETD_CK(cudaLaunchKernel(op.src_fn, dim3(op.src_blocks), dim3(128), args, op.L.k.smem, s));
         break;
     }
     case Op::FAILCODE: etd_fail_code<<<1, 1, 0, s>>>(p.status, p.codes + p.G); break;
@@ -1556,8 +1612,9 @@ static void debug_transform(Plan& p, int species, int axis, int back, int ell, i
         if (!apply_q || ell < 1) throw ConfigError("Thomas plans support only apply_q with ell in 1..3");
         ETD_CK(cudaMemcpyAsync(p.W + (size_t)species * v.F, p.W, (size_t)v.F * 8, cudaMemcpyDeviceToDevice,
                                p.stream));
-        Op o = p.thomas_op("dbg_thomas", axis, TH_STORE, p.W, p.Z, nullptr, 1, ell);
-        o.targs.f_first = species;
+        Op o = p.thomas_op("dbg_thomas", axis, TH_STORE, p.W, p.Z, 1, ell, species);
+        ensure_thomas_scratch(p, p.th_need);
+        o.targs.scratch = p.thscr;
         run_op(p, o, p.stream);
         result = p.Z + (size_t)species * v.F;
     } else if (apply_q) {

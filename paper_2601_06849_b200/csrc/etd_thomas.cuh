@@ -5,20 +5,33 @@
 //
 // Q_ell(tau A) b = sum_l 2 Re( r_{ell,l} (tau A - s_l)^{-1} b ) with the LU
 // factors of (tau A - s_l) precomputed on the host exactly as factor_pole
-// (thomas.cpp:14-29): mul_i = e / piv_{i-1}, piv_i = c - mul_i e.  One thread
-// owns one pencil (a line of the field along the axis) and runs the forward
-// elimination and the back substitution sequentially; consecutive threads own
-// consecutive x positions for the y and z axes (coalesced), consecutive rows
-// for the x axis (each thread's 32-byte sectors are re-used from L1 on the next
-// three steps).  The forward values live in a [rhs][j][thread] complex scratch
-// so a warp's scratch traffic is coalesced on every axis.
+// (thomas.cpp:14-29): mul_i = e / piv_{i-1}, piv_i = c - mul_i e.
+//
+// Work split: a CTA of 128 threads owns a tile of 128 pencils (lines of the
+// field along the axis), one thread per pencil, and walks the axis with a TMA
+// ring of stages (J axis points x 128 pencils x L operands, mbarrier full/empty
+// as in the transform kernels), so the sequential recurrences never wait on
+// individual global loads:
+//   MODE 1 (y/z axes):  5D box {16 x, J, 8 x-blocks, 1, 1}, 128B swizzle
+//                       -> [x-block][J][16]   (the pencils are 128 consecutive x)
+//   MODE 0 (x axis):    3D box {J=8, 128 rows, 1} per operand, 64B swizzle
+//                       -> [row][8]           (the pencils are 128 consecutive rows)
+// The forward elimination streams the axis once (all poles together) and keeps
+// one checkpoint per chunk of K points; the back substitution streams it again
+// in reverse, recomputes each chunk's forward values from its checkpoint in
+// registers (the same operations, hence the same bits), finishes every pole of
+// the chunk and runs the epilogue.  HBM traffic per point and operand: two reads
+// plus the output write; the checkpoints (2 / K of a complex per point) stay
+// mostly in L2.  CTAs are persistent over the tiles.
 //
 // Arithmetic follows std::complex<double> operation by operation (products
-// and sums as __dmul_rn / __dadd_rn, so nvcc does not fuse them): the y/z
-// applies multiply by the host-computed 1/piv (solve_axis_planes), the x
-// applies divide by piv (solve_axis_x) with Smith's algorithm.  Whether the
-// reference's g++ build contracts its complex products into FMAs depends on
-// its flags, so parity is stated as a tolerance (tests/test_gpu_thomas.py).
+// and sums as __dmul_rn / __dadd_rn, so nvcc does not fuse them), with the
+// back substitution in the solve_axis_planes form on every axis: multiply by
+// the host-computed 1/piv (thomas.cpp:69-83; solve_axis_x divides by piv,
+// which differs in the last bit), e w taken componentwise (e is real), and only
+// the real part of r w formed.  Whether the reference's g++ build contracts its
+// complex products into FMAs depends on its flags, so parity is stated as a
+// tolerance (tests/test_gpu_thomas.py).
 #pragma once
 #include "etd_kernels.cuh"
 
@@ -27,27 +40,25 @@ namespace etd {
 enum ThomasEpi { TH_STORE = 0, TH_WHAT = 1, TH_UPDATE = 2 };
 
 struct ThomasArgs {
-    const double* in;         // operand stack, stride F
     double* out;              // output stack, stride F
-    const double* aux;        // TH_UPDATE: the What stack
     long long F;
     int n;                    // extent along the axis
-    long long es;             // element stride along the axis
-    long long npencil;        // pencils per field
-    long long pin, sa, sb;    // pencil q starts at (q % pin) sa + (q / pin) sb
-    int nfields;              // TH_STORE / TH_UPDATE: fields of this launch (field f -> species f % ns)
-    int f_first;              // first field of the launch
+    long long es, so;         // element strides along the axis / the outer index (MODE 1)
+    long long pitch;          // row pitch (MODE 0)
+    int npen;                 // pencils per outer index: nx (MODE 1) or rows (MODE 0)
+    int ptiles;               // 128-pencil tiles per outer index
+    int nouter;               // MODE 1: outer extent (nz for y, ny for z); MODE 0: 1
+    long long ntiles;         // ptiles * nouter * launch fields
+    int f_first;              // first field of the launch (TH_STORE / TH_UPDATE)
+    int fin_off;              // TH_UPDATE: stack offset of the fw operands (What at 0)
     int ns;
     int npoles;
-    int xdiv;                 // 1: divide by piv (thomas.cpp:42-46); 0: multiply by 1/piv (:69-83)
     int ell;                  // residue set of TH_STORE / TH_UPDATE
     const double2* fac;       // [species][pole][3][n]: mul, piv, 1/piv
     double2 e[2];             // off-diagonal tau off kappa (thomas.cpp:95), per species
     double2 res[2][3][2];     // [species][ell-1][pole]
     double tau;
-    double2* scratch;         // [rhs][n][T]
-    double* acc;              // [rhs][n][T] partial sums over poles (npoles > 1)
-    long long T;              // launched threads
+    double2* scratch;         // checkpoints [rhs][pole][chunk][CTA][128]
     // TH_WHAT source evaluation (x pencils: row r -> y = r % ny, z = r / ny)
     int ny;
     int gj0, gz0;
@@ -59,143 +70,292 @@ struct ThomasArgs {
     int commit;
 };
 
+__host__ __device__ constexpr int thomas_rhs(int epi, int ns) { return epi == TH_WHAT ? 2 * ns : 1; }
+__host__ __device__ constexpr int thomas_chunk(int rhs) { return rhs >= 2 ? 4 : 8; }
+
+template <int MODE, int EPI, int NS>
+struct ThomasCfg {
+    static constexpr int R = thomas_rhs(EPI, NS);          // right-hand sides per pencil
+    static constexpr int K = thomas_chunk(R);              // back-substitution chunk
+    static constexpr int P = 128;                          // pencils (threads) per tile
+    static constexpr int J = MODE == 0 ? 8 : 16;           // axis points per stage
+    static constexpr int L = MODE == 0 ? (EPI == TH_WHAT ? 2 * NS : EPI == TH_UPDATE ? 2 : 1) : 1;
+    static constexpr int STAGES = L >= 4 ? 3 : 4;
+    static constexpr int OP_DBL = P * J;
+    static constexpr int STAGE_DBL = L * OP_DBL;
+    static constexpr uint32_t TX_BYTES = STAGE_DBL * 8;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_DBL * 8 + 1024 + 2 * STAGES * 8 + 16;
+    static_assert(J % K == 0, "chunks tile the stages");
+};
+
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
                         __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
 }
-// Smith's complex division (a + bi) / (c + di)
-__device__ __forceinline__ double2 cdiv(double2 n, double2 d) {
-    const double a = n.x, b = n.y, c = d.x, dd = d.y;
-    if (fabs(c) < fabs(dd)) {
-        const double ratio = __ddiv_rn(c, dd);
-        const double denom = __dadd_rn(__dmul_rn(c, ratio), dd);
-        return make_double2(__ddiv_rn(__dadd_rn(__dmul_rn(a, ratio), b), denom),
-                            __ddiv_rn(__dsub_rn(__dmul_rn(b, ratio), a), denom));
-    }
-    const double ratio = __ddiv_rn(dd, c);
-    const double denom = __dadd_rn(__dmul_rn(dd, ratio), c);
-    return make_double2(__ddiv_rn(__dadd_rn(__dmul_rn(b, ratio), a), denom),
-                        __ddiv_rn(__dsub_rn(b, __dmul_rn(a, ratio)), denom));
-}
 
-template <int EPI, int NS, int SK>
-__global__ void __launch_bounds__(256, 2) etd_thomas(const ThomasArgs a) {
-    constexpr int R = EPI == TH_WHAT ? 2 * NS : 1;
-    __shared__ int stop;
-    if (threadIdx.x == 0) stop = *reinterpret_cast<volatile int*>(&a.status->fail);
+template <int MODE, int EPI, int NS, int SK, int NP>
+__global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtensorMap tm, const ThomasArgs a) {
+    using C = ThomasCfg<MODE, EPI, NS>;
+    constexpr int R = C::R, K = C::K, J = C::J, L = C::L, S = C::STAGES, P = C::P;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    double* smem = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::STAGE_DBL);
+    uint64_t* empty = full + S;
+    int* flag = reinterpret_cast<int*>(empty + S);
+    const int t = threadIdx.x, lane = t & 31;
+    if (t == 0) {
+        flag[0] = *reinterpret_cast<volatile int*>(&a.status->fail);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], P / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
-    if (stop) return;
-    const long long T = a.T;
-    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const long long items = EPI == TH_WHAT ? a.npencil : a.npencil * a.nfields;
+    if (flag[0] != 0) return;
+
     const int n = a.n;
-    const long long es = a.es;
+    const int nt = (n + J - 1) / J, nc = (n + K - 1) / K;
+    const int G = gridDim.x;
+    const int my_tiles = a.ntiles > (long long)blockIdx.x ? (int)((a.ntiles - blockIdx.x + G - 1) / G) : 0;
+    const int per_tile = 2 * nt;               // stages: forward then backward per tile
+    const int total = my_tiles * per_tile;
     const double srcA = (EPI == TH_WHAT && SK == 4) ? exp(-a.sp[0] * (a.status->t + a.tau)) : 0.0;
+
+    // ---- producer (thread 0): stage q = (tile i, step s), axis tile forward then reverse
+    auto issue = [&](int q) {
+        const int slot = q % S;
+        const int i = q / per_tile, s = q - i * per_tile;
+        const int jt = s < nt ? s : per_tile - 1 - s;
+        const long long w = blockIdx.x + (long long)i * G;
+        double* dst = smem + slot * C::STAGE_DBL;
+        mbar_expect_tx(&full[slot], C::TX_BYTES);
+        const int pb = (int)(w % a.ptiles);
+        const int rest = (int)(w / a.ptiles);
+        if constexpr (MODE == 1) {
+            const int o = rest % a.nouter, f = a.f_first + rest / a.nouter;
+            tma_load_5d(dst, &tm, &full[slot], 0, jt * J, pb * (P / 16), o, f);
+        } else {
+            const int f = a.f_first + rest;
+#pragma unroll
+            for (int op = 0; op < L; ++op) {
+                const int fld = EPI == TH_WHAT ? op : (op == 0 ? a.fin_off + f : f);
+                tma_load_3d(dst + op * C::OP_DBL, &tm, &full[slot], jt * J, pb * P, fld);
+            }
+        }
+    };
+    int issued = 0;
+    if (t == 0) {
+        tma_prefetch(&tm);
+        for (; issued < total && issued < S; ++issued) issue(issued);
+    }
+    int q = 0;
+    auto acquire = [&]() -> const double* {
+        const int slot = q % S;
+        mbar_wait(&full[slot], (uint32_t)((q / S) & 1));
+        return smem + slot * C::STAGE_DBL;
+    };
+    auto release = [&]() {
+        const int slot = q % S;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        ++q;
+        // refill the slot of the stage before last (every warp is normally past it)
+        if (t == 0)
+            for (; issued < total && issued <= q + S - 2; ++issued) {
+                mbar_wait(&empty[issued % S], (uint32_t)((issued / S - 1) & 1));
+                issue(issued);
+            }
+    };
+    // operand `op` at axis offset jj of this thread's pencil
+    auto rd = [&](const double* st, int op, int jj) -> double {
+        if constexpr (MODE == 1) return st[(t >> 4) * (J * 16) + swz(jj, t & 15)];
+        else return st[op * C::OP_DBL + t * 8 + ((((jj >> 1) ^ ((t >> 1) & 3)) << 1) | (jj & 1))];
+    };
+    auto opr = [](int r) { return EPI == TH_WHAT ? r : 0; };
+    // checkpoints of this thread: (r, l, c) at cpt[((r * NP + l) * nc + c) * G * P]
+    double2* cpt = a.scratch + (long long)blockIdx.x * P + t;
+    const long long cstr = (long long)G * P;
+
     int bad = 0, dom = 0;
-    for (long long it = tid; it < items; it += T) {
-        const int f0 = EPI == TH_WHAT ? 0 : a.f_first + (int)(it / a.npencil);
-        const long long q = EPI == TH_WHAT ? it : it % a.npencil;
-        const long long base = (q % a.pin) * a.sa + (q / a.pin) * a.sb;
-        // right-hand sides: TH_WHAT solves (w1_c, ell 1) and (w2_c, ell 2) for every
-        // species c (stack [w1u,(w1v),w2u,(w2v)]); the others one field
-        const double* src[R];
-        const double2* fc[R];
-        double2 e[R], rr[R][2];
+    for (int i = 0; i < my_tiles; ++i) {
+        const long long w = blockIdx.x + (long long)i * G;
+        const int pb = (int)(w % a.ptiles);
+        const int rest = (int)(w / a.ptiles);
+        const int pen = pb * P + t;  // x (MODE 1) or row (MODE 0)
+        const bool valid = pen < a.npen;
+        int f;
+        long long base;
+        if constexpr (MODE == 1) {
+            f = a.f_first + rest / a.nouter;
+            base = pen + (rest % a.nouter) * a.so;
+        } else {
+            f = a.f_first + rest;
+            base = (long long)pen * a.pitch;
+        }
+        // per rhs: factor rows (mul, 1/piv) of each pole, off-diagonal, residues
+        const double2* mul[R][NP];
+        const double2* inv[R][NP];
+        double er[R];
+        double2 res[R][NP];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int fld = EPI == TH_WHAT ? r : f0;
-            const int c = EPI == TH_WHAT ? r % NS : f0 % a.ns;
+            const int c = EPI == TH_WHAT ? r % NS : f % a.ns;
             const int ell = EPI == TH_WHAT ? (r < NS ? 1 : 2) : a.ell;
-            src[r] = a.in + (long long)fld * a.F + base;
-            fc[r] = a.fac + (long long)c * a.npoles * 3 * n;
-            e[r] = a.e[c];
-            rr[r][0] = a.res[c][ell - 1][0];
-            rr[r][1] = a.res[c][ell - 1][1];
+            er[r] = a.e[c].x;
+#pragma unroll
+            for (int l = 0; l < NP; ++l) {
+                mul[r][l] = a.fac + ((long long)c * NP + l) * 3 * n;
+                inv[r][l] = mul[r][l] + 2 * n;
+                res[r][l] = a.res[c][ell - 1][l];
+            }
         }
-        for (int l = 0; l < a.npoles; ++l) {
-            // forward elimination w_i = b_i - mul_i w_{i-1} (thomas.cpp:38-39, 56-64)
-            double2 wp[R];
+
+        // ---- forward elimination w_i = b_i - mul_i w_{i-1} (thomas.cpp:38-39, 56-64),
+        // checkpointing w_{cK-1} before every chunk c
+        double2 wp[R][NP];
+        auto fwd_point = [&](const double* st, int jj, int j) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                wp[r] = make_double2(__ldg(src[r]), 0.0);
-                a.scratch[(long long)r * n * T + tid] = wp[r];
-            }
-#pragma unroll 4
-            for (int j = 1; j < n; ++j) {
+                const double b = rd(st, opr(r), jj);
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const double b = __ldg(src[r] + j * es);
-                    const double2 m = __ldg(fc[r] + (long long)l * 3 * n + j);
-                    const double2 mw = cmul(m, wp[r]);
-                    wp[r] = make_double2(__dsub_rn(b, mw.x), -mw.y);
-                    a.scratch[((long long)r * n + j) * T + tid] = wp[r];
-                }
-            }
-            // back substitution w_i = (w_i - e w_{i+1}) / piv_i and
-            // out_i += 2 Re(r w_i) (thomas.cpp:40-46, 65-84)
-            const bool last = l == a.npoles - 1;
-            double2 wn[R];
-#pragma unroll 2
-            for (int j = n - 1; j >= 0; --j) {
-                double v[R];
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    double2 w = a.scratch[((long long)r * n + j) * T + tid];
-                    if (j < n - 1) {
-                        const double2 ew = cmul(e[r], wn[r]);
-                        w = make_double2(__dsub_rn(w.x, ew.x), __dsub_rn(w.y, ew.y));
-                    }
-                    const double2* fl = fc[r] + (long long)l * 3 * n;
-                    w = a.xdiv ? cdiv(w, __ldg(fl + n + j)) : cmul(w, __ldg(fl + 2 * n + j));
-                    wn[r] = w;
-                    const double2 rw = cmul(l == 0 ? rr[r][0] : rr[r][1], w);
-                    const double c = __dmul_rn(2.0, rw.x);
-                    const long long ai = ((long long)r * n + j) * T + tid;
-                    v[r] = l == 0 ? __dadd_rn(0.0, c) : __dadd_rn(a.acc[ai], c);
-                    if (!last) a.acc[ai] = v[r];
-                }
-                if (!last) continue;
-                const long long o = base + j * es;
-                if constexpr (EPI == TH_STORE) {
-                    a.out[(long long)f0 * a.F + o] = v[0];
-                } else if constexpr (EPI == TH_UPDATE) {
-                    // U1 = What + tau Q3(fw) (stepper.cpp:225, 252)
-                    const double u1 = __dadd_rn(__ldg(a.aux + (long long)f0 * a.F + o), __dmul_rn(a.tau, v[0]));
-                    a.out[(long long)f0 * a.F + o] = u1;
-                    bad |= !isfinite(u1);
-                } else {
-                    // What = Q1(w1) + tau Q2(w2); fw = f(t + tau, What) - w2
-                    double W[NS], f[NS];
-#pragma unroll
-                    for (int c = 0; c < NS; ++c) W[c] = __dadd_rn(v[c], __dmul_rn(a.tau, v[NS + c]));
-                    if constexpr (NS == 1) {
-                        double ustar = 0.0;
-                        if constexpr (SK == 4) {
-                            const long long row = q;
-                            const int jy = (int)(row % a.ny) + a.gj0, kz = (int)(row / a.ny) + a.gz0;
-                            ustar = srcA * (a.sinx[j] * a.siny[jy] * (a.sinz ? a.sinz[kz] : 1.0));
-                        }
-                        f[0] = src1<SK>(a.sp, W[0], ustar);
-                        if constexpr (SK == 3)
-                            if (j == 0 && q == 0 && a.gj0 == 0 && a.gz0 == 0)
-                                f[0] = __longlong_as_double(0x7ff8000000000000ll);
-                        dom |= src_domain_violation<SK>(W[0]);
+                for (int l = 0; l < NP; ++l) {
+                    if (j == 0) {
+                        wp[r][l] = make_double2(b, 0.0);
                     } else {
-                        src2<SK>(a.sp, W[0], W[1], f[0], f[1]);
-                    }
-#pragma unroll
-                    for (int c = 0; c < NS; ++c) {
-                        bad |= !isfinite(f[c]);
-                        a.out[(long long)c * a.F + o] = W[c];
-                        a.out[(long long)(NS + c) * a.F + o] =
-                            __dsub_rn(f[c], __ldg(a.in + (long long)(NS + c) * a.F + o));
+                        const double2 mw = cmul(__ldg(mul[r][l] + j), wp[r][l]);
+                        wp[r][l] = make_double2(__dsub_rn(b, mw.x), -mw.y);
                     }
                 }
             }
+        };
+        auto checkpoint = [&](int c) {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int l = 0; l < NP; ++l) cpt[((long long)(r * NP + l) * nc + c) * cstr] = wp[r][l];
+        };
+        for (int jt = 0; jt < nt; ++jt) {
+            const double* st = acquire();
+            const int j0 = jt * J;
+            if (jt > 0 && j0 + J <= n) {  // interior stage: no guards
+#pragma unroll
+                for (int jj = 0; jj < J; ++jj) {
+                    if (jj % K == 0) checkpoint((j0 + jj) / K);
+                    fwd_point(st, jj, j0 + jj);
+                }
+            } else {
+#pragma unroll
+                for (int jj = 0; jj < J; ++jj) {
+                    const int j = j0 + jj;
+                    if (j < n) {
+                        if (jj % K == 0 && j > 0) checkpoint(j / K);
+                        fwd_point(st, jj, j);
+                    }
+                }
+            }
+            release();
+        }
+
+        // ---- back substitution w_i = (w_i - e w_{i+1}) / piv_i, out_i += 2 Re(r w_i)
+        // (thomas.cpp:40-46, 65-84), chunk by chunk from the end of the axis: the
+        // chunk's forward values are recomputed from its checkpoint (same bits)
+        double2 wn[R][NP];
+        for (int jt = nt - 1; jt >= 0; --jt) {
+            const double* st = acquire();
+#pragma unroll 1
+            for (int cc = J / K - 1; cc >= 0; --cc) {
+                const int j0 = jt * J + cc * K, c = j0 / K;
+                if (j0 >= n) continue;
+                const bool edge = c == 0 || j0 + K >= n;  // first chunk, or holds j = n - 1
+                double v[R][K];
+#pragma unroll
+                for (int l = 0; l < NP; ++l) {
+                    double2 wv[R][K];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        double2 prev = c > 0 ? cpt[((long long)(r * NP + l) * nc + c) * cstr] : make_double2(0.0, 0.0);
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            const int j = j0 + k;
+                            if (edge && j >= n) break;
+                            const double b = rd(st, opr(r), cc * K + k);
+                            if (edge && j == 0) {
+                                prev = make_double2(b, 0.0);
+                            } else {
+                                const double2 mw = cmul(__ldg(mul[r][l] + j), prev);
+                                prev = make_double2(__dsub_rn(b, mw.x), -mw.y);
+                            }
+                            wv[r][k] = prev;
+                        }
+                    }
+#pragma unroll
+                    for (int k = K - 1; k >= 0; --k) {
+                        const int j = j0 + k;
+                        if (edge && j >= n) continue;
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            double2 x = wv[r][k];
+                            if (!edge || j < n - 1) {
+                                // e is real (tau off kappa): e w componentwise
+                                x = make_double2(__dsub_rn(x.x, __dmul_rn(er[r], wn[r][l].x)),
+                                                 __dsub_rn(x.y, __dmul_rn(er[r], wn[r][l].y)));
+                            }
+                            x = cmul(x, __ldg(inv[r][l] + j));
+                            wn[r][l] = x;
+                            const double con = __dmul_rn(
+                                2.0, __dsub_rn(__dmul_rn(res[r][l].x, x.x), __dmul_rn(res[r][l].y, x.y)));
+                            v[r][k] = l == 0 ? __dadd_rn(0.0, con) : __dadd_rn(v[r][k], con);
+                        }
+                    }
+                }
+                if (!valid) continue;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int j = j0 + k;
+                    if (edge && j >= n) continue;
+                    const long long o = base + (MODE == 0 ? (long long)j : j * a.es);
+                    if constexpr (EPI == TH_STORE) {
+                        a.out[(long long)f * a.F + o] = v[0][k];
+                    } else if constexpr (EPI == TH_UPDATE) {
+                        // U1 = What + tau Q3(fw) (stepper.cpp:225, 252)
+                        const double u1 = __dadd_rn(rd(st, 1, cc * K + k), __dmul_rn(a.tau, v[0][k]));
+                        a.out[(long long)f * a.F + o] = u1;
+                        bad |= !isfinite(u1);
+                    } else {
+                        // What = Q1(w1) + tau Q2(w2); fw = f(t + tau, What) - w2
+                        double W[NS], fv[NS];
+#pragma unroll
+                        for (int s = 0; s < NS; ++s) W[s] = __dadd_rn(v[s][k], __dmul_rn(a.tau, v[NS + s][k]));
+                        if constexpr (NS == 1) {
+                            double ustar = 0.0;
+                            if constexpr (SK == 4) {
+                                const int jy = pen % a.ny + a.gj0, kz = pen / a.ny + a.gz0;
+                                ustar = srcA * (a.sinx[j] * a.siny[jy] * (a.sinz ? a.sinz[kz] : 1.0));
+                            }
+                            fv[0] = src1<SK>(a.sp, W[0], ustar);
+                            if constexpr (SK == 3)
+                                if (j == 0 && pen == 0 && a.gj0 == 0 && a.gz0 == 0)
+                                    fv[0] = __longlong_as_double(0x7ff8000000000000ll);
+                            dom |= src_domain_violation<SK>(W[0]);
+                        } else {
+                            src2<SK>(a.sp, W[0], W[1], fv[0], fv[1]);
+                        }
+#pragma unroll
+                        for (int s = 0; s < NS; ++s) {
+                            bad |= !isfinite(fv[s]);
+                            a.out[(long long)s * a.F + o] = W[s];
+                            a.out[(long long)(NS + s) * a.F + o] = __dsub_rn(fv[s], rd(st, NS + s, cc * K + k));
+                        }
+                    }
+                }
+            }
+            release();
         }
     }
+
     const int any_dom = __syncthreads_or(dom), any_bad = __syncthreads_or(bad);
-    if (threadIdx.x == 0) {
+    if (t == 0) {
         if (any_dom || any_bad) {
             int kind = EPI == TH_WHAT ? 2 : EPI == TH_UPDATE ? 3 : 1;
             if (any_dom) kind = 5;

@@ -23,7 +23,7 @@ TH = etd.BackendKind.Thomas
 
 
 @needs_ref
-@pytest.mark.parametrize("dim,n", [(2, 31), (3, 15), (2, 100), (3, 24)])
+@pytest.mark.parametrize("dim,n", [(2, 31), (3, 15), (2, 100), (3, 24), (2, 64), (3, 32), (2, 8), (3, 4)])
 @pytest.mark.parametrize("family", [0, 1])
 def test_apply_q_thomas_vs_reference(dim, n, family):
     tau, kappa, q = 0.02, 0.7, 1.0
