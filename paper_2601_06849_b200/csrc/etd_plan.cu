@@ -190,12 +190,15 @@ struct ThomasSpec {
     const void* fn = nullptr;
     int smem = 0;
     int occ = 0;  // resident CTAs per SM (set once the smem attribute is applied)
+    int pencils = 128;  // pencils per tile (64 for the lane-pair split predictor)
 };
 template <int MODE, int EPI, int NS, int SK>
 static ThomasSpec thomas_spec(int np) {
     const void* fn = np == 1 ? reinterpret_cast<const void*>(etd_thomas<MODE, EPI, NS, SK, 1>)
                              : reinterpret_cast<const void*>(etd_thomas<MODE, EPI, NS, SK, 2>);
-    return {fn, ThomasCfg<MODE, EPI, NS>::SMEM_BYTES, 0};
+    const int smem = np == 1 ? ThomasCfg<MODE, EPI, NS>::template smem_bytes<1>()
+                             : ThomasCfg<MODE, EPI, NS>::template smem_bytes<2>();
+    return {fn, smem, 0, ThomasCfg<MODE, EPI, NS>::P};
 }
 template <int MODE, int EPI, int NS>
 static ThomasSpec thomas_sk(int sk, int np) {
@@ -653,35 +656,37 @@ struct Plan {
         a.commit = epi == TH_UPDATE;
         const int nfl = epi == TH_WHAT ? 1 : nfields;
         const unsigned long long nst = 2ull * ns;
+        const ThomasSpec k = pick_thomas(mode, epi, ns, d.src_kind, a.npoles);
+        const int PP = k.pencils;
         if (mode == 1) {
             const bool z = axis == 2;
             a.es = z ? v.plane : v.pitch;
             a.so = z ? v.pitch : v.plane;
             a.npen = v.nx;
             a.nouter = z ? v.ny : v.nz;
-            a.ptiles = (v.nx + 127) / 128;
+            a.ptiles = (v.nx + PP - 1) / PP;
             // {x%16, axis, x/16, outer, field}, box {16, 16, 8, 1, 1} -> [x-block][16][16]
             const unsigned long long dims[5] = {16, (unsigned long long)a.n, (unsigned long long)((v.nx + 15) / 16),
                                                 (unsigned long long)a.nouter, nst};
             const unsigned long long st[4] = {(unsigned long long)a.es, 16, (unsigned long long)a.so,
                                               (unsigned long long)v.F};
-            const unsigned box[5] = {16, 16, 8, 1, 1};
+            const unsigned box[5] = {16, 16, (unsigned)(PP / 16), 1, 1};
             o.L.tmA = make_map(stack, 5, dims, st, box);
         } else {
             a.pitch = v.pitch;
             a.npen = v.ny * v.nz;
             a.nouter = 1;
-            a.ptiles = (a.npen + 127) / 128;
-            // {x, row, field}, box {8, 128, 1}, 64B swizzle -> [row][8]
+            a.ptiles = (a.npen + PP - 1) / PP;
+            // {x, row, field}, box {16, pencils, 1}, 128B swizzle -> [row][16]
             const unsigned long long dims[3] = {(unsigned long long)v.nx, (unsigned long long)a.npen, nst};
             const unsigned long long st[2] = {(unsigned long long)v.pitch, (unsigned long long)v.F};
-            const unsigned box[3] = {8, 128, 1};
-            o.L.tmA = make_map(stack, 3, dims, st, box, CU_TENSOR_MAP_SWIZZLE_64B);
+            const unsigned box[3] = {16, (unsigned)PP, 1};
+            o.L.tmA = make_map(stack, 3, dims, st, box);
         }
         a.ntiles = (long long)a.ptiles * a.nouter * nfl;
-        const ThomasSpec k = pick_thomas(mode, epi, ns, d.src_kind, a.npoles);
         const long long G = std::max<long long>(1, std::min<long long>(a.ntiles, (long long)nsm * k.occ));
-        const long long R = thomas_rhs(epi, ns), K = thomas_chunk((int)R);
+        // checkpoints per thread: rhs per thread x poles x chunks (128 threads per CTA)
+        const long long R = (epi == TH_WHAT && ns == 2) ? 2 : thomas_rhs(epi, ns), K = thomas_chunk((int)R);
         th_need = std::max(th_need, R * a.npoles * ((a.n + K - 1) / K) * G * 128);
         o.targs = a;
         o.src_fn = k.fn;
@@ -913,7 +918,9 @@ static void build_plan(Plan& p, const etd_desc& d) {
                 }
             }
         }
-        ETD_CK(cudaMalloc(&p.thfac[a], hf.size() * sizeof(double2)));
+        // padded by one stage of rows: the kernels stage factor slices [jt J, jt J + J)
+        ETD_CK(cudaMalloc(&p.thfac[a], (hf.size() + 64) * sizeof(double2)));
+        ETD_CK(cudaMemset(p.thfac[a], 0, (hf.size() + 64) * sizeof(double2)));
         ETD_CK(cudaMemcpy(p.thfac[a], hf.data(), hf.size() * sizeof(double2), cudaMemcpyHostToDevice));
         tb.fac = p.thfac[a];
     }

@@ -14,8 +14,9 @@
 // individual global loads:
 //   MODE 1 (y/z axes):  5D box {16 x, J, 8 x-blocks, 1, 1}, 128B swizzle
 //                       -> [x-block][J][16]   (the pencils are 128 consecutive x)
-//   MODE 0 (x axis):    3D box {J=8, 128 rows, 1} per operand, 64B swizzle
-//                       -> [row][8]           (the pencils are 128 consecutive rows)
+//   MODE 0 (x axis):    3D box {J=16, 128 rows, 1} per operand, 128B swizzle
+//                       -> [row][16]          (the pencils are 128 consecutive rows)
+// The stage also carries the rows of mul and 1/piv it needs (bulk copies).
 // The forward elimination streams the axis once (all poles together) and keeps
 // one checkpoint per chunk of K points; the back substitution streams it again
 // in reverse, recomputes each chunk's forward values from its checkpoint in
@@ -75,18 +76,36 @@ __host__ __device__ constexpr int thomas_chunk(int rhs) { return rhs >= 2 ? 4 : 
 
 template <int MODE, int EPI, int NS>
 struct ThomasCfg {
-    static constexpr int R = thomas_rhs(EPI, NS);          // right-hand sides per pencil
+    // The coupled two-species predictor (TH_WHAT, NS = 2) splits a pencil over a
+    // lane pair, one species per lane (2 rhs per thread instead of 4: half the
+    // registers, twice the resident warps); the pair swaps its What values with
+    // one shuffle for the coupled source.
+    static constexpr bool SPLIT = EPI == TH_WHAT && NS == 2;
+    static constexpr int R = SPLIT ? 2 : thomas_rhs(EPI, NS);  // right-hand sides per thread
     static constexpr int K = thomas_chunk(R);              // back-substitution chunk
-    static constexpr int P = 128;                          // pencils (threads) per tile
-    static constexpr int J = MODE == 0 ? 8 : 16;           // axis points per stage
+    static constexpr int T = 128;                          // threads per CTA
+    static constexpr int P = SPLIT ? 64 : 128;             // pencils per tile
+    static constexpr int J = 16;                           // axis points per stage
     static constexpr int L = MODE == 0 ? (EPI == TH_WHAT ? 2 * NS : EPI == TH_UPDATE ? 2 : 1) : 1;
-    static constexpr int STAGES = L >= 4 ? 3 : 4;
+    static constexpr int STAGES = 3;
     static constexpr int OP_DBL = P * J;
     static constexpr int STAGE_DBL = L * OP_DBL;
-    static constexpr uint32_t TX_BYTES = STAGE_DBL * 8;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_DBL * 8 + 1024 + 2 * STAGES * 8 + 16;
+    static constexpr int NSU = EPI == TH_WHAT ? NS : 1;    // species whose factors a stage carries
+    static constexpr int FAC_BYTES = J * 16;               // one factor row slice (mul or 1/piv)
+    template <int NP>
+    static constexpr int smem_bytes() {
+        return STAGES * STAGE_DBL * 8 + STAGES * NSU * NP * 2 * FAC_BYTES + 1024 + 2 * STAGES * 8 + 16;
+    }
     static_assert(J % K == 0, "chunks tile the stages");
 };
+
+// non-tensor bulk copy global -> shared, completing on an mbarrier
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
@@ -97,9 +116,13 @@ template <int MODE, int EPI, int NS, int SK, int NP>
 __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtensorMap tm, const ThomasArgs a) {
     using C = ThomasCfg<MODE, EPI, NS>;
     constexpr int R = C::R, K = C::K, J = C::J, L = C::L, S = C::STAGES, P = C::P;
+    constexpr bool SPLIT = C::SPLIT;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     double* smem = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::STAGE_DBL);
+    // factor row slices per stage: [stage][species u][pole][mul, 1/piv][J]
+    double2* fsl = reinterpret_cast<double2*>(smem + S * C::STAGE_DBL);
+    constexpr int FS_STAGE = C::NSU * NP * 2 * J;  // double2 per stage
+    uint64_t* full = reinterpret_cast<uint64_t*>(fsl + S * FS_STAGE);
     uint64_t* empty = full + S;
     int* flag = reinterpret_cast<int*>(empty + S);
     const int t = threadIdx.x, lane = t & 31;
@@ -107,7 +130,7 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
         flag[0] = *reinterpret_cast<volatile int*>(&a.status->fail);
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], P / 32);
+            mbar_init(&empty[s], C::T / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -129,16 +152,32 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
         const int jt = s < nt ? s : per_tile - 1 - s;
         const long long w = blockIdx.x + (long long)i * G;
         double* dst = smem + slot * C::STAGE_DBL;
-        mbar_expect_tx(&full[slot], C::TX_BYTES);
+        // the forward sweep needs neither the 1/piv rows nor (TH_UPDATE) the What operand
+        const bool fwd = s < nt;
+        const int nops = (EPI == TH_UPDATE && fwd) ? 1 : L, nrows = fwd ? 1 : 2;
+        mbar_expect_tx(&full[slot], (uint32_t)(nops * C::OP_DBL * 8 + C::NSU * NP * nrows * C::FAC_BYTES));
         const int pb = (int)(w % a.ptiles);
         const int rest = (int)(w / a.ptiles);
+        {
+            // the stage's rows of mul and 1/piv (the factor arrays are padded past n)
+            const int f0 = MODE == 1 ? a.f_first + rest / a.nouter : a.f_first + rest;
+#pragma unroll
+            for (int u = 0; u < C::NSU; ++u) {
+                const int c = EPI == TH_WHAT ? u : f0 % a.ns;
+#pragma unroll
+                for (int l = 0; l < NP; ++l)
+                    for (int m = 0; m < nrows; ++m)
+                        bulk_load(fsl + slot * FS_STAGE + ((u * NP + l) * 2 + m) * J,
+                                  a.fac + (((long long)c * NP + l) * 3 + 2 * m) * n + jt * J, C::FAC_BYTES,
+                                  &full[slot]);
+            }
+        }
         if constexpr (MODE == 1) {
             const int o = rest % a.nouter, f = a.f_first + rest / a.nouter;
             tma_load_5d(dst, &tm, &full[slot], 0, jt * J, pb * (P / 16), o, f);
         } else {
             const int f = a.f_first + rest;
-#pragma unroll
-            for (int op = 0; op < L; ++op) {
+            for (int op = 0; op < nops; ++op) {
                 const int fld = EPI == TH_WHAT ? op : (op == 0 ? a.fin_off + f : f);
                 tma_load_3d(dst + op * C::OP_DBL, &tm, &full[slot], jt * J, pb * P, fld);
             }
@@ -167,22 +206,25 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                 issue(issued);
             }
     };
+    // this thread's pencil within the tile, and (SPLIT) its species
+    const int tp = SPLIT ? t >> 1 : t, sl = SPLIT ? t & 1 : 0;
     // operand `op` at axis offset jj of this thread's pencil
     auto rd = [&](const double* st, int op, int jj) -> double {
-        if constexpr (MODE == 1) return st[(t >> 4) * (J * 16) + swz(jj, t & 15)];
-        else return st[op * C::OP_DBL + t * 8 + ((((jj >> 1) ^ ((t >> 1) & 3)) << 1) | (jj & 1))];
+        if constexpr (MODE == 1) return st[(tp >> 4) * (J * 16) + swz(jj, tp & 15)];
+        else return st[op * C::OP_DBL + swz(tp, jj)];
     };
-    auto opr = [](int r) { return EPI == TH_WHAT ? r : 0; };
+    // operand (= global rhs index for TH_WHAT) of this thread's rhs r
+    auto opr = [&](int r) { return EPI == TH_WHAT ? (SPLIT ? r * NS + sl : r) : 0; };
     // checkpoints of this thread: (r, l, c) at cpt[((r * NP + l) * nc + c) * G * P]
-    double2* cpt = a.scratch + (long long)blockIdx.x * P + t;
-    const long long cstr = (long long)G * P;
+    double2* cpt = a.scratch + (long long)blockIdx.x * C::T + t;
+    const long long cstr = (long long)G * C::T;
 
     int bad = 0, dom = 0;
     for (int i = 0; i < my_tiles; ++i) {
         const long long w = blockIdx.x + (long long)i * G;
         const int pb = (int)(w % a.ptiles);
         const int rest = (int)(w / a.ptiles);
-        const int pen = pb * P + t;  // x (MODE 1) or row (MODE 0)
+        const int pen = pb * P + tp;  // x (MODE 1) or row (MODE 0)
         const bool valid = pen < a.npen;
         int f;
         long long base;
@@ -193,23 +235,23 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
             f = a.f_first + rest;
             base = (long long)pen * a.pitch;
         }
-        // per rhs: factor rows (mul, 1/piv) of each pole, off-diagonal, residues
-        const double2* mul[R][NP];
-        const double2* inv[R][NP];
+        // per rhs: off-diagonal and residues; factor rows come from the stage
         double er[R];
         double2 res[R][NP];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int c = EPI == TH_WHAT ? r % NS : f % a.ns;
-            const int ell = EPI == TH_WHAT ? (r < NS ? 1 : 2) : a.ell;
+            const int c = EPI == TH_WHAT ? (SPLIT ? sl : r % NS) : f % a.ns;
+            const int ell = EPI == TH_WHAT ? (SPLIT ? r + 1 : (r < NS ? 1 : 2)) : a.ell;
             er[r] = a.e[c].x;
 #pragma unroll
-            for (int l = 0; l < NP; ++l) {
-                mul[r][l] = a.fac + ((long long)c * NP + l) * 3 * n;
-                inv[r][l] = mul[r][l] + 2 * n;
-                res[r][l] = a.res[c][ell - 1][l];
-            }
+            for (int l = 0; l < NP; ++l) res[r][l] = a.res[c][ell - 1][l];
         }
+        // factor slice of rhs r, pole l, row m (0 mul, 1 1/piv) in the stage at `st`
+        auto fs = [&](const double* st, int r, int l, int m) -> const double2* {
+            const int slot = (int)((st - smem) / C::STAGE_DBL);
+            const int u = EPI == TH_WHAT ? (SPLIT ? sl : r % NS) : 0;
+            return fsl + slot * FS_STAGE + ((u * NP + l) * 2 + m) * J;
+        };
 
         // ---- forward elimination w_i = b_i - mul_i w_{i-1} (thomas.cpp:38-39, 56-64),
         // checkpointing w_{cK-1} before every chunk c
@@ -223,7 +265,7 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                     if (j == 0) {
                         wp[r][l] = make_double2(b, 0.0);
                     } else {
-                        const double2 mw = cmul(__ldg(mul[r][l] + j), wp[r][l]);
+                        const double2 mw = cmul(fs(st, r, l, 0)[jj], wp[r][l]);
                         wp[r][l] = make_double2(__dsub_rn(b, mw.x), -mw.y);
                     }
                 }
@@ -283,7 +325,7 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                             if (edge && j == 0) {
                                 prev = make_double2(b, 0.0);
                             } else {
-                                const double2 mw = cmul(__ldg(mul[r][l] + j), prev);
+                                const double2 mw = cmul(fs(st, r, l, 0)[cc * K + k], prev);
                                 prev = make_double2(__dsub_rn(b, mw.x), -mw.y);
                             }
                             wv[r][k] = prev;
@@ -301,13 +343,34 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                                 x = make_double2(__dsub_rn(x.x, __dmul_rn(er[r], wn[r][l].x)),
                                                  __dsub_rn(x.y, __dmul_rn(er[r], wn[r][l].y)));
                             }
-                            x = cmul(x, __ldg(inv[r][l] + j));
+                            x = cmul(x, fs(st, r, l, 1)[cc * K + k]);
                             wn[r][l] = x;
                             const double con = __dmul_rn(
                                 2.0, __dsub_rn(__dmul_rn(res[r][l].x, x.x), __dmul_rn(res[r][l].y, x.y)));
                             v[r][k] = l == 0 ? __dadd_rn(0.0, con) : __dadd_rn(v[r][k], con);
                         }
                     }
+                }
+                if constexpr (SPLIT) {
+                    // What of this lane's species; the pair swaps them for f(t + tau, What)
+                    // (all lanes of the warp take this path: same chunk, same guards)
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const int j = j0 + k;
+                        if (edge && j >= n) continue;
+                        const double Wm = __dadd_rn(v[0][k], __dmul_rn(a.tau, v[1][k]));
+                        const double Wo = __shfl_xor_sync(0xffffffffu, Wm, 1);
+                        if (!valid) continue;
+                        const double Wu = sl == 0 ? Wm : Wo, Wv = sl == 0 ? Wo : Wm;
+                        double fu, fv;
+                        src2<SK>(a.sp, Wu, Wv, fu, fv);
+                        const double fm = sl == 0 ? fu : fv;
+                        bad |= !isfinite(fm);
+                        const long long o = base + j;
+                        a.out[(long long)sl * a.F + o] = Wm;
+                        a.out[(long long)(NS + sl) * a.F + o] = __dsub_rn(fm, rd(st, NS + sl, cc * K + k));
+                    }
+                    continue;
                 }
                 if (!valid) continue;
 #pragma unroll
@@ -322,7 +385,7 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                         const double u1 = __dadd_rn(rd(st, 1, cc * K + k), __dmul_rn(a.tau, v[0][k]));
                         a.out[(long long)f * a.F + o] = u1;
                         bad |= !isfinite(u1);
-                    } else {
+                    } else if constexpr (!SPLIT) {
                         // What = Q1(w1) + tau Q2(w2); fw = f(t + tau, What) - w2
                         double W[NS], fv[NS];
 #pragma unroll
