@@ -101,13 +101,15 @@ int etd_slab_range(const etd_handle* h, int* z0, int* z1);
 /* The balanced partition every sharded plan uses for z planes (x/y stages) and
  * y rows (z stage): rank r gets [lo, hi), sizes differ by at most one.  Host only. */
 int etd_zslab_partition(int n, int world_size, int rank, int* lo, int* hi);
-/* The data movement of one sharded step for rank `rank` (host only): records of
- * 12 int64 {kind(0 copy2d,1 send,2 recv), phase(0 pack,1 fwd,2 back,3 unpack),
+/* The data movement of one sharded step for rank `rank` (host only), with the
+ * z stage split into `chunks` chunks of each rank's y rows (plans use 4): records
+ * of 13 int64 {kind(0 copy2d,1 send,2 recv), phase(0 pack,1 fwd,2 back,3 unpack),
  * peer, dst_buf, dst_off, dst_pitch, src_buf, src_off, src_pitch, width, height,
- * count}, element units; buffers 0 state,1 send,2 zin,3 wz,4 recv,5 w.
+ * count, chunk}, element units; buffers 0 state,1 send,2 zin,3 wz,4 recv,5 w
+ * (zin / wz: the chunk blocks [2 nspecies][nz][chunk rows][pitch] back to back).
  * out may be NULL to query *count. */
 int etd_sharded_schedule(int nx, int ny, int nz, int nspecies, int world_size, int rank, long long pitch,
-                         long long* out, int capacity, int* count);
+                         int chunks, long long* out, int capacity, int* count);
 /* 128-byte ncclUniqueId for etd_desc.nccl_unique_id (rank 0 creates, all ranks
  * receive it out of band, e.g. over torch.distributed). */
 int etd_nccl_unique_id(void* out128);

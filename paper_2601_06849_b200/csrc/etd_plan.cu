@@ -315,7 +315,10 @@ struct Piece {
 };
 
 struct Op {
-    enum Kind { KERNEL, SOURCE, COPY2D, EXCHANGE, FAILCODE, COMMIT, THOMAS } kind = KERNEL;
+    enum Kind { KERNEL, SOURCE, COPY2D, EXCHANGE, FAILCODE, COMMIT, THOMAS, NOP } kind = KERNEL;
+    // sharded steps: 1 = run on the communication stream; events (indices into
+    // Plan::sev) waited on before / recorded after the op (ignored by virtual ranks)
+    int strm = 0, wait_ev = -1, rec_ev = -1;
     Launch L;                                    // KERNEL (and SOURCE/THOMAS: name/flops/bytes)
     SourceArgs sargs{};                          // SOURCE
     ThomasArgs targs{};                          // THOMAS
@@ -356,6 +359,14 @@ static void partition(int n, int G, int r, int& lo, int& hi) {
 // into device ops and etd_sharded_schedule exports them for the CPU
 // multi-process test (tests/test_dist_cpu.py), which runs the same schedule
 // over gloo.
+//
+// The z stage runs in `C` chunks of each rank's y rows so the exchanges overlap
+// the z transforms: the forward exchange of chunk k+1 and the backward
+// exchange of chunk k-1 run on the communication stream while chunk k's source
+// pass and z transforms run on the compute stream.  Chunk k of rank r owns the
+// rows partition(njr, C, k) of its y-row range; its z-stage buffers are a
+// separate [field][z][row][x] block (zin/Zz/Wz are the concatenation of the
+// chunk blocks), so every exchanged piece lands contiguously.
 enum SchedBuf { SB_STATE = 0, SB_SEND = 1, SB_ZIN = 2, SB_WZ = 3, SB_RECV = 4, SB_W = 5 };
 enum SchedKind { SK_COPY = 0, SK_SEND = 1, SK_RECV = 2 };
 enum SchedPhase { SP_PACK = 0, SP_FWD = 1, SP_BACK = 2, SP_UNPACK = 3 };
@@ -364,57 +375,97 @@ struct SchedRec {
     long long dbuf, doff, dpitch;   // COPY: 2D copy, width/height in elements/rows
     long long sbuf, soff, spitch;   // SEND/RECV: buffer in (sbuf|dbuf), offset, count
     long long width, height, count;
+    long long chunk;                // z-stage chunk the record belongs to
 };
+static constexpr int kZChunks = 4;  // z-stage chunks of a sharded step
 
-static std::vector<SchedRec> sharded_schedule(int nx, int ny, int nz, int ns, int G, int r, long long pitch) {
+// Rows [lo, hi) (relative to rank s's first y row) of chunk k, and the
+// element offset of rank r's chunk-k z-stage block (2 ns fields of nz * rows * pitch).
+struct ZChunks {
+    int G, C;
+    std::vector<int> zl, zh, jl, jh;
+    long long ns2, pitch, nz;
+    void rows(int s, int k, int& lo, int& hi) const { partition(jh[s] - jl[s], C, k, lo, hi); }
+    long long nrows(int s, int k) const { int a, b; rows(s, k, a, b); return b - a; }
+    long long base(int r, int k) const {
+        long long o = 0;
+        for (int i = 0; i < k; ++i) o += ns2 * nz * nrows(r, i) * pitch;
+        return o;
+    }
+};
+static ZChunks zchunks(int ny, int nz, int ns, int G, long long pitch, int C) {
+    ZChunks z{G, C, std::vector<int>(G), std::vector<int>(G), std::vector<int>(G), std::vector<int>(G),
+              2LL * ns, pitch, nz};
+    for (int s = 0; s < G; ++s) {
+        partition(nz, G, s, z.zl[s], z.zh[s]);
+        partition(ny, G, s, z.jl[s], z.jh[s]);
+    }
+    return z;
+}
+
+static std::vector<SchedRec> sharded_schedule(int nx, int ny, int nz, int ns, int G, int r, long long pitch,
+                                              int C) {
     (void)nx;
-    std::vector<int> zl(G), zh(G), jl(G), jh(G);
-    for (int s = 0; s < G; ++s) {
-        partition(nz, G, s, zl[s], zh[s]);
-        partition(ny, G, s, jl[s], jh[s]);
-    }
-    const long long nzr = zh[r] - zl[r], njr = jh[r] - jl[r];
-    const long long plane = pitch * ny, F = plane * nzr;            // slab field
-    const long long planez = pitch * njr, Fz = planez * nz;         // z-stage field
-    std::vector<long long> sblock(G), roff(G);
+    const ZChunks zc = zchunks(ny, nz, ns, G, pitch, C);
+    const long long nzr = zc.zh[r] - zc.zl[r];
+    const long long plane = pitch * ny, F = plane * nzr;  // slab field
+    // send blocks (peer s, chunk k): [c < ns][z in my slab][rows of (s,k)][x]
+    // receive blocks (peer s, chunk k): [c < 2 ns][z in my slab][rows of (s,k)][x]
+    std::vector<long long> sblock(G * C), rblock(G * C);
     long long so = 0, ro = 0;
-    for (int s = 0; s < G; ++s) {
-        const long long njs = jh[s] - jl[s];
-        sblock[s] = so;
-        so += ns * nzr * njs * pitch;
-        roff[s] = ro;
-        ro += nzr * njs * pitch;
-    }
+    for (int s = 0; s < G; ++s)
+        for (int k = 0; k < C; ++k) {
+            const long long nk = zc.nrows(s, k);
+            sblock[s * C + k] = so;
+            so += ns * nzr * nk * pitch;
+            rblock[s * C + k] = ro;
+            ro += 2 * ns * nzr * nk * pitch;
+        }
     std::vector<SchedRec> out;
-    // pack: state[c][zl][j in rows(s)][:] -> send[s][c][zl][jj][:]
-    for (int s = 0; s < G; ++s) {
-        const long long njs = jh[s] - jl[s];
-        for (int c = 0; c < ns; ++c)
-            out.push_back({SK_COPY, SP_PACK, s, SB_SEND, sblock[s] + c * nzr * njs * pitch, njs * pitch, SB_STATE,
-                           c * F + jl[s] * pitch, plane, njs * pitch, nzr, njs * pitch * nzr});
-    }
-    // forward exchange: (s, c) blocks; receiver stores z in slab(s) contiguously
-    for (int s = 0; s < G; ++s) {
-        const long long njs = jh[s] - jl[s], nzs = zh[s] - zl[s];
-        for (int c = 0; c < ns; ++c) {
-            out.push_back({SK_SEND, SP_FWD, s, 0, 0, 0, SB_SEND, sblock[s] + c * nzr * njs * pitch, 0, 0, 0,
-                           nzr * njs * pitch});
-            out.push_back({SK_RECV, SP_FWD, s, SB_ZIN, c * Fz + zl[s] * planez, 0, 0, 0, 0, 0, 0, nzs * planez});
+    auto rec = [&](SchedRec x) { out.push_back(x); };
+    // pack: state[c][my z][rows of (s,k)] -> send[(s,k)][c]
+    for (int s = 0; s < G; ++s)
+        for (int k = 0; k < C; ++k) {
+            int a, b;
+            zc.rows(s, k, a, b);
+            const long long nk = b - a;
+            if (nk == 0) continue;
+            for (int c = 0; c < ns; ++c)
+                rec({SK_COPY, SP_PACK, s, SB_SEND, sblock[s * C + k] + c * nzr * nk * pitch, nk * pitch, SB_STATE,
+                     c * F + (zc.jl[s] + a) * pitch, plane, nk * pitch, nzr, nk * pitch * nzr, k});
         }
-    }
-    // backward exchange of the 2ns z-filtered fields
-    for (int c = 0; c < 2 * ns; ++c)
+    for (int k = 0; k < C; ++k) {
+        const long long mk = zc.nrows(r, k), planek = pitch * mk, Fk = planek * nz, bk = zc.base(r, k);
+        // forward exchange of chunk k: my rows' z planes from every peer
         for (int s = 0; s < G; ++s) {
-            const long long njs = jh[s] - jl[s], nzs = zh[s] - zl[s];
-            out.push_back({SK_SEND, SP_BACK, s, 0, 0, 0, SB_WZ, c * Fz + zl[s] * planez, 0, 0, 0, nzs * planez});
-            out.push_back({SK_RECV, SP_BACK, s, SB_RECV, c * F + roff[s], 0, 0, 0, 0, 0, 0, nzr * njs * pitch});
+            const long long nks = zc.nrows(s, k), nzs = zc.zh[s] - zc.zl[s];
+            for (int c = 0; c < ns; ++c) {
+                if (nks) rec({SK_SEND, SP_FWD, s, 0, 0, 0, SB_SEND, sblock[s * C + k] + c * nzr * nks * pitch, 0, 0, 0,
+                              nzr * nks * pitch, k});
+                if (mk) rec({SK_RECV, SP_FWD, s, SB_ZIN, bk + c * Fk + zc.zl[s] * planek, 0, 0, 0, 0, 0, 0,
+                             nzs * planek, k});
+            }
         }
-    // unpack: recv[c][s][zl][jj][:] -> W[c][zl][j in rows(s)][:]
-    for (int c = 0; c < 2 * ns; ++c)
-        for (int s = 0; s < G; ++s) {
-            const long long njs = jh[s] - jl[s];
-            out.push_back({SK_COPY, SP_UNPACK, s, SB_W, c * F + jl[s] * pitch, plane, SB_RECV, c * F + roff[s],
-                           njs * pitch, njs * pitch, nzr, njs * pitch * nzr});
+        // backward exchange of chunk k: the 2 ns z-filtered fields back to the slab owners
+        for (int c = 0; c < 2 * ns; ++c)
+            for (int s = 0; s < G; ++s) {
+                const long long nks = zc.nrows(s, k), nzs = zc.zh[s] - zc.zl[s];
+                if (mk) rec({SK_SEND, SP_BACK, s, 0, 0, 0, SB_WZ, bk + c * Fk + zc.zl[s] * planek, 0, 0, 0,
+                             nzs * planek, k});
+                if (nks) rec({SK_RECV, SP_BACK, s, SB_RECV, rblock[s * C + k] + c * nzr * nks * pitch, 0, 0, 0, 0, 0,
+                              0, nzr * nks * pitch, k});
+            }
+    }
+    // unpack: recv[(s,k)][c][my z][rows] -> W[c][my z][rows of (s,k)]
+    for (int s = 0; s < G; ++s)
+        for (int k = 0; k < C; ++k) {
+            int a, b;
+            zc.rows(s, k, a, b);
+            const long long nk = b - a;
+            if (nk == 0) continue;
+            for (int c = 0; c < 2 * ns; ++c)
+                rec({SK_COPY, SP_UNPACK, s, SB_W, c * F + (zc.jl[s] + a) * pitch, plane, SB_RECV,
+                     rblock[s * C + k] + c * nzr * nk * pitch, nk * pitch, nk * pitch, nzr, nk * pitch * nzr, k});
         }
     return out;
 }
@@ -427,7 +478,12 @@ struct Plan {
     int nx = 1, ny = 1, nz = 1;      // global interior extents
     int npad[3] = {0, 0, 0};
     long long pitch = 0;
-    View slab, zst;                  // x/y-stage (z-slab) view, z-stage (y-rows) view
+    View slab;                       // x/y-stage (z-slab) view
+    std::vector<View> zch;           // sharded: z-stage views of this rank's y-row chunks
+    std::vector<long long> zbase;    //   and their offsets in zin / Zz / Wz
+    int zC = 1;                      // z-stage chunks
+    cudaStream_t xstream = nullptr;  // sharded: exchange stream (high priority)
+    std::vector<cudaEvent_t> sev;    // sharded: stream-ordering events
     std::vector<int> zlo, zhi, jlo, jhi;
     double tau = 0;
     cudaStream_t stream = nullptr;
@@ -482,6 +538,8 @@ struct Plan {
         if (status_host) cudaFreeHost(status_host);
         if (comm) Nccl::get().CommDestroy(comm);
         for (auto e : xev) cudaEventDestroy(e);
+        for (auto e : sev) cudaEventDestroy(e);
+        if (xstream) cudaStreamDestroy(xstream);
         if (cstream) cudaStreamDestroy(cstream);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -844,10 +902,18 @@ static void build_plan(Plan& p, const etd_desc& d) {
     const int R = p.rank;
     p.slab = View{p.nx, p.ny, p.zhi[R] - p.zlo[R], p.pitch, p.pitch * p.ny, 0, 0, p.zlo[R]};
     p.slab.F = p.slab.plane * p.slab.nz;
-    p.zst = p.slab;
     if (p.sharded) {
-        p.zst = View{p.nx, p.jhi[R] - p.jlo[R], p.nz, p.pitch, p.pitch * (p.jhi[R] - p.jlo[R]), 0, p.jlo[R], 0};
-        p.zst.F = p.zst.plane * p.zst.nz;
+        p.zC = kZChunks;
+        if (const char* e = std::getenv("ETD_ZCHUNKS")) p.zC = std::max(1, std::atoi(e));
+        const ZChunks zc = zchunks(p.ny, p.nz, p.ns, p.G, p.pitch, p.zC);
+        for (int k = 0; k < p.zC; ++k) {
+            int a, b;
+            zc.rows(R, k, a, b);
+            View v{p.nx, b - a, p.nz, p.pitch, p.pitch * (b - a), 0, p.jlo[R] + a, 0};
+            v.F = v.plane * v.nz;
+            p.zch.push_back(v);
+            p.zbase.push_back(zc.base(R, k));
+        }
     }
 
     ETD_CK(cudaStreamCreateWithFlags(&p.stream, cudaStreamNonBlocking));
@@ -860,7 +926,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
     alloc(p.Z, F * 2 * p.ns);
     alloc(p.W, F * 2 * p.ns);
     if (p.sharded) {
-        const size_t Fz = (size_t)p.zst.F;
+        const size_t Fz = (size_t)p.pitch * (p.jhi[R] - p.jlo[R]) * p.nz;
         alloc(p.sendbuf, F * p.ns);
         alloc(p.zin, Fz * 2 * p.ns);
         alloc(p.Zz, Fz * 2 * p.ns);
@@ -1027,7 +1093,6 @@ static void build_plan(Plan& p, const etd_desc& d) {
     const char* fenv = std::getenv("ETD_FUSED_SOURCE");
     const bool fused = fenv && fenv[0] == '1';
     const View& V = p.slab;
-    const View& VZ = p.zst;
     for (int par = 0; par < 2; ++par) {
         auto& L = p.steps[par];
         L.clear();
@@ -1064,31 +1129,71 @@ static void build_plan(Plan& p, const etd_desc& d) {
             first_transform(V, 2, const_cast<double*>(in), p.Z);
             L.push_back(kernel_op(p.transform(V, "z_back", 2, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
         } else if (p.dim == 3) {
-            // ---- z-stage on y-row partitions: pack, exchange, filter, exchange back, unpack ----
-            const auto sched = sharded_schedule(p.nx, p.ny, p.nz, ns, p.G, p.rank, p.pitch);
+            // ---- z stage on y-row chunks: pack; forward exchanges (comm stream);
+            // per chunk source + z transforms (compute stream) overlapping the next
+            // chunk's forward and the previous chunk's backward exchange; unpack ----
+            const int C = p.zC;
+            const int EV_PACK = 0, EV_B = 1;
+            auto EV_F = [&](int k) { return 2 + k; };
+            auto EV_Z = [&](int k) { return 2 + C + k; };
+            const auto sched = sharded_schedule(p.nx, p.ny, p.nz, ns, p.G, p.rank, p.pitch, C);
             double* bufs[6] = {const_cast<double*>(in), p.sendbuf, p.zin, p.Wz, p.recvb, p.W};
-            auto add_phase = [&](int phase, const char* name) {
+            auto exchange = [&](int phase, int k, const char* name) {
                 Op ex;
                 ex.kind = Op::EXCHANGE;
                 ex.name = name;
+                ex.strm = 1;
                 for (const auto& r : sched) {
-                    if (r.phase != phase) continue;
-                    if (r.kind == SK_COPY)
-                        L.push_back(copy_op(name, bufs[r.dbuf] + r.doff, r.dpitch * 8, bufs[r.sbuf] + r.soff,
-                                            r.spitch * 8, r.width * 8, r.height));
-                    else if (r.kind == SK_SEND)
+                    if (r.phase != phase || r.chunk != k) continue;
+                    if (r.kind == SK_SEND)
                         ex.sends.push_back({(int)r.peer, bufs[r.sbuf] + r.soff, (size_t)r.count * 8});
-                    else
+                    else if (r.kind == SK_RECV)
                         ex.recvs.push_back({(int)r.peer, bufs[r.dbuf] + r.doff, (size_t)r.count * 8});
                 }
-                if (!ex.sends.empty()) L.push_back(ex);
+                return ex;
             };
-            add_phase(SP_PACK, "pack");
-            add_phase(SP_FWD, "a2a_fwd");
-            first_transform(VZ, 2, p.zin, p.Zz);
-            L.push_back(kernel_op(p.transform(VZ, "z_back", 2, true, 2 * ns, EPI_STORE, false, p.Zz, p.Wz)));
-            add_phase(SP_BACK, "a2a_back");
-            add_phase(SP_UNPACK, "unpack");
+            auto copies = [&](int phase, const char* name) {
+                const size_t first = L.size();
+                for (const auto& r : sched)
+                    if (r.phase == phase && r.kind == SK_COPY)
+                        L.push_back(copy_op(name, bufs[r.dbuf] + r.doff, r.dpitch * 8, bufs[r.sbuf] + r.soff,
+                                            r.spitch * 8, r.width * 8, r.height));
+                return first;
+            };
+            copies(SP_PACK, "pack");
+            L.back().rec_ev = EV_PACK;
+            for (int k = 0; k < C; ++k) {
+                Op f = exchange(SP_FWD, k, "a2a_fwd");
+                if (k == 0) f.wait_ev = EV_PACK;
+                f.rec_ev = EV_F(k);
+                L.push_back(f);
+            }
+            for (int k = 0; k < C; ++k) {
+                const View& vk = p.zch[k];
+                const size_t first = L.size();
+                if (vk.ny > 0) {
+                    double* zin_k = p.zin + p.zbase[k];
+                    double* zz_k = p.Zz + p.zbase[k];
+                    double* wz_k = p.Wz + p.zbase[k];
+                    first_transform(vk, 2, zin_k, zz_k);
+                    L.push_back(kernel_op(p.transform(vk, "z_back", 2, true, 2 * ns, EPI_STORE, false, zz_k, wz_k)));
+                } else {
+                    // an empty chunk keeps the op list aligned across virtual ranks
+                    for (int i = 0; i < (fused ? 2 : 3); ++i) {
+                        Op o;
+                        o.kind = Op::NOP;
+                        o.name = "z_empty";
+                        L.push_back(o);
+                    }
+                }
+                L[first].wait_ev = EV_F(k);
+                L.back().rec_ev = EV_Z(k);
+                Op b = exchange(SP_BACK, k, "a2a_back");
+                b.wait_ev = EV_Z(k);
+                b.rec_ev = EV_B;
+                L.push_back(b);
+            }
+            L[copies(SP_UNPACK, "unpack")].wait_ev = EV_B;
         }
         if (p.dim == 3) {
             L.push_back(kernel_op(p.transform(V, "y_fwd", 1, false, 2 * ns, EPI_SCALE, false, p.W, p.Z)));
@@ -1127,6 +1232,13 @@ static void build_plan(Plan& p, const etd_desc& d) {
         }
     }
     if (p.thomas) ensure_thomas_scratch(p, p.th_need);
+    if (p.sharded && !p.local_group) {
+        int lo = 0, hi = 0;
+        ETD_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        ETD_CK(cudaStreamCreateWithPriority(&p.xstream, cudaStreamNonBlocking, hi));
+        p.sev.resize(2 + 2 * p.zC);
+        for (auto& e : p.sev) ETD_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     p.stats.clear();
     for (auto& op : p.steps[0])
         if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS)
@@ -1141,9 +1253,19 @@ static void launch(const Launch& L, cudaStream_t s) {
 }
 
 // One op of one rank.  EXCHANGE over NCCL here; virtual-rank groups route
-// exchanges through run_group_exchange instead.
-static void run_op(Plan& p, const Op& op, cudaStream_t s) {
+// exchanges through group_steps instead.
+static void run_op_body(Plan& p, const Op& op, cudaStream_t s);
+static void run_op(Plan& p, const Op& op, cudaStream_t s0) {
+    const bool ev = p.xstream && !p.local_group;
+    const cudaStream_t s = (ev && op.strm == 1) ? p.xstream : s0;
+    if (ev && op.wait_ev >= 0) ETD_CK(cudaStreamWaitEvent(s, p.sev[op.wait_ev], 0));
+    run_op_body(p, op, s);
+    if (ev && op.rec_ev >= 0) ETD_CK(cudaEventRecord(p.sev[op.rec_ev], s));
+}
+
+static void run_op_body(Plan& p, const Op& op, cudaStream_t s) {
     switch (op.kind) {
+    case Op::NOP: break;
     case Op::KERNEL: launch(op.L, s); break;
     case Op::COPY2D:
         ETD_CK(cudaMemcpy2DAsync(op.dst, op.dpitch, op.src, op.spitch, op.width, op.height,
@@ -1727,11 +1849,11 @@ int etd_zslab_partition(int n, int world_size, int rank, int* lo, int* hi) {
 }
 
 int etd_sharded_schedule(int nx, int ny, int nz, int nspecies, int world_size, int rank, long long pitch,
-                         long long* out, int capacity, int* count) {
+                         int chunks, long long* out, int capacity, int* count) {
     if (!count || world_size < 1 || rank < 0 || rank >= world_size || world_size > nz || world_size > ny ||
-        nspecies < 1 || nspecies > 2 || pitch < nx)
+        nspecies < 1 || nspecies > 2 || pitch < nx || chunks < 1)
         return ETD_ERR_CONFIG;
-    const auto recs = etd::sharded_schedule(nx, ny, nz, nspecies, world_size, rank, pitch);
+    const auto recs = etd::sharded_schedule(nx, ny, nz, nspecies, world_size, rank, pitch, chunks);
     *count = (int)recs.size();
     if (out) {
         if (capacity < (int)recs.size()) return ETD_ERR_CONFIG;

@@ -2,9 +2,10 @@
 
 Each rank fetches ITS schedule from the extension (etd_sharded_schedule — the
 same records build_plan turns into device copies / NCCL send-recv) and runs it
-on host buffers with gloo point-to-point messages.  Checks: the forward
-exchange lands exactly the y-row block of every z plane in the z-stage layout,
-and the backward exchange + unpack rebuild the z-slab layout.  Also the NCCL
+on host buffers with gloo point-to-point messages, chunk by chunk as the device
+overlaps them.  Checks: the forward exchange of every z-stage chunk lands
+exactly that chunk's y rows of every z plane in the chunk's z-stage block, and
+the backward exchanges + unpack rebuild the z-slab layout.  Also the NCCL
 unique-id bootstrap used by bench.py (rank 0 creates, broadcast over the
 process group)."""
 import ctypes as C
@@ -29,23 +30,27 @@ def _free_port():
     return p
 
 
-def _schedule(L, nx, ny, nz, ns, G, r, pitch):
+NF = 13  # int64 fields per schedule record
+
+
+def _schedule(L, nx, ny, nz, ns, G, r, pitch, chunks):
     cnt = C.c_int()
-    assert L.etd_sharded_schedule(nx, ny, nz, ns, G, r, pitch, None, 0, C.byref(cnt)) == 0
-    out = np.zeros(cnt.value * 12, dtype=np.int64)
-    assert L.etd_sharded_schedule(nx, ny, nz, ns, G, r, pitch, out.ctypes.data_as(C.c_void_p), cnt.value,
+    assert L.etd_sharded_schedule(nx, ny, nz, ns, G, r, pitch, chunks, None, 0, C.byref(cnt)) == 0
+    out = np.zeros(cnt.value * NF, dtype=np.int64)
+    assert L.etd_sharded_schedule(nx, ny, nz, ns, G, r, pitch, chunks, out.ctypes.data_as(C.c_void_p), cnt.value,
                                   C.byref(cnt)) == 0
-    return out.reshape(-1, 12)
+    return out.reshape(-1, NF)
 
 
-def _worker(rank, world, port, shape, ns, result_q):
+def _worker(rank, world, port, shape, ns, chunks, result_q):
     import sys
     sys.path.insert(0, ROOT)
     import paper_2601_06849_b200 as etd
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         L = etd.lib()
-        L.etd_sharded_schedule.argtypes = [C.c_int] * 6 + [C.c_longlong, C.c_void_p, C.c_int, C.POINTER(C.c_int)]
+        L.etd_sharded_schedule.argtypes = [C.c_int] * 6 + [C.c_longlong, C.c_int, C.c_void_p, C.c_int,
+                                                           C.POINTER(C.c_int)]
         nx, ny, nz = shape
         pitch = (nx + 31) // 32 * 32
         z0, z1 = etd.zslab_partition(nz, world, rank)
@@ -55,18 +60,25 @@ def _worker(rank, world, port, shape, ns, result_q):
         rng = np.random.default_rng(0)
         U = np.zeros((ns, nz, ny, pitch))
         U[..., :nx] = rng.standard_normal((ns, nz, ny, nx))
-        bufs = {0: U[:, z0:z1].reshape(-1).copy(), 1: np.zeros(ns * F), 2: np.full(ns * Fz, np.nan),
+        bufs = {0: U[:, z0:z1].reshape(-1).copy(), 1: np.zeros(ns * F), 2: np.full(2 * ns * Fz, np.nan),
                 3: np.zeros(2 * ns * Fz), 4: np.zeros(2 * ns * F), 5: np.full(2 * ns * F, np.nan)}
-        sched = _schedule(L, nx, ny, nz, ns, world, rank, pitch)
+        sched = _schedule(L, nx, ny, nz, ns, world, rank, pitch, chunks)
+        # this rank's z-stage chunks: rows [a, b) of its y range, block offset in zin / wz
+        spans, base, off = [], [], 0
+        for k in range(chunks):
+            a, b = etd.zslab_partition(njr, chunks, k) if chunks <= njr else ((k, k + 1) if k < njr else (njr, njr))
+            spans.append((a, b))
+            base.append(off)
+            off += 2 * ns * nz * (b - a) * pitch
 
         def copy2d(r):
-            _, _, _, db, do, dp, sb, so, sp, w, h, _ = [int(x) for x in r]
+            _, _, _, db, do, dp, sb, so, sp, w, h, _, _ = [int(x) for x in r]
             for row in range(h):
                 bufs[db][do + row * dp: do + row * dp + w] = bufs[sb][so + row * sp: so + row * sp + w]
 
-        def exchange(phase):
-            sends = [r for r in sched if r[1] == phase and r[0] == 1]
-            recvs = [r for r in sched if r[1] == phase and r[0] == 2]
+        def exchange(phase, k):
+            sends = [r for r in sched if r[1] == phase and r[0] == 1 and r[12] == k]
+            recvs = [r for r in sched if r[1] == phase and r[0] == 2 and r[12] == k]
             reqs, landing = [], []
             tag_s, tag_r = {}, {}
             for r in sends:
@@ -99,14 +111,23 @@ def _worker(rank, world, port, shape, ns, result_q):
         for r in sched:
             if r[1] == 0:
                 copy2d(r)
-        exchange(1)
-        zin = bufs[2].reshape(ns, nz, njr, pitch)
-        ok_fwd = np.array_equal(zin, U[:, :, j0:j1, :])
-        # stand-in z-stage output: a known function of global coordinates
-        c_, z_, j_, x_ = np.meshgrid(np.arange(2 * ns), np.arange(nz), np.arange(j0, j1), np.arange(pitch),
-                                     indexing="ij")
-        bufs[3][:] = (c_ * 1e6 + z_ * 1e4 + j_ * 1e2 + x_).reshape(-1)
-        exchange(2)
+        for k in range(chunks):  # all forward exchanges first, as the comm stream issues them
+            exchange(1, k)
+        ok_fwd = True
+        for k, (a, b) in enumerate(spans):
+            nk = b - a
+            if nk == 0:
+                continue
+            blk = bufs[2][base[k]: base[k] + ns * nz * nk * pitch].reshape(ns, nz, nk, pitch)
+            ok_fwd &= np.array_equal(blk, U[:, :, j0 + a:j0 + b, :])
+            # stand-in z-stage output of the chunk: a known function of global coordinates
+            c_, z_, j_, x_ = np.meshgrid(np.arange(2 * ns), np.arange(nz), np.arange(j0 + a, j0 + b),
+                                         np.arange(pitch), indexing="ij")
+            bufs[3][base[k]: base[k] + 2 * ns * nz * nk * pitch] = (c_ * 1e6 + z_ * 1e4 + j_ * 1e2 + x_).reshape(-1)
+            exchange(2, k)
+        for k in range(chunks):
+            if spans[k][1] == spans[k][0]:
+                exchange(2, k)  # an empty chunk of this rank still receives its peers' rows
         for r in sched:
             if r[1] == 3:
                 copy2d(r)
@@ -123,12 +144,13 @@ def _worker(rank, world, port, shape, ns, result_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,shape,ns", [(2, (13, 11, 9), 2), (3, (21, 7, 10), 1), (2, (33, 16, 16), 1)])
-def test_sharded_schedule_over_gloo(world, shape, ns):
+@pytest.mark.parametrize("world,shape,ns,chunks", [(2, (13, 11, 9), 2, 4), (3, (21, 7, 10), 1, 4),
+                                                   (2, (33, 16, 16), 1, 1), (3, (9, 5, 6), 2, 3)])
+def test_sharded_schedule_over_gloo(world, shape, ns, chunks):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, ns, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, ns, chunks, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=180) for _ in range(world)]
