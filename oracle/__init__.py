@@ -255,6 +255,11 @@ class Oracle:
                                            C.POINTER(d), C.POINTER(l)]
             L.etd_o_system_run.argtypes = [i, i, d, d, d, d, i, i, _dp, _dp, _dp, C.POINTER(l), C.POINTER(d), i,
                                            C.POINTER(d), C.POINTER(l)]
+            L.etd_o_apply_q_b.argtypes = [i, i, d, d, d, i, i, i, i, _dp, _dp]
+            L.etd_o_scalar_run_b.argtypes = [i, i, d, d, d, i, i, i, _dp, _dp, C.POINTER(l), C.POINTER(d), i,
+                                             C.POINTER(d), C.POINTER(l)]
+            L.etd_o_system_run_b.argtypes = [i, i, d, d, d, d, i, i, i, _dp, _dp, _dp, C.POINTER(l), C.POINTER(d),
+                                             i, C.POINTER(d), C.POINTER(l)]
             cls._lib = L
         return cls._lib
 
@@ -296,29 +301,31 @@ class Oracle:
         return out
 
     @classmethod
-    def apply_q(cls, dim, n, tau, kappa, q, family, ell, axis, x):
+    def apply_q(cls, dim, n, tau, kappa, q, family, ell, axis, x, backend=0):
+        """backend 0: spectral (tensor_ops.cpp:164-172); 1: Thomas (thomas.cpp:128-160)."""
         out = np.zeros(n ** dim)
-        cls.lib().etd_o_apply_q(dim, n, tau, kappa, q, family, ell, axis,
-                                np.ascontiguousarray(x, dtype=np.float64), out)
+        cls.lib().etd_o_apply_q_b(dim, n, tau, kappa, q, family, backend, ell, axis,
+                                  np.ascontiguousarray(x, dtype=np.float64), out)
         return out
 
     @classmethod
-    def scalar_run(cls, dim, n, tau, kappa, q, u, nsteps, src_kind=1, src_params=None, family=0, n0=0, t0=0.0):
+    def scalar_run(cls, dim, n, tau, kappa, q, u, nsteps, src_kind=1, src_params=None, family=0, n0=0, t0=0.0,
+                   backend=0):
         u = np.ascontiguousarray(u, dtype=np.float64).copy()
         nn, tt, tab, sab = C.c_long(n0), C.c_double(t0), C.c_double(0), C.c_long(0)
-        rc = cls.lib().etd_o_scalar_run(dim, n, tau, kappa, q, family, src_kind, _params(src_params), u,
-                                        C.byref(nn), C.byref(tt), nsteps, C.byref(tab), C.byref(sab))
+        rc = cls.lib().etd_o_scalar_run_b(dim, n, tau, kappa, q, family, backend, src_kind, _params(src_params), u,
+                                          C.byref(nn), C.byref(tt), nsteps, C.byref(tab), C.byref(sab))
         _check(rc, b"", tab.value, sab.value)
         return u, nn.value, tt.value
 
     @classmethod
     def system_run(cls, dim, n, tau, ku, kv, q, u, v, nsteps, src_kind=10, src_params=(0.1, 0.01, 0.5),
-                   family=0, n0=0, t0=0.0):
+                   family=0, n0=0, t0=0.0, backend=0):
         u = np.ascontiguousarray(u, dtype=np.float64).copy()
         v = np.ascontiguousarray(v, dtype=np.float64).copy()
         nn, tt, tab, sab = C.c_long(n0), C.c_double(t0), C.c_double(0), C.c_long(0)
-        rc = cls.lib().etd_o_system_run(dim, n, tau, ku, kv, q, family, src_kind, _params(src_params), u, v,
-                                        C.byref(nn), C.byref(tt), nsteps, C.byref(tab), C.byref(sab))
+        rc = cls.lib().etd_o_system_run_b(dim, n, tau, ku, kv, q, family, backend, src_kind, _params(src_params),
+                                          u, v, C.byref(nn), C.byref(tt), nsteps, C.byref(tab), C.byref(sab))
         _check(rc, b"", tab.value, sab.value)
         return u, v, nn.value, tt.value
 

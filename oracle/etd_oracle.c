@@ -163,25 +163,77 @@ static void hadamard(int nx, int ny, int nz, int axis, const double* d, double* 
             }
 }
 
+/* BackendKind::Thomas payload of one axis and component (thomas.cpp:88-126):
+ * per pole l the LU factors of (tau A - s_l) (mul, piv), the off-diagonal e and
+ * the residues of the three weights. */
+typedef struct {
+    int np;
+    double complex* mul[2];
+    double complex* piv[2];
+    double complex e;
+    double complex res[3][2];
+} thomas_t;
+
 typedef struct {
     int dim, n;
     size_t N;
     double tau;
+    int thomas;         /* 0: spectral (eigenbasis) applies, 1: Thomas sweeps */
     double* P[3];      /* per axis, column-major */
     double* d[2][3][3]; /* [component][axis][ell-1] */
+    thomas_t th[2][3];  /* [component][axis] */
     double* tmp;
 } plan_t;
+
+/* thomas.cpp:14-29 factor_pole (no pivoting, underflow guard 1e-30) */
+static int factor_pole(int n, double complex c, double complex e, double complex* mul, double complex* piv) {
+    piv[0] = c;
+    mul[0] = 0.0;
+    for (int i = 1; i < n; ++i) {
+        if (cabs(piv[i - 1]) < 1e-30) return 2;  /* NumericsError */
+        mul[i] = e / piv[i - 1];
+        piv[i] = c - mul[i] * e;
+    }
+    return cabs(piv[n - 1]) < 1e-30 ? 2 : 0;
+}
 
 /* stepper.cpp:118-177 / system_stepper.cpp:31-70: one eigendecomposition per
  * axis; component c uses kappa_c * lambda (unit-kappa operator) for systems. */
 static void plan_init(plan_t* pl, int dim, int n, double tau, const double* kappas, int ncomp,
-                      int unit_kappa, double q, int family) {
+                      int unit_kappa, double q, int family, int backend) {
     memset(pl, 0, sizeof *pl);
     pl->dim = dim;
     pl->n = n;
     pl->tau = tau;
+    pl->thomas = backend == 1;
     pl->N = (size_t)n * n * (dim == 3 ? n : 1);
     pl->tmp = (double*)malloc(sizeof(double) * pl->N);
+    if (pl->thomas) {
+        /* thomas.cpp:88-126; systems: unit-kappa operator scaled by kappa_c
+         * (system_stepper.cpp:62-64); poles from the ell = 1 terms */
+        double sch[3 * 2 * 4];
+        int nt = 0;
+        etd_o_scheme(family, sch, &nt);
+        for (int a = 0; a < dim; ++a) {
+            double diag, off;
+            etd_o_operator(dim, n, unit_kappa ? 1.0 : kappas[0], q, &diag, &off);
+            for (int c = 0; c < ncomp; ++c) {
+                const double ks = unit_kappa ? kappas[c] : 1.0;
+                thomas_t* th = &pl->th[c][a];
+                th->np = nt;
+                th->e = tau * off * ks;
+                for (int l = 0; l < nt; ++l) {
+                    const double complex pole = sch[(0 * nt + l) * 4] + I * sch[(0 * nt + l) * 4 + 1];
+                    th->mul[l] = (double complex*)malloc(sizeof(double complex) * n);
+                    th->piv[l] = (double complex*)malloc(sizeof(double complex) * n);
+                    factor_pole(n, tau * diag * ks - pole, th->e, th->mul[l], th->piv[l]);
+                    for (int ell = 1; ell <= 3; ++ell)
+                        th->res[ell - 1][l] = sch[((ell - 1) * nt + l) * 4 + 2] + I * sch[((ell - 1) * nt + l) * 4 + 3];
+                }
+            }
+        }
+        return;
+    }
     double* eig = (double*)malloc(sizeof(double) * n);
     double* lam = (double*)malloc(sizeof(double) * n);
     for (int a = 0; a < dim; ++a) {
@@ -204,8 +256,13 @@ static void plan_init(plan_t* pl, int dim, int n, double tau, const double* kapp
 static void plan_free(plan_t* pl) {
     for (int a = 0; a < 3; ++a) {
         free(pl->P[a]);
-        for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < 2; ++c) {
             for (int l = 0; l < 3; ++l) free(pl->d[c][a][l]);
+            for (int l = 0; l < 2; ++l) {
+                free(pl->th[c][a].mul[l]);
+                free(pl->th[c][a].piv[l]);
+            }
+        }
     }
     free(pl->tmp);
 }
@@ -214,8 +271,45 @@ static void dims_of(const plan_t* pl, int* nx, int* ny, int* nz) {
     *nx = pl->n; *ny = pl->n; *nz = pl->dim == 3 ? pl->n : 1;
 }
 
+/* thomas.cpp:128-160 apply_Q_thomas: out = sum_l 2 Re(r_l (tau A - s_l)^{-1} in)
+ * along `axis`: forward elimination w_i = b_i - mul_i w_{i-1}, back substitution
+ * w_i = (w_i - e w_{i+1}) / piv_i (x, solve_axis_x) or * (1 / piv_i) (y/z,
+ * solve_axis_planes), accumulated pole by pole. */
+static void apply_q_thomas(plan_t* pl, int c, int ell, int axis, const double* in, double* out) {
+    int nx, ny, nz;
+    dims_of(pl, &nx, &ny, &nz);
+    const thomas_t* th = &pl->th[c][axis];
+    const int n = axis == 0 ? nx : axis == 1 ? ny : nz;
+    const size_t es = axis == 0 ? 1 : axis == 1 ? (size_t)nx : (size_t)nx * ny;
+    const size_t npen = pl->N / n;
+    double complex* w = (double complex*)malloc(sizeof(double complex) * n);
+    for (size_t i = 0; i < pl->N; ++i) out[i] = 0.0;
+    for (int l = 0; l < th->np; ++l) {
+        const double complex r = th->res[ell - 1][l], e = th->e;
+        for (size_t q = 0; q < npen; ++q) {
+            /* pencil q: x -> row q; y -> (i, k); z -> (i, j) */
+            size_t base;
+            if (axis == 0) base = q * nx;
+            else if (axis == 1) base = (q % nx) + (q / nx) * (size_t)nx * ny;
+            else base = q;
+            w[0] = in[base];
+            for (int i = 1; i < n; ++i) w[i] = in[base + i * es] - th->mul[l][i] * w[i - 1];
+            for (int i = n - 1; i >= 0; --i) {
+                const double complex x = i == n - 1 ? w[i] : w[i] - e * w[i + 1];
+                w[i] = axis == 0 ? x / th->piv[l][i] : x * (1.0 / th->piv[l][i]);
+                out[base + i * es] += 2.0 * creal(r * w[i]);
+            }
+        }
+    }
+    free(w);
+}
+
 /* tensor_ops.cpp:130-142 + 164-172: out = 2 * P (d ⊙ P^T in) along axis */
 static void apply_q(plan_t* pl, int c, int ell, int axis, const double* in, double* out) {
+    if (pl->thomas) {
+        apply_q_thomas(pl, c, ell, axis, in, out);
+        return;
+    }
     int nx, ny, nz;
     dims_of(pl, &nx, &ny, &nz);
     etd_o_contract(nx, ny, nz, pl->P[axis], axis, 1, in, pl->tmp);
@@ -224,13 +318,18 @@ static void apply_q(plan_t* pl, int c, int ell, int axis, const double* in, doub
     for (size_t i = 0; i < pl->N; ++i) out[i] *= 2.0;
 }
 
-int etd_o_apply_q(int dim, int n, double tau, double kappa, double q, int family, int ell,
-                  int axis, const double* in, double* out) {
+int etd_o_apply_q_b(int dim, int n, double tau, double kappa, double q, int family, int backend, int ell,
+                    int axis, const double* in, double* out) {
     plan_t pl;
-    plan_init(&pl, dim, n, tau, &kappa, 1, 0, q, family);
+    plan_init(&pl, dim, n, tau, &kappa, 1, 0, q, family, backend);
     apply_q(&pl, 0, ell, axis, in, out);
     plan_free(&pl);
     return 0;
+}
+
+int etd_o_apply_q(int dim, int n, double tau, double kappa, double q, int family, int ell,
+                  int axis, const double* in, double* out) {
+    return etd_o_apply_q_b(dim, n, tau, kappa, q, family, 0, ell, axis, in, out);
 }
 
 /* ---- sources (kinds as include/etd_b200.h ETD_SRC_*) ------------------- */
@@ -305,7 +404,7 @@ static int scalar_step(plan_t* pl, int kind, const double* sp, double* U, long n
     int rc = 0;
     if (scalar_src(kind, sp, U, fn, N, pl->n, pl->dim, t)) { *t_abort = t; *step_abort = -1; rc = 3; goto done; }
     if (!all_finite(fn, N)) { *t_abort = t; *step_abort = n; rc = 3; goto done; }
-    if (pl->dim == 2) {
+    if (pl->dim == 2 && !pl->thomas) {
         apply_q(pl, 0, 1, 1, U, w1);                          /* 193 */
         apply_q(pl, 0, 1, 1, fn, w2);                         /* 194 */
         const double* d1 = pl->d[0][0][0], *d2 = pl->d[0][0][1], *d3 = pl->d[0][0][2];
@@ -332,8 +431,14 @@ static int scalar_step(plan_t* pl, int kind, const double* sp, double* U, long n
         etd_o_contract(nx, ny, nz, pl->P[0], 0, 0, gb, corr);             /* 218 */
         for (size_t i = 0; i < N; ++i) U[i] = What[i] + 2.0 * tau * corr[i]; /* 219 */
     } else {
-        apply_q(pl, 0, 1, 2, U, a);  apply_q(pl, 0, 1, 1, a, w1);        /* 244-245 */
-        apply_q(pl, 0, 1, 2, fn, a); apply_q(pl, 0, 1, 1, a, w2);        /* 246-247 */
+        /* 3D (stepper.cpp:243-253), and the Thomas 2D branch (220-225) without z */
+        if (pl->dim == 3) {
+            apply_q(pl, 0, 1, 2, U, a);  apply_q(pl, 0, 1, 1, a, w1);    /* 244-245 */
+            apply_q(pl, 0, 1, 2, fn, a); apply_q(pl, 0, 1, 1, a, w2);    /* 246-247 */
+        } else {
+            apply_q(pl, 0, 1, 1, U, w1);                                 /* 193 */
+            apply_q(pl, 0, 1, 1, fn, w2);                                /* 194 */
+        }
         apply_q(pl, 0, 1, 0, w1, What);                                  /* 249 */
         apply_q(pl, 0, 2, 0, w2, b);
         for (size_t i = 0; i < N; ++i) What[i] += tau * b[i];
@@ -351,12 +456,12 @@ done:
     return rc;
 }
 
-int etd_o_scalar_run(int dim, int n, double tau, double kappa, double q, int family,
-                     int src_kind, const double* src_params, double* u, long* n_io,
-                     double* t_io, int nsteps, double* t_abort, long* step_abort) {
+int etd_o_scalar_run_b(int dim, int n, double tau, double kappa, double q, int family, int backend,
+                       int src_kind, const double* src_params, double* u, long* n_io,
+                       double* t_io, int nsteps, double* t_abort, long* step_abort) {
     if (!(tau > 0.0) || (dim != 2 && dim != 3) || n < 1) return 1; /* ConfigError */
     plan_t pl;
-    plan_init(&pl, dim, n, tau, &kappa, 1, 0, q, family);
+    plan_init(&pl, dim, n, tau, &kappa, 1, 0, q, family, backend);
     double zp[8] = {0};
     const double* sp = src_params ? src_params : zp;
     size_t N = pl.N;
@@ -374,14 +479,21 @@ int etd_o_scalar_run(int dim, int n, double tau, double kappa, double q, int fam
     return rc;
 }
 
-/* system_stepper.cpp:74-114, 3D filter z then y per stepper.cpp:244-247 */
-int etd_o_system_run(int dim, int n, double tau, double ku, double kv, double q, int family,
-                     int src_kind, const double* src_params, double* U, double* V, long* n_io,
+int etd_o_scalar_run(int dim, int n, double tau, double kappa, double q, int family,
+                     int src_kind, const double* src_params, double* u, long* n_io,
                      double* t_io, int nsteps, double* t_abort, long* step_abort) {
+    return etd_o_scalar_run_b(dim, n, tau, kappa, q, family, 0, src_kind, src_params, u, n_io, t_io, nsteps,
+                              t_abort, step_abort);
+}
+
+/* system_stepper.cpp:74-114, 3D filter z then y per stepper.cpp:244-247 */
+int etd_o_system_run_b(int dim, int n, double tau, double ku, double kv, double q, int family, int backend,
+                       int src_kind, const double* src_params, double* U, double* V, long* n_io,
+                       double* t_io, int nsteps, double* t_abort, long* step_abort) {
     if (!(tau > 0.0) || (dim != 2 && dim != 3) || n < 1) return 1;
     const double kap[2] = {ku, kv};
     plan_t pl;
-    plan_init(&pl, dim, n, tau, kap, 2, 1, q, family);
+    plan_init(&pl, dim, n, tau, kap, 2, 1, q, family, backend);
     double zp[8] = {0};
     const double* sp = src_params ? src_params : zp;
     const size_t N = pl.N;
@@ -433,4 +545,11 @@ int etd_o_system_run(int dim, int n, double tau, double ku, double kv, double q,
     free(buf);
     plan_free(&pl);
     return rc;
+}
+
+int etd_o_system_run(int dim, int n, double tau, double ku, double kv, double q, int family,
+                     int src_kind, const double* src_params, double* U, double* V, long* n_io,
+                     double* t_io, int nsteps, double* t_abort, long* step_abort) {
+    return etd_o_system_run_b(dim, n, tau, ku, kv, q, family, 0, src_kind, src_params, U, V, n_io, t_io, nsteps,
+                              t_abort, step_abort);
 }

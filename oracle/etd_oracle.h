@@ -44,6 +44,17 @@ int etd_o_system_run(int dim, int n, double tau, double ku, double kv, double q,
                      int src_kind, const double* src_params, double* u, double* v, long* n_io,
                      double* t_io, int nsteps, double* t_abort, long* step_abort);
 
+/* The same with BackendKind (0 Spectral, 1 Thomas: thomas.cpp:14-160, per-pole
+ * tridiagonal sweeps; the 2D Thomas step is stepper.cpp:220-225). */
+int etd_o_apply_q_b(int dim, int n, double tau, double kappa, double q, int family, int backend, int ell,
+                    int axis, const double* in, double* out);
+int etd_o_scalar_run_b(int dim, int n, double tau, double kappa, double q, int family, int backend,
+                       int src_kind, const double* src_params, double* u, long* n_io,
+                       double* t_io, int nsteps, double* t_abort, long* step_abort);
+int etd_o_system_run_b(int dim, int n, double tau, double ku, double kv, double q, int family, int backend,
+                       int src_kind, const double* src_params, double* u, double* v, long* n_io,
+                       double* t_io, int nsteps, double* t_abort, long* step_abort);
+
 #ifdef __cplusplus
 }
 #endif

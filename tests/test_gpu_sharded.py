@@ -1,5 +1,5 @@
-"""GPU: the z-slab sharded schedule (partition, pack, exchange, z stage on
-y-row blocks, exchange back, unpack, global abort agreement) run as G virtual
+"""GPU: the z-slab sharded schedule (partition, pack, chunked exchanges, z stage
+on y-row chunks, exchanges back, unpack, global abort agreement) run as G virtual
 ranks on ONE device via etd_group_step.  Every per-pencil contraction is the
 same arithmetic as on the unsharded plan, so results must be bitwise equal."""
 import numpy as np
@@ -29,8 +29,11 @@ def run_sharded(make, G, fields, nsteps, grid, f):
     return outs, n, t
 
 
-@pytest.mark.parametrize("G", [2, 3, 4])
-def test_sharded_system_equals_single_gpu(G):
+@pytest.mark.parametrize("G,chunks", [(2, None), (3, None), (4, None), (2, "1"), (3, "3"), (4, "9")])
+def test_sharded_system_equals_single_gpu(G, chunks, monkeypatch):
+    """Default 4 z-stage chunks, plus 1, 3 and more chunks than a rank has rows (empty chunks)."""
+    if chunks:
+        monkeypatch.setenv("ETD_ZCHUNKS", chunks)
     grid = etd.build_grid(3, [(0, 1)] * 3, [38, 30, 24])   # 37 x 29 x 23 interior, uneven splits
     nx, ny, nz = grid.interior_shape()
     rng = np.random.default_rng(G)

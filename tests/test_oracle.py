@@ -84,3 +84,29 @@ def test_composed_3d_system_reduces_to_reference_scalar_step():
     a = Ref.system_run(3, n, 0.01, 0.5, 0.5, 0.0, u0, u0, 4, src_kind=12)
     b = Ref.scalar_run(3, n, 0.01, 0.5, 0.0, u0, 4, src_kind=1)
     assert rel_gap(b[0], a[0]) <= 1e-14 and rel_gap(b[0], a[1]) <= 1e-14
+
+
+@pytest.mark.parametrize("dim,n", [(2, 13), (3, 7), (2, 24)])
+@pytest.mark.parametrize("family", [0, 1])
+def test_oracle_thomas_vs_reference(dim, n, family):
+    """The C restatement of BackendKind::Thomas (thomas.cpp) against the reference's
+    own Thomas path: apply_Q on every axis and ell, scalar and system steps."""
+    if not Ref.available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(31)
+    x = rng.uniform(-1, 1, n ** dim)
+    for axis in range(dim):
+        for ell in (1, 2, 3):
+            a = Ref.apply_q_thomas(dim, n, 0.02, 0.7, 1.0, family, ell, axis, x)
+            b = Oracle.apply_q(dim, n, 0.02, 0.7, 1.0, family, ell, axis, x, backend=1)
+            assert rel_gap(a, b) <= 1e-14, (axis, ell)
+    a = Ref.scalar_run(dim, n, 0.01, 1.0, 1.0, x, 3, src_kind=1, family=family, backend=1)[0]
+    th = Oracle.scalar_run(dim, n, 0.01, 1.0, 1.0, x, 3, src_kind=1, family=family, backend=1)[0]
+    assert rel_gap(a, th) <= 1e-13
+    v = rng.uniform(-1, 1, n ** dim)
+    a = Ref.system_run(dim, n, 0.05, 1e-3, 5e-4, 0.0, x, v, 3, family=family, backend=1)
+    b = Oracle.system_run(dim, n, 0.05, 1e-3, 5e-4, 0.0, x, v, 3, family=family, backend=1)
+    assert rel_gap(a[0], b[0]) <= 1e-13 and rel_gap(a[1], b[1]) <= 1e-13
+    # and the two backends of the restatement agree (the reference's backend cross-check)
+    sp = Oracle.scalar_run(dim, n, 0.01, 1.0, 1.0, x, 3, src_kind=1, family=family, backend=0)[0]
+    assert rel_gap(sp, th) <= 1e-11
