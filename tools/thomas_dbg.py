@@ -1,5 +1,8 @@
+"""Thomas-backend smoke over sizes (dev tool): two steps of a scalar plan per size.
+python tools/thomas_dbg.py DIM N [N ...]"""
+import os
 import sys, numpy as np
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2601_06849_b200 as etd
 dim = int(sys.argv[1]); sizes = [int(x) for x in sys.argv[2:]]
 for n in sizes:
