@@ -193,6 +193,10 @@ int etd_setup_dvector(int n, const double* lambda, double tau, int family, int e
 /* rational.cpp:133-177: out[(ell-1)*nterms + t] = {pole.re, pole.im, res.re, res.im} */
 int etd_setup_scheme(int family, double* out, int* nterms);
 
+/* stepper.cpp:38-46: phi_1(x) = (1 - e^{-x})/x, phi_2(x) = (x - 1 + e^{-x})/x^2 with
+ * the reference's series branch below x = 1e-4 (which = 1 or 2; NaN otherwise). */
+double etd_setup_phi(int which, double x);
+
 /* ABI version. */
 int etd_abi_version(void);
 

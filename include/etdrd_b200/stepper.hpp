@@ -265,6 +265,20 @@ inline StepperState advance(const StepperPlan& plan, const StepperState& state, 
     return out;
 }
 
+// stepper.cpp:182-257: the split steps `advance` dispatches to (one step each).
+inline StepperState etd2rkds_step_2d(const StepperPlan& plan, const StepperState& state, const SourceFunction& f) {
+    if (plan.grid.dim != 2) throw ConfigError("2D step on non-2D plan");
+    return advance(plan, state, f);
+}
+inline StepperState etd2rkds_step_3d(const StepperPlan& plan, const StepperState& state, const SourceFunction& f) {
+    if (plan.grid.dim != 3) throw ConfigError("3D step on non-3D plan");
+    return advance(plan, state, f);
+}
+
+// stepper.cpp:38-46
+inline double phi1(double x) { return etd_setup_phi(1, x); }
+inline double phi2(double x) { return etd_setup_phi(2, x); }
+
 struct SystemPlan {
     Grid grid;
     double tau = 0.0, kappa_u = 1.0, kappa_v = 1.0, q = 0.0;

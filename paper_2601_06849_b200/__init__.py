@@ -7,7 +7,8 @@ runs in hand-written sm_100a CUDA (``csrc/``) behind the C-ABI
 """
 from .etd import (BackendKind, ConfigError, DeviceError, DeviceSource, Grid, MemoryGuardError, NumericsError,
                   PadeFamily, SourceKind, StepperAbort, StepperPlan, StepperState, SystemPlan, SystemState,
-                  advance, allen_cahn_cubic, allen_cahn_manufactured, singular, build_grid, etd2rkds_step_system, fhn_classic, fhn_cubic,
+                  advance, etd2rkds_step_2d, etd2rkds_step_3d, etd2rkds_reference_step, etd2rk_nonsplit_step, phi1, phi2,
+                  allen_cahn_cubic, allen_cahn_manufactured, singular, build_grid, etd2rkds_step_system, fhn_classic, fhn_cubic,
                   fill_config_ic, lib, make_plan, make_system_plan, poly3, setup_axis, setup_dvector,
                   setup_scheme, unit_box_grid, zslab_partition, nccl_unique_id, group_step)
 from . import configs, harness

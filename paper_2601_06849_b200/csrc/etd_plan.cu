@@ -1811,6 +1811,10 @@ int guarded(etd_handle* h, F&& f) {
 
 extern "C" {
 
+double etd_setup_phi(int which, double x) {
+    return which == 1 ? etd::phi1(x) : which == 2 ? etd::phi2(x) : std::nan("");
+}
+
 int etd_abi_version(void) { return ETD_B200_ABI_VERSION; }
 
 int etd_create(const etd_desc* desc, etd_handle** out) {

@@ -242,6 +242,8 @@ def lib():
         L.etd_zslab_partition.argtypes = [i, i, i, C.POINTER(i), C.POINTER(i)]
         L.etd_nccl_unique_id.argtypes = [vp]
         L.etd_group_step.argtypes = [C.POINTER(vp), i, i]
+        L.etd_setup_phi.argtypes = [i, d]
+        L.etd_setup_phi.restype = d
         _lib = L
     return _lib
 
@@ -446,6 +448,13 @@ class _PlanBase:
                                          _ptr(out)), self.handle)
         return out
 
+    def apply_Q(self, ell: int, field_values: np.ndarray, axis: int, species: int = 0) -> np.ndarray:
+        """StepperPlan::apply_Q (stepper.cpp:106-116): Q_ell(tau A_axis) applied along
+        `axis` to a host field, on the plan's backend (eigenbasis transforms or Thomas)."""
+        if ell < 1 or ell > 3:
+            raise ConfigError("ell must be 1, 2, or 3")
+        return self.debug_transform(field_values, axis, ell=ell, apply_q=True, species=species)
+
     def close(self):
         self._h.close()
 
@@ -529,6 +538,48 @@ def advance(plan: StepperPlan, state: StepperState, f: DeviceSource, nsteps: int
     u_out = np.empty_like(u_in)
     n, t = plan.advance_ptr(u_in.ctypes.data, 0, u_out.ctypes.data, 0, state.n, state.t, nsteps)
     return StepperState(n, t, u_out.reshape(shape))
+
+
+def etd2rkds_step_2d(plan: StepperPlan, state: StepperState, f: DeviceSource) -> StepperState:
+    """stepper.cpp:182-229 (one step; `advance` dispatches here for 2D plans)."""
+    if not isinstance(plan, StepperPlan) or plan.grid.dim != 2:
+        raise ConfigError("2D step on non-2D plan")
+    if plan.family == EXACT_FAMILY:
+        raise ConfigError("2D split step requires the spectral or thomas backend")
+    return advance(plan, state, f)
+
+
+def etd2rkds_step_3d(plan: StepperPlan, state: StepperState, f: DeviceSource) -> StepperState:
+    """stepper.cpp:233-257"""
+    if not isinstance(plan, StepperPlan) or plan.grid.dim != 3:
+        raise ConfigError("3D step on non-3D plan")
+    if plan.family == EXACT_FAMILY:
+        raise ConfigError("3D split step requires the spectral or thomas backend")
+    return advance(plan, state, f)
+
+
+def etd2rkds_reference_step(plan: StepperPlan, state: StepperState, f: DeviceSource) -> StepperState:
+    """stepper.cpp:259-295: the exact-exponential step (plans made with
+    BackendKind.ExactExpReference)."""
+    if not isinstance(plan, StepperPlan) or plan.family != EXACT_FAMILY:
+        raise ConfigError("reference step requires the exact backend")
+    return advance(plan, state, f)
+
+
+def etd2rk_nonsplit_step(plan, state, f):
+    """stepper.cpp:297-316: BackendKind.NonSplitBanded is not implemented on the
+    device (make_plan refuses it), so no plan can take this step."""
+    raise ConfigError("non-split step requires the nonsplit backend")
+
+
+def phi1(x: float) -> float:
+    """stepper.cpp:38-41: (1 - e^{-x})/x, series below x = 1e-4."""
+    return float(lib().etd_setup_phi(1, float(x)))
+
+
+def phi2(x: float) -> float:
+    """stepper.cpp:43-46: (x - 1 + e^{-x})/x^2, series below x = 1e-4."""
+    return float(lib().etd_setup_phi(2, float(x)))
 
 
 def etd2rkds_step_system(plan: SystemPlan, state: SystemState, f: DeviceSource, nsteps: int = 1) -> SystemState:

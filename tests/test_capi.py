@@ -136,3 +136,19 @@ def test_config_ic_deterministic_and_slab_consistent():
     assert abs(v.mean()) < 0.01 and abs(v.std() - 0.1) < 0.01
     u0 = configs.initial_state(configs.CONFIGS[0], 31)[0].reshape(31, 31)
     assert np.all(np.isfinite(u0)) and abs(u0.max()) < 3.0
+
+
+def test_phi_functions_match_reference_expressions():
+    """stepper.cpp:38-46 (host exports, no GPU needed)."""
+    import math
+    for x in (0.0, 5e-5, 1e-4, 0.37, 2.0, 30.0):
+        p1 = 1.0 - x / 2.0 + x * x / 6.0 - x * x * x / 24.0 if x < 1e-4 else (1.0 - math.exp(-x)) / x
+        p2 = 0.5 - x / 6.0 + x * x / 24.0 - x * x * x / 120.0 if x < 1e-4 else (x - 1.0 + math.exp(-x)) / (x * x)
+        assert etd.phi1(x) == p1 and etd.phi2(x) == p2
+
+
+def test_step_entry_points_reject_wrong_plans():
+    with pytest.raises(etd.ConfigError):
+        etd.etd2rk_nonsplit_step(None, None, None)
+    with pytest.raises(etd.ConfigError):
+        etd.etd2rkds_step_2d(None, None, None)

@@ -349,3 +349,29 @@ def test_exact_exponential_backend_beyond_reference_cap():
     p4 = etd.advance(etd.make_plan(g, 1e-4, 1.0, 0.0, scheme=1), etd.StepperState(0, 0.0, u0),
                      etd.allen_cahn_cubic(), nsteps=5)
     assert np.all(np.isfinite(ex.U)) and rel_gap(ex.U, p4.U) < 1e-2
+
+
+def test_direct_step_entry_points_and_apply_Q():
+    """etd2rkds_step_2d / _3d / etd2rkds_reference_step (stepper.cpp:182-295) and
+    StepperPlan::apply_Q (stepper.cpp:106-116) through the mirror."""
+    R = ref_or_oracle()
+    for dim, n in ((2, 31), (3, 15)):
+        g = etd.unit_box_grid(dim, n + 1)
+        u0 = np.random.default_rng(40 + dim).uniform(-1, 1, n ** dim)
+        plan = etd.make_plan(g, 0.01, 1.0, 1.0)
+        step = etd.etd2rkds_step_2d if dim == 2 else etd.etd2rkds_step_3d
+        other = etd.etd2rkds_step_3d if dim == 2 else etd.etd2rkds_step_2d
+        got = step(plan, etd.StepperState(0, 0.0, u0), etd.allen_cahn_cubic())
+        want = R.scalar_run(dim, n, 0.01, 1.0, 1.0, u0, 1, src_kind=1)[0]
+        assert got.n == 1 and rel_gap(want, got.U) <= STEP_TOL
+        with pytest.raises(etd.ConfigError):
+            other(plan, etd.StepperState(0, 0.0, u0), etd.allen_cahn_cubic())
+        with pytest.raises(etd.ConfigError):
+            etd.etd2rkds_reference_step(plan, etd.StepperState(0, 0.0, u0), etd.allen_cahn_cubic())
+        for axis in range(dim):
+            q = plan.apply_Q(2, u0, axis)
+            assert rel_gap(R.apply_q(dim, n, 0.01, 1.0, 1.0, 0, 2, axis, u0), q) <= 1e-12
+        ex = etd.make_plan(g, 0.01, 1.0, 1.0, backend=etd.BackendKind.ExactExpReference)
+        a = etd.etd2rkds_reference_step(ex, etd.StepperState(0, 0.0, u0), etd.allen_cahn_cubic())
+        b = etd.advance(ex, etd.StepperState(0, 0.0, u0), etd.allen_cahn_cubic())
+        assert np.array_equal(a.U, b.U)
