@@ -653,18 +653,19 @@ struct Plan {
         const int nax = n_axis(v, axis);
         const long long mext = axis == 0 ? (long long)v.ny * v.nz : v.nx;
         const unsigned gz = mode == 0 ? 1u : (axis == 1 ? (unsigned)v.nz : (unsigned)v.ny);
-        // Tile class (measured):
-        //  * unit-stride (x) kernels on large grids: 2 CTAs/SM, 32 accumulators (T=3)
-        //  * otherwise the 8-warp tile (T=0) while it fills >= 3/4 of a wave
-        //  * else 4-warp 64x64 (T=1, S <= 2) if that fills a wave, else 32x32 (T=2)
+        // Tile class (measured per stage on configs 0-4, tools/tile_sweep.py):
+        //  * short contractions (n <= 255): 32x32 tiles (T=2) — pipeline fill and
+        //    drain dominate larger tiles at 16 k-tiles
+        //  * otherwise 2 CTAs/SM with 32 accumulators (T=3) when that fills two waves
+        //  * else the 8-warp tile (T=0) when it fills two waves, else T=2
         auto ctas = [&](int t) {
             const KernelSpec k = pick(mode, S, epi, pro, d.src_kind, t);
             return (long long)((nax + k.bn - 1) / k.bn) * ((mext + k.bm - 1) / k.bm) * gz;
         };
         int tile;
-        if (mode == 0 && ctas(3) >= 2 * 148) tile = 3;
-        else if (ctas(0) >= 111) tile = 0;
-        else if (S <= 2 && ctas(1) >= 148) tile = 1;
+        if (nax <= 255) tile = 2;
+        else if (ctas(3) >= 2 * 148) tile = 3;
+        else if (ctas(0) >= 2 * 148) tile = 0;
         else tile = 2;
         if (const char* f = std::getenv("ETD_FORCE_TILE"))  // tests: exercise every tile class
             if (f[0] >= '0' && f[0] <= '3' && f[1] == 0) tile = f[0] - '0';
