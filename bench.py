@@ -229,12 +229,18 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
         per = [(float(a), s) for a, (_, s) in zip(t.tolist(), per)]
     dom_ms, dom = max((x for x in per if x[1]["flops_per_launch"] > 0), key=lambda x: x[0])
     achieved = dom["flops_per_launch"] / (dom_ms * 1e-3) * 1e-12
-    traffic = None
+    traffic, traffic_stage = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
             tr = json.load(open(tpath)).get(f"cfg{cfg.id}_n{n}", {})
-            traffic = tr.get(dom["name"])
+            # z_fwd and y_fwd (z_back and y_back) are the same kernel on the same
+            # shape; the slowest of the pair flips run to run
+            twin = {"y_fwd": "z_fwd", "z_fwd": "y_fwd", "y_back": "z_back", "z_back": "y_back"}
+            for name in (dom["name"], twin.get(dom["name"])):
+                if name in tr:
+                    traffic, traffic_stage = tr[name], name
+                    break
         except (OSError, ValueError):
             traffic = None
     transform_ms = sum(a for a, st in per if st["flops_per_launch"] > 0)
@@ -251,7 +257,8 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
                 "frac": round(gbs / 6552.0, 4)}
 
     roofline = {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic, "kernel": dom["name"],
+                "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic, "traffic_stage": traffic_stage,
+                "kernel": dom["name"],
                 "peak_source": FP64_PEAK_NOTE,
                 "algorithmic_flops_per_launch": dom["flops_per_launch"],
                 "all_transforms": {"tflops": round(transform_flops / (transform_ms * 1e-3) * 1e-12, 3),
