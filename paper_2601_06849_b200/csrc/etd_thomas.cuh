@@ -87,7 +87,7 @@ struct ThomasCfg {
     static constexpr int P = SPLIT ? 64 : 128;             // pencils per tile
     static constexpr int J = 16;                           // axis points per stage
     static constexpr int L = MODE == 0 ? (EPI == TH_WHAT ? 2 * NS : EPI == TH_UPDATE ? 2 : 1) : 1;
-    static constexpr int STAGES = MODE == 0 ? 2 : 3;  // x: double buffering keeps 3 CTAs per SM
+    static constexpr int STAGES = 3;
     static constexpr int OP_DBL = P * J;
     static constexpr int STAGE_DBL = L * OP_DBL;
     static constexpr int NSU = EPI == TH_WHAT ? NS : 1;    // species whose factors a stage carries
