@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define ETD_B200_ABI_VERSION 2
+#define ETD_B200_ABI_VERSION 3
 
 /* Status codes (0 = OK).  errors.hpp:8-30; CLI mapping cli.cpp:204-217. */
 enum etd_status {
@@ -162,6 +162,18 @@ int etd_set_profiling(etd_handle* h, int on);
 int etd_stage_count(const etd_handle* h);
 int etd_stage_info(const etd_handle* h, int i, char* name, size_t len, double* ms_total,
                    long* launches, double* flops_per_launch, double* bytes_per_launch);
+/* FLOPs per launch of stage i as executed (the parity-split transform does
+ * 2 (2h) h / n per point, h = (n+1)/2) and as the dense n x n contraction would
+ * (2 n per point, SURVEY §8(d)'s algorithmic count). */
+int etd_stage_flops(const etd_handle* h, int i, double* executed, double* dense);
+/* Which axes run parity-split transforms (P(n-1-i,k) = (-1)^k P(i,k) of the DST-I
+ * eigenbasis, operators.cpp:43-53): out[a] = 1 for a folded axis a < dim. */
+int etd_parity_split(const etd_handle* h, int* out);
+/* The host-built parity-split half matrices of one axis (etd_plan.cu
+ * fold_matrices): forward and backward, 2h interleaved rows x h columns; mode 0
+ * stores rows contiguous with leading dimension round_up(h, 16), mode 1 the
+ * transpose [h][2h].  Returns ETD_ERR_CONFIG unless h % 8 == 0.  Host only. */
+int etd_setup_fold_matrices(int n, int mode, double* ff, double* fb);
 
 /* Single eigenbasis transform on host data, for kernel-level parity tests:
  * out = op(P_axis) contracted along `axis` (tensor_ops.cpp:107-119 contract_axis

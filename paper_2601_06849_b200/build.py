@@ -10,14 +10,15 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libetd_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["etd_setup.cpp", "etd_plan.cu"]
-HEADERS = ["etd_setup.hpp", "etd_kernels.cuh", "etd_thomas.cuh"]
+SOURCES = ["etd_setup.cpp", "etd_plan.cu", "etd_specs_dense.cu", "etd_specs_fold.cu"]
+HEADERS = ["etd_setup.hpp", "etd_kernels.cuh", "etd_thomas.cuh", "etd_registry.cuh"]
 
 
 def _nvcc() -> str:
@@ -41,9 +42,9 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
         return LIB
     objdir = os.path.join(CSRC, "_obj")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
     common = ["-O3", "-std=c++20", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
-    for src in SOURCES:
+
+    def compile_one(src):
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
         cmd = [nvcc, *ARCH, *common, "-lineinfo", "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
@@ -55,9 +56,15 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
-        if verbose or ptxas_verbose:
-            sys.stdout.write(r.stdout + r.stderr)
-        objs.append(obj)
+        return obj, r.stdout + r.stderr
+
+    # the translation units compile in parallel (the kernel variants dominate)
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        res = list(ex.map(compile_one, SOURCES))
+    objs = [o for o, _ in res]
+    if verbose or ptxas_verbose:
+        for _, log in res:
+            sys.stdout.write(log)
     tmp = LIB + ".tmp"
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)

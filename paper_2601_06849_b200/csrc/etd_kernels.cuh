@@ -20,6 +20,33 @@
 // The field is always the A operand (M-dim = pencils or x), the n x n transform
 // matrix is the B operand (L2-resident), the contracted axis is K and the
 // transformed axis is N, so every epilogue scales along N by d[n].
+//
+// Parity split (FOLD).  The eigenbasis is the DST-I matrix (operators.cpp:43-53),
+// P(i,k) = c sin((i+1)(k+1) pi/(n+1)), so P(n-1-i, k) = (-1)^k P(i, k): even modes
+// are symmetric about the pencil centre and odd modes antisymmetric.  With
+// h = (n+1)/2 every transform splits exactly into two h x h dense contractions,
+// half the DMMA work of the n x n one:
+//   FOLD 1 (physical -> modes):  s_i = g_i + g_{n-1-i},  d_i = g_i - g_{n-1-i}  (i < h)
+//          ghat_{2q} = sum_i P(i,2q) s_i,   ghat_{2q+1} = sum_i P(i,2q+1) d_i
+//          (for odd n the centre i = h-1 enters s twice: its column is halved).
+//          The two A boxes of a stage are the k range and its mirror; s and d are
+//          formed on the fragments in registers (one DADD per fragment, reused
+//          over WN/16 DMMAs).
+//   FOLD 2 (modes -> physical):  o_i = sum_q P(i,2q) ghat_{2q},  e_i = sum_q P(i,2q+1) ghat_{2q+1}
+//          g_i = o_i + e_i,  g_{n-1-i} = o_i - e_i  (i < h; e of the centre is exactly 0).
+//          The two A boxes are the even-mode and odd-mode k ranges.
+//   FOLD 3 (x forward, odd n): as FOLD 1, but the mirror box is read at k0 from an
+//          x-reversed copy of the operand (tmA2, written by y_back): TMA needs a
+//          16-byte aligned innermost start, and the mirror of an aligned 16-block
+//          of a pencil with a centre point starts at an odd x.
+//   FOLD 4 (x forward of a pre-folded operand): the operand already holds s at
+//          [0, h) and d at [h, n) (x_back_src writes f(What) that way); boxes at
+//          k0 and h + k0, no DADD.
+// Mode space is stored parity-major: position q < h holds mode 2q, h + q holds
+// 2q + 1 (d-vectors are permuted to match).  The B matrix interleaves the two
+// groups by 8 rows (rows 16b..16b+7 even group, 16b+8..16b+15 odd group of the
+// same 8 outputs), so n-fragment j uses the first A box for even j and the
+// second for odd j, and under FOLD 2 the o and e of an output sit in one thread.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -72,6 +99,9 @@ struct ContractArgs {
     const double* sinz;
     int outer0;             // first outer index (MODE 1) of a chunked launch
     int mtile0;             // first M tile of a chunked launch
+    int kext;               // contraction extent (n_axis; h under FOLD)
+    int fold_h;             // FOLD: h = (n_axis + 1) / 2, a multiple of 8
+    double* out_rev;        // MODE 1 EPI_STORE: also store each output at x' = m_extent-1-x (FOLD 3 input)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -173,21 +203,25 @@ __device__ __forceinline__ void src2(const double* p, double u, double v, double
 }
 
 // ------------------------------------------------------------- tile geometry
-template <int MODE, int S, int EPI, bool PRO, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
+template <int MODE, int S, int EPI, bool PRO, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int FOLD = 0>
 struct ContractCfg {
     static constexpr int BK = 16;
+    static constexpr int AB = FOLD ? 2 : 1;                // A boxes per stage (FOLD: two k ranges)
     static constexpr int NW = WARPS_M * WARPS_N;          // consumer warps
     static constexpr int THREADS = 32 * NW;               // lane 0 of warp 0 also drives TMA
     static constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
     static constexpr int MF = WM / 8, NF = WN / 8;        // 8x8 DMMA fragments per warp
     static constexpr int L = PRO ? S / 2 : S;             // operands fetched by TMA
-    static constexpr int A_DBL = L * BM * BK;             // f(U) operands never touch smem
+    static constexpr int A1_DBL = L * BM * BK;            // one A box (f(U) operands never touch smem)
+    static constexpr int A_DBL = AB * A1_DBL;
     static constexpr int B_DBL = BN * BK;
     static constexpr int STAGE_DBL = A_DBL + B_DBL;
-    static constexpr uint32_t TX_BYTES = (L * BM + BN) * BK * 8;
+    static constexpr uint32_t TX_BYTES = (AB * L * BM + BN) * BK * 8;
     static constexpr int SMEM_BYTES = STAGES * STAGE_DBL * 8 + 1024 + 2 * STAGES * 8 + 64;
     static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile");
     static_assert(BM % 16 == 0 && BN % 16 == 0, "cta tile");
+    static_assert(FOLD == 0 || (WN % 16 == 0 && !PRO), "FOLD pairs 8-row fragments; no source prologue");
+    static_assert(FOLD < 3 || MODE == 0, "FOLD 3/4 are x-axis variants");
 };
 
 // 128B-swizzled [rows][16 doubles] tile: element (row, col), TMA SWIZZLE_128B
@@ -197,11 +231,13 @@ __device__ __forceinline__ int swz(int row, int col) {
 
 // ------------------------------------------------------------- the kernel
 template <int MODE, int S, int EPI, bool PRO, int SK, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES,
-          int MINB = 1>
+          int MINB = 1, int FOLD = 0>
 __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     etd_contract(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const ContractArgs args) {
-    using C = ContractCfg<MODE, S, EPI, PRO, BM, BN, WARPS_M, WARPS_N, STAGES>;
+                 const __grid_constant__ CUtensorMap tmA2, const ContractArgs args) {
+    constexpr bool FWD_FOLD = FOLD == 1 || FOLD == 3 || FOLD == 4;  // output in parity-major mode order
+    constexpr bool COMBINE = FOLD == 1 || FOLD == 3;                 // (g, g_mirror) -> (s, d) in registers
+    using C = ContractCfg<MODE, S, EPI, PRO, BM, BN, WARPS_M, WARPS_N, STAGES, FOLD>;
     constexpr int BK = C::BK;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the 128B swizzle atoms; pointer arithmetic on the
@@ -215,7 +251,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     const int n0 = blockIdx.x * BN;
     const int m0 = (blockIdx.y + args.mtile0) * BM;
     const int outer = blockIdx.z + args.outer0;
-    const int KT = (args.n_axis + BK - 1) / BK;
+    const int KT = (args.kext + BK - 1) / BK;
 
     // A step aborted earlier in this launch sequence poisons every later kernel
     // (stepper.cpp:18-23: the step throws, the input state survives).
@@ -239,22 +275,31 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     //   MODE 1  A: 5D {x%16, k, x/16, outer, op} box {16,16,BM/16,1,L} -> [op][pb][16][16]
     //   MODE 0  B: 2D {k, n}                     box {16, BN}         -> [BN][16]
     //   MODE 1  B: 3D {n%16, k, n/16}            box {16, 16, BN/16}  -> [nb][16][16]
+    //   FOLD 1: second A box = the mirror k range [n - k0 - 16, n - k0) (read reversed)
+    //   FOLD 2/4: second A box = the odd-group k range [h + k0, h + k0 + 16)
+    //   FOLD 3: second A box = [k0, k0 + 16) of the x-reversed copy (tmA2)
+    // (coordinates off the tensor read as +0.0, which the zero B columns absorb)
     auto issue = [&](int kt, int stage) {
         double* sA = smem + stage * C::STAGE_DBL;
         double* sB = sA + C::A_DBL;
         mbar_expect_tx(&full[stage], C::TX_BYTES);
         const int k0 = kt * BK;
+        const int k1 = FOLD == 1 ? args.n_axis - k0 - BK : FOLD == 3 ? k0 : args.fold_h + k0;
         if constexpr (MODE == 0) {
             tma_load_3d(sA, &tmA, &full[stage], k0, m0, 0);
+            if constexpr (FOLD != 0)
+                tma_load_3d(sA + C::A1_DBL, FOLD == 3 ? &tmA2 : &tmA, &full[stage], k1, m0, 0);
             tma_load_2d(sB, &tmB, &full[stage], k0, n0);
         } else {
             tma_load_5d(sA, &tmA, &full[stage], 0, k0, m0 >> 4, outer, 0);
+            if constexpr (FOLD != 0) tma_load_5d(sA + C::A1_DBL, &tmA, &full[stage], 0, k1, m0 >> 4, outer, 0);
             tma_load_3d(sB, &tmB, &full[stage], 0, k0, n0 >> 4);
         }
     };
     if (tid == 0) {
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
+        if constexpr (FOLD == 3) tma_prefetch(&tmA2);
         for (int kt = 0; kt < KT && kt < STAGES; ++kt) issue(kt, kt);
     }
     {
@@ -275,7 +320,11 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
         auto kperm = [&](int st) {
             return MODE == 0 ? (2 * st + (l & 1) + 8 * (l >> 1)) : (2 * l + (st & 1) + 8 * (st >> 1));
         };
-        auto load_frags = [&](int stg, int st, double (&a)[S][C::MF], double (&b)[C::NF]) {
+        // a2: the second A box (FOLD); FOLD 1 turns (a, a2) = (g_k, g_mirror) into (s, d).
+        // The mirror box is read at 15 - k: the swizzle slot maps by an XOR, so the
+        // reversed reads stay bank-conflict free.
+        auto load_frags = [&](int stg, int st, double (&a)[S][C::MF], double (&a2)[S][C::MF],
+                              double (&b)[C::NF]) {
             const double* sA = smem + stg * C::STAGE_DBL;
             const double* sB = sA + C::A_DBL;
             const int kk = kperm(st);
@@ -291,7 +340,22 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                     const int mm = wm0 + i * 8 + g;
                     const double* base = sA + s * BM * BK;
                     a[s][i] = MODE == 0 ? base[swz(mm, kk)] : base[(mm >> 4) * 256 + swz(kk, mm & 15)];
+                    if constexpr (FOLD != 0) {
+                        const double* b2 = base + C::A1_DBL;
+                        const int k2 = FOLD == 1 ? BK - 1 - kk : kk;
+                        a2[s][i] = MODE == 0 ? b2[swz(mm, k2)] : b2[(mm >> 4) * 256 + swz(k2, mm & 15)];
+                    }
                 }
+            if constexpr (COMBINE) {
+#pragma unroll
+                for (int s = 0; s < C::L; ++s)
+#pragma unroll
+                    for (int i = 0; i < C::MF; ++i) {
+                        const double x = a[s][i], y = a2[s][i];
+                        a[s][i] = x + y;
+                        a2[s][i] = x - y;
+                    }
+            }
         };
         // e^{-lambda t} for the manufactured source: t of the input state (prologue)
         // or t + tau (the x_back_src epilogue), from the device step status
@@ -337,23 +401,25 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                 }
             }
         };
-        auto mma = [&](const double (&a)[S][C::MF], const double (&b)[C::NF]) {
+        auto mma = [&](const double (&a)[S][C::MF], const double (&a2)[S][C::MF], const double (&b)[C::NF]) {
 #pragma unroll
             for (int s = 0; s < S; ++s)
 #pragma unroll
                 for (int i = 0; i < C::MF; ++i)
 #pragma unroll
-                    for (int j = 0; j < C::NF; ++j) dmma884(acc[s][i][j][0], acc[s][i][j][1], a[s][i], b[j]);
+                    for (int j = 0; j < C::NF; ++j)
+                        dmma884(acc[s][i][j][0], acc[s][i][j][1], (FOLD != 0 && (j & 1)) ? a2[s][i] : a[s][i],
+                                b[j]);
         };
 
         // Flat (k-tile, step) stream with a one-step lookahead that also crosses
         // stage boundaries: fragments (and source math) of the next step are in
         // flight while the DMMAs of the current step issue.
-        double fa[2][S][C::MF], fb[2][C::NF];
+        double fa[2][S][C::MF], fa2[2][S][C::MF], fb[2][C::NF];
         int stage = 0;
         uint32_t phase = 0;
         mbar_wait(&full[0], 0);
-        load_frags(0, 0, fa[0], fb[0]);
+        load_frags(0, 0, fa[0], fa2[0], fb[0]);
         apply_src(0, 0, fa[0]);
         for (int kt = 0; kt < KT; ++kt) {
             const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
@@ -362,13 +428,13 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
             for (int st = 0; st < BK / 4; ++st) {
                 const int cur = st & 1, nxt = cur ^ 1;
                 if (st < BK / 4 - 1) {
-                    load_frags(stage, st + 1, fa[nxt], fb[nxt]);
+                    load_frags(stage, st + 1, fa[nxt], fa2[nxt], fb[nxt]);
                 } else if (kt + 1 < KT) {
                     // look ahead into the next stage
                     mbar_wait(&full[nstage], nphase);
-                    load_frags(nstage, 0, fa[nxt], fb[nxt]);
+                    load_frags(nstage, 0, fa[nxt], fa2[nxt], fb[nxt]);
                 }
-                mma(fa[cur], fb[cur]);
+                mma(fa[cur], fa2[cur], fb[cur]);
                 if (st == BK / 4 - 1) {
                     // Release this stage only now: the DMMAs above could not issue
                     // before their fragment loads from this stage had returned, so no
@@ -392,13 +458,19 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
         }
 
         // ===================== fused epilogue =====================
-        // Thread owns C(m, n..n+1) for each (i, j): adjacent n.  Aux inputs of a
-        // row are loaded up front (independent of this kernel's stores, so the
-        // loads overlap instead of serialising behind possible aliasing);
-        // MODE 0 stores the (n, n+1) pair as one 16-byte STG.
+        // Thread owns C(m, r..r+1) for each (i, j): adjacent B rows r.  The epilogue
+        // walks NF column pairs (col, col+1) of the output:
+        //   FOLD 0: pair j = rows (r, r+1) = columns (r, r+1)
+        //   FOLD 1: pair j = mode positions of rows r, r+1 (parity-major)
+        //   FOLD 2: pairs j < NF/2 are the outputs (i, i+1) = o + e of fragments
+        //           (2j, 2j+1); pairs j >= NF/2 their mirrors (n-2-i, n-1-i) = o - e
+        // Aux inputs of a row are loaded up front (independent of this kernel's
+        // stores, so the loads overlap instead of serialising behind possible
+        // aliasing); MODE 0 stores an aligned pair as one 16-byte STG.
         const int ns = args.nspecies;
         double* __restrict__ outp = args.out;
         const double* __restrict__ auxp = args.aux;
+        constexpr int NP = C::NF;
         auto offset = [&](int m, int n) -> long long {
             if constexpr (MODE == 0) return (long long)m * args.pitch + n;
             else return args.zaxis ? (long long)outer * args.pitch + (long long)n * args.plane + m
@@ -407,8 +479,11 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
         auto store = [&](int o, int m, int n, double v0, double v1, bool two) {
             double* base = outp + (long long)o * args.out_stride;
             if constexpr (MODE == 0) {
-                if (two) *reinterpret_cast<double2*>(base + offset(m, n)) = make_double2(v0, v1);
-                else base[offset(m, n)] = v0;
+                if (two && !(n & 1)) *reinterpret_cast<double2*>(base + offset(m, n)) = make_double2(v0, v1);
+                else {
+                    base[offset(m, n)] = v0;
+                    if (two) base[offset(m, n + 1)] = v1;
+                }
             } else {
                 base[offset(m, n)] = v0;
                 if (two) base[offset(m, n + 1)] = v1;
@@ -417,54 +492,153 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
         auto dpair = [&](const double* d, int c, int n) {
             return __ldg(reinterpret_cast<const double2*>(d + c * args.dstride + n));
         };
+        // column of pair jp and how many of (col, col+1) are in range
+        auto pair_col = [&](int jp, bool& v0, bool& v1) -> int {
+            if constexpr (FOLD == 0) {
+                const int r = n0 + wn0 + jp * 8 + 2 * l;
+                v0 = r < args.n_axis;
+                v1 = r + 1 < args.n_axis;
+                return r;
+            } else if constexpr (FWD_FOLD) {
+                const int r = n0 + wn0 + jp * 8 + 2 * l;
+                const int c = (r >> 4) * 8 + (r & 7) + ((r >> 3) & 1) * args.fold_h;
+                const bool in = r < 2 * args.fold_h;
+                v0 = in && c < args.n_axis;
+                v1 = in && c + 1 < args.n_axis;
+                return c;
+            } else {
+                const int jj = jp < NP / 2 ? jp : jp - NP / 2;
+                const int r = n0 + wn0 + 2 * jj * 8 + 2 * l;
+                const int io = (r >> 4) * 8 + (r & 7);
+                v0 = v1 = io < args.fold_h;
+                return jp < NP / 2 ? io : args.n_axis - 2 - io;
+            }
+        };
+        auto val = [&](int s, int i, int jp, int e) -> double {
+            if constexpr (FOLD != 2) return acc[s][i][jp][e];
+            else {
+                const int jj = jp < NP / 2 ? jp : jp - NP / 2;
+                if (jp < NP / 2) return acc[s][i][2 * jj][e] + acc[s][i][2 * jj + 1][e];
+                return acc[s][i][2 * jj][1 - e] - acc[s][i][2 * jj + 1][1 - e];
+            }
+        };
 #pragma unroll
         for (int i = 0; i < C::MF; ++i) {
             const int m = m0 + wm0 + i * 8 + g;
             if (m >= args.m_extent) continue;
             constexpr bool HAS_AUX = EPI == EPI_CORR || EPI == EPI_UPDATE;
-            double av[HAS_AUX ? S : 1][C::NF][2];
+            double av[HAS_AUX ? S : 1][NP][2];
             if constexpr (HAS_AUX) {
 #pragma unroll
-                for (int j = 0; j < C::NF; ++j) {
-                    const int nb = n0 + wn0 + j * 8 + 2 * l;
+                for (int jp = 0; jp < NP; ++jp) {
+                    bool in0, in1;
+                    const int nb = pair_col(jp, in0, in1);
 #pragma unroll
                     for (int c = 0; c < S; ++c) {
                         const double* a = auxp + (long long)c * args.aux_stride;
-                        if (MODE == 0 && nb + 1 < args.n_axis) {
+                        if (MODE == 0 && in1 && !(nb & 1)) {
                             const double2 t = __ldg(reinterpret_cast<const double2*>(a + offset(m, nb)));
-                            av[c][j][0] = t.x;
-                            av[c][j][1] = t.y;
+                            av[c][jp][0] = t.x;
+                            av[c][jp][1] = t.y;
                         } else {
-                            av[c][j][0] = nb < args.n_axis ? __ldg(a + offset(m, nb)) : 0.0;
-                            av[c][j][1] = nb + 1 < args.n_axis ? __ldg(a + offset(m, nb + 1)) : 0.0;
+                            av[c][jp][0] = in0 ? __ldg(a + offset(m, nb)) : 0.0;
+                            av[c][jp][1] = in1 ? __ldg(a + offset(m, nb + 1)) : 0.0;
                         }
                     }
                 }
             }
 #pragma unroll
-            for (int j = 0; j < C::NF; ++j) {
-                const int nb = n0 + wn0 + j * 8 + 2 * l;
-                if (nb >= args.n_axis) continue;
-                const bool two = nb + 1 < args.n_axis;
+            for (int jp = 0; jp < NP; ++jp) {
+                bool in0, two;
+                const int nb = pair_col(jp, in0, two);
+                if (!in0) continue;
                 if constexpr (EPI == EPI_STORE) {
 #pragma unroll
-                    for (int s = 0; s < S; ++s) store(s, m, nb, acc[s][i][j][0], acc[s][i][j][1], two);
+                    for (int s = 0; s < S; ++s) store(s, m, nb, val(s, i, jp, 0), val(s, i, jp, 1), two);
+                    if constexpr (MODE == 1)
+                        if (args.out_rev) {
+                            // x-reversed copy for the next (x) stage's FOLD 3 mirror boxes
+                            const int mr = args.m_extent - 1 - m;
+#pragma unroll
+                            for (int s = 0; s < S; ++s) {
+                                double* base = args.out_rev + (long long)s * args.out_stride;
+                                base[offset(mr, nb)] = val(s, i, jp, 0);
+                                if (two) base[offset(mr, nb + 1)] = val(s, i, jp, 1);
+                            }
+                        }
+                } else if constexpr (EPI == EPI_WHAT_SRC && FOLD == 2) {
+                    // Each direct pair (io, io+1) handles its mirror (n-1-io, n-2-io) too:
+                    // What at both, f(t+tau, What) at both (checks), and f stored folded
+                    // for x_fwd_corr (FOLD 4): s = f + f_mirror at [io, io+2), d = f - f_mirror
+                    // at [h + io, h + io + 2) (the centre's d = 0 is not stored).
+                    if (jp < NP / 2) {
+                        const int mc = args.n_axis - 2 - nb;  // mirror pair columns (mc, mc + 1)
+                        double w[2][S][2];                    // [direct, mirror][species][pair elem]
+#pragma unroll
+                        for (int c = 0; c < S; ++c)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                w[0][c][e] = val(c, i, jp, e);
+                                w[1][c][e] = val(c, i, jp + NP / 2, e);
+                            }
+                        double f[2][2][2] = {};               // [direct, mirror][species][pair elem]
+#pragma unroll
+                        for (int side = 0; side < 2; ++side)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int x = side == 0 ? nb + e : mc + e;
+                                if constexpr (S == 1) {
+                                    double ustar = 0.0;
+                                    if constexpr (SK == 4) {
+                                        const int jj = m % args.ny_local + args.gj0, kz = m / args.ny_local + args.gz0;
+                                        ustar = src_a * (args.sinx[x] * args.siny[jj] * (args.sinz ? args.sinz[kz] : 1.0));
+                                    }
+                                    f[side][0][e] = src1<SK>(args.sp, w[side][0][e], ustar);
+                                    if constexpr (SK == 3)
+                                        if (x == 0 && m == 0 && args.gz0 == 0 && args.gj0 == 0)
+                                            f[side][0][e] = __longlong_as_double(0x7ff8000000000000ll);
+                                    bad |= (int)!isfinite(f[side][0][e]);
+                                    dom |= src_domain_violation<SK>(w[side][0][e]);
+                                } else {
+                                    src2<SK>(args.sp, w[side][0][e], w[side][1][e], f[side][0][e], f[side][1][e]);
+                                    bad |= (int)!(isfinite(f[side][0][e]) && isfinite(f[side][1][e]));
+                                }
+                            }
+                        const int h = args.fold_h;
+#pragma unroll
+                        for (int c = 0; c < S; ++c) {
+                            store(c, m, nb, w[0][c][0], w[0][c][1], true);
+                            store(c, m, mc, w[1][c][0], w[1][c][1], true);
+                            // mirror of column nb + e is mc + 1 - e
+                            store(S + c, m, nb, f[0][c][0] + f[1][c][1], f[0][c][1] + f[1][c][0], true);
+                            if (h + nb + 1 < args.n_axis)
+                                store(S + c, m, h + nb, f[0][c][0] - f[1][c][1], f[0][c][1] - f[1][c][0], true);
+                            else if (h + nb < args.n_axis)
+                                store(S + c, m, h + nb, f[0][c][0] - f[1][c][1], 0.0, false);
+                        }
+                    }
                 } else if constexpr (EPI == EPI_SCALE) {
 #pragma unroll
                     for (int s = 0; s < S; ++s) {
                         const double2 d = dpair(args.dA, s % ns, nb);
-                        store(s, m, nb, acc[s][i][j][0] * d.x, acc[s][i][j][1] * d.y, two);
+                        store(s, m, nb, val(s, i, jp, 0) * d.x, val(s, i, jp, 1) * d.y, two);
                     }
                 } else if constexpr (EPI == EPI_MIX) {
 #pragma unroll
                     for (int c = 0; c < S / 2; ++c) {
                         const double2 da = dpair(args.dA, c, nb), db = dpair(args.dB, c, nb);
-                        const double* w1 = acc[c][i][j];
-                        const double* w2 = acc[S / 2 + c][i][j];
-                        store(c, m, nb, da.x * w1[0] + db.x * w2[0], da.y * w1[1] + db.y * w2[1], two);
-                        store(S / 2 + c, m, nb, w2[0], w2[1], two);
+                        const double w10 = val(c, i, jp, 0), w11 = val(c, i, jp, 1);
+                        const double w20 = val(S / 2 + c, i, jp, 0), w21 = val(S / 2 + c, i, jp, 1);
+                        store(c, m, nb, da.x * w10 + db.x * w20, da.y * w11 + db.y * w21, two);
+                        store(S / 2 + c, m, nb, w20, w21, two);
                     }
                 } else if constexpr (EPI == EPI_WHAT_SRC) {
+                    double w[S][2];
+#pragma unroll
+                    for (int c = 0; c < S; ++c) {
+                        w[c][0] = val(c, i, jp, 0);
+                        w[c][1] = val(c, i, jp, 1);
+                    }
                     double f0[2], f1[2] = {0.0, 0.0};
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
@@ -477,32 +651,32 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                                                       (args.sinz ? args.sinz[kz] : 1.0))
                                            : 0.0;
                             }
-                            f0[e] = src1<SK>(args.sp, acc[0][i][j][e], ustar);
+                            f0[e] = src1<SK>(args.sp, w[0][e], ustar);
                             if constexpr (SK == 3)
                                 if (nb + e == 0 && m == 0 && args.gz0 == 0 && args.gj0 == 0)
                                     f0[e] = __longlong_as_double(0x7ff8000000000000ll);
                             bad |= (int)in & (int)!isfinite(f0[e]);
-                            dom |= (int)in & src_domain_violation<SK>(acc[0][i][j][e]);
+                            dom |= (int)in & src_domain_violation<SK>(w[0][e]);
                         } else {
-                            src2<SK>(args.sp, acc[0][i][j][e], acc[1][i][j][e], f0[e], f1[e]);
+                            src2<SK>(args.sp, w[0][e], w[1][e], f0[e], f1[e]);
                             bad |= (int)in & (int)!(isfinite(f0[e]) && isfinite(f1[e]));
                         }
                     }
 #pragma unroll
-                    for (int c = 0; c < S; ++c) store(c, m, nb, acc[c][i][j][0], acc[c][i][j][1], two);
+                    for (int c = 0; c < S; ++c) store(c, m, nb, w[c][0], w[c][1], two);
                     store(S, m, nb, f0[0], f0[1], two);
                     if constexpr (S == 2) store(3, m, nb, f1[0], f1[1], two);
                 } else if constexpr (EPI == EPI_CORR) {
 #pragma unroll
                     for (int c = 0; c < S; ++c) {
                         const double2 d = dpair(args.dA, c, nb);
-                        store(c, m, nb, (acc[c][i][j][0] - av[c][j][0]) * d.x, (acc[c][i][j][1] - av[c][j][1]) * d.y,
-                              two);
+                        store(c, m, nb, (val(c, i, jp, 0) - av[c][jp][0]) * d.x,
+                              (val(c, i, jp, 1) - av[c][jp][1]) * d.y, two);
                     }
                 } else if constexpr (EPI == EPI_UPDATE) {
 #pragma unroll
                     for (int c = 0; c < S; ++c) {
-                        const double u0 = av[c][j][0] + acc[c][i][j][0], u1 = av[c][j][1] + acc[c][i][j][1];
+                        const double u0 = av[c][jp][0] + val(c, i, jp, 0), u1 = av[c][jp][1] + val(c, i, jp, 1);
                         bad |= !isfinite(u0) || (two && !isfinite(u1));
                         store(c, m, nb, u0, u1, two);
                     }
@@ -560,10 +734,10 @@ __host__ __device__ inline int fail_kind(int code) {
     const int order = code / 10, domain = code % 10 == 0;
     return domain ? (order == 1 ? 4 : 5) : order;
 }
-__global__ void etd_fail_code(const StepStatus* st, int* code) {
+static __global__ void etd_fail_code(const StepStatus* st, int* code) {
     *code = fail_code(*reinterpret_cast<const volatile int*>(&st->fail));
 }
-__global__ void etd_commit(StepStatus* st, const int* codes, int ncodes, double tau) {
+static __global__ void etd_commit(StepStatus* st, const int* codes, int ncodes, double tau) {
     int g = 1000;
     for (int i = 0; i < ncodes; ++i) g = min(g, codes[i]);
     if (g < 1000) {
@@ -636,7 +810,7 @@ __global__ void __launch_bounds__(256) etd_source(const SourceArgs a) {
 
 // Order-independent checksum of a buffer (debugging aid, ETD_DEBUG_CHECKSUM):
 // wrapping sum of the raw 64-bit patterns and of index-mixed patterns.
-__global__ void etd_checksum(const double* __restrict__ f, long long n, unsigned long long* out) {
+static __global__ void etd_checksum(const double* __restrict__ f, long long n, unsigned long long* out) {
     unsigned long long a = 0, b = 0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const unsigned long long x = (unsigned long long)__double_as_longlong(f[i]);
@@ -648,7 +822,7 @@ __global__ void etd_checksum(const double* __restrict__ f, long long n, unsigned
 }
 
 // Positions where two buffers differ bitwise (debugging aid).
-__global__ void etd_diff_positions(const double* a, const double* b, long long n, unsigned long long* count,
+static __global__ void etd_diff_positions(const double* a, const double* b, long long n, unsigned long long* count,
                                    long long* pos, int cap) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         if (__double_as_longlong(a[i]) != __double_as_longlong(b[i])) {
@@ -659,7 +833,7 @@ __global__ void etd_diff_positions(const double* a, const double* b, long long n
 
 // Finiteness scan of one padded field (snapshot save/load refuse non-finite
 // data, field.cpp:46-49, 79).  Pads are +0.0, so the whole allocation is scanned.
-__global__ void etd_nonfinite_scan(const double* __restrict__ f, long long n, int* flag) {
+static __global__ void etd_nonfinite_scan(const double* __restrict__ f, long long n, int* flag) {
     int bad = 0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         bad |= (__double2hiint(f[i]) & 0x7ff00000) == 0x7ff00000;

@@ -32,7 +32,7 @@
 #include <vector>
 
 #include "../../include/etd_b200.h"
-#include "etd_kernels.cuh"
+#include "etd_registry.cuh"
 #include "etd_thomas.cuh"
 #include "etd_setup.hpp"
 
@@ -91,81 +91,12 @@ static CUtensorMap make_map(const double* base, int rank, const unsigned long lo
     return m;
 }
 
-// ------------------------------------------------------------ kernel registry
-struct KernelSpec {
-    const void* fn;
-    int threads, smem, bm, bn, S;
-};
-
-template <int MODE, int S, int EPI, bool PRO, int SK, int BM, int BN, int WMW, int WNW, int ST, int MINB = 1>
-static KernelSpec make_spec() {
-    using Cfg = ContractCfg<MODE, S, EPI, PRO, BM, BN, WMW, WNW, ST>;
-    auto k = etd_contract<MODE, S, EPI, PRO, SK, BM, BN, WMW, WNW, ST, MINB>;
-    return {reinterpret_cast<const void*>(k), Cfg::THREADS, Cfg::SMEM_BYTES, BM, BN, S};
-}
-
-// Tile classes.  T=0 (large grids): 8 warps, 64 FP64 accumulators per thread.
-// T=1 (mid, e.g. 2D n~1000) and T=2 (tiny, n~128): 4-warp CTAs with smaller
-// tiles so that a launch still spreads over the 148 SMs (the step of a 2D
-// 1023^2 grid has only ~1e6 outputs per transform; of a 127^2 grid ~16k).
-// Source-prologue kernels use an Mx1 warp grid so that each A element's f(U) is
-// evaluated by exactly one warp (it runs on the shared FP64/DMMA pipe).
-template <int MODE, int S, int EPI, bool PRO, int SK, int T>
-static KernelSpec spec() {
-    if constexpr (T == 3 && !PRO) {  // large grids, unit-stride kernels: 2 CTAs/SM, 32 accumulators/thread
-        if constexpr (S == 4) return make_spec<MODE, 4, EPI, PRO, SK, 32, 64, 2, 4, 4, 2>();
-        else if constexpr (S == 2) return make_spec<MODE, 2, EPI, PRO, SK, 32, 128, 2, 4, 4, 2>();
-        else return make_spec<MODE, 1, EPI, PRO, SK, 64, 128, 2, 4, 4, 2>();
-    } else if constexpr (T == 2) {
-        if constexpr (PRO) return make_spec<MODE, S, EPI, PRO, SK, 32, 32, 4, 1, 4>();
-        else return make_spec<MODE, S, EPI, PRO, SK, 32, 32, 2, 2, 4>();
-    } else if constexpr (T == 1 && S <= 2) {
-        if constexpr (PRO) return make_spec<MODE, S, EPI, PRO, SK, 64, 64, 4, 1, 6>();
-        else return make_spec<MODE, S, EPI, PRO, SK, 64, 64, 2, 2, 6>();
-    } else {
-        if constexpr (S == 1) return make_spec<MODE, 1, EPI, PRO, SK, 128, 128, 4, 2, 6>();
-        else if constexpr (S == 2 && PRO) return make_spec<MODE, 2, EPI, PRO, SK, 64, 128, 8, 1, 8>();
-        else if constexpr (S == 2) return make_spec<MODE, 2, EPI, PRO, SK, 64, 128, 2, 4, 6>();
-        else if constexpr (PRO) return make_spec<MODE, 4, EPI, PRO, SK, 64, 64, 8, 1, 8>();
-        else return make_spec<MODE, 4, EPI, PRO, SK, 64, 64, 2, 4, 5>();
-    }
-}
-
-// Kernels that evaluate the source are instantiated per source kind; every
-// other kernel ignores sk.
-static KernelSpec pick(int mode, int S, int epi, bool pro, int sk = 0, int tile = 0) {
+// fold: 0 dense, 1-4 parity split (etd_kernels.cuh).  Kernels that evaluate the
+// source are instantiated per source kind; every other kernel ignores sk.
+static KernelSpec pick(int mode, int S, int epi, bool pro, int sk = 0, int tile = 0, int fold = 0) {
     const bool uses_src = pro || epi == EPI_WHAT_SRC;
     if (!uses_src) sk = 0;
-#define ETD_SPEC(M, SS, E, P, K)                                                                \
-    if (mode == M && S == SS && epi == E && pro == P && sk == K)                                \
-        return tile == 3 ? spec<M, SS, E, P, K, 3>() : tile == 2 ? spec<M, SS, E, P, K, 2>()   \
-               : tile == 1 ? spec<M, SS, E, P, K, 1>() : spec<M, SS, E, P, K, 0>();
-#define ETD_SCALAR_KINDS(M, SS, E, P) ETD_SPEC(M, SS, E, P, 0) ETD_SPEC(M, SS, E, P, 1) ETD_SPEC(M, SS, E, P, 2) \
-    ETD_SPEC(M, SS, E, P, 3) ETD_SPEC(M, SS, E, P, 4) ETD_SPEC(M, SS, E, P, 5)
-#define ETD_PAIR_KINDS(M, SS, E, P) ETD_SPEC(M, SS, E, P, 0) ETD_SPEC(M, SS, E, P, 10) ETD_SPEC(M, SS, E, P, 11) \
-    ETD_SPEC(M, SS, E, P, 12) ETD_SPEC(M, SS, E, P, 13)
-    ETD_SCALAR_KINDS(1, 2, EPI_SCALE, true)
-    ETD_PAIR_KINDS(1, 4, EPI_SCALE, true)
-    ETD_SCALAR_KINDS(0, 1, EPI_WHAT_SRC, false)
-    ETD_PAIR_KINDS(0, 2, EPI_WHAT_SRC, false)
-    ETD_SPEC(1, 2, EPI_SCALE, false, 0)
-    ETD_SPEC(1, 4, EPI_SCALE, false, 0)
-    ETD_SPEC(1, 2, EPI_STORE, false, 0)
-    ETD_SPEC(1, 4, EPI_STORE, false, 0)
-    ETD_SPEC(1, 1, EPI_SCALE, false, 0)
-    ETD_SPEC(1, 1, EPI_STORE, false, 0)
-    ETD_SPEC(0, 2, EPI_MIX, false, 0)
-    ETD_SPEC(0, 4, EPI_MIX, false, 0)
-    ETD_SPEC(0, 1, EPI_CORR, false, 0)
-    ETD_SPEC(0, 2, EPI_CORR, false, 0)
-    ETD_SPEC(0, 1, EPI_UPDATE, false, 0)
-    ETD_SPEC(0, 2, EPI_UPDATE, false, 0)
-    ETD_SPEC(0, 1, EPI_SCALE, false, 0)
-    ETD_SPEC(0, 1, EPI_STORE, false, 0)
-#undef ETD_PAIR_KINDS
-#undef ETD_SCALAR_KINDS
-#undef ETD_SPEC
-    throw ConfigError("no kernel variant for this stage / source kind");
+    return fold ? pick_fold(mode, S, epi, sk, tile, fold) : pick_dense(mode, S, epi, pro, sk, tile);
 }
 
 static const void* pick_source(int sk) {
@@ -298,13 +229,14 @@ struct Nccl {
 // ------------------------------------------------------------ the plan
 struct Launch {
     std::string name;
-    int mode = 0, S = 1, epi = 0, tile = 0;
+    int mode = 0, S = 1, epi = 0, tile = 0, fold = 0;
     bool pro = false;
     KernelSpec k;
     dim3 grid;
-    CUtensorMap tmA, tmB;
+    CUtensorMap tmA, tmB, tmA2;  // tmA2: FOLD 3's x-reversed operand (= tmA otherwise)
     ContractArgs args;
     double flops = 0, bytes = 0;
+    double dense_flops = 0;  // the same transform as a dense n x n contraction
 };
 
 // A piece of an exchange: `bytes` at `ptr` to (send) or from (recv) rank `peer`.
@@ -337,6 +269,7 @@ struct StageStat {
     double ms = 0;
     long launches = 0;
     double flops = 0, bytes = 0;
+    double dense_flops = 0;
 };
 
 // Logical extents + strides of one buffer family (the slab, or the z-stage rows).
@@ -498,7 +431,14 @@ struct Plan {
     int* codes = nullptr;            // sharded: [G] gathered fail codes; codes[G] = own
     double* PR[3] = {nullptr, nullptr, nullptr};
     double* PTR[3] = {nullptr, nullptr, nullptr};
-    double* dvec = nullptr;          // [axis][slot 9][species 2][dmax]
+    // parity split (etd_kernels.cuh, FOLD): per axis h and the interleaved h-column
+    // matrices of the forward (FF) and backward (FB) half transforms, stored in the
+    // axis' B layout (x: [2h][ldx] rows; y/z: [h][2h], output index contiguous)
+    bool fold[3] = {false, false, false};
+    int fh[3] = {0, 0, 0};
+    double* FF[3] = {nullptr, nullptr, nullptr};
+    double* FB[3] = {nullptr, nullptr, nullptr};
+    double* dvec = nullptr;          // [order 2][axis][slot 9][species 2][dmax]; order 1 = parity-major
     double* sintab[3] = {nullptr, nullptr, nullptr};  // sin(pi * coord) per axis (global extents)
     int dmax = 0;
     StepStatus* status = nullptr;
@@ -530,10 +470,8 @@ struct Plan {
         for (double* t : sintab) if (t) cudaFree(t);
         for (double2* t : thfac) if (t) cudaFree(t);
         if (thscr) cudaFree(thscr);
-        for (int a = 0; a < 3; ++a) {
-            if (PR[a]) cudaFree(PR[a]);
-            if (PTR[a]) cudaFree(PTR[a]);
-        }
+        for (int a = 0; a < 3; ++a)
+            for (double* m : {PR[a], PTR[a], FF[a], FB[a]}) if (m) cudaFree(m);
         if (status) cudaFree(status);
         if (status_host) cudaFreeHost(status_host);
         if (comm) Nccl::get().CommDestroy(comm);
@@ -544,7 +482,11 @@ struct Plan {
         if (stream) cudaStreamDestroy(stream);
     }
 
-    const double* dv(int axis, int slot) const { return dvec + ((size_t)axis * 9 + slot) * 2 * dmax; }
+    // d-vector slot of an axis in natural mode order, or parity-major on folded axes
+    const double* dv(int axis, int slot) const { return dvn(axis, slot, fold[axis]); }
+    const double* dvn(int axis, int slot, bool parity_major) const {
+        return dvec + (((size_t)(parity_major ? 3 : 0) + axis) * 9 + slot) * 2 * dmax;
+    }
     static int n_axis(const View& v, int a) { return a == 0 ? v.nx : a == 1 ? v.ny : v.nz; }
 
     // ---- maps over stacked fields (one TMA box per stage per operand set) ----
@@ -582,10 +524,26 @@ struct Plan {
         const unsigned box[3] = {16, 16, (unsigned)(bn / 16)};
         return make_map(M, 3, dims, st, box);
     }
+    // parity-split B: 2h interleaved rows x h columns (fold_matrices layout)
+    CUtensorMap mapB_fold(const double* M, int axis, int mode, int bn) const {
+        const unsigned long long h = fh[axis];
+        if (mode == 0) {
+            const unsigned long long dims[2] = {h, 2 * h};
+            const unsigned long long st[1] = {(unsigned long long)round16(h)};
+            const unsigned box[2] = {16, (unsigned)bn};
+            return make_map(M, 2, dims, st, box);
+        }
+        const unsigned long long dims[3] = {16, h, 2 * h / 16};
+        const unsigned long long st[2] = {2 * h, 16};
+        const unsigned box[3] = {16, 16, (unsigned)(bn / 16)};
+        return make_map(M, 3, dims, st, box);
+    }
+    static unsigned long long round16(unsigned long long x) { return (x + 15) / 16 * 16; }
 
     ContractArgs base_args(const View& v, int axis) const {
         ContractArgs a{};
         a.n_axis = n_axis(v, axis);
+        a.kext = a.n_axis;
         a.m_extent = axis == 0 ? v.ny * v.nz : v.nx;
         a.zaxis = axis == 2;
         a.nspecies = ns;
@@ -641,9 +599,19 @@ struct Plan {
     }
 
     // A transform along `axis` of `S` stacked operands at `in` (L loaded), M = P^T (fwd) or P.
+    // Folded axes run the parity-split kernels unless `dense` (the dense n x n
+    // contraction; kernel-level tests of a single direction use it).
+    // x forward transforms fold as FOLD 3 (mirror from the x-reversed operand
+    // `in_rev`) or FOLD 4 (`in` pre-folded); y/z forward as FOLD 1; backward FOLD 2.
     Launch transform(const View& v, const std::string& name, int axis, bool back, int S, int epi, bool pro,
-                     const double* in, double* out) const {
+                     const double* in, double* out, bool dense = false, const double* in_rev = nullptr) const {
         Launch L;
+        int fold = (this->fold[axis] && !dense && !pro) ? (back ? 2 : 1) : 0;
+        if (fold == 1 && axis == 0) {
+            if (epi == EPI_CORR) fold = 4;
+            else if (in_rev) fold = 3;
+            else throw ConfigError("x forward parity split needs the x-reversed operand");
+        }
         L.name = name;
         const int mode = axis == 0 ? 0 : 1;
         L.mode = mode;
@@ -658,31 +626,44 @@ struct Plan {
         //    drain dominate larger tiles at 16 k-tiles
         //  * otherwise 2 CTAs/SM with 32 accumulators (T=3) when that fills two waves
         //  * else the 8-warp tile (T=0) when it fills two waves, else T=2
+        const int nrows = fold ? 2 * fh[axis] : nax;  // B rows = N extent of the launch
+        const int kext = fold ? fh[axis] : nax;
         auto ctas = [&](int t) {
-            const KernelSpec k = pick(mode, S, epi, pro, d.src_kind, t);
-            return (long long)((nax + k.bn - 1) / k.bn) * ((mext + k.bm - 1) / k.bm) * gz;
+            const KernelSpec k = pick(mode, S, epi, pro, d.src_kind, t, fold);
+            return (long long)((nrows + k.bn - 1) / k.bn) * ((mext + k.bm - 1) / k.bm) * gz;
         };
         int tile;
-        if (nax <= 255) tile = 2;
+        if (kext <= (fold ? 128 : 255)) tile = 2;
         else if (ctas(3) >= 2 * 148) tile = 3;
         else if (ctas(0) >= 2 * 148) tile = 0;
         else tile = 2;
         if (const char* f = std::getenv("ETD_FORCE_TILE"))  // tests: exercise every tile class
             if (f[0] >= '0' && f[0] <= '3' && f[1] == 0) tile = f[0] - '0';
         L.tile = tile;
-        L.k = pick(mode, S, epi, pro, d.src_kind, tile);
+        L.fold = fold;
+        L.k = pick(mode, S, epi, pro, d.src_kind, tile, fold);
         const int loaded = pro ? S / 2 : S;
-        // fwd (M = P^T): mode 0 needs row-major P^T, mode 1 row-major P; back swaps
-        const double* M = (mode == 0) != back ? PTR[axis] : PR[axis];
         L.tmA = mode == 0 ? mapA_x(v, in, loaded, L.k.bm) : mapA_yz(v, in, loaded, axis == 2, L.k.bm);
-        L.tmB = mapB(M, axis, mode, L.k.bn);
+        L.tmA2 = fold == 3 ? mapA_x(v, in_rev, loaded, L.k.bm) : L.tmA;
+        if (fold) {
+            L.tmB = mapB_fold(back ? FB[axis] : FF[axis], axis, mode, L.k.bn);
+        } else {
+            // fwd (M = P^T): mode 0 needs row-major P^T, mode 1 row-major P; back swaps
+            const double* M = (mode == 0) != back ? PTR[axis] : PR[axis];
+            L.tmB = mapB(M, axis, mode, L.k.bn);
+        }
         L.args = base_args(v, axis);
         L.args.out = out;
-        const unsigned gx = (nax + L.k.bn - 1) / L.k.bn;
+        L.args.kext = kext;
+        L.args.fold_h = fh[axis];
+        const unsigned gx = (nrows + L.k.bn - 1) / L.k.bn;
         const unsigned gy = (unsigned)((mext + L.k.bm - 1) / L.k.bm);
         L.grid = dim3(gx, gy, gz);
         const double pts = (double)v.nx * v.ny * v.nz;
-        L.flops = 2.0 * nax * pts * S;
+        // executed (= algorithmic) FLOPs of this launch: 2 n per point dense,
+        // 2 (2h) h / n per point split (half)
+        L.flops = 2.0 * ((double)nrows * kext / nax) * pts * S;
+        L.dense_flops = 2.0 * nax * pts * S;
         int outs = S, aux = 0;
         if (epi == EPI_WHAT_SRC) outs = 2 * S;
         if (epi == EPI_CORR || epi == EPI_UPDATE) aux = S;
@@ -797,7 +778,7 @@ static void set_source(Plan& p, int kind, const double* params) {
             } else if (op.kind == Op::KERNEL) {
                 op.L.args.src_kind = kind;
                 for (int i = 0; i < 8; ++i) op.L.args.sp[i] = p.d.src_params[i];
-                op.L.k = pick(op.L.mode, op.L.S, op.L.epi, op.L.pro, kind, op.L.tile);
+                op.L.k = pick(op.L.mode, op.L.S, op.L.epi, op.L.pro, kind, op.L.tile, op.L.fold);
             }
     drop_graphs(p);
 }
@@ -864,6 +845,46 @@ static void ensure_thomas_scratch(Plan& p, long long need) {
     for (auto& steps : p.steps)
         for (auto& op : steps)
             if (op.kind == Op::THOMAS) op.targs.scratch = p.thscr;
+}
+
+// Parity-split half matrices of one axis (etd_kernels.cuh, FOLD) from the
+// reference eigenvector matrix Pc (column-major, P(i,k) = Pc[k n + i],
+// operators.cpp:43-53).  h = (n+1)/2; row r of the 2h interleaved rows is
+// (block b = r/16, t = r%16): group t/8 (0: even modes, 1: odd modes), index
+// q = 8b + t%8.
+//   forward  FF[r][c] = P(c, k), k = 2q + group  (the output mode), c < h the folded
+//            input index; for odd n the centre column c = h-1 is halved in the even
+//            group (s counts it twice) and zero in the odd group (d is 0 there)
+//   backward FB[r][c] = P(q, k), k = 2c + group  (the input mode), q the output
+//            index; the centre row of the odd group is exactly 0 so that the centre
+//            output is o + 0 = o - 0
+// Entries with k >= n are 0.  mode 0 (x) stores [2h][round16(h)] (row r
+// contiguous); mode 1 (y/z) stores the transpose [h][2h].
+static void fold_matrices(const std::vector<double>& Pc, int n, int mode, std::vector<double>& ff,
+                          std::vector<double>& fb) {
+    const int h = (n + 1) / 2;
+    const bool odd = n & 1;
+    const int ld = mode == 0 ? (h + 15) / 16 * 16 : 2 * h;
+    ff.assign(mode == 0 ? (size_t)2 * h * ld : (size_t)h * ld, 0.0);
+    fb.assign(ff.size(), 0.0);
+    auto P = [&](int i, int k) { return Pc[(size_t)k * n + i]; };
+    auto at = [&](std::vector<double>& m, int r, int c) -> double& {
+        return mode == 0 ? m[(size_t)r * ld + c] : m[(size_t)c * ld + r];
+    };
+    for (int r = 0; r < 2 * h; ++r) {
+        const int grp = (r >> 3) & 1, q = (r >> 4) * 8 + (r & 7);
+        if (q >= h) continue;
+        for (int c = 0; c < h; ++c) {
+            const int kf = 2 * q + grp;
+            if (kf < n) {
+                double v = P(c, kf);
+                if (odd && c == h - 1) v = grp == 0 ? 0.5 * v : 0.0;
+                at(ff, r, c) = v;
+            }
+            const int kb = 2 * c + grp;
+            if (kb < n) at(fb, r, c) = (odd && q == h - 1 && grp == 1) ? 0.0 : P(q, kb);
+        }
+    }
 }
 
 static void build_plan(Plan& p, const etd_desc& d) {
@@ -942,7 +963,24 @@ static void build_plan(Plan& p, const etd_desc& d) {
     const bool exact = d.family == ETD_EXACT;
     const PadeScheme scheme = pade_scheme(exact ? 0 : d.family);
     p.thomas = d.backend == ETD_THOMAS;
-    std::vector<double> hd((size_t)3 * 9 * 2 * p.dmax, 0.0);
+    std::vector<double> hd((size_t)2 * 3 * 9 * 2 * p.dmax, 0.0);
+    // Parity split on every spectral axis whose half extent h = (n+1)/2 is a
+    // multiple of 8 (n = 16m - 1 or 16m: all BASELINE configs); ETD_DENSE=1 turns
+    // it off.  A fused source prologue (ETD_FUSED_SOURCE=1) keeps its axis dense.
+    {
+        const char* dn = std::getenv("ETD_DENSE");
+        const bool dense_env = dn && dn[0] == '1';
+        const char* fenv0 = std::getenv("ETD_FUSED_SOURCE");
+        const bool fused0 = fenv0 && fenv0[0] == '1';
+        const char* fa = std::getenv("ETD_FOLD_AXES");  // bit mask (tests / dev tools)
+        const int axes = fa ? std::atoi(fa) : 7;
+        for (int a = 0; a < d.dim; ++a) {
+            const int h = (d.n[a] + 1) / 2;
+            p.fh[a] = h;
+            p.fold[a] = !p.thomas && !dense_env && h % 8 == 0 && (axes >> a & 1) &&
+                        !(fused0 && a == (d.dim == 3 ? 2 : 1));
+        }
+    }
     for (int a = 0; a < d.dim && p.thomas; ++a) {
         // build_thomas_payload (thomas.cpp:88-126) per species: c = tau diag k - s_l,
         // e = tau off k; systems scale the unit-kappa operator by kappa_c
@@ -1006,13 +1044,28 @@ static void build_plan(Plan& p, const etd_desc& d) {
         ETD_CK(cudaMalloc(&p.PTR[a], ptr.size() * 8));
         ETD_CK(cudaMemcpy(p.PR[a], pr.data(), pr.size() * 8, cudaMemcpyHostToDevice));
         ETD_CK(cudaMemcpy(p.PTR[a], ptr.data(), ptr.size() * 8, cudaMemcpyHostToDevice));
+        if (p.fold[a]) {
+            std::vector<double> ff, fb;
+            fold_matrices(Pc, n, a == 0 ? 0 : 1, ff, fb);
+            ETD_CK(cudaMalloc(&p.FF[a], ff.size() * 8));
+            ETD_CK(cudaMalloc(&p.FB[a], fb.size() * 8));
+            ETD_CK(cudaMemcpy(p.FF[a], ff.data(), ff.size() * 8, cudaMemcpyHostToDevice));
+            ETD_CK(cudaMemcpy(p.FB[a], fb.data(), fb.size() * 8, cudaMemcpyHostToDevice));
+        }
         for (int c = 0; c < p.ns; ++c) {
             std::vector<double> lc(lam);
             if (sys)
                 for (auto& x : lc) x *= d.kappa[c];
+            // natural order, and parity-major (position q < h: mode 2q; h + q: mode 2q + 1)
+            const int h = p.fh[a];
             auto put = [&](int slot, const std::vector<double>& v, double sc) {
                 double* o = hd.data() + (((size_t)a * 9 + slot) * 2 + c) * p.dmax;
+                double* op = hd.data() + (((size_t)(3 + a) * 9 + slot) * 2 + c) * p.dmax;
                 for (int i = 0; i < n; ++i) o[i] = sc * v[i];
+                for (int pos = 0; pos < n; ++pos) {
+                    const int k = pos < h ? 2 * pos : 2 * (pos - h) + 1;
+                    op[pos] = k < n ? sc * v[k] : 0.0;
+                }
             };
             if (exact) {
                 // BackendKind::ExactExpReference (stepper.cpp:145-170, 259-295): the same
@@ -1071,14 +1124,15 @@ static void build_plan(Plan& p, const etd_desc& d) {
                 for (int e = 0; e < 6; ++e)
                     for (int pro = 0; pro < 2; ++pro)
                         for (int sk : {0, 1, 2, 3, 4, 5, 10, 11, 12, 13})
-                            for (int tile = 0; tile < 4; ++tile) {
-                                try {
-                                    KernelSpec ks = pick(mode, S, e, pro != 0, sk, tile);
-                                    ETD_CK(cudaFuncSetAttribute(ks.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                                ks.smem));
-                                } catch (const ConfigError&) {
+                            for (int tile = 0; tile < 4; ++tile)
+                                for (int fold = 0; fold < 5; ++fold) {
+                                    try {
+                                        KernelSpec ks = pick(mode, S, e, pro != 0, sk, tile, fold);
+                                        ETD_CK(cudaFuncSetAttribute(
+                                            ks.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ks.smem));
+                                    } catch (const ConfigError&) {
+                                    }
                                 }
-                            }
         attr_done = true;
     }
 
@@ -1202,8 +1256,12 @@ static void build_plan(Plan& p, const etd_desc& d) {
         } else {
             first_transform(V, 1, const_cast<double*>(in), p.Z);
         }
+        // folded x: y_back also writes the x-reversed W into the idle output state
+        // buffer (free until x_back_upd writes U' there, after x_fwd_mix read it)
+        double* wrev = p.fold[0] ? out : nullptr;
         L.push_back(kernel_op(p.transform(V, "y_back", 1, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
-        L.push_back(kernel_op(p.transform(V, "x_fwd_mix", 0, false, 2 * ns, EPI_MIX, false, p.W, p.Z)));
+        L.back().L.args.out_rev = wrev;
+        L.push_back(kernel_op(p.transform(V, "x_fwd_mix", 0, false, 2 * ns, EPI_MIX, false, p.W, p.Z, false, wrev)));
         L.back().L.args.dA = p.dv(0, 0);
         L.back().L.args.dB = p.dv(0, 1);
         L.push_back(kernel_op(p.transform(V, "x_back_src", 0, true, ns, EPI_WHAT_SRC, false, p.Z, p.W)));
@@ -1243,13 +1301,13 @@ static void build_plan(Plan& p, const etd_desc& d) {
     p.stats.clear();
     for (auto& op : p.steps[0])
         if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS)
-            p.stats.push_back({op.L.name, 0, 0, op.L.flops, op.L.bytes});
+            p.stats.push_back({op.L.name, 0, 0, op.L.flops, op.L.bytes, op.L.dense_flops});
     ETD_CK(cudaStreamSynchronize(p.stream));
 }
 
 static void launch(const Launch& L, cudaStream_t s) {
-    void* args[3] = {const_cast<CUtensorMap*>(&L.tmA), const_cast<CUtensorMap*>(&L.tmB),
-                     const_cast<ContractArgs*>(&L.args)};
+    void* args[4] = {const_cast<CUtensorMap*>(&L.tmA), const_cast<CUtensorMap*>(&L.tmB),
+                     const_cast<CUtensorMap*>(&L.tmA2), const_cast<ContractArgs*>(&L.args)};
     ETD_CK(cudaLaunchKernel(L.k.fn, L.grid, dim3(L.k.threads), args, L.k.smem, s));
 }
 
@@ -1749,15 +1807,27 @@ static void debug_transform(Plan& p, int species, int axis, int back, int ell, i
         result = p.Z + (size_t)species * v.F;
     } else if (apply_q) {
         if (ell < 1) throw ConfigError("apply_q needs ell in 1..3");
-        Launch f = p.transform(v, "dbg_fwd", axis, false, 1, EPI_SCALE, false, p.W, p.Z);
+        // folded x: the forward reads its mirror from a host-reversed copy (FOLD 3)
+        double* rev = nullptr;
+        if (axis == 0 && p.fold[0]) {
+            std::vector<double> hr((size_t)v.nx * v.ny * v.nz);
+            for (size_t r = 0; r < (size_t)v.ny * v.nz; ++r)
+                for (int i = 0; i < v.nx; ++i) hr[r * v.nx + i] = in[r * v.nx + (v.nx - 1 - i)];
+            rev = p.state[1 - p.cur];
+            ETD_CK(cudaMemcpy2DAsync(rev, v.pitch * 8, hr.data(), (size_t)v.nx * 8, (size_t)v.nx * 8,
+                                     (size_t)v.ny * v.nz, cudaMemcpyHostToDevice, p.stream));
+            ETD_CK(cudaStreamSynchronize(p.stream));
+        }
+        Launch f = p.transform(v, "dbg_fwd", axis, false, 1, EPI_SCALE, false, p.W, p.Z, false, rev);
         f.args.dA = p.dv(axis, 6 + ell - 1) + species * p.dmax;
         Launch b = p.transform(v, "dbg_back", axis, true, 1, EPI_STORE, false, p.Z, p.W + v.F);
         launch(f, p.stream);
         launch(b, p.stream);
         result = p.W + v.F;
     } else {
-        Launch f = p.transform(v, "dbg", axis, back != 0, 1, ell ? EPI_SCALE : EPI_STORE, false, p.W, p.Z);
-        if (ell) f.args.dA = p.dv(axis, 3 + ell - 1) + species * p.dmax;
+        // one direction in natural mode order: the dense kernel
+        Launch f = p.transform(v, "dbg", axis, back != 0, 1, ell ? EPI_SCALE : EPI_STORE, false, p.W, p.Z, true);
+        if (ell) f.args.dA = p.dvn(axis, 3 + ell - 1, false) + species * p.dmax;
         launch(f, p.stream);
         result = p.Z;
     }
@@ -1989,6 +2059,35 @@ int etd_stage_info(const etd_handle* h, int i, char* name, size_t len, double* m
     if (launches) *launches = s.launches;
     if (flops) *flops = s.flops;
     if (bytes) *bytes = s.bytes;
+    return ETD_OK;
+}
+
+int etd_stage_flops(const etd_handle* h, int i, double* executed, double* dense) {
+    if (!h || i < 0 || i >= (int)h->plan->stats.size()) return ETD_ERR_CONFIG;
+    const auto& s = h->plan->stats[i];
+    if (executed) *executed = s.flops;
+    if (dense) *dense = s.dense_flops > 0 ? s.dense_flops : s.flops;
+    return ETD_OK;
+}
+
+int etd_parity_split(const etd_handle* h, int* out) {
+    if (!h || !out) return ETD_ERR_CONFIG;
+    for (int a = 0; a < h->plan->dim; ++a) out[a] = h->plan->fold[a] ? 1 : 0;
+    return ETD_OK;
+}
+
+int etd_setup_fold_matrices(int n, int mode, double* ff, double* fb) {
+    if (n < 2 || ((n + 1) / 2) % 8 != 0 || (mode != 0 && mode != 1) || !ff || !fb) return ETD_ERR_CONFIG;
+    try {
+        const etd::AxisOperator op = etd::axis_operator(n, 0.0, 1.0, 1, 1.0, 0.0);
+        std::vector<double> Pc, lam, a, b;
+        etd::eigensystem(op, Pc, lam);
+        etd::fold_matrices(Pc, n, mode, a, b);
+        std::memcpy(ff, a.data(), a.size() * 8);
+        std::memcpy(fb, b.data(), b.size() * 8);
+    } catch (...) {
+        return ETD_ERR_CONFIG;
+    }
     return ETD_OK;
 }
 

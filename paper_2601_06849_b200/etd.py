@@ -232,6 +232,9 @@ def lib():
         L.etd_set_profiling.argtypes = [vp, i]
         L.etd_stage_count.argtypes = [vp]
         L.etd_stage_info.argtypes = [vp, i, C.c_char_p, sz, C.POINTER(d), C.POINTER(l), C.POINTER(d), C.POINTER(d)]
+        L.etd_stage_flops.argtypes = [vp, i, C.POINTER(d), C.POINTER(d)]
+        L.etd_parity_split.argtypes = [vp, C.POINTER(C.c_int)]
+        L.etd_setup_fold_matrices.argtypes = [i, i, vp, vp]
         L.etd_debug_transform.argtypes = [vp, i, i, i, i, i, vp, vp]
         L.etd_fill_config_ic.argtypes = [i, C.c_ulonglong, i, i, i, i, vp]
         L.etd_setup_axis.argtypes = [i, d, d, i, d, d, vp, vp]
@@ -436,9 +439,18 @@ class _PlanBase:
             name = C.create_string_buffer(64)
             ms, la, fl, by = C.c_double(), C.c_long(), C.c_double(), C.c_double()
             lib().etd_stage_info(self.handle, i, name, 64, C.byref(ms), C.byref(la), C.byref(fl), C.byref(by))
+            ex, dn = C.c_double(), C.c_double()
+            lib().etd_stage_flops(self.handle, i, C.byref(ex), C.byref(dn))
             out.append({"name": name.value.decode(), "ms_total": ms.value, "launches": la.value,
-                        "flops_per_launch": fl.value, "bytes_per_launch": by.value})
+                        "flops_per_launch": fl.value, "bytes_per_launch": by.value,
+                        "dense_flops_per_launch": dn.value})
         return out
+
+    def parity_split(self) -> tuple:
+        """Per axis: whether the eigenbasis transforms run parity-split (h x h halves)."""
+        a = (C.c_int * 3)()
+        _raise(lib().etd_parity_split(self.handle, a), self.handle)
+        return tuple(bool(a[i]) for i in range(self.grid.dim))
 
     def debug_transform(self, x: np.ndarray, axis: int, back: bool = False, ell: int = 0, apply_q: bool = False,
                         species: int = 0) -> np.ndarray:

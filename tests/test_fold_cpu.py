@@ -1,0 +1,107 @@
+"""CPU: the parity-split half matrices the plan uploads (etd_setup_fold_matrices)
+reproduce the dense eigenbasis transform exactly in exact arithmetic and to
+rounding in FP64, for odd and even n and both storage layouts.
+
+The identity: the DST-I eigenbasis P(i,k) = c sin((i+1)(k+1)pi/(n+1))
+(operators.cpp:43-53) has P(n-1-i, k) = (-1)^k P(i, k), so with s_i = g_i + g_{n-1-i},
+d_i = g_i - g_{n-1-i} (i < h = (n+1)/2) the forward transform is
+ghat_{2q} = sum_i P(i,2q) s_i and ghat_{2q+1} = sum_i P(i,2q+1) d_i, and the
+backward one is g_i = o_i + e_i, g_{n-1-i} = o_i - e_i with o, e the even / odd
+mode sums.  This file restates the kernels' index maps (etd_kernels.cuh FOLD) in
+numpy on top of the library's matrices."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2601_06849_b200 as etd
+from oracle import Oracle
+
+
+def fold_mats(n, mode):
+    h = (n + 1) // 2
+    ld = (h + 15) // 16 * 16 if mode == 0 else 2 * h
+    size = 2 * h * ld if mode == 0 else h * ld
+    ff, fb = np.zeros(size), np.zeros(size)
+    rc = etd.lib().etd_setup_fold_matrices(n, mode, ff.ctypes.data_as(C.c_void_p), fb.ctypes.data_as(C.c_void_p))
+    assert rc == 0
+    if mode == 0:
+        return ff.reshape(2 * h, ld)[:, :h], fb.reshape(2 * h, ld)[:, :h]
+    return ff.reshape(h, 2 * h).T, fb.reshape(h, 2 * h).T   # -> [row][col]
+
+
+def parity_major(n):
+    h = (n + 1) // 2
+    return [2 * q for q in range(h)] + [2 * q + 1 for q in range(n - h)]
+
+
+def fold_forward(g, FF, n):
+    """FOLD 1/3/4: rows r of the interleaved matrix -> parity-major positions."""
+    h = (n + 1) // 2
+    i = np.arange(h)
+    s = g[..., i] + g[..., n - 1 - i]
+    d = g[..., i] - g[..., n - 1 - i]
+    out = np.zeros(g.shape[:-1] + (n,))
+    for r in range(2 * h):
+        grp, pos = (r >> 3) & 1, (r >> 4) * 8 + (r & 7) + ((r >> 3) & 1) * h
+        if pos < n:
+            out[..., pos] = (d if grp else s) @ FF[r]
+    return out
+
+
+def fold_backward(gh, FB, n):
+    """FOLD 2: even / odd mode groups -> o, e -> g_i = o + e, g_{n-1-i} = o - e."""
+    h = (n + 1) // 2
+    S = gh[..., :h]
+    A = np.concatenate([gh[..., h:], np.zeros(gh.shape[:-1] + (2 * h - n,))], -1)
+    out = np.zeros(gh.shape[:-1] + (n,))
+    for r in range(0, 2 * h, 16):
+        for t in range(8):
+            io = (r >> 4) * 8 + t
+            if io < h:
+                o, e = S @ FB[r + t], A @ FB[r + 8 + t]
+                out[..., io] = o + e
+                out[..., n - 1 - io] = o - e
+    return out
+
+
+@pytest.mark.parametrize("n", [15, 16, 31, 47, 48, 63, 127, 255])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fold_matrices_reproduce_dense_transform(n, mode):
+    FF, FB = fold_mats(n, mode)
+    P, _ = Oracle.spectral_factor(n, 2.0, -1.0)   # the reference P (column-major flattening)
+    P = np.asarray(P).reshape(n, n).T if np.asarray(P).ndim == 1 else np.asarray(P)
+    g = np.random.default_rng(n).uniform(-1, 1, (5, n))
+    perm = parity_major(n)
+    dense_fwd = g @ P                          # ghat_k = sum_i P(i,k) g_i
+    assert np.max(np.abs(fold_forward(g, FF, n) - dense_fwd[:, perm])) <= 1e-13 * n
+    gh = np.random.default_rng(n + 1).uniform(-1, 1, (5, n))   # parity-major modes
+    nat = np.zeros_like(gh)
+    nat[:, perm] = gh
+    assert np.max(np.abs(fold_backward(gh, FB, n) - nat @ P.T)) <= 1e-13 * n
+
+
+def test_fold_centre_entries_exact():
+    """Odd n: the centre column of the even forward group is P/2 (s counts the
+    centre twice), the odd group's centre entries are exactly 0 (so the centre
+    output is o + 0 = o - 0 bitwise)."""
+    n = 31
+    h = 16
+    FF, FB = fold_mats(n, 0)
+    P, _ = Oracle.spectral_factor(n, 2.0, -1.0)
+    P = np.asarray(P).reshape(n, n).T if np.asarray(P).ndim == 1 else np.asarray(P)
+    for r in range(2 * h):
+        grp, q = (r >> 3) & 1, (r >> 4) * 8 + (r & 7)
+        if grp == 0:
+            assert FF[r, h - 1] == 0.5 * P[h - 1, 2 * q]
+        else:
+            assert FF[r, h - 1] == 0.0
+            if q == h - 1:
+                assert np.all(FB[r] == 0.0)
+
+
+def test_fold_matrices_refuse_unfoldable_n():
+    buf = np.zeros(4096)
+    p = buf.ctypes.data_as(C.c_void_p)
+    assert etd.lib().etd_setup_fold_matrices(25, 0, p, p) != 0   # h = 13
+    assert etd.lib().etd_setup_fold_matrices(31, 2, p, p) != 0   # bad layout
