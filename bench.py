@@ -210,6 +210,7 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
     stats = plan.stage_stats()
+    parity = list(plan.parity_split())
     plan.set_profiling(False)
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
@@ -247,11 +248,14 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
     transform_flops = sum(st["flops_per_launch"] for _, st in per)
     comm_ms = ms - sum(a for a, _ in per)  # exchange + pack/unpack + commit (sharded), launch gaps
 
+    dense_flops = sum(st.get("dense_flops_per_launch", st["flops_per_launch"]) for _, st in per)
+
     def stage_line(a, st):
         if st["flops_per_launch"] > 0:
             return {"name": st["name"], "ms": round(a, 3), "bound": "tensor",
                     "tflops": round(st["flops_per_launch"] / (a * 1e-3) * 1e-12, 2),
-                    "frac": round(st["flops_per_launch"] / (a * 1e-3) * 1e-12 / FP64_PEAK_TFLOPS, 4)}
+                    "frac": round(st["flops_per_launch"] / (a * 1e-3) * 1e-12 / FP64_PEAK_TFLOPS, 4),
+                    "dense_equiv_tflops": round(st.get("dense_flops_per_launch", 0) / (a * 1e-3) * 1e-12, 2)}
         gbs = st["bytes_per_launch"] / (a * 1e-3) * 1e-9
         return {"name": st["name"], "ms": round(a, 3), "bound": "hbm", "gbs": round(gbs, 1),
                 "frac": round(gbs / 6552.0, 4)}
@@ -261,9 +265,16 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
                 "kernel": dom["name"],
                 "peak_source": FP64_PEAK_NOTE,
                 "algorithmic_flops_per_launch": dom["flops_per_launch"],
+                "dense_flops_per_launch": dom.get("dense_flops_per_launch"),
                 "all_transforms": {"tflops": round(transform_flops / (transform_ms * 1e-3) * 1e-12, 3),
                                    "frac": round(transform_flops / (transform_ms * 1e-3) * 1e-12 / FP64_PEAK_TFLOPS, 4),
-                                   "ms_per_step": round(transform_ms, 3)},
+                                   "ms_per_step": round(transform_ms, 3),
+                                   "dense_equiv_tflops": round(dense_flops / (transform_ms * 1e-3) * 1e-12, 3)},
+                "parity_split": parity,
+                "flops_note": ("achieved/frac count the FLOPs the transforms execute: on parity-split axes "
+                               "(DST-I even/odd modes, DESIGN.md §4a) 2(2h)h/n per point and transform, h=(n+1)/2, "
+                               "half of the dense 2n (SURVEY §8(d)); dense_equiv_tflops = 26 n N per species-step "
+                               "over the same time"),
                 "stages": [stage_line(a, st) for a, st in per],
                 "non_kernel_ms_per_step": round(comm_ms, 3),
                 "hbm_peak_gbs": 6552.0}
@@ -328,7 +339,8 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
                                     "kind": "reference", "sample": f"unavailable: {e}"}
     plan.close()
     if world == 1 and not args.no_alt:
-        line["alt_backends"] = {"thomas": thomas_backend(args, cfg, n, ics, local_rank)}
+        line["alt_backends"] = {"dense_transforms": alt_plan(args, cfg, n, ics, local_rank, "dense"),
+                                "thomas": alt_plan(args, cfg, n, ics, local_rank, "thomas")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -336,15 +348,25 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
     return 0
 
 
-def thomas_backend(args, cfg, n, ics, local_rank):
-    """The same step with BackendKind::Thomas (per-pole complex tridiagonal
-    sweeps, thomas.cpp) on the same inputs: device-resident, CUDA events on the
-    plan's stream.  Reported next to the headline, which stays the eigenbasis
-    transform path the north star names."""
+def alt_plan(args, cfg, n, ics, local_rank, kind):
+    """The same step on the same inputs with
+      kind "dense":  the dense n x n eigenbasis contractions (ETD_DENSE=1, no parity
+                     split) — the roofline of the plain DMMA contraction kernel;
+      kind "thomas": BackendKind::Thomas (per-pole complex tridiagonal sweeps,
+                     thomas.cpp).
+    Device-resident, CUDA events on the plan's stream.  Reported next to the
+    headline, which stays the eigenbasis-transform path the north star names."""
     import torch
     from paper_2601_06849_b200 import configs, etd
     try:
-        tp = configs.make_plan(cfg, n, device=local_rank, backend=etd.BackendKind.Thomas)
+        if kind == "dense":
+            os.environ["ETD_DENSE"] = "1"
+            try:
+                tp = configs.make_plan(cfg, n, device=local_rank)
+            finally:
+                os.environ.pop("ETD_DENSE", None)
+        else:
+            tp = configs.make_plan(cfg, n, device=local_rank, backend=etd.BackendKind.Thomas)
     except Exception as e:  # e.g. out of memory on a smaller device
         return {"value": None, "note": f"unavailable: {e}"}
     try:
@@ -361,14 +383,28 @@ def thomas_backend(args, cfg, n, ics, local_rank):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
         stages = []
+        tr_ms = tr_fl = 0.0
         for st in tp.stage_stats():
             a = st["ms_total"] / max(1, st["launches"])
+            if kind == "dense" and st["flops_per_launch"] > 0:
+                tf = st["flops_per_launch"] / (a * 1e-3) * 1e-12
+                tr_ms, tr_fl = tr_ms + a, tr_fl + st["flops_per_launch"]
+                stages.append({"name": st["name"], "ms": round(a, 3), "bound": "tensor", "tflops": round(tf, 2),
+                               "frac": round(tf / FP64_PEAK_TFLOPS, 4)})
+                continue
             gbs = st["bytes_per_launch"] / (a * 1e-3) * 1e-9
             stages.append({"name": st["name"], "ms": round(a, 3), "bound": "hbm", "gbs": round(gbs, 1),
                            "frac": round(gbs / 6552.0, 4)})
-        return {"value": cfg.points(n) * cfg.nspecies / (ms * 1e-3), "unit": "grid-point updates/s",
-                "ms_per_step": ms, "stages": stages,
-                "note": "BackendKind::Thomas on the device; algorithmic bytes = stage inputs + outputs"}
+        out = {"value": cfg.points(n) * cfg.nspecies / (ms * 1e-3), "unit": "grid-point updates/s",
+               "ms_per_step": ms, "stages": stages}
+        if kind == "dense":
+            tf = tr_fl / (tr_ms * 1e-3) * 1e-12
+            out["all_transforms"] = {"tflops": round(tf, 3), "frac": round(tf / FP64_PEAK_TFLOPS, 4),
+                                     "ms_per_step": round(tr_ms, 3)}
+            out["note"] = "dense n x n DMMA contractions (ETD_DENSE=1): 26 n N FLOPs per species-step"
+        else:
+            out["note"] = "BackendKind::Thomas on the device; algorithmic bytes = stage inputs + outputs"
+        return out
     finally:
         tp.close()
 

@@ -39,9 +39,10 @@
 //          x-reversed copy of the operand (tmA2, written by y_back): TMA needs a
 //          16-byte aligned innermost start, and the mirror of an aligned 16-block
 //          of a pencil with a centre point starts at an odd x.
-//   FOLD 4 (x forward of a pre-folded operand): the operand already holds s at
-//          [0, h) and d at [h, n) (x_back_src writes f(What) that way); boxes at
-//          k0 and h + k0, no DADD.
+//   FOLD 4 (forward of a pre-folded operand): the operand already holds s at
+//          [0, h) and d at [h, n) along the axis (x_back_src writes f(What) that
+//          way; the source pass writes the first transform's stack that way);
+//          boxes at k0 and h + k0, no DADD.
 // Mode space is stored parity-major: position q < h holds mode 2q, h + q holds
 // 2q + 1 (d-vectors are permuted to match).  The B matrix interleaves the two
 // groups by 8 rows (rows 16b..16b+7 even group, 16b+8..16b+15 odd group of the
@@ -221,7 +222,7 @@ struct ContractCfg {
     static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile");
     static_assert(BM % 16 == 0 && BN % 16 == 0, "cta tile");
     static_assert(FOLD == 0 || (WN % 16 == 0 && !PRO), "FOLD pairs 8-row fragments; no source prologue");
-    static_assert(FOLD < 3 || MODE == 0, "FOLD 3/4 are x-axis variants");
+    static_assert(FOLD != 3 || MODE == 0, "FOLD 3 is an x-axis variant");
 };
 
 // 128B-swizzled [rows][16 doubles] tile: element (row, col), TMA SWIZZLE_128B
@@ -320,9 +321,8 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
         auto kperm = [&](int st) {
             return MODE == 0 ? (2 * st + (l & 1) + 8 * (l >> 1)) : (2 * l + (st & 1) + 8 * (st >> 1));
         };
-        // a2: the second A box (FOLD); FOLD 1 turns (a, a2) = (g_k, g_mirror) into (s, d).
-        // The mirror box is read at 15 - k: the swizzle slot maps by an XOR, so the
-        // reversed reads stay bank-conflict free.
+        // a2: the second A box (FOLD).  The mirror box is read at 15 - k: the swizzle
+        // slot maps by an XOR, so the reversed reads stay bank-conflict free.
         auto load_frags = [&](int stg, int st, double (&a)[S][C::MF], double (&a2)[S][C::MF],
                               double (&b)[C::NF]) {
             const double* sA = smem + stg * C::STAGE_DBL;
@@ -346,6 +346,10 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                         a2[s][i] = MODE == 0 ? b2[swz(mm, k2)] : b2[(mm >> 4) * 256 + swz(k2, mm & 15)];
                     }
                 }
+        };
+        // FOLD 1/3: (a, a2) = (g_k, g_mirror) -> (s, d).  Issued after the current
+        // step's DMMAs, so the DADDs never wait on the fragment loads they consume.
+        auto combine = [&](double (&a)[S][C::MF], double (&a2)[S][C::MF]) {
             if constexpr (COMBINE) {
 #pragma unroll
                 for (int s = 0; s < C::L; ++s)
@@ -420,6 +424,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
         uint32_t phase = 0;
         mbar_wait(&full[0], 0);
         load_frags(0, 0, fa[0], fa2[0], fb[0]);
+        combine(fa[0], fa2[0]);
         apply_src(0, 0, fa[0]);
         for (int kt = 0; kt < KT; ++kt) {
             const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
@@ -444,6 +449,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[stage]);
                 }
+                if (st < BK / 4 - 1 || kt + 1 < KT) combine(fa[nxt], fa2[nxt]);
                 if (st < BK / 4 - 1) apply_src(kt, st + 1, fa[nxt]);
                 else if (kt + 1 < KT) apply_src(kt + 1, 0, fa[nxt]);
             }
@@ -767,7 +773,95 @@ struct SourceArgs {
     const double* siny;
     const double* sinz;
     StepStatus* status;
+    // Parity split of the first transform's axis (1 = y, 2 = z; 0 = none): the pass
+    // reads U(,V) at a row and its mirror, evaluates f at both, and writes the
+    // folded stack [U,(V),fU,(fV)] to `fold_out` (s at row r < h, d at row h + r;
+    // the centre row of an odd extent has no d) for a FOLD 4 first transform.
+    int fold;
+    int fh;
+    double* fold_out;
 };
+
+template <int SK>
+__device__ __forceinline__ void source_point(const SourceArgs& a, double srcA, int i, int j, int kz, const double* u,
+                                             double* f, int& bad, int& dom) {
+    if (a.nspecies == 1) {
+        double ustar = 0.0;
+        if constexpr (SK == 4)
+            ustar = srcA * (a.sinx[i] * a.siny[j + a.gj0] * (a.sinz ? a.sinz[kz + a.gz0] : 1.0));
+        f[0] = src1<SK>(a.sp, u[0], ustar);
+        if constexpr (SK == 3)
+            if (i == 0 && j + a.gj0 == 0 && kz + a.gz0 == 0) f[0] = __longlong_as_double(0x7ff8000000000000ll);
+        bad |= !isfinite(f[0]);
+        dom |= src_domain_violation<SK>(u[0]);
+    } else {
+        src2<SK>(a.sp, u[0], u[1], f[0], f[1]);
+        bad |= !(isfinite(f[0]) && isfinite(f[1]));
+    }
+}
+
+// Folded source pass body (SourceArgs::fold): row pairs (r, nf-1-r) along the
+// folded axis, r < h; NS species known at compile time so every per-species
+// value stays in registers.
+template <int SK, int NS>
+__device__ __forceinline__ void source_fold_rows(const SourceArgs& a, double srcA, int nj, int& bad, int& dom) {
+    const int nf = a.fold == 2 ? a.nz : a.ny, h = a.fh;
+    const long long rows = a.fold == 2 ? (long long)h * nj : (long long)a.nz * h;
+    for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+        int kz, j, kz2, j2;
+        if (a.fold == 2) {
+            kz = (int)(r / nj), j = a.j0 + (int)(r % nj), kz2 = nf - 1 - kz, j2 = j;
+        } else {
+            kz = (int)(r / h), j = (int)(r % h), kz2 = kz, j2 = nf - 1 - j;
+        }
+        const bool has_d = h + (a.fold == 2 ? kz : j) < nf;
+        const long long o1 = kz * a.plane + (long long)j * a.pitch, o2 = kz2 * a.plane + (long long)j2 * a.pitch;
+        const long long od = a.fold == 2 ? (h + kz) * a.plane + (long long)j * a.pitch
+                                         : kz * a.plane + (long long)(h + j) * a.pitch;
+        // two adjacent x per thread: 16-byte loads/stores (rows are pitch aligned;
+        // the pad column past an odd nx is +0.0 and is written back as +0.0)
+        for (int i = 2 * threadIdx.x; i < a.nx; i += 2 * blockDim.x) {
+            double2 u1[NS], u2[NS];
+#pragma unroll
+            for (int c = 0; c < NS; ++c) {
+                u1[c] = *reinterpret_cast<const double2*>(a.buf + c * a.F + o1 + i);
+                u2[c] = *reinterpret_cast<const double2*>(a.buf + c * a.F + o2 + i);
+            }
+            double f1[NS][2], f2[NS][2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                double x1[2], x2[2], g1[2] = {0.0, 0.0}, g2[2] = {0.0, 0.0};
+#pragma unroll
+                for (int c = 0; c < NS; ++c) {
+                    x1[c] = e ? u1[c].y : u1[c].x;
+                    x2[c] = e ? u2[c].y : u2[c].x;
+                }
+                if (i + e < a.nx) {
+                    source_point<SK>(a, srcA, i + e, j, kz, x1, g1, bad, dom);
+                    source_point<SK>(a, srcA, i + e, j2, kz2, x2, g2, bad, dom);
+                }
+#pragma unroll
+                for (int c = 0; c < NS; ++c) {
+                    f1[c][e] = g1[c];
+                    f2[c][e] = g2[c];
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < NS; ++c) {
+                double2* S = reinterpret_cast<double2*>(a.fold_out + c * a.F + o1 + i);
+                double2* Sf = reinterpret_cast<double2*>(a.fold_out + (NS + c) * a.F + o1 + i);
+                *S = make_double2(u1[c].x + u2[c].x, u1[c].y + u2[c].y);
+                *Sf = make_double2(f1[c][0] + f2[c][0], f1[c][1] + f2[c][1]);
+                if (has_d) {
+                    double2* D = reinterpret_cast<double2*>(a.fold_out + c * a.F + od + i);
+                    double2* Df = reinterpret_cast<double2*>(a.fold_out + (NS + c) * a.F + od + i);
+                    *D = make_double2(u1[c].x - u2[c].x, u1[c].y - u2[c].y);
+                    *Df = make_double2(f1[c][0] - f2[c][0], f1[c][1] - f2[c][1]);
+                }
+            }
+        }
+    }
+}
 
 template <int SK>
 __global__ void __launch_bounds__(256) etd_source(const SourceArgs a) {
@@ -777,8 +871,15 @@ __global__ void __launch_bounds__(256) etd_source(const SourceArgs a) {
     if (stop) return;
     const double srcA = SK == 4 ? exp(-a.sp[0] * a.status->t) : 0.0;
     const int nj = a.j1 - a.j0;
-    const long long rows = (long long)a.nz * nj;
     int bad = 0, dom = 0;
+    if (a.fold) {
+        if (a.nspecies == 1) source_fold_rows<SK, 1>(a, srcA, nj, bad, dom);
+        else source_fold_rows<SK, 2>(a, srcA, nj, bad, dom);
+        const int any_dom = __syncthreads_or(dom), any_bad = __syncthreads_or(bad);
+        if (threadIdx.x == 0 && (any_dom || any_bad)) atomicCAS(&a.status->fail, 0, any_dom ? 4 : 1);
+        return;
+    }
+    const long long rows = (long long)a.nz * nj;
     for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
         const int kz = (int)(r / nj), j = a.j0 + (int)(r % nj);
         const long long base = kz * a.plane + (long long)j * a.pitch;

@@ -566,13 +566,17 @@ struct Plan {
         return a;
     }
 
-    // The per-step source pass f(t, U(,V)) into the f slots of the stack at `buf`.
-    Op source_op(const View& v, double* buf) const {
+    // The per-step source pass f(t, U(,V)) into the f slots of the stack at `buf`,
+    // or (fold_axis 1/2) the whole stack folded along that axis into `fold_out`.
+    Op source_op(const View& v, double* buf, double* fold_out = nullptr, int fold_axis = 0) const {
         Op o;
         o.kind = Op::SOURCE;
         o.name = "source";
         o.L.name = "source";
         SourceArgs& a = o.sargs;
+        a.fold = 0;
+        a.fh = 0;
+        a.fold_out = nullptr;
         a.buf = buf;
         a.F = v.F;
         a.pitch = v.pitch;
@@ -595,6 +599,12 @@ struct Plan {
         const double pts = (double)v.nx * v.ny * v.nz;
         o.L.flops = 0.0;
         o.L.bytes = pts * 8.0 * 2 * ns;  // read U(,V), write fU(,fV)
+        if (fold_axis) {
+            a.fold = fold_axis;
+            a.fh = fh[fold_axis];
+            a.fold_out = fold_out;
+            o.L.bytes = pts * 8.0 * 3 * ns;  // read U(,V), write the folded [U,(V),fU,(fV)]
+        }
         return o;
     }
 
@@ -604,9 +614,11 @@ struct Plan {
     // x forward transforms fold as FOLD 3 (mirror from the x-reversed operand
     // `in_rev`) or FOLD 4 (`in` pre-folded); y/z forward as FOLD 1; backward FOLD 2.
     Launch transform(const View& v, const std::string& name, int axis, bool back, int S, int epi, bool pro,
-                     const double* in, double* out, bool dense = false, const double* in_rev = nullptr) const {
+                     const double* in, double* out, bool dense = false, const double* in_rev = nullptr,
+                     bool prefolded = false) const {
         Launch L;
         int fold = (this->fold[axis] && !dense && !pro) ? (back ? 2 : 1) : 0;
+        if (fold == 1 && prefolded) fold = 4;
         if (fold == 1 && axis == 0) {
             if (epi == EPI_CORR) fold = 4;
             else if (in_rev) fold = 3;
@@ -633,7 +645,16 @@ struct Plan {
             return (long long)((nrows + k.bn - 1) / k.bn) * ((mext + k.bm - 1) / k.bm) * gz;
         };
         int tile;
-        if (kext <= (fold ? 128 : 255)) tile = 2;
+        if (fold) {
+            // parity-split kernels (tools/tile_sweep.py on configs 1-4, profiles/r01_tile_sweep_fold.txt):
+            //  * S = 4 has one class (32x128, 8 warps)
+            //  * 2 CTAs/SM when that fills two waves, except the S = 2 update (T=3 spills)
+            //  * else the 8-warp tile down to ~2/3 of a wave (2D n = 1023 y stages), else 32x32
+            if (S == 4) tile = 0;
+            else if (ctas(3) >= 2 * 148 && !(epi == EPI_UPDATE && S == 2)) tile = 3;
+            else if (ctas(0) >= 100) tile = 0;
+            else tile = 2;
+        } else if (kext <= 255) tile = 2;
         else if (ctas(3) >= 2 * 148) tile = 3;
         else if (ctas(0) >= 2 * 148) tile = 0;
         else tile = 2;
@@ -1174,14 +1195,19 @@ static void build_plan(Plan& p, const etd_desc& d) {
         // slots of the state stack (default; "source" + "z_fwd"/"y_fwd"), or fused
         // into the first transform's prologue (ETD_FUSED_SOURCE=1, "z_fwd_src"):
         // measured 265 vs 246 + 5.5 ms per config-4 step.
-        auto first_transform = [&](const View& vv, int axis, double* stack, double* dst) {
+        // A parity-split first axis gets its stack folded by the source pass (into
+        // `scratch`, free until the axis' backward transform writes it), so the
+        // forward transform runs FOLD 4 with no s/d adds in its main loop.
+        auto first_transform = [&](const View& vv, int axis, double* stack, double* dst, double* scratch) {
             const char* nm = axis == 2 ? (fused ? "z_fwd_src" : "z_fwd") : (fused ? "y_fwd_src" : "y_fwd");
-            if (!fused) L.push_back(p.source_op(vv, stack));
-            L.push_back(kernel_op(p.transform(vv, nm, axis, false, 2 * ns, EPI_SCALE, fused, stack, dst)));
+            const bool pf = !fused && p.fold[axis];
+            if (!fused) L.push_back(p.source_op(vv, stack, pf ? scratch : nullptr, pf ? axis : 0));
+            L.push_back(kernel_op(p.transform(vv, nm, axis, false, 2 * ns, EPI_SCALE, fused, pf ? scratch : stack,
+                                              dst, false, nullptr, pf)));
             L.back().L.args.dA = p.dv(axis, 0);
         };
         if (p.dim == 3 && !p.sharded) {
-            first_transform(V, 2, const_cast<double*>(in), p.Z);
+            first_transform(V, 2, const_cast<double*>(in), p.Z, p.W);
             L.push_back(kernel_op(p.transform(V, "z_back", 2, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
         } else if (p.dim == 3) {
             // ---- z stage on y-row chunks: pack; forward exchanges (comm stream);
@@ -1230,7 +1256,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
                     double* zin_k = p.zin + p.zbase[k];
                     double* zz_k = p.Zz + p.zbase[k];
                     double* wz_k = p.Wz + p.zbase[k];
-                    first_transform(vk, 2, zin_k, zz_k);
+                    first_transform(vk, 2, zin_k, zz_k, wz_k);
                     L.push_back(kernel_op(p.transform(vk, "z_back", 2, true, 2 * ns, EPI_STORE, false, zz_k, wz_k)));
                 } else {
                     // an empty chunk keeps the op list aligned across virtual ranks
@@ -1254,7 +1280,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
             L.push_back(kernel_op(p.transform(V, "y_fwd", 1, false, 2 * ns, EPI_SCALE, false, p.W, p.Z)));
             L.back().L.args.dA = p.dv(1, 0);
         } else {
-            first_transform(V, 1, const_cast<double*>(in), p.Z);
+            first_transform(V, 1, const_cast<double*>(in), p.Z, p.W);
         }
         // folded x: y_back also writes the x-reversed W into the idle output state
         // buffer (free until x_back_upd writes U' there, after x_fwd_mix read it)

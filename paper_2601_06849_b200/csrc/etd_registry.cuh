@@ -27,8 +27,9 @@ static KernelSpec make_spec() {
 // at the dense kernel's level.
 template <int MODE, int S, int EPI, int SK, int T, int FOLD>
 static KernelSpec fold_spec() {
-    if constexpr (T == 3 && S <= 2) {  // 2 CTAs/SM, 32 accumulators/thread
-        if constexpr (S == 2) return make_spec<MODE, 2, EPI, false, SK, 32, 128, 4, 2, 3, 2, FOLD>();
+    if constexpr (T == 3) {  // 2 CTAs/SM, 32 accumulators/thread
+        if constexpr (S == 4) return make_spec<MODE, 4, EPI, false, SK, 32, 64, 4, 2, 2, 2, FOLD>();
+        else if constexpr (S == 2) return make_spec<MODE, 2, EPI, false, SK, 32, 128, 4, 2, 3, 2, FOLD>();
         else return make_spec<MODE, 1, EPI, false, SK, 64, 128, 4, 2, 3, 2, FOLD>();
     } else if constexpr (T == 2) {
         return make_spec<MODE, S, EPI, false, SK, 32, 32, 2, 2, 4, 1, FOLD>();

@@ -6,10 +6,10 @@ namespace etd {
 KernelSpec pick_fold(int mode, int S, int epi, int sk, int tile, int fold) {
     const bool pro = false;
     const bool fwd = epi == EPI_SCALE || epi == EPI_MIX || epi == EPI_CORR;
-    if (pro || fwd != (fold != 2) || (fold >= 3 && mode != 0))
+    if (pro || fwd != (fold != 2) || (fold == 3 && mode != 0))
         throw ConfigError("no parity-split variant for this stage");
 #define ETD_FSPEC(M, SS, E, K, F)                                                                           \
-    if (mode == M && S == SS && epi == E && sk == K)                                                        \
+    if (mode == M && S == SS && epi == E && sk == K && fold == F)                                           \
         return tile == 3 ? fold_spec<M, SS, E, K, 3, F>() : tile == 2 ? fold_spec<M, SS, E, K, 2, F>()      \
                : tile == 1 ? fold_spec<M, SS, E, K, 1, F>() : fold_spec<M, SS, E, K, 0, F>();
     ETD_FSPEC(1, 1, EPI_SCALE, 0, 1) ETD_FSPEC(1, 2, EPI_SCALE, 0, 1) ETD_FSPEC(1, 4, EPI_SCALE, 0, 1)
@@ -22,6 +22,8 @@ KernelSpec pick_fold(int mode, int S, int epi, int sk, int tile, int fold) {
     }
     if (fold == 4) {
         ETD_FSPEC(0, 1, EPI_CORR, 0, 4) ETD_FSPEC(0, 2, EPI_CORR, 0, 4)
+        // the first (y in 2D, z in 3D) transform of the source pass's folded stack
+        ETD_FSPEC(1, 2, EPI_SCALE, 0, 4) ETD_FSPEC(1, 4, EPI_SCALE, 0, 4)
     }
     ETD_FSPEC(0, 1, EPI_UPDATE, 0, 2) ETD_FSPEC(0, 2, EPI_UPDATE, 0, 2)
     ETD_FSPEC(0, 1, EPI_STORE, 0, 2)
