@@ -780,6 +780,7 @@ struct SourceArgs {
     int fold;
     int fh;
     double* fold_out;
+    int x0, x1;             // x-column range of this launch (the pipelined advance's upload chunks)
 };
 
 template <int SK>
@@ -800,6 +801,20 @@ __device__ __forceinline__ void source_point(const SourceArgs& a, double srcA, i
     }
 }
 
+// A block's threads cover `span` x items of a row; narrow x ranges (the pipelined
+// advance's column chunks) put several rows in one block.
+struct RowMap {
+    int span, rpb, sub, lane;
+};
+__device__ __forceinline__ RowMap row_map(int items) {
+    RowMap m;
+    m.span = items >= (int)blockDim.x ? (int)blockDim.x : (items > 0 ? items : 1);
+    m.rpb = blockDim.x / m.span;
+    m.sub = threadIdx.x / m.span;
+    m.lane = threadIdx.x % m.span;
+    return m;
+}
+
 // Folded source pass body (SourceArgs::fold): row pairs (r, nf-1-r) along the
 // folded axis, r < h; NS species known at compile time so every per-species
 // value stays in registers.
@@ -807,7 +822,10 @@ template <int SK, int NS>
 __device__ __forceinline__ void source_fold_rows(const SourceArgs& a, double srcA, int nj, int& bad, int& dom) {
     const int nf = a.fold == 2 ? a.nz : a.ny, h = a.fh;
     const long long rows = a.fold == 2 ? (long long)h * nj : (long long)a.nz * h;
-    for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int items = (a.x1 - a.x0 + 1) / 2;
+    const RowMap rm = row_map(items);
+    if (rm.sub >= rm.rpb) return;
+    for (long long r = (long long)blockIdx.x * rm.rpb + rm.sub; r < rows; r += (long long)gridDim.x * rm.rpb) {
         int kz, j, kz2, j2;
         if (a.fold == 2) {
             kz = (int)(r / nj), j = a.j0 + (int)(r % nj), kz2 = nf - 1 - kz, j2 = j;
@@ -820,7 +838,8 @@ __device__ __forceinline__ void source_fold_rows(const SourceArgs& a, double src
                                          : kz * a.plane + (long long)(h + j) * a.pitch;
         // two adjacent x per thread: 16-byte loads/stores (rows are pitch aligned;
         // the pad column past an odd nx is +0.0 and is written back as +0.0)
-        for (int i = 2 * threadIdx.x; i < a.nx; i += 2 * blockDim.x) {
+        for (int w = rm.lane; w < items; w += rm.span) {
+            const int i = a.x0 + 2 * w;
             double2 u1[NS], u2[NS];
 #pragma unroll
             for (int c = 0; c < NS; ++c) {
@@ -880,10 +899,12 @@ __global__ void __launch_bounds__(256) etd_source(const SourceArgs a) {
         return;
     }
     const long long rows = (long long)a.nz * nj;
-    for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const RowMap rm = row_map(a.x1 - a.x0);
+    for (long long r = (long long)blockIdx.x * rm.rpb + rm.sub; rm.sub < rm.rpb && r < rows;
+         r += (long long)gridDim.x * rm.rpb) {
         const int kz = (int)(r / nj), j = a.j0 + (int)(r % nj);
         const long long base = kz * a.plane + (long long)j * a.pitch;
-        for (int i = threadIdx.x; i < a.nx; i += blockDim.x) {
+        for (int i = a.x0 + rm.lane; i < a.x1; i += rm.span) {
             const long long o = base + i;
             if (a.nspecies == 1) {
                 const double u = a.buf[o];

@@ -577,6 +577,8 @@ struct Plan {
         a.fold = 0;
         a.fh = 0;
         a.fold_out = nullptr;
+        a.x0 = 0;
+        a.x1 = v.nx;
         a.buf = buf;
         a.F = v.F;
         a.pitch = v.pitch;
@@ -1560,41 +1562,54 @@ static void group_steps(std::vector<Plan*>& ps, int nsteps) {
     if (!err.empty()) throw AbortError(err, et, es);
 }
 
-// Host-buffer advance (the reference's value-semantics call shape) with the
-// host<->device copies pipelined against compute.
-//  * upload: y-row chunks on a copy stream; the z stage (z_fwd_src, z_back —
-//    independent per (x, y) pencil) of the first step runs per y-row chunk as
-//    soon as its rows land.
-//  * download: the y and x stages of the last step (independent per z plane /
-//    per x pencil) run per z-plane chunk; each chunk's rows of U' are copied
-//    back while the next chunk computes.  x-stage tiles of chunk c cover pencil
-//    rows [B_{c-1}, B_c) with B_c = 128*floor(k1*ny/128) <= k1*ny, so a chunk
-//    only reads rows whose y stage has finished and never rows of a later chunk.
-//  * the step commit moves to one etd_commit after the chunks.
-// 3D, unsharded plans; everything else takes set_state / etd_step / get_state.
+// Host-buffer advance (the reference's value-semantics call shape): unsharded
+// plans whose step is source + column (z / y) stages + x stage run it with the
+// host<->device copies pipelined against compute (advance_overlapped below); the
+// step commit moves to one etd_commit after the chunks.  Everything else takes
+// set_state / etd_step / get_state.
 static constexpr int kXferChunks = 16;
 
-// index of the first y-stage op: ops [0, iy) are the z stage (source pass,
-// z_fwd(_src), z_back), ops [iy, end) the y and x stages
-static int y_stage_index(const Plan& p) {
+// Index of the first x-stage op.  Everything before it (the source pass and the
+// z / y stages) treats x as a batch index, so it can run on x-column ranges.
+static int x_stage_index(const Plan& p) {
     const auto& ops = p.steps[0];
     for (size_t k = 0; k < ops.size(); ++k)
-        if (ops[k].kind == Op::KERNEL && ops[k].L.name == "y_fwd") return (int)k;
+        if (ops[k].kind == Op::KERNEL && ops[k].L.mode == 0) return (int)k;
     return -1;
 }
 
 static bool overlap_eligible(const Plan& p, int nsteps) {
-    if (p.dim != 3 || p.sharded || p.profiling || nsteps < 1) return false;
+    if (p.sharded || p.profiling || nsteps < 1) return false;
     const auto& ops = p.steps[0];
-    for (const auto& op : ops)
+    const int ix = x_stage_index(p);
+    if (ix <= 0 || ops.back().L.name != "x_back_upd") return false;
+    for (int k = 0; k < (int)ops.size(); ++k) {
+        const Op& op = ops[k];
         if (op.kind != Op::KERNEL && op.kind != Op::SOURCE) return false;
-    return y_stage_index(p) > 0 && ops.back().L.name == "x_back_upd";
+        if (op.kind == Op::KERNEL && op.L.mode != (k < ix ? 1 : 0)) return false;
+        if (op.kind == Op::SOURCE && k >= ix) return false;
+    }
+    return true;
 }
 
+// Host-buffer advance with the copies hidden behind compute:
+//  * upload in x-column ranges (strided 2D copies; 55.6 GB/s down to 256-byte row
+//    pieces, tools/xfer2d_probe.py).  The first step's source pass and z / y stages
+//    run on each range as soon as it lands: they need every y and z of a column but
+//    nothing of its neighbours, so ~540 ms of config-4 work covers the ~310 ms upload.
+//  * the last step's x stage runs in row chunks (multiples of 128 rows, the largest
+//    x-stage tile height); each chunk's rows of U' stream back while the next computes.
+//    The y stage is complete before the x stage starts, so a chunk never reads rows
+//    a later chunk still has to produce, and x_back_upd's U' (written over the
+//    x-reversed W copy in the output state buffer) only lands on rows x_fwd_mix
+//    has already consumed.
 static void advance_overlapped(Plan& p, const double* const* hin, double* const* hout, long n, double t,
                                int nsteps) {
     const View& V = p.slab;
-    const int C = std::max(1, std::min(kXferChunks, std::min(V.ny, V.nz)));
+    const int XW = std::max(64, round_up((V.nx + kXferChunks - 1) / kXferChunks, 64));
+    const int CX = (V.nx + XW - 1) / XW;
+    const long long R = (long long)V.ny * V.nz;
+    const int C = (int)std::max(1LL, std::min<long long>(kXferChunks, R / 128));
     if (!p.cstream) {
         ETD_CK(cudaStreamCreateWithFlags(&p.cstream, cudaStreamNonBlocking));
         p.xev.resize(2 * kXferChunks + 1);
@@ -1610,83 +1625,64 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
     ETD_CK(cudaMemcpyAsync(p.status, p.status_host, sizeof(StepStatus), cudaMemcpyHostToDevice, p.stream));
     ETD_CK(cudaEventRecord(ev_start, p.stream));
     ETD_CK(cudaStreamWaitEvent(p.cstream, ev_start, 0));
-    auto jlo = [&](int c) { return (int)((long long)c * V.ny / C); };
-    auto zlo = [&](int c) { return (int)((long long)c * V.nz / C); };
-    const long long R = (long long)V.ny * V.nz;
-    auto rowb = [&](int c) {  // x-stage row boundary after chunk c-1 (c = 0..C)
-        if (c >= C) return R;
-        return (long long)zlo(c) * V.ny / 128 * 128;
-    };
+    auto rowb = [&](int c) { return c >= C ? R : R * c / C / 128 * 128; };  // x-stage row chunk bounds
     double* st_in = p.state[p.cur];
-    for (int c = 0; c < C; ++c) {
-        const int j0 = jlo(c), j1 = jlo(c + 1);
-        for (int sp = 0; sp < p.ns; ++sp) {
-            cudaMemcpy3DParms m{};
-            m.srcPtr = make_cudaPitchedPtr(const_cast<double*>(hin[sp]), (size_t)V.nx * 8, V.nx, V.ny);
-            m.dstPtr = make_cudaPitchedPtr(st_in + (size_t)sp * V.F, (size_t)V.pitch * 8, V.nx, V.ny);
-            m.srcPos = make_cudaPos(0, j0, 0);
-            m.dstPos = make_cudaPos(0, j0, 0);
-            m.extent = make_cudaExtent((size_t)V.nx * 8, j1 - j0, V.nz);
-            m.kind = cudaMemcpyHostToDevice;
-            ETD_CK(cudaMemcpy3DAsync(&m, p.cstream));
-        }
+    for (int c = 0; c < CX; ++c) {
+        const int x0 = c * XW, x1 = std::min(V.nx, x0 + XW);
+        for (int sp = 0; sp < p.ns; ++sp)
+            ETD_CK(cudaMemcpy2DAsync(st_in + (size_t)sp * V.F + x0, (size_t)V.pitch * 8, hin[sp] + x0,
+                                     (size_t)V.nx * 8, (size_t)(x1 - x0) * 8, (size_t)R, cudaMemcpyHostToDevice,
+                                     p.cstream));
         ETD_CK(cudaEventRecord(ev_in[c], p.cstream));
     }
-    const int iy = y_stage_index(p);
+    const int ix = x_stage_index(p);
     for (int s = 0; s < nsteps; ++s) {
         const auto& ops = p.steps[(p.cur + s) & 1];
         const bool first = s == 0, last = s == nsteps - 1;
-        // z stage
+        // source + z / y stages: per x-column range in the first step
         if (first) {
-            for (int c = 0; c < C; ++c) {
+            for (int c = 0; c < CX; ++c) {
                 ETD_CK(cudaStreamWaitEvent(p.stream, ev_in[c], 0));
-                const int j0 = jlo(c), j1 = jlo(c + 1);
-                if (j1 == j0) continue;
-                for (int k = 0; k < iy; ++k) {
+                const int x0 = c * XW, x1 = std::min(V.nx, x0 + XW);
+                for (int k = 0; k < ix; ++k) {
                     if (ops[k].kind == Op::SOURCE) {
                         Op o = ops[k];
-                        o.sargs.j0 = j0;
-                        o.sargs.j1 = j1;
+                        o.sargs.x0 = x0;
+                        o.sargs.x1 = x1;
                         run_op(p, o, p.stream);
                     } else {
                         Launch L = ops[k].L;
-                        L.args.outer0 = j0;
-                        L.grid.z = j1 - j0;
+                        L.args.mtile0 = x0 / L.k.bm;
+                        L.grid.y = (unsigned)((x1 + L.k.bm - 1) / L.k.bm - x0 / L.k.bm);
                         launch(L, p.stream);
                     }
                 }
             }
         } else {
-            for (int k = 0; k < iy; ++k) run_op(p, ops[k], p.stream);
+            for (int k = 0; k < ix; ++k) run_op(p, ops[k], p.stream);
         }
-        // y and x stages
+        // x stage
         if (!last) {
-            for (size_t k = iy; k < ops.size(); ++k) run_op(p, ops[k], p.stream);
+            for (size_t k = ix; k < ops.size(); ++k) run_op(p, ops[k], p.stream);
             continue;
         }
         const Op& upd = ops.back();
         for (int c = 0; c < C; ++c) {
-            for (size_t k = iy; k < ops.size(); ++k) {
+            const long long r0 = rowb(c), r1 = rowb(c + 1);
+            if (r1 <= r0) continue;
+            for (size_t k = ix; k < ops.size(); ++k) {
                 Launch L = ops[k].L;
-                if (L.mode == 1) {  // y stage: outer index is z
-                    L.args.outer0 = zlo(c);
-                    L.grid.z = zlo(c + 1) - zlo(c);
-                } else {            // x stage: pencil-row tiles
-                    const long long r0 = rowb(c), r1 = rowb(c + 1);
-                    L.args.mtile0 = (int)(r0 / L.k.bm);
-                    L.grid.y = (unsigned)((r1 + L.k.bm - 1) / L.k.bm - r0 / L.k.bm);
-                    L.args.commit = 0;
-                }
-                if (L.grid.y && L.grid.z) launch(L, p.stream);
+                L.args.mtile0 = (int)(r0 / L.k.bm);
+                L.grid.y = (unsigned)((r1 + L.k.bm - 1) / L.k.bm - r0 / L.k.bm);
+                L.args.commit = 0;
+                launch(L, p.stream);
             }
             ETD_CK(cudaEventRecord(ev_out[c], p.stream));
             ETD_CK(cudaStreamWaitEvent(p.cstream, ev_out[c], 0));
-            const long long r0 = rowb(c), r1 = rowb(c + 1);
-            if (r1 > r0)
-                for (int sp = 0; sp < p.ns; ++sp)
-                    ETD_CK(cudaMemcpy2DAsync(hout[sp] + r0 * V.nx, (size_t)V.nx * 8,
-                                             upd.L.args.out + (size_t)sp * V.F + r0 * V.pitch, (size_t)V.pitch * 8,
-                                             (size_t)V.nx * 8, (size_t)(r1 - r0), cudaMemcpyDeviceToHost, p.cstream));
+            for (int sp = 0; sp < p.ns; ++sp)
+                ETD_CK(cudaMemcpy2DAsync(hout[sp] + r0 * V.nx, (size_t)V.nx * 8,
+                                         upd.L.args.out + (size_t)sp * V.F + r0 * V.pitch, (size_t)V.pitch * 8,
+                                         (size_t)V.nx * 8, (size_t)(r1 - r0), cudaMemcpyDeviceToHost, p.cstream));
         }
         etd_commit<<<1, 1, 0, p.stream>>>(p.status, nullptr, 0, p.tau);
     }

@@ -171,3 +171,35 @@ def test_fold_halves_the_transform_flops():
     h = (n + 1) // 2
     assert st["z_back"]["flops_per_launch"] == pytest.approx(2.0 * 2 * h * h / n * pts * 2)
     assert st["z_back"]["dense_flops_per_launch"] == pytest.approx(2.0 * n * pts * 2)
+
+
+@pytest.mark.parametrize("shape", [(127, 31, 47), (200, 41, 1), (255, 63, 1), (130, 20, 33)])
+def test_pipelined_advance_x_column_chunks_equal_device_resident_steps(shape):
+    """etd_advance uploads in x-column ranges and runs the first step's source and
+    z / y stages per range, then the last step's x stage in row chunks with the
+    download behind it: bitwise equal to upload + etd_step + download (2D and 3D,
+    folded and dense axes, several column chunks, ragged last chunk)."""
+    nx, ny, nz = shape
+    dim = 3 if nz > 1 else 2
+    grid = etd.build_grid(dim, [(0, 1)] * dim, [s + 1 for s in shape[:dim]])
+    N = nx * ny * nz
+    rng = np.random.default_rng(N)
+    u0, v0 = rng.uniform(-1, 1, N), rng.uniform(-0.5, 0.5, N)
+    f = etd.fhn_cubic()
+    for steps in (1, 2):
+        plan = etd.make_system_plan(grid, 0.05, 1e-3, 5e-4, 0.0)
+        a = etd.etd2rkds_step_system(plan, etd.SystemState(4, 0.2, u0, v0), f, nsteps=steps)
+        plan2 = etd.make_system_plan(grid, 0.05, 1e-3, 5e-4, 0.0, source=f)
+        plan2.upload(0, u0, 4, 0.2)
+        plan2.upload(1, v0, 4, 0.2)
+        plan2.step(steps)
+        bu, n, t = plan2.download(0)
+        bv, _, _ = plan2.download(1)
+        assert np.array_equal(a.U, bu) and np.array_equal(a.V, bv), (shape, steps)
+        assert a.n == n == 4 + steps
+    g1 = etd.make_plan(grid, 0.01, 1.0, 1.0)
+    s1 = etd.advance(g1, etd.StepperState(0, 0.0, u0), etd.allen_cahn_cubic(), nsteps=1)
+    g2 = etd.make_plan(grid, 0.01, 1.0, 1.0, source=etd.allen_cahn_cubic())
+    g2.upload(0, u0)
+    g2.step(1)
+    assert np.array_equal(s1.U, g2.download(0)[0])
