@@ -1567,7 +1567,7 @@ static void group_steps(std::vector<Plan*>& ps, int nsteps) {
 // host<->device copies pipelined against compute (advance_overlapped below); the
 // step commit moves to one etd_commit after the chunks.  Everything else takes
 // set_state / etd_step / get_state.
-static constexpr int kXferChunks = 16;
+static constexpr int kXferChunks = 32;
 
 // Index of the first x-stage op.  Everything before it (the source pass and the
 // z / y stages) treats x as a batch index, so it can run on x-column ranges.
@@ -1606,7 +1606,12 @@ static bool overlap_eligible(const Plan& p, int nsteps) {
 static void advance_overlapped(Plan& p, const double* const* hin, double* const* hout, long n, double t,
                                int nsteps) {
     const View& V = p.slab;
-    const int XW = std::max(64, round_up((V.nx + kXferChunks - 1) / kXferChunks, 64));
+    const int ix = x_stage_index(p);
+    // column chunk width: a multiple of every column-stage tile height (BM)
+    int bm = 32;
+    for (int k = 0; k < ix; ++k)
+        if (p.steps[0][k].kind == Op::KERNEL) bm = std::max(bm, p.steps[0][k].L.k.bm);
+    const int XW = round_up((V.nx + kXferChunks - 1) / kXferChunks, bm);
     const int CX = (V.nx + XW - 1) / XW;
     const long long R = (long long)V.ny * V.nz;
     const int C = (int)std::max(1LL, std::min<long long>(kXferChunks, R / 128));
@@ -1635,7 +1640,6 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
                                      p.cstream));
         ETD_CK(cudaEventRecord(ev_in[c], p.cstream));
     }
-    const int ix = x_stage_index(p);
     for (int s = 0; s < nsteps; ++s) {
         const auto& ops = p.steps[(p.cur + s) & 1];
         const bool first = s == 0, last = s == nsteps - 1;
