@@ -211,6 +211,7 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
     ms = e0.elapsed_time(e1) / args.steps
     stats = plan.stage_stats()
     parity = list(plan.parity_split())
+    fold_level = list(plan.fold_level())
     plan.set_profiling(False)
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
@@ -237,7 +238,9 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
             tr = json.load(open(tpath)).get(f"cfg{cfg.id}_n{n}", {})
             # z_fwd and y_fwd (z_back and y_back) are the same kernel on the same
             # shape; the slowest of the pair flips run to run
-            twin = {"y_fwd": "z_fwd", "z_fwd": "y_fwd", "y_back": "z_back", "z_back": "y_back"}
+            twin = {"y_fwd": "z_fwd", "z_fwd": "y_fwd", "y_back": "z_back", "z_back": "y_back",
+                    "y_fwd_even": "z_fwd_even", "z_fwd_even": "y_fwd_even",
+                    "y_fwd_odd": "z_fwd_odd", "z_fwd_odd": "y_fwd_odd"}
             for name in (dom["name"], twin.get(dom["name"])):
                 if name in tr:
                     traffic, traffic_stage = tr[name], name
@@ -271,10 +274,13 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
                                    "ms_per_step": round(transform_ms, 3),
                                    "dense_equiv_tflops": round(dense_flops / (transform_ms * 1e-3) * 1e-12, 3)},
                 "parity_split": parity,
+                "fold_level": fold_level,
                 "flops_note": ("achieved/frac count the FLOPs the transforms execute: on parity-split axes "
                                "(DST-I even/odd modes, DESIGN.md §4a) 2(2h)h/n per point and transform, h=(n+1)/2, "
-                               "half of the dense 2n (SURVEY §8(d)); dense_equiv_tflops = 26 n N per species-step "
-                               "over the same time"),
+                               "half of the dense 2n (SURVEY §8(d)); with the second-level split (fold_level 2, "
+                               "DESIGN.md §4b) a forward transform runs two launches of 2(2H)H/n, H=h/2, a quarter "
+                               "of the dense FLOPs; dense_equiv_tflops = 26 n N per species-step over the same time; "
+                               "fold_* stages are the HBM-bound stack passes of the second-level split"),
                 "stages": [stage_line(a, st) for a, st in per],
                 "non_kernel_ms_per_step": round(comm_ms, 3),
                 "hbm_peak_gbs": 6552.0}

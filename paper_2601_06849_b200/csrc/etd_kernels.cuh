@@ -43,6 +43,15 @@
 //          [0, h) and d at [h, n) along the axis (x_back_src writes f(What) that
 //          way; the source pass writes the first transform's stack that way);
 //          boxes at k0 and h + k0, no DADD.
+//   FOLD 5 (second-level split, even-mode group of a forward transform): the
+//          even-mode half is DST-III shaped, P(i, 2(h-1-q)) = (-1)^i P(i, 2q), so
+//          with s split by the parity of i (boxes at kbase + k0 and kbase + H + k0,
+//          H = h/2) a_q = sum_{i even} P(i,2q) s_i, b_q = sum_{i odd} P(i,2q) s_i give
+//          ghat_{2q} = a + b and ghat_{2(h-1-q)} = a - b: the FOLD 2 dataflow
+//          (two h/2-long contractions, +/- in the epilogue) with a forward epilogue.
+//          The odd-mode half is a DST-I of size h-1 and runs as FOLD 4 on its own
+//          folded stack (boxes at kbase = h), output positions from nbase = h.
+//          The stacks come from etd_fold2 (below); DESIGN.md §4b.
 // Mode space is stored parity-major: position q < h holds mode 2q, h + q holds
 // 2q + 1 (d-vectors are permuted to match).  The B matrix interleaves the two
 // groups by 8 rows (rows 16b..16b+7 even group, 16b+8..16b+15 odd group of the
@@ -103,6 +112,8 @@ struct ContractArgs {
     int kext;               // contraction extent (n_axis; h under FOLD)
     int fold_h;             // FOLD: h = (n_axis + 1) / 2, a multiple of 8
     double* out_rev;        // MODE 1 EPI_STORE: also store each output at x' = m_extent-1-x (FOLD 3 input)
+    int kbase;              // FOLD 2/4/5: axis coordinate of the first A box (second-level split groups)
+    int nbase;              // FOLD 4: first output position (second-level split, odd-mode group)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -238,6 +249,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                  const __grid_constant__ CUtensorMap tmA2, const ContractArgs args) {
     constexpr bool FWD_FOLD = FOLD == 1 || FOLD == 3 || FOLD == 4;  // output in parity-major mode order
     constexpr bool COMBINE = FOLD == 1 || FOLD == 3;                 // (g, g_mirror) -> (s, d) in registers
+    constexpr bool BFLY = FOLD == 2 || FOLD == 5;                    // outputs (o + e, o - e) from paired fragments
     using C = ContractCfg<MODE, S, EPI, PRO, BM, BN, WARPS_M, WARPS_N, STAGES, FOLD>;
     constexpr int BK = C::BK;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -285,14 +297,15 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
         double* sB = sA + C::A_DBL;
         mbar_expect_tx(&full[stage], C::TX_BYTES);
         const int k0 = kt * BK;
-        const int k1 = FOLD == 1 ? args.n_axis - k0 - BK : FOLD == 3 ? k0 : args.fold_h + k0;
+        const int k1 = (FOLD == 1 ? args.n_axis - k0 - BK : FOLD == 3 ? k0 : args.fold_h + k0) + args.kbase;
+        const int ka = k0 + args.kbase;
         if constexpr (MODE == 0) {
-            tma_load_3d(sA, &tmA, &full[stage], k0, m0, 0);
+            tma_load_3d(sA, &tmA, &full[stage], ka, m0, 0);
             if constexpr (FOLD != 0)
                 tma_load_3d(sA + C::A1_DBL, FOLD == 3 ? &tmA2 : &tmA, &full[stage], k1, m0, 0);
             tma_load_2d(sB, &tmB, &full[stage], k0, n0);
         } else {
-            tma_load_5d(sA, &tmA, &full[stage], 0, k0, m0 >> 4, outer, 0);
+            tma_load_5d(sA, &tmA, &full[stage], 0, ka, m0 >> 4, outer, 0);
             if constexpr (FOLD != 0) tma_load_5d(sA + C::A1_DBL, &tmA, &full[stage], 0, k1, m0 >> 4, outer, 0);
             tma_load_3d(sB, &tmB, &full[stage], 0, k0, n0 >> 4);
         }
@@ -507,7 +520,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                 return r;
             } else if constexpr (FWD_FOLD) {
                 const int r = n0 + wn0 + jp * 8 + 2 * l;
-                const int c = (r >> 4) * 8 + (r & 7) + ((r >> 3) & 1) * args.fold_h;
+                const int c = (r >> 4) * 8 + (r & 7) + ((r >> 3) & 1) * args.fold_h + args.nbase;
                 const bool in = r < 2 * args.fold_h;
                 v0 = in && c < args.n_axis;
                 v1 = in && c + 1 < args.n_axis;
@@ -521,7 +534,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
             }
         };
         auto val = [&](int s, int i, int jp, int e) -> double {
-            if constexpr (FOLD != 2) return acc[s][i][jp][e];
+            if constexpr (!BFLY) return acc[s][i][jp][e];
             else {
                 const int jj = jp < NP / 2 ? jp : jp - NP / 2;
                 if (jp < NP / 2) return acc[s][i][2 * jj][e] + acc[s][i][2 * jj + 1][e];
@@ -928,6 +941,111 @@ __global__ void __launch_bounds__(256) etd_source(const SourceArgs a) {
     }
     const int any_dom = __syncthreads_or(dom), any_bad = __syncthreads_or(bad);
     if (threadIdx.x == 0 && (any_dom || any_bad)) atomicCAS(&a.status->fail, 0, any_dom ? 4 : 1);
+}
+
+// ------------------------------------------------------------- second-level fold pass
+// Stack of a forward transform along one axis of extent n = 4H - 1 (h = 2H) for the
+// second-level parity split (FOLD 5 + FOLD 4 launches).  With
+// s_i = g_i + g_{n-1-i} (i < h; the centre s_{h-1} = 2 g_{h-1}) and
+// d_i = g_i - g_{n-1-i} (i < h-1) the output positions along the axis are
+//   [0, H)       s at even i   (s_{2k} at k)
+//   [H, 2H)      s at odd i    (s_{2k+1} at H + k)
+//   [2H, 3H)     d_k + d_{2H-2-k}   (the centre k = H-1: 2 d_{H-1})
+//   [3H, 4H-1)   d_k - d_{2H-2-k}
+// One work item is the orbit {k, n-1-k, 2H-2-k, 2H+k} of k < H-1 (4 in, 4 out);
+// k = H-1 also carries the centre of s.  `from1`: the input already holds the
+// first-level stack (s at [0, h), d at [h, n); x_back_src writes f(What) so).
+// HBM-bound: every element is read once and written once.
+struct Fold2Args {
+    const double* in;
+    double* out;
+    long long Fin, Fout;    // field strides of the input / output stacks
+    int nf;                 // fields
+    int axis;               // 0 x (unit stride), 1 y, 2 z
+    int n, H;
+    int from1;
+    long long pitch, plane;
+    int nx, ny, nz;
+    int x0, x1;             // y/z: x-column range (x0 even)
+    long long r0, r1;       // x: row range (row = y + ny z)
+};
+
+__device__ __forceinline__ int fold2_spos(int i, int H) { return (i & 1) ? H + (i >> 1) : (i >> 1); }
+
+template <class T, class Get>
+__device__ __forceinline__ void fold2_orbit(int k, int H, bool from1, const Get& get, T (&o)[6]) {
+    // o: s_k, s_c (c = 2H-2-k), dd_s, dd_d, s_centre (k = H-1 only)
+    const int n = 4 * H - 1, c = 2 * H - 2 - k;
+    T si, sc, di, dc;
+    if (from1) {
+        si = get(k); sc = get(c); di = get(2 * H + k); dc = get(2 * H + c);
+    } else {
+        const T ga = get(k), gb = get(n - 1 - k), gc = get(c), ge = get(n - 1 - c);
+        si = ga + gb; di = ga - gb; sc = gc + ge; dc = gc - ge;
+    }
+    o[0] = si; o[1] = sc; o[2] = di + dc; o[3] = di - dc;
+    if (k == H - 1) o[4] = from1 ? get(2 * H - 1) : get(2 * H - 1) + get(2 * H - 1);
+}
+
+__device__ __forceinline__ double2 operator+(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 operator-(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+static __global__ void __launch_bounds__(256) etd_fold2(const Fold2Args a) {
+    const int H = a.H;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    if (a.axis == 0) {
+        const long long rows = a.r1 - a.r0, total = rows * H;
+        for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += stride) {
+            const int k = (int)(t % H);
+            const long long row = a.r0 + t / H;
+            for (int f = 0; f < a.nf; ++f) {
+                const double* src = a.in + f * a.Fin + row * a.pitch;
+                double* dst = a.out + f * a.Fout + row * a.pitch;
+                double o[6];
+                fold2_orbit(k, H, a.from1, [&](int i) { return src[i]; }, o);
+                const int c = 2 * H - 2 - k;
+                dst[fold2_spos(k, H)] = o[0];
+                if (c != k) dst[fold2_spos(c, H)] = o[1];
+                if (k == H - 1) {
+                    dst[2 * H + k] = o[2];  // c = k here: 2 d_{H-1}, and no difference term
+                    dst[2 * H - 1] = o[4];
+                } else {
+                    dst[2 * H + k] = o[2];
+                    dst[3 * H + k] = o[3];
+                }
+            }
+        }
+        return;
+    }
+    // y / z: x pairs are the fast index (16-byte accesses), orbits along the axis
+    const long long sk = a.axis == 1 ? a.pitch : a.plane, so = a.axis == 1 ? a.plane : a.pitch;
+    const int nouter = a.axis == 1 ? a.nz : a.ny;
+    const int items = (a.x1 - a.x0 + 1) / 2;
+    const long long total = (long long)nouter * H * items;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int w = (int)(t % items);
+        const long long r = t / items;
+        const int k = (int)(r % H), outer = (int)(r / H);
+        const int x = a.x0 + 2 * w;
+        for (int f = 0; f < a.nf; ++f) {
+            const double* src = a.in + f * a.Fin + outer * so + x;
+            double* dst = a.out + f * a.Fout + outer * so + x;
+            auto get = [&](int i) { return *reinterpret_cast<const double2*>(src + i * sk); };
+            double2 o[6];
+            fold2_orbit(k, H, a.from1, get, o);
+            auto put = [&](int i, double2 v) { *reinterpret_cast<double2*>(dst + i * sk) = v; };
+            const int c = 2 * H - 2 - k;
+            put(fold2_spos(k, H), o[0]);
+            if (c != k) put(fold2_spos(c, H), o[1]);
+            if (k == H - 1) {
+                put(2 * H + k, o[2]);
+                put(2 * H - 1, o[4]);
+            } else {
+                put(2 * H + k, o[2]);
+                put(3 * H + k, o[3]);
+            }
+        }
+    }
 }
 
 // Order-independent checksum of a buffer (debugging aid, ETD_DEBUG_CHECKSUM):

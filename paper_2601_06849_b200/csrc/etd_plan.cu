@@ -247,13 +247,14 @@ struct Piece {
 };
 
 struct Op {
-    enum Kind { KERNEL, SOURCE, COPY2D, EXCHANGE, FAILCODE, COMMIT, THOMAS, NOP } kind = KERNEL;
+    enum Kind { KERNEL, SOURCE, COPY2D, EXCHANGE, FAILCODE, COMMIT, THOMAS, NOP, FOLD } kind = KERNEL;
     // sharded steps: 1 = run on the communication stream; events (indices into
     // Plan::sev) waited on before / recorded after the op (ignored by virtual ranks)
     int strm = 0, wait_ev = -1, rec_ev = -1;
     Launch L;                                    // KERNEL (and SOURCE/THOMAS: name/flops/bytes)
     SourceArgs sargs{};                          // SOURCE
     ThomasArgs targs{};                          // THOMAS
+    Fold2Args fargs{};                           // FOLD (second-level split stack, etd_fold2)
     int th_epi = 0;
     const void* src_fn = nullptr;                // SOURCE / THOMAS kernel
     unsigned src_blocks = 0;
@@ -438,7 +439,13 @@ struct Plan {
     int fh[3] = {0, 0, 0};
     double* FF[3] = {nullptr, nullptr, nullptr};
     double* FB[3] = {nullptr, nullptr, nullptr};
-    double* dvec = nullptr;          // [order 2][axis][slot 9][species 2][dmax]; order 1 = parity-major
+    // second-level split: forward = etd_fold2 stack + FOLD 5 (GA, even
+    // modes) + FOLD 4 (GB, odd modes); FB then reads the level-2 mode positions
+    bool fold2[3] = {false, false, false};
+    bool fold2_all = false;          // every axis split twice: the step runs the level-2 schedule
+    double* GA[3] = {nullptr, nullptr, nullptr};
+    double* GB[3] = {nullptr, nullptr, nullptr};
+    double* dvec = nullptr;          // [order 3][axis][slot 9][species 2][dmax]; order 1 = parity-major, 2 = level 2
     double* sintab[3] = {nullptr, nullptr, nullptr};  // sin(pi * coord) per axis (global extents)
     int dmax = 0;
     StepStatus* status = nullptr;
@@ -471,7 +478,7 @@ struct Plan {
         for (double2* t : thfac) if (t) cudaFree(t);
         if (thscr) cudaFree(thscr);
         for (int a = 0; a < 3; ++a)
-            for (double* m : {PR[a], PTR[a], FF[a], FB[a]}) if (m) cudaFree(m);
+            for (double* m : {PR[a], PTR[a], FF[a], FB[a], GA[a], GB[a]}) if (m) cudaFree(m);
         if (status) cudaFree(status);
         if (status_host) cudaFreeHost(status_host);
         if (comm) Nccl::get().CommDestroy(comm);
@@ -483,9 +490,9 @@ struct Plan {
     }
 
     // d-vector slot of an axis in natural mode order, or parity-major on folded axes
-    const double* dv(int axis, int slot) const { return dvn(axis, slot, fold[axis]); }
-    const double* dvn(int axis, int slot, bool parity_major) const {
-        return dvec + (((size_t)(parity_major ? 3 : 0) + axis) * 9 + slot) * 2 * dmax;
+    const double* dv(int axis, int slot) const { return dvn(axis, slot, fold[axis] ? (fold2[axis] ? 2 : 1) : 0); }
+    const double* dvn(int axis, int slot, int order) const {
+        return dvec + (((size_t)3 * order + axis) * 9 + slot) * 2 * dmax;
     }
     static int n_axis(const View& v, int a) { return a == 0 ? v.nx : a == 1 ? v.ny : v.nz; }
 
@@ -524,9 +531,9 @@ struct Plan {
         const unsigned box[3] = {16, 16, (unsigned)(bn / 16)};
         return make_map(M, 3, dims, st, box);
     }
-    // parity-split B: 2h interleaved rows x h columns (fold_matrices layout)
-    CUtensorMap mapB_fold(const double* M, int axis, int mode, int bn) const {
-        const unsigned long long h = fh[axis];
+    // parity-split B: 2h interleaved rows x h columns (fold_matrices layout; GA/GB with h = H)
+    CUtensorMap mapB_fold(const double* M, int axis, int mode, int bn, int hh = 0) const {
+        const unsigned long long h = hh ? hh : fh[axis];
         if (mode == 0) {
             const unsigned long long dims[2] = {h, 2 * h};
             const unsigned long long st[1] = {(unsigned long long)round16(h)};
@@ -610,18 +617,57 @@ struct Plan {
         return o;
     }
 
+    // The second-level split stack (etd_fold2) of `nf` fields along `axis`: in -> out
+    // (stacks with field stride v.F); from1: `in` holds the first-level stack.
+    Op fold_op(const View& v, const std::string& name, int axis, const double* in, double* out, int nf,
+               bool from1 = false) const {
+        Op o;
+        o.kind = Op::FOLD;
+        o.name = name;
+        o.L.name = name;
+        o.L.mode = axis == 0 ? 0 : 1;
+        Fold2Args& a = o.fargs;
+        a.in = in;
+        a.out = out;
+        a.Fin = a.Fout = v.F;
+        a.nf = nf;
+        a.axis = axis;
+        a.n = n_axis(v, axis);
+        a.H = fh[axis] / 2;
+        a.from1 = from1 ? 1 : 0;
+        a.pitch = v.pitch;
+        a.plane = v.plane;
+        a.nx = v.nx;
+        a.ny = v.ny;
+        a.nz = v.nz;
+        a.x0 = 0;
+        a.x1 = v.nx;
+        a.r0 = 0;
+        a.r1 = (long long)v.ny * v.nz;
+        const double pts = (double)v.nx * v.ny * v.nz;
+        o.L.flops = 0.0;
+        o.L.bytes = pts * 8.0 * 2 * nf;
+        o.src_blocks = 148u * 16u;
+        return o;
+    }
+
     // A transform along `axis` of `S` stacked operands at `in` (L loaded), M = P^T (fwd) or P.
     // Folded axes run the parity-split kernels unless `dense` (the dense n x n
     // contraction; kernel-level tests of a single direction use it).
     // x forward transforms fold as FOLD 3 (mirror from the x-reversed operand
     // `in_rev`) or FOLD 4 (`in` pre-folded); y/z forward as FOLD 1; backward FOLD 2.
+    // part 1 / 2: the even- / odd-mode launch of a second-level split forward
+    // transform (FOLD 5 / FOLD 4) of the etd_fold2 stack at `in`.
     Launch transform(const View& v, const std::string& name, int axis, bool back, int S, int epi, bool pro,
                      const double* in, double* out, bool dense = false, const double* in_rev = nullptr,
-                     bool prefolded = false) const {
+                     bool prefolded = false, int part = 0) const {
         Launch L;
         int fold = (this->fold[axis] && !dense && !pro) ? (back ? 2 : 1) : 0;
         if (fold == 1 && prefolded) fold = 4;
-        if (fold == 1 && axis == 0) {
+        if (part) {
+            if (!fold2[axis] || back || pro || dense) throw ConfigError("second-level split needs a fold2 forward");
+            fold = part == 1 ? 5 : 4;
+        } else if (fold == 1 && axis == 0) {
             if (epi == EPI_CORR) fold = 4;
             else if (in_rev) fold = 3;
             else throw ConfigError("x forward parity split needs the x-reversed operand");
@@ -640,8 +686,9 @@ struct Plan {
         //    drain dominate larger tiles at 16 k-tiles
         //  * otherwise 2 CTAs/SM with 32 accumulators (T=3) when that fills two waves
         //  * else the 8-warp tile (T=0) when it fills two waves, else T=2
-        const int nrows = fold ? 2 * fh[axis] : nax;  // B rows = N extent of the launch
-        const int kext = fold ? fh[axis] : nax;
+        const int H2 = fh[axis] / 2;
+        const int nrows = part ? 2 * H2 : fold ? 2 * fh[axis] : nax;  // B rows = N extent of the launch
+        const int kext = part ? H2 : fold ? fh[axis] : nax;
         auto ctas = [&](int t) {
             const KernelSpec k = pick(mode, S, epi, pro, d.src_kind, t, fold);
             return (long long)((nrows + k.bn - 1) / k.bn) * ((mext + k.bm - 1) / k.bm) * gz;
@@ -668,7 +715,9 @@ struct Plan {
         const int loaded = pro ? S / 2 : S;
         L.tmA = mode == 0 ? mapA_x(v, in, loaded, L.k.bm) : mapA_yz(v, in, loaded, axis == 2, L.k.bm);
         L.tmA2 = fold == 3 ? mapA_x(v, in_rev, loaded, L.k.bm) : L.tmA;
-        if (fold) {
+        if (part) {
+            L.tmB = mapB_fold(part == 1 ? GA[axis] : GB[axis], axis, mode, L.k.bn, H2);
+        } else if (fold) {
             L.tmB = mapB_fold(back ? FB[axis] : FF[axis], axis, mode, L.k.bn);
         } else {
             // fwd (M = P^T): mode 0 needs row-major P^T, mode 1 row-major P; back swaps
@@ -679,6 +728,14 @@ struct Plan {
         L.args.out = out;
         L.args.kext = kext;
         L.args.fold_h = fh[axis];
+        if (part == 1) {
+            L.args.n_axis = 2 * H2;  // the FOLD 2 mirror pairs (q, h-1-q) of the even-mode group
+            L.args.fold_h = H2;
+        } else if (part == 2) {
+            L.args.fold_h = H2;
+            L.args.kbase = 2 * H2;
+            L.args.nbase = 2 * H2;
+        }
         const unsigned gx = (nrows + L.k.bn - 1) / L.k.bn;
         const unsigned gy = (unsigned)((mext + L.k.bm - 1) / L.k.bm);
         L.grid = dim3(gx, gy, gz);
@@ -686,11 +743,11 @@ struct Plan {
         // executed (= algorithmic) FLOPs of this launch: 2 n per point dense,
         // 2 (2h) h / n per point split (half)
         L.flops = 2.0 * ((double)nrows * kext / nax) * pts * S;
-        L.dense_flops = 2.0 * nax * pts * S;
+        L.dense_flops = 2.0 * nax * pts * S * (part ? 0.5 : 1.0);
         int outs = S, aux = 0;
         if (epi == EPI_WHAT_SRC) outs = 2 * S;
         if (epi == EPI_CORR || epi == EPI_UPDATE) aux = S;
-        L.bytes = pts * 8.0 * (loaded + outs + aux);
+        L.bytes = pts * 8.0 * (loaded + outs + aux) * (part ? 0.5 : 1.0);
         return L;
     }
 
@@ -910,6 +967,61 @@ static void fold_matrices(const std::vector<double>& Pc, int n, int mode, std::v
     }
 }
 
+// Second-level split of an axis with n = 4H - 1, h = 2H.  Mode
+// positions: p < h -> mode 2p; h + c -> mode 4c + 1 (c < H), 4(c - H) + 3 (c >= H).
+static int fold2_mode(int pos, int n) {
+    const int h = (n + 1) / 2, H = h / 2;
+    if (pos < h) return 2 * pos;
+    const int c = pos - h;
+    return c < H ? 4 * c + 1 : 4 * (c - H) + 3;
+}
+// GA (FOLD 5, even modes): row r = (block b = r/16, t = r%16): group t/8 = parity of
+//    the input index i = 2c + group, output q = 8b + t%8 < H; GA[r][c] = P(i, 2q),
+//    the centre i = h-1 (odd group, c = H-1) halved (the stack's s counts it twice).
+// GB (FOLD 4, odd modes) = the first-level forward matrix of the DST-I
+//    Pm(i, q) = P(i, 2q+1), i, q < h-1 (fold_matrices on size 2H - 1).
+// FB (first-level backward, FOLD 2) with its odd-group columns in the level-2
+//    position order: FB[r][c] = P(q, fold2_mode(h + c)) for group 1.
+// Layouts as fold_matrices with H for h (GA, GB) and h (FB).
+static void fold2_matrices(const std::vector<double>& Pc, int n, int mode, std::vector<double>& ga,
+                           std::vector<double>& gb, std::vector<double>& fb) {
+    const int h = (n + 1) / 2, H = h / 2, m = h - 1;
+    auto P = [&](int i, int k) { return Pc[(size_t)k * n + i]; };
+    {
+        const int ld = mode == 0 ? (H + 15) / 16 * 16 : 2 * H;
+        ga.assign(mode == 0 ? (size_t)2 * H * ld : (size_t)H * ld, 0.0);
+        auto at = [&](int r, int c) -> double& { return mode == 0 ? ga[(size_t)r * ld + c] : ga[(size_t)c * ld + r]; };
+        for (int r = 0; r < 2 * H; ++r) {
+            const int grp = (r >> 3) & 1, q = (r >> 4) * 8 + (r & 7);
+            if (q >= H) continue;
+            for (int c = 0; c < H; ++c) {
+                const int i = 2 * c + grp;
+                at(r, c) = (i == h - 1 ? 0.5 : 1.0) * P(i, 2 * q);
+            }
+        }
+    }
+    {
+        std::vector<double> Pm((size_t)m * m), unused;
+        for (int q = 0; q < m; ++q)
+            for (int i = 0; i < m; ++i) Pm[(size_t)q * m + i] = P(i, 2 * q + 1);
+        fold_matrices(Pm, m, mode, gb, unused);
+    }
+    {
+        std::vector<double> ff;
+        fold_matrices(Pc, n, mode, ff, fb);
+        const int ld = mode == 0 ? (h + 15) / 16 * 16 : 2 * h;
+        auto at = [&](int r, int c) -> double& { return mode == 0 ? fb[(size_t)r * ld + c] : fb[(size_t)c * ld + r]; };
+        for (int r = 0; r < 2 * h; ++r) {
+            const int grp = (r >> 3) & 1, q = (r >> 4) * 8 + (r & 7);
+            if (q >= h || grp == 0) continue;
+            for (int c = 0; c < h; ++c) {
+                const int kb = c < h - 1 ? fold2_mode(h + c, n) : n;
+                at(r, c) = (kb < n && q != h - 1) ? P(q, kb) : 0.0;
+            }
+        }
+    }
+}
+
 static void build_plan(Plan& p, const etd_desc& d) {
     validate(d);
     p.d = d;
@@ -986,7 +1098,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
     const bool exact = d.family == ETD_EXACT;
     const PadeScheme scheme = pade_scheme(exact ? 0 : d.family);
     p.thomas = d.backend == ETD_THOMAS;
-    std::vector<double> hd((size_t)2 * 3 * 9 * 2 * p.dmax, 0.0);
+    std::vector<double> hd((size_t)3 * 3 * 9 * 2 * p.dmax, 0.0);
     // Parity split on every spectral axis whose half extent h = (n+1)/2 is a
     // multiple of 8 (n = 16m - 1 or 16m: all BASELINE configs); ETD_DENSE=1 turns
     // it off.  A fused source prologue (ETD_FUSED_SOURCE=1) keeps its axis dense.
@@ -1003,6 +1115,18 @@ static void build_plan(Plan& p, const etd_desc& d) {
             p.fold[a] = !p.thomas && !dense_env && h % 8 == 0 && (axes >> a & 1) &&
                         !(fused0 && a == (d.dim == 3 ? 2 : 1));
         }
+        // Second-level split where n = 4H - 1 with H a multiple of 8
+        // (n = 32m - 1: every BASELINE config); the step uses it when every axis has
+        // it.  ETD_FOLD2=0 turns it off.
+        const char* f2 = std::getenv("ETD_FOLD2");
+        const bool f2_off = f2 && f2[0] == '0';
+        p.fold2_all = !f2_off && !fused0;
+        for (int a = 0; a < d.dim; ++a) {
+            p.fold2[a] = p.fold[a] && !f2_off && (d.n[a] & 1) && p.fh[a] % 16 == 0;
+            p.fold2_all = p.fold2_all && p.fold2[a];
+        }
+        // mixed levels are not scheduled: every axis keeps §4a then
+        for (int a = 0; a < d.dim; ++a) p.fold2[a] = p.fold2[a] && p.fold2_all;
     }
     for (int a = 0; a < d.dim && p.thomas; ++a) {
         // build_thomas_payload (thomas.cpp:88-126) per species: c = tau diag k - s_l,
@@ -1055,7 +1179,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
     for (int a = 0; a < d.dim && !p.thomas; ++a) {
         const int n = d.n[a], np = p.npad[a];
         const AxisOperator op = axis_operator(n, d.low[a], d.high[a], d.dim, sys ? 1.0 : d.kappa[0], d.q);
-        std::vector<double> Pc, lam;
+        std::vector<double> Pc, lam, fb2_tmp;
         eigensystem(op, Pc, lam);
         std::vector<double> pr((size_t)np * np, 0.0), ptr((size_t)np * np, 0.0);
         for (int i = 0; i < n; ++i)
@@ -1067,9 +1191,18 @@ static void build_plan(Plan& p, const etd_desc& d) {
         ETD_CK(cudaMalloc(&p.PTR[a], ptr.size() * 8));
         ETD_CK(cudaMemcpy(p.PR[a], pr.data(), pr.size() * 8, cudaMemcpyHostToDevice));
         ETD_CK(cudaMemcpy(p.PTR[a], ptr.data(), ptr.size() * 8, cudaMemcpyHostToDevice));
+        if (p.fold2[a]) {
+            std::vector<double> ga, gb;
+            fold2_matrices(Pc, n, a == 0 ? 0 : 1, ga, gb, fb2_tmp);
+            ETD_CK(cudaMalloc(&p.GA[a], ga.size() * 8));
+            ETD_CK(cudaMalloc(&p.GB[a], gb.size() * 8));
+            ETD_CK(cudaMemcpy(p.GA[a], ga.data(), ga.size() * 8, cudaMemcpyHostToDevice));
+            ETD_CK(cudaMemcpy(p.GB[a], gb.data(), gb.size() * 8, cudaMemcpyHostToDevice));
+        }
         if (p.fold[a]) {
             std::vector<double> ff, fb;
             fold_matrices(Pc, n, a == 0 ? 0 : 1, ff, fb);
+            if (p.fold2[a]) fb.swap(fb2_tmp);  // backward reads the level-2 mode positions
             ETD_CK(cudaMalloc(&p.FF[a], ff.size() * 8));
             ETD_CK(cudaMalloc(&p.FB[a], fb.size() * 8));
             ETD_CK(cudaMemcpy(p.FF[a], ff.data(), ff.size() * 8, cudaMemcpyHostToDevice));
@@ -1084,10 +1217,15 @@ static void build_plan(Plan& p, const etd_desc& d) {
             auto put = [&](int slot, const std::vector<double>& v, double sc) {
                 double* o = hd.data() + (((size_t)a * 9 + slot) * 2 + c) * p.dmax;
                 double* op = hd.data() + (((size_t)(3 + a) * 9 + slot) * 2 + c) * p.dmax;
+                double* o2 = hd.data() + (((size_t)(6 + a) * 9 + slot) * 2 + c) * p.dmax;
                 for (int i = 0; i < n; ++i) o[i] = sc * v[i];
                 for (int pos = 0; pos < n; ++pos) {
                     const int k = pos < h ? 2 * pos : 2 * (pos - h) + 1;
                     op[pos] = k < n ? sc * v[k] : 0.0;
+                    if (p.fold2[a]) {
+                        const int k2 = fold2_mode(pos, n);
+                        o2[pos] = k2 < n ? sc * v[k2] : 0.0;
+                    }
                 }
             };
             if (exact) {
@@ -1148,7 +1286,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
                     for (int pro = 0; pro < 2; ++pro)
                         for (int sk : {0, 1, 2, 3, 4, 5, 10, 11, 12, 13})
                             for (int tile = 0; tile < 4; ++tile)
-                                for (int fold = 0; fold < 5; ++fold) {
+                                for (int fold = 0; fold < 6; ++fold) {
                                     try {
                                         KernelSpec ks = pick(mode, S, e, pro != 0, sk, tile, fold);
                                         ETD_CK(cudaFuncSetAttribute(
@@ -1200,7 +1338,28 @@ static void build_plan(Plan& p, const etd_desc& d) {
         // A parity-split first axis gets its stack folded by the source pass (into
         // `scratch`, free until the axis' backward transform writes it), so the
         // forward transform runs FOLD 4 with no s/d adds in its main loop.
+        // Second-level split (p.fold2_all): every forward transform is
+        // an etd_fold2 stack (src -> tmp) and its even/odd-mode launches (tmp -> dst).
+        const bool f2 = p.fold2_all;
+        auto fwd2 = [&](const View& vv, const std::string& nm, int axis, int S, int epi, const double* src,
+                        double* tmp, double* dst, bool from1, const double* dA, const double* dB = nullptr,
+                        const double* aux = nullptr) {
+            L.push_back(p.fold_op(vv, "fold_" + nm, axis, src, tmp, S, from1));
+            for (int part = 1; part <= 2; ++part) {
+                L.push_back(kernel_op(p.transform(vv, nm + (part == 1 ? "_even" : "_odd"), axis, false, S, epi,
+                                                  false, tmp, dst, false, nullptr, false, part)));
+                L.back().L.args.dA = dA;
+                L.back().L.args.dB = dB;
+                L.back().L.args.aux = aux;
+            }
+        };
         auto first_transform = [&](const View& vv, int axis, double* stack, double* dst, double* scratch) {
+            if (f2) {
+                L.push_back(p.source_op(vv, stack));
+                fwd2(vv, axis == 2 ? "z_fwd" : "y_fwd", axis, 2 * ns, EPI_SCALE, stack, scratch, dst, false,
+                     p.dv(axis, 0));
+                return;
+            }
             const char* nm = axis == 2 ? (fused ? "z_fwd_src" : "z_fwd") : (fused ? "y_fwd_src" : "y_fwd");
             const bool pf = !fused && p.fold[axis];
             if (!fused) L.push_back(p.source_op(vv, stack, pf ? scratch : nullptr, pf ? axis : 0));
@@ -1262,7 +1421,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
                     L.push_back(kernel_op(p.transform(vk, "z_back", 2, true, 2 * ns, EPI_STORE, false, zz_k, wz_k)));
                 } else {
                     // an empty chunk keeps the op list aligned across virtual ranks
-                    for (int i = 0; i < (fused ? 2 : 3); ++i) {
+                    for (int i = 0; i < (fused ? 2 : f2 ? 5 : 3); ++i) {
                         Op o;
                         o.kind = Op::NOP;
                         o.name = "z_empty";
@@ -1278,6 +1437,25 @@ static void build_plan(Plan& p, const etd_desc& d) {
             }
             L[copies(SP_UNPACK, "unpack")].wait_ev = EV_B;
         }
+        if (f2) {
+            // y stage, then the x stage on (Xa = y_back's output, Xb = the other buffer)
+            double *Xa, *Xb;
+            if (p.dim == 3) {
+                fwd2(V, "y_fwd", 1, 2 * ns, EPI_SCALE, p.W, p.Z, p.W, false, p.dv(1, 0));
+                L.push_back(kernel_op(p.transform(V, "y_back", 1, true, 2 * ns, EPI_STORE, false, p.W, p.Z)));
+                Xa = p.Z, Xb = p.W;
+            } else {
+                first_transform(V, 1, const_cast<double*>(in), p.Z, p.W);
+                L.push_back(kernel_op(p.transform(V, "y_back", 1, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
+                Xa = p.W, Xb = p.Z;
+            }
+            const size_t Fs = (size_t)ns * V.F;
+            fwd2(V, "x_fwd_mix", 0, 2 * ns, EPI_MIX, Xa, Xb, Xa, false, p.dv(0, 0), p.dv(0, 1));
+            L.push_back(kernel_op(p.transform(V, "x_back_src", 0, true, ns, EPI_WHAT_SRC, false, Xa, Xb)));
+            fwd2(V, "x_fwd_corr", 0, ns, EPI_CORR, Xb + Fs, Xa, Xb + Fs, true, p.dv(0, 2), nullptr, Xa + Fs);
+            L.push_back(kernel_op(p.transform(V, "x_back_upd", 0, true, ns, EPI_UPDATE, false, Xb + Fs, out)));
+            L.back().L.args.aux = Xb;
+        } else {
         if (p.dim == 3) {
             L.push_back(kernel_op(p.transform(V, "y_fwd", 1, false, 2 * ns, EPI_SCALE, false, p.W, p.Z)));
             L.back().L.args.dA = p.dv(1, 0);
@@ -1298,6 +1476,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
         L.back().L.args.dA = p.dv(0, 2);
         L.push_back(kernel_op(p.transform(V, "x_back_upd", 0, true, ns, EPI_UPDATE, false, p.Z, out)));
         L.back().L.args.aux = p.W;
+        }
         if (p.sharded) {
             // global abort agreement, then commit on every rank
             Op fc;
@@ -1328,7 +1507,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
     }
     p.stats.clear();
     for (auto& op : p.steps[0])
-        if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS)
+        if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS || op.kind == Op::FOLD)
             p.stats.push_back({op.L.name, 0, 0, op.L.flops, op.L.bytes, op.L.dense_flops});
     ETD_CK(cudaStreamSynchronize(p.stream));
 }
@@ -1366,6 +1545,11 @@ static void run_op_body(Plan& p, const Op& op, cudaStream_t s) {
     case Op::THOMAS: {
         void* args[2] = {const_cast<CUtensorMap*>(&op.L.tmA), const_cast<ThomasArgs*>(&op.targs)};
         ETD_CK(cudaLaunchKernel(op.src_fn, dim3(op.src_blocks), dim3(128), args, op.L.k.smem, s));
+        break;
+    }
+    case Op::FOLD: {
+        void* args[1] = {const_cast<Fold2Args*>(&op.fargs)};
+        ETD_CK(cudaLaunchKernel(reinterpret_cast<const void*>(etd_fold2), dim3(op.src_blocks), dim3(256), args, 0, s));
         break;
     }
     case Op::FAILCODE: etd_fail_code<<<1, 1, 0, s>>>(p.status, p.codes + p.G); break;
@@ -1474,7 +1658,7 @@ static void do_steps(Plan& p, int nsteps) {
                 }
                 if (!p.profiling) continue;
                 const size_t e = rec();
-                if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS)
+                if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS || op.kind == Op::FOLD)
                     spans.push_back({prev, kidx++});
                 prev = e;
             }
@@ -1574,7 +1758,8 @@ static constexpr int kXferChunks = 32;
 static int x_stage_index(const Plan& p) {
     const auto& ops = p.steps[0];
     for (size_t k = 0; k < ops.size(); ++k)
-        if (ops[k].kind == Op::KERNEL && ops[k].L.mode == 0) return (int)k;
+        if ((ops[k].kind == Op::KERNEL && ops[k].L.mode == 0) || (ops[k].kind == Op::FOLD && ops[k].fargs.axis == 0))
+            return (int)k;
     return -1;
 }
 
@@ -1585,8 +1770,8 @@ static bool overlap_eligible(const Plan& p, int nsteps) {
     if (ix <= 0 || ops.back().L.name != "x_back_upd") return false;
     for (int k = 0; k < (int)ops.size(); ++k) {
         const Op& op = ops[k];
-        if (op.kind != Op::KERNEL && op.kind != Op::SOURCE) return false;
-        if (op.kind == Op::KERNEL && op.L.mode != (k < ix ? 1 : 0)) return false;
+        if (op.kind != Op::KERNEL && op.kind != Op::SOURCE && op.kind != Op::FOLD) return false;
+        if ((op.kind == Op::KERNEL || op.kind == Op::FOLD) && op.L.mode != (k < ix ? 1 : 0)) return false;
         if (op.kind == Op::SOURCE && k >= ix) return false;
     }
     return true;
@@ -1654,6 +1839,11 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
                         o.sargs.x0 = x0;
                         o.sargs.x1 = x1;
                         run_op(p, o, p.stream);
+                    } else if (ops[k].kind == Op::FOLD) {
+                        Op o = ops[k];
+                        o.fargs.x0 = x0;
+                        o.fargs.x1 = x1;
+                        run_op(p, o, p.stream);
                     } else {
                         Launch L = ops[k].L;
                         L.args.mtile0 = x0 / L.k.bm;
@@ -1675,6 +1865,13 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
             const long long r0 = rowb(c), r1 = rowb(c + 1);
             if (r1 <= r0) continue;
             for (size_t k = ix; k < ops.size(); ++k) {
+                if (ops[k].kind == Op::FOLD) {
+                    Op o = ops[k];
+                    o.fargs.r0 = r0;
+                    o.fargs.r1 = r1;
+                    run_op(p, o, p.stream);
+                    continue;
+                }
                 Launch L = ops[k].L;
                 L.args.mtile0 = (int)(r0 / L.k.bm);
                 L.grid.y = (unsigned)((r1 + L.k.bm - 1) / L.k.bm - r0 / L.k.bm);
@@ -1835,6 +2032,19 @@ static void debug_transform(Plan& p, int species, int axis, int back, int ell, i
         if (ell < 1) throw ConfigError("apply_q needs ell in 1..3");
         // folded x: the forward reads its mirror from a host-reversed copy (FOLD 3)
         double* rev = nullptr;
+        if (p.fold2[axis]) {
+            // second-level split: stack -> even/odd-mode launches -> backward
+            double* tmp = p.state[1 - p.cur];
+            run_op(p, p.fold_op(v, "dbg_fold", axis, p.W, tmp, 1), p.stream);
+            for (int part = 1; part <= 2; ++part) {
+                Launch f = p.transform(v, "dbg_fwd", axis, false, 1, EPI_SCALE, false, tmp, p.Z, false, nullptr,
+                                       false, part);
+                f.args.dA = p.dv(axis, 6 + ell - 1) + species * p.dmax;
+                launch(f, p.stream);
+            }
+            launch(p.transform(v, "dbg_back", axis, true, 1, EPI_STORE, false, p.Z, p.W + v.F), p.stream);
+            result = p.W + v.F;
+        } else {
         if (axis == 0 && p.fold[0]) {
             std::vector<double> hr((size_t)v.nx * v.ny * v.nz);
             for (size_t r = 0; r < (size_t)v.ny * v.nz; ++r)
@@ -1850,10 +2060,11 @@ static void debug_transform(Plan& p, int species, int axis, int back, int ell, i
         launch(f, p.stream);
         launch(b, p.stream);
         result = p.W + v.F;
+        }
     } else {
         // one direction in natural mode order: the dense kernel
         Launch f = p.transform(v, "dbg", axis, back != 0, 1, ell ? EPI_SCALE : EPI_STORE, false, p.W, p.Z, true);
-        if (ell) f.args.dA = p.dvn(axis, 3 + ell - 1, false) + species * p.dmax;
+        if (ell) f.args.dA = p.dvn(axis, 3 + ell - 1, 0) + species * p.dmax;
         launch(f, p.stream);
         result = p.Z;
     }
@@ -2114,6 +2325,30 @@ int etd_setup_fold_matrices(int n, int mode, double* ff, double* fb) {
     } catch (...) {
         return ETD_ERR_CONFIG;
     }
+    return ETD_OK;
+}
+
+int etd_setup_fold2_matrices(int n, int mode, double* ga, double* gb, double* fb) {
+    const int h = (n + 1) / 2;
+    if (n < 2 || !(n & 1) || h % 16 != 0 || (mode != 0 && mode != 1) || !ga || !gb || !fb) return ETD_ERR_CONFIG;
+    try {
+        const etd::AxisOperator op = etd::axis_operator(n, 0.0, 1.0, 1, 1.0, 0.0);
+        std::vector<double> Pc, lam, a, b, c;
+        etd::eigensystem(op, Pc, lam);
+        etd::fold2_matrices(Pc, n, mode, a, b, c);
+        std::memcpy(ga, a.data(), a.size() * 8);
+        std::memcpy(gb, b.data(), b.size() * 8);
+        std::memcpy(fb, c.data(), c.size() * 8);
+    } catch (...) {
+        return ETD_ERR_CONFIG;
+    }
+    return ETD_OK;
+}
+
+int etd_fold_level(const etd_handle* h, int* out) {
+    if (!h || !out) return ETD_ERR_CONFIG;
+    const auto& p = *h->plan;
+    for (int a = 0; a < 3; ++a) out[a] = a < p.dim ? (p.fold2_all && p.fold2[a] ? 2 : p.fold[a] ? 1 : 0) : 0;
     return ETD_OK;
 }
 

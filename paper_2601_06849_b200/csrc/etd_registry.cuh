@@ -1,6 +1,6 @@
 // etd_registry.cuh — contraction kernel variants (tile classes x epilogues x
 // source kinds x parity split) and their launch specs.  The instantiations are
-// split over etd_specs_dense.cu and etd_specs_fold.cu so nvcc compiles them in
+// split over etd_specs_dense.cu, etd_specs_fold.cu and etd_specs_fold2.cu so nvcc compiles them in
 // parallel; etd_plan.cu only calls pick().
 #pragma once
 #include "etd_kernels.cuh"
@@ -71,5 +71,6 @@ static KernelSpec spec() {
 
 KernelSpec pick_dense(int mode, int S, int epi, bool pro, int sk, int tile);
 KernelSpec pick_fold(int mode, int S, int epi, int sk, int tile, int fold);
+KernelSpec pick_fold2(int mode, int S, int epi, int sk, int tile, int fold);
 
 }  // namespace etd

@@ -1,4 +1,5 @@
-// etd_specs_fold.cu — parity-split (FOLD 1-4) contraction kernel instantiations.
+// etd_specs_fold.cu — parity-split (FOLD 1-4) contraction kernel instantiations
+// (FOLD 5 and the second-level FOLD 4 variants: etd_specs_fold2.cu).
 #include "etd_registry.cuh"
 
 namespace etd {
@@ -32,7 +33,7 @@ KernelSpec pick_fold(int mode, int S, int epi, int sk, int tile, int fold) {
     ETD_FSPEC(0, 2, EPI_WHAT_SRC, 0, 2) ETD_FSPEC(0, 2, EPI_WHAT_SRC, 10, 2) ETD_FSPEC(0, 2, EPI_WHAT_SRC, 11, 2)
     ETD_FSPEC(0, 2, EPI_WHAT_SRC, 12, 2) ETD_FSPEC(0, 2, EPI_WHAT_SRC, 13, 2)
 #undef ETD_FSPEC
-    throw ConfigError("no parity-split variant for this stage / source kind");
+    return pick_fold2(mode, S, epi, sk, tile, fold);
     }
 
 }  // namespace etd

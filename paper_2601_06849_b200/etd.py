@@ -235,6 +235,8 @@ def lib():
         L.etd_stage_flops.argtypes = [vp, i, C.POINTER(d), C.POINTER(d)]
         L.etd_parity_split.argtypes = [vp, C.POINTER(C.c_int)]
         L.etd_setup_fold_matrices.argtypes = [i, i, vp, vp]
+        L.etd_setup_fold2_matrices.argtypes = [i, i, vp, vp, vp]
+        L.etd_fold_level.argtypes = [vp, C.POINTER(C.c_int)]
         L.etd_debug_transform.argtypes = [vp, i, i, i, i, i, vp, vp]
         L.etd_fill_config_ic.argtypes = [i, C.c_ulonglong, i, i, i, i, vp]
         L.etd_setup_axis.argtypes = [i, d, d, i, d, d, vp, vp]
@@ -451,6 +453,12 @@ class _PlanBase:
         a = (C.c_int * 3)()
         _raise(lib().etd_parity_split(self.handle, a), self.handle)
         return tuple(bool(a[i]) for i in range(self.grid.dim))
+
+    def fold_level(self) -> tuple:
+        """Per axis: 0 dense, 1 first-level parity split, 2 second level (§4b)."""
+        a = (C.c_int * 3)()
+        _raise(lib().etd_fold_level(self.handle, a), self.handle)
+        return tuple(a[i] for i in range(self.grid.dim))
 
     def debug_transform(self, x: np.ndarray, axis: int, back: bool = False, ell: int = 0, apply_q: bool = False,
                         species: int = 0) -> np.ndarray:

@@ -105,3 +105,99 @@ def test_fold_matrices_refuse_unfoldable_n():
     p = buf.ctypes.data_as(C.c_void_p)
     assert etd.lib().etd_setup_fold_matrices(25, 0, p, p) != 0   # h = 13
     assert etd.lib().etd_setup_fold_matrices(31, 2, p, p) != 0   # bad layout
+
+
+# ---------------------------------------------------------------- second level
+def fold2_mats(n, mode):
+    h = (n + 1) // 2
+    H = h // 2
+    ldH = (H + 15) // 16 * 16 if mode == 0 else 2 * H
+    ldh = (h + 15) // 16 * 16 if mode == 0 else 2 * h
+    ga = np.zeros(2 * H * ldH if mode == 0 else H * ldH)
+    gb = np.zeros_like(ga)
+    fb = np.zeros(2 * h * ldh if mode == 0 else h * ldh)
+    vp = lambda a: a.ctypes.data_as(C.c_void_p)
+    assert etd.lib().etd_setup_fold2_matrices(n, mode, vp(ga), vp(gb), vp(fb)) == 0
+    if mode == 0:
+        return ga.reshape(2 * H, ldH)[:, :H], gb.reshape(2 * H, ldH)[:, :H], fb.reshape(2 * h, ldh)[:, :h]
+    return ga.reshape(H, 2 * H).T, gb.reshape(H, 2 * H).T, fb.reshape(h, 2 * h).T
+
+
+def fold2_modes(n):
+    """mode of each level-2 position: p < h -> 2p; h + c -> 4c + 1 (c < H), 4(c - H) + 3."""
+    h = (n + 1) // 2
+    H = h // 2
+    return [2 * p for p in range(h)] + [4 * c + 1 for c in range(H)] + [4 * c + 3 for c in range(H - 1)]
+
+
+def fold2_stack(g, n, from1=False):
+    """etd_fold2 restated: [s even i | s odd i | d_k + d_{2H-2-k} | d_k - d_{2H-2-k}]."""
+    h = (n + 1) // 2
+    H = h // 2
+    if from1:
+        s, d = g[..., :h], g[..., h:]
+    else:
+        i = np.arange(h)
+        s = g[..., i] + g[..., n - 1 - i]
+        d = (g[..., i] - g[..., n - 1 - i])[..., :h - 1]
+    k = np.arange(H)
+    c = 2 * H - 2 - k
+    dd_s = d[..., k] + d[..., c]
+    dd_d = (d[..., k] - d[..., c])[..., :H - 1]
+    return np.concatenate([s[..., 0::2], s[..., 1::2], dd_s, dd_d], -1)
+
+
+def fold2_forward(st, GA, GB, n):
+    """FOLD 5 (GA: boxes [0,H), [H,2H); +/- to positions q, h-1-q) and FOLD 4 (GB: boxes
+    [2H,3H), [3H,4H-1); positions 2H + 8b + t%8 + group H)."""
+    h = (n + 1) // 2
+    H = h // 2
+    out = np.zeros(st.shape[:-1] + (n,))
+    A0, A1 = st[..., :H], st[..., H:2 * H]
+    B0 = st[..., 2 * H:3 * H]
+    B1 = np.concatenate([st[..., 3 * H:], np.zeros(st.shape[:-1] + (1,))], -1)
+    for r in range(0, 2 * H, 16):
+        for t in range(8):
+            q = (r >> 4) * 8 + t
+            if q < H:
+                a, b = A0 @ GA[r + t], A1 @ GA[r + 8 + t]
+                out[..., q] = a + b
+                out[..., h - 1 - q] = a - b
+    for r in range(2 * H):
+        grp = (r >> 3) & 1
+        pos = 2 * H + (r >> 4) * 8 + (r & 7) + grp * H
+        if pos < n:
+            out[..., pos] = (B1 if grp else B0) @ GB[r]
+    return out
+
+
+@pytest.mark.parametrize("n", [31, 63, 127, 255, 511])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fold2_reproduces_dense_transform(n, mode):
+    GA, GB, FB2 = fold2_mats(n, mode)
+    P, _ = Oracle.spectral_factor(n, 2.0, -1.0)
+    P = np.asarray(P).reshape(n, n).T if np.asarray(P).ndim == 1 else np.asarray(P)
+    modes = fold2_modes(n)
+    assert sorted(modes) == list(range(n))
+    rng = np.random.default_rng(n)
+    g = rng.uniform(-1, 1, (5, n))
+    dense_fwd = g @ P
+    got = fold2_forward(fold2_stack(g, n), GA, GB, n)
+    assert np.max(np.abs(got - dense_fwd[:, modes])) <= 1e-13 * n
+    # the x corrector's input: x_back_src writes the first-level stack of f(What)
+    h = (n + 1) // 2
+    i = np.arange(h)
+    first = np.concatenate([g[:, i] + g[:, n - 1 - i], (g[:, i] - g[:, n - 1 - i])[:, :h - 1]], -1)
+    got1 = fold2_forward(fold2_stack(first, n, from1=True), GA, GB, n)
+    assert np.max(np.abs(got1 - dense_fwd[:, modes])) <= 1e-13 * n
+    # backward: the first-level FOLD 2 kernel reading level-2 positions
+    gh = rng.uniform(-1, 1, (5, n))          # level-2 positions
+    nat = np.zeros_like(gh)
+    nat[:, modes] = gh
+    assert np.max(np.abs(fold_backward(gh, FB2, n) - nat @ P.T)) <= 1e-13 * n
+
+
+def test_fold2_matrices_reject_ineligible_sizes():
+    p = C.c_void_p(0)
+    assert etd.lib().etd_setup_fold2_matrices(47, 0, p, p, p) != 0   # h = 24: H not a multiple of 8
+    assert etd.lib().etd_setup_fold2_matrices(64, 0, p, p, p) != 0   # even n

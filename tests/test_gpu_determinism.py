@@ -12,20 +12,28 @@ from paper_2601_06849_b200 import configs
 
 pytestmark = pytest.mark.gpu
 
-STAGES = ["source", "z_fwd", "z_back", "y_fwd", "y_back", "x_fwd_mix", "x_back_src", "x_fwd_corr", "x_back_upd"]
+STAGES_L1 = ["z_fwd", "z_back", "y_fwd", "y_back", "x_fwd_mix", "x_back_src", "x_fwd_corr", "x_back_upd"]
+STAGES_L2 = ["z_fwd_even", "z_fwd_odd", "z_back", "y_fwd_even", "y_fwd_odd", "y_back", "x_fwd_mix_even",
+             "x_fwd_mix_odd", "x_back_src", "x_fwd_corr_even", "x_fwd_corr_odd", "x_back_upd"]
 
 
-def test_stage_kernels_are_deterministic():
+@pytest.mark.parametrize("level", [1, 2])
+def test_stage_kernels_are_deterministic(level, monkeypatch):
+    if level == 1:
+        monkeypatch.setenv("ETD_FOLD2", "0")
     cfg = configs.CONFIGS[4]
     n = 383
     plan = configs.make_plan(cfg, n)
+    assert plan.fold_level() == (level,) * 3
+    stages = STAGES_L2 if level == 2 else STAGES_L1
+    assert [s["name"] for s in plan.stage_stats() if s["flops_per_launch"] > 0] == stages
     for s, a in enumerate(configs.initial_state(cfg, n)):
         plan.upload(s, a)
     plan.step(1)
     L = etd.lib()
     L.etd_debug_repeat_op.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_longlong),
                                       C.c_void_p, C.c_int]
-    for name in STAGES[1:]:
+    for name in stages:
         for out in (0, 1):
             mm = C.c_longlong(-1)
             rc = L.etd_debug_repeat_op(plan.handle, name.encode(), out, 6, C.byref(mm), None, 0)

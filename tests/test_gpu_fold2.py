@@ -1,0 +1,148 @@
+"""GPU: the second-level parity split (etd_kernels.cuh FOLD 5 and
+etd_fold2).
+
+On axes with n = 4H - 1, H a multiple of 8 (n = 32m - 1: every BASELINE config),
+each forward transform is an HBM-bound stack pass (etd_fold2) followed by two
+launches of H-long contractions: the even-mode group (DST-III halves, FOLD 5) and
+the odd-mode group (the DST-I of size h - 1 split again, FOLD 4).  The backward
+transforms stay first-level, reading the level-2 mode positions.  These tests
+run the level-2 path against the reference (oracle/_ref, else the C
+restatement), the first-level path (ETD_FOLD2=0) and the dense path
+(ETD_DENSE=1) over 2D/3D, scalar and two-species steps, every tile class, the
+pipelined host-buffer advance, aborts and the z-slab sharded schedule.
+"""
+import numpy as np
+import pytest
+
+import paper_2601_06849_b200 as etd
+from oracle import Oracle, Ref, rel_gap
+
+pytestmark = pytest.mark.gpu
+
+STEP_TOL = 1e-11
+
+
+def R():
+    return Ref if Ref.available() else Oracle
+
+
+def plans(make, monkeypatch):
+    """(level-2, level-1, dense) plans of the same problem."""
+    p2 = make()
+    monkeypatch.setenv("ETD_FOLD2", "0")
+    p1 = make()
+    monkeypatch.delenv("ETD_FOLD2")
+    monkeypatch.setenv("ETD_DENSE", "1")
+    pd = make()
+    monkeypatch.delenv("ETD_DENSE")
+    return p2, p1, pd
+
+
+@pytest.mark.parametrize("dim,n", [(2, 31), (2, 63), (2, 127), (3, 31), (3, 63)])
+def test_fold2_apply_q_and_scalar_steps(dim, n, monkeypatch):
+    g = etd.unit_box_grid(dim, n + 1)
+    x = np.random.default_rng(n + dim).uniform(-0.5, 0.5, n ** dim)
+    tau, kappa, q = 0.02, 0.7, 1.0
+    p2, p1, pd = plans(lambda: etd.make_plan(g, tau, kappa, q, source=etd.allen_cahn_cubic()), monkeypatch)
+    assert p2.fold_level() == (2,) * dim and p1.fold_level() == (1,) * dim and pd.fold_level() == (0,) * dim
+    for axis in range(dim):
+        for ell in (1, 2, 3):
+            a = p2.apply_Q(ell, x, axis)
+            want = R().apply_q(dim, n, tau, kappa, q, 0, ell, axis, x)
+            assert np.max(np.abs(a - want)) <= 1e-12, (axis, ell)
+            assert np.max(np.abs(a - pd.apply_Q(ell, x, axis))) <= 1e-13, (axis, ell)
+    s0 = etd.StepperState(0, 0.0, x)
+    a = etd.advance(p2, s0, etd.allen_cahn_cubic(), nsteps=4)
+    b = etd.advance(p1, s0, etd.allen_cahn_cubic(), nsteps=4)
+    want = R().scalar_run(dim, n, tau, kappa, q, x, 4, src_kind=1)[0]
+    assert rel_gap(want, a.U) <= STEP_TOL
+    assert rel_gap(b.U, a.U) <= 1e-13
+    assert a.n == 4 and abs(a.t - 4 * tau) < 1e-15
+
+
+@pytest.mark.parametrize("n", [31, 63])
+def test_fold2_system_3d_vs_reference_and_level1(n, monkeypatch):
+    g = etd.unit_box_grid(3, n + 1)
+    rng = np.random.default_rng(n)
+    u0, v0 = rng.uniform(-1, 1, n ** 3), rng.uniform(-0.5, 0.5, n ** 3)
+    p2, p1, _ = plans(lambda: etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0), monkeypatch)
+    st = etd.SystemState(0, 0.0, u0, v0)
+    a = etd.etd2rkds_step_system(p2, st, etd.fhn_cubic(), nsteps=3)
+    b = etd.etd2rkds_step_system(p1, st, etd.fhn_cubic(), nsteps=3)
+    wu, wv = R().system_run(3, n, 0.05, 1e-3, 5e-4, 0.0, u0, v0, 3)[:2]
+    assert rel_gap(wu, a.U) <= STEP_TOL and rel_gap(wv, a.V) <= STEP_TOL
+    assert rel_gap(b.U, a.U) <= 1e-13 and rel_gap(b.V, a.V) <= 1e-13
+
+
+def test_fold2_config_physics_2d_system(monkeypatch):
+    n = 63
+    g = etd.unit_box_grid(2, n + 1)
+    rng = np.random.default_rng(5)
+    u0, v0 = rng.uniform(-1, 1, n * n), rng.uniform(-0.5, 0.5, n * n)
+    p2 = etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0)
+    assert p2.fold_level() == (2, 2)
+    a = etd.etd2rkds_step_system(p2, etd.SystemState(0, 0.0, u0, v0), etd.fhn_cubic(), nsteps=3)
+    wu, wv = R().system_run(2, n, 0.05, 1e-3, 5e-4, 0.0, u0, v0, 3)[:2]
+    assert rel_gap(wu, a.U) <= STEP_TOL and rel_gap(wv, a.V) <= STEP_TOL
+
+
+@pytest.mark.parametrize("tile", ["0", "1", "2", "3"])
+def test_fold2_every_tile_class(tile, monkeypatch):
+    monkeypatch.setenv("ETD_FORCE_TILE", tile)
+    n = 63
+    g = etd.unit_box_grid(3, n + 1)
+    rng = np.random.default_rng(int(tile) + 90)
+    u0, v0 = rng.uniform(-1, 1, n ** 3), rng.uniform(-1, 1, n ** 3)
+    sp = etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0)
+    assert sp.fold_level() == (2, 2, 2)
+    got = etd.etd2rkds_step_system(sp, etd.SystemState(0, 0.0, u0, v0), etd.fhn_cubic(), nsteps=2)
+    wu, wv = R().system_run(3, n, 0.05, 1e-3, 5e-4, 0.0, u0, v0, 2)[:2]
+    assert rel_gap(wu, got.U) <= STEP_TOL and rel_gap(wv, got.V) <= STEP_TOL
+
+
+def test_fold2_pipelined_advance_equals_resident_steps():
+    from paper_2601_06849_b200 import configs
+    cfg = configs.CONFIGS[4]
+    n = 255
+    ics = configs.initial_state(cfg, n)
+    plan = configs.make_plan(cfg, n)
+    assert plan.fold_level() == (2, 2, 2)
+    st = etd.etd2rkds_step_system(plan, etd.SystemState(0, 0.0, *ics), cfg.source, nsteps=2)  # host buffers
+    plan.upload(0, ics[0])
+    plan.upload(1, ics[1])
+    plan.step(2)
+    u, nn, _ = plan.download(0)
+    v, _, _ = plan.download(1)
+    assert nn == 2
+    assert np.array_equal(u, st.U) and np.array_equal(v, st.V)
+
+
+def test_fold2_abort_keeps_input_state():
+    """test_stepper.cpp:304-321 on the level-2 schedule: the input state's t and n."""
+    n = 31
+    g = etd.unit_box_grid(2, n + 1)
+    plan = etd.make_plan(g, 0.01, 1.0, 1.0)
+    assert plan.fold_level() == (2, 2)
+    u0 = np.random.default_rng(7).uniform(-0.5, 0.5, n * n)
+    with pytest.raises(etd.StepperAbort) as ei:
+        etd.advance(plan, etd.StepperState(4, 0.25, u0), etd.DeviceSource(etd.SourceKind.NAN_PROBE))
+    assert ei.value.t == pytest.approx(0.25) and ei.value.step == 4
+    u, nn, t = plan.download(0)
+    assert nn == 4 and np.array_equal(u, u0)
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_fold2_sharded_virtual_ranks_bitwise(G):
+    from test_gpu_sharded import run_sharded
+    n = 63
+    grid = etd.unit_box_grid(3, n + 1)
+    rng = np.random.default_rng(G)
+    u0, v0 = rng.uniform(-1, 1, n ** 3), rng.uniform(-0.5, 0.5, n ** 3)
+    f = etd.fhn_cubic()
+    make = lambda **kw: etd.SystemPlan(grid, 0.05, 1e-3, 5e-4, 0.0, source=f, **kw)
+    single = make()
+    assert single.fold_level() == (2, 2, 2)
+    want = etd.etd2rkds_step_system(single, etd.SystemState(0, 0.0, u0, v0), f, nsteps=2)
+    (u, v), nn, _ = run_sharded(make, G, [u0, v0], 2, grid, f)
+    assert nn == 2
+    assert np.array_equal(u, want.U) and np.array_equal(v, want.V)
