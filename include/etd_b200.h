@@ -175,11 +175,13 @@ int etd_parity_split(const etd_handle* h, int* out);
  * transpose [h][2h].  Returns ETD_ERR_CONFIG unless h % 8 == 0.  Host only. */
 int etd_setup_fold_matrices(int n, int mode, double* ff, double* fb);
 /* The second-level split matrices of one axis with n = 4H - 1, H % 8 == 0
- * (etd_plan.cu fold2_matrices): ga (FOLD 5, even modes) and gb
- * (FOLD 4, odd modes) with 2H interleaved rows x H columns, and the first-level
- * backward matrix fb reading the level-2 mode positions (layout as
- * etd_setup_fold_matrices).  Returns ETD_ERR_CONFIG otherwise.  Host only. */
-int etd_setup_fold2_matrices(int n, int mode, double* ga, double* gb, double* fb);
+ * (etd_plan.cu fold2_matrices): forward ga (FOLD 5, even modes)
+ * and gb (FOLD 4, odd modes), backward go (FOLD 4 over sigma/delta) and ge
+ * (FOLD 2, odd modes), each 2H interleaved rows x H columns; fb = the
+ * first-level backward matrix reading the level-2 mode positions (2h rows x h).
+ * Layouts as etd_setup_fold_matrices; go/ge may be NULL.  Returns
+ * ETD_ERR_CONFIG otherwise.  Host only. */
+int etd_setup_fold2_matrices(int n, int mode, double* ga, double* gb, double* fb, double* go, double* ge);
 /* Parity-split level the step runs per axis: 0 dense, 1 first level (§4a),
  * 2 second level (§4b); out[a] for a < 3. */
 int etd_fold_level(const etd_handle* h, int* out);

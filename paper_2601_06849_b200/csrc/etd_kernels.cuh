@@ -113,7 +113,10 @@ struct ContractArgs {
     int fold_h;             // FOLD: h = (n_axis + 1) / 2, a multiple of 8
     double* out_rev;        // MODE 1 EPI_STORE: also store each output at x' = m_extent-1-x (FOLD 3 input)
     int kbase;              // FOLD 2/4/5: axis coordinate of the first A box (second-level split groups)
-    int nbase;              // FOLD 4: first output position (second-level split, odd-mode group)
+    int nbase;              // FOLD 2/4: first output position (second-level split groups)
+    int sd_out;             // FOLD 5: store the even-mode pairs as (sigma, delta) = (X_q + X_{h-1-q},
+                            // X_q - X_{h-1-q}) at (q, H + q): the level-2 backward's input (EPI_MIX: the
+                            // mix outputs only; w2b stays in mode positions for EPI_CORR)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -530,7 +533,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                 const int r = n0 + wn0 + 2 * jj * 8 + 2 * l;
                 const int io = (r >> 4) * 8 + (r & 7);
                 v0 = v1 = io < args.fold_h;
-                return jp < NP / 2 ? io : args.n_axis - 2 - io;
+                return (jp < NP / 2 ? io : args.n_axis - 2 - io) + args.nbase;
             }
         };
         auto val = [&](int s, int i, int jp, int e) -> double {
@@ -564,6 +567,64 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                             av[c][jp][1] = in1 ? __ldg(a + offset(m, nb + 1)) : 0.0;
                         }
                     }
+                }
+            }
+            if constexpr (FOLD == 5 && (EPI == EPI_SCALE || EPI == EPI_MIX || EPI == EPI_CORR)) {
+                if (args.sd_out) {
+                    // final values at the direct pair (q, q+1) and the mirror pair
+                    // (h-2-q, h-1-q); mirror of q + e is element 1 - e of the mirror pair
+#pragma unroll
+                    for (int jp = 0; jp < NP / 2; ++jp) {
+                        bool in0, two, im0, im1;
+                        const int nb = pair_col(jp, in0, two);
+                        const int nm = pair_col(jp + NP / 2, im0, im1);
+                        if (!in0) continue;
+                        double vd[S][2], vm[S][2];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            if constexpr (EPI == EPI_SCALE) {
+                                const double2 dd = dpair(args.dA, 0, nb), dm = dpair(args.dA, 0, nm);
+#pragma unroll
+                                for (int c = 0; c < S; ++c) {
+                                    const double2 d1 = c % ns ? dpair(args.dA, c % ns, nb) : dd;
+                                    const double2 d2 = c % ns ? dpair(args.dA, c % ns, nm) : dm;
+                                    vd[c][e] = val(c, i, jp, e) * (e ? d1.y : d1.x);
+                                    vm[c][e] = val(c, i, jp + NP / 2, e) * (e ? d2.y : d2.x);
+                                }
+                            } else if constexpr (EPI == EPI_MIX) {
+#pragma unroll
+                                for (int c = 0; c < S / 2; ++c) {
+                                    const double2 da = dpair(args.dA, c, nb), db = dpair(args.dB, c, nb);
+                                    const double2 ma = dpair(args.dA, c, nm), mb = dpair(args.dB, c, nm);
+                                    const double w1 = val(c, i, jp, e), w2 = val(S / 2 + c, i, jp, e);
+                                    const double x1 = val(c, i, jp + NP / 2, e), x2 = val(S / 2 + c, i, jp + NP / 2, e);
+                                    vd[c][e] = (e ? da.y : da.x) * w1 + (e ? db.y : db.x) * w2;
+                                    vm[c][e] = (e ? ma.y : ma.x) * x1 + (e ? mb.y : mb.x) * x2;
+                                    vd[S / 2 + c][e] = w2;
+                                    vm[S / 2 + c][e] = x2;
+                                }
+                            } else {
+#pragma unroll
+                                for (int c = 0; c < S; ++c) {
+                                    const double2 d1 = dpair(args.dA, c, nb), d2 = dpair(args.dA, c, nm);
+                                    vd[c][e] = (val(c, i, jp, e) - av[c][jp][e]) * (e ? d1.y : d1.x);
+                                    vm[c][e] = (val(c, i, jp + NP / 2, e) - av[c][jp + NP / 2][e]) * (e ? d2.y : d2.x);
+                                }
+                            }
+                        }
+                        constexpr int NSD = EPI == EPI_MIX ? S / 2 : S;  // outputs the backward consumes
+#pragma unroll
+                        for (int c = 0; c < S; ++c) {
+                            if (c < NSD) {
+                                store(c, m, nb, vd[c][0] + vm[c][1], vd[c][1] + vm[c][0], true);
+                                store(c, m, args.fold_h + nb, vd[c][0] - vm[c][1], vd[c][1] - vm[c][0], true);
+                            } else {
+                                store(c, m, nb, vd[c][0], vd[c][1], true);
+                                store(c, m, nm, vm[c][0], vm[c][1], true);
+                            }
+                        }
+                    }
+                    continue;
                 }
             }
 #pragma unroll
@@ -794,6 +855,7 @@ struct SourceArgs {
     int fh;
     double* fold_out;
     int x0, x1;             // x-column range of this launch (the pipelined advance's upload chunks)
+    int fold2;              // with `fold`: write the second-level stack (etd_fold2 layout)
 };
 
 template <int SK>
@@ -895,6 +957,9 @@ __device__ __forceinline__ void source_fold_rows(const SourceArgs& a, double src
     }
 }
 
+template <int SK, int NS>
+__device__ void source_fold2_rows(const SourceArgs& a, double srcA, int nj, int& bad, int& dom);
+
 template <int SK>
 __global__ void __launch_bounds__(256) etd_source(const SourceArgs a) {
     __shared__ int stop;
@@ -905,7 +970,10 @@ __global__ void __launch_bounds__(256) etd_source(const SourceArgs a) {
     const int nj = a.j1 - a.j0;
     int bad = 0, dom = 0;
     if (a.fold) {
-        if (a.nspecies == 1) source_fold_rows<SK, 1>(a, srcA, nj, bad, dom);
+        if (a.fold2) {
+            if (a.nspecies == 1) source_fold2_rows<SK, 1>(a, srcA, nj, bad, dom);
+            else source_fold2_rows<SK, 2>(a, srcA, nj, bad, dom);
+        } else if (a.nspecies == 1) source_fold_rows<SK, 1>(a, srcA, nj, bad, dom);
         else source_fold_rows<SK, 2>(a, srcA, nj, bad, dom);
         const int any_dom = __syncthreads_or(dom), any_bad = __syncthreads_or(bad);
         if (threadIdx.x == 0 && (any_dom || any_bad)) atomicCAS(&a.status->fail, 0, any_dom ? 4 : 1);
@@ -1043,6 +1111,248 @@ static __global__ void __launch_bounds__(256) etd_fold2(const Fold2Args a) {
             } else {
                 put(2 * H + k, o[2]);
                 put(3 * H + k, o[3]);
+            }
+        }
+    }
+}
+
+// Source pass writing the second-level stack of [U,(V),fU,(fV)] along the first
+// transform's axis (SourceArgs::fold2): one work item is an orbit
+// {k, n-1-k, 2H-2-k, 2H+k} (k = H-1: {k, n-1-k} and the centre) of rows along the
+// folded axis and an x pair; f is evaluated at every orbit point (fail kinds as
+// the plain pass), then etd_fold2's butterflies are applied per field.
+template <int SK, int NS>
+__device__ void source_fold2_rows(const SourceArgs& a, double srcA, int nj, int& bad, int& dom) {
+    const bool zf = a.fold == 2;
+    const int n = zf ? a.nz : a.ny, H = a.fh / 2;
+    const long long sk = zf ? a.plane : a.pitch;
+    const int nouter = zf ? nj : a.nz;
+    const int items = (a.x1 - a.x0 + 1) / 2;
+    const long long total = (long long)nouter * H * items;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int w = (int)(t % items);
+        const long long r = t / items;
+        const int k = (int)(r % H), outer = (int)(r / H);
+        const int x = a.x0 + 2 * w;
+        const int j0 = zf ? a.j0 + outer : 0, kz0 = zf ? 0 : outer;  // fixed (y, z) of the orbit's rows
+        const long long base = zf ? (long long)j0 * a.pitch + x : (long long)kz0 * a.plane + x;
+        const int c = 2 * H - 2 - k;
+        const int np = k == H - 1 ? 3 : 4;
+        const int pts[4] = {k, n - 1 - k, k == H - 1 ? 2 * H - 1 : c, n - 1 - c};
+        double2 u[NS][4], f[NS][4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            if (p >= np) break;
+            const long long o = base + pts[p] * sk;
+#pragma unroll
+            for (int s = 0; s < NS; ++s) u[s][p] = *reinterpret_cast<const double2*>(a.buf + s * a.F + o);
+            const int jj = zf ? j0 : pts[p], kk = zf ? pts[p] : kz0;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                double uv[2], fv[2] = {0.0, 0.0};
+#pragma unroll
+                for (int s = 0; s < NS; ++s) uv[s] = e ? u[s][p].y : u[s][p].x;
+                if (x + e < a.nx) source_point<SK>(a, srcA, x + e, jj, kk, uv, fv, bad, dom);
+#pragma unroll
+                for (int s = 0; s < NS; ++s) {
+                    if (e) f[s][p].y = fv[s];
+                    else f[s][p].x = fv[s];
+                }
+            }
+        }
+#pragma unroll
+        for (int fld = 0; fld < 2 * NS; ++fld) {
+            const double2* V = fld < NS ? u[fld] : f[fld - NS];
+            auto get = [&](int i) {
+                return i == k ? V[0] : i == n - 1 - k ? V[1] : (k == H - 1 ? V[2] : i == c ? V[2] : V[3]);
+            };
+            double2 o[6];
+            fold2_orbit(k, H, false, get, o);
+            double* dst = a.fold_out + fld * a.F + base;
+            auto put = [&](int i, double2 v) { *reinterpret_cast<double2*>(dst + i * sk) = v; };
+            put(fold2_spos(k, H), o[0]);
+            if (c != k) put(fold2_spos(c, H), o[1]);
+            put(2 * H + k, o[2]);
+            if (k == H - 1) put(2 * H - 1, o[4]);
+            else put(3 * H + k, o[3]);
+        }
+    }
+}
+
+// ------------------------------------------------------------- second-level unfold pass
+// The level-2 backward transform contracts into an intermediate
+// stack along the axis: [o at even i (H) | o at odd i (H) | e (2H - 1)] (the FOLD 4
+// launch over (sigma, delta) and the FOLD 2 launch over the odd-mode group).  This
+// pass finishes it: g_i = o_i + e_i, g_{n-1-i} = o_i - e_i (i < h - 1), g_{h-1} = o_{h-1},
+// with the stage's pointwise epilogue fused (x stage only):
+//   UF_STORE     g -> out (nf fields)
+//   UF_WHAT_SRC  What = g -> out; f(t + tau, What) with its checks (fail 2 / 5); f
+//                written as x_fwd_corr's level-2 stack into fout (etd_fold2 layout)
+//   UF_UPDATE    U1 = aux + g -> out; check (fail 3); the last block commits the step
+// x: one thread per (row, orbit {k, n-1-k, 2H-2-k, 2H+k}); y/z (UF_STORE): 16-byte
+// x pairs per (outer, i).
+enum Unfold : int { UF_STORE = 0, UF_WHAT_SRC = 1, UF_UPDATE = 2 };
+
+struct Unfold2Args {
+    const double* in;
+    double* out;
+    long long Fin, Fout;
+    int nf;                 // UF_STORE: fields; else species
+    int axis, n, H;
+    long long pitch, plane;
+    int nx, ny, nz;
+    int x0, x1;             // y/z: x-column range (x0 even)
+    long long r0, r1;       // x: row range
+    const double* aux;      // UF_UPDATE: What (stride Faux)
+    long long Faux;
+    double* fout;           // UF_WHAT_SRC: f(What) level-2 stack (stride Fout)
+    StepStatus* status;
+    double tau;
+    int commit;
+    double sp[8];
+    const double* sinx;
+    const double* siny;
+    const double* sinz;
+    int ny_local, gj0, gz0;
+};
+
+template <int SK, int UF>
+static __global__ void __launch_bounds__(256) etd_unfold2(const Unfold2Args a) {
+    __shared__ int stop;
+    if (threadIdx.x == 0) stop = *reinterpret_cast<volatile int*>(&a.status->fail);
+    __syncthreads();
+    if (stop) return;
+    const int H = a.H, n = a.n;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    int bad = 0, dom = 0;
+    if (a.axis != 0) {
+        // y / z, UF_STORE: pairs (i, n-1-i)
+        const long long sk = a.axis == 1 ? a.pitch : a.plane, so = a.axis == 1 ? a.plane : a.pitch;
+        const int nouter = a.axis == 1 ? a.nz : a.ny;
+        const int items = (a.x1 - a.x0 + 1) / 2, h = 2 * H;
+        const long long total = (long long)nouter * h * items;
+        for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += stride) {
+            const int w = (int)(t % items);
+            const long long r = t / items;
+            const int i = (int)(r % h), outer = (int)(r / h);
+            const int x = a.x0 + 2 * w;
+            for (int f = 0; f < a.nf; ++f) {
+                const double* src = a.in + f * a.Fin + outer * so + x;
+                double* dst = a.out + f * a.Fout + outer * so + x;
+                const double2 o = *reinterpret_cast<const double2*>(src + fold2_spos(i, H) * sk);
+                if (i == h - 1) {
+                    *reinterpret_cast<double2*>(dst + i * sk) = o;
+                } else {
+                    const double2 e = *reinterpret_cast<const double2*>(src + (2 * H + i) * sk);
+                    *reinterpret_cast<double2*>(dst + i * sk) = o + e;
+                    *reinterpret_cast<double2*>(dst + (n - 1 - i) * sk) = o - e;
+                }
+            }
+        }
+        return;
+    }
+    const double src_a = SK == 4 ? exp(-a.sp[0] * (a.status->t + a.tau)) : 0.0;
+    constexpr int NS = UF == UF_STORE ? 4 : 2;  // register bound on the species loop
+    const long long rows = a.r1 - a.r0, total = rows * H;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int k = (int)(t % H);
+        const long long row = a.r0 + t / H;
+        const int c = 2 * H - 2 - k;
+        // orbit points: 0: k, 1: n-1-k, 2: c, 3: n-1-c, 4: centre h-1 (k = H-1 only; then c = k)
+        const int np = k == H - 1 ? 3 : 4;
+        int pts[5] = {k, n - 1 - k, c, n - 1 - c, 2 * H - 1};
+        if (k == H - 1) pts[2] = 2 * H - 1;  // slots 0, 1, 2 = k, n-1-k, centre
+        const int nloop = UF == UF_STORE ? a.nf : a.nf;
+        double g[NS][5];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            if (s >= nloop) break;
+            const double* src = a.in + s * a.Fin + row * a.pitch;
+            const double ok = src[fold2_spos(k, H)], ek = src[2 * H + k];
+            g[s][0] = ok + ek;
+            g[s][1] = ok - ek;
+            if (k == H - 1) {
+                g[s][2] = src[fold2_spos(2 * H - 1, H)];
+            } else {
+                const double oc = src[fold2_spos(c, H)], ec = src[2 * H + c];
+                g[s][2] = oc + ec;
+                g[s][3] = oc - ec;
+            }
+        }
+        if constexpr (UF == UF_STORE) {
+            for (int s = 0; s < nloop && s < NS; ++s) {
+                double* dst = a.out + s * a.Fout + row * a.pitch;
+                for (int p = 0; p < np; ++p) dst[pts[p]] = g[s][p];
+            }
+        } else if constexpr (UF == UF_UPDATE) {
+            for (int s = 0; s < nloop && s < NS; ++s) {
+                double* dst = a.out + s * a.Fout + row * a.pitch;
+                const double* au = a.aux + s * a.Faux + row * a.pitch;
+                for (int p = 0; p < np; ++p) {
+                    const double u = au[pts[p]] + g[s][p];
+                    bad |= !isfinite(u);
+                    dst[pts[p]] = u;
+                }
+            }
+        } else {
+            // What, f(t + tau, What) at every orbit point, then f's level-2 stack
+            double fv[2][5];
+            const int jj = (int)(row % a.ny_local) + a.gj0, kz = (int)(row / a.ny_local) + a.gz0;
+            for (int p = 0; p < np; ++p) {
+                const int x = pts[p];
+                if (a.nf == 1) {
+                    double ustar = 0.0;
+                    if constexpr (SK == 4) ustar = src_a * (a.sinx[x] * a.siny[jj] * (a.sinz ? a.sinz[kz] : 1.0));
+                    fv[0][p] = src1<SK>(a.sp, g[0][p], ustar);
+                    if constexpr (SK == 3)
+                        if (x == 0 && jj == 0 && kz == 0) fv[0][p] = __longlong_as_double(0x7ff8000000000000ll);
+                    bad |= !isfinite(fv[0][p]);
+                    dom |= src_domain_violation<SK>(g[0][p]);
+                } else {
+                    src2<SK>(a.sp, g[0][p], g[1][p], fv[0][p], fv[1][p]);
+                    bad |= !(isfinite(fv[0][p]) && isfinite(fv[1][p]));
+                }
+            }
+            for (int s = 0; s < a.nf && s < 2; ++s) {
+                double* dst = a.out + s * a.Fout + row * a.pitch;
+                for (int p = 0; p < np; ++p) dst[pts[p]] = g[s][p];
+                // f by global index along the orbit -> etd_fold2 stack positions
+                const double* F = fv[s];
+                auto get = [&](int i) {
+                    return i == k ? F[0] : i == n - 1 - k ? F[1] : (k == H - 1 ? F[2] : i == c ? F[2] : F[3]);
+                };
+                double o[6];
+                fold2_orbit(k, H, false, get, o);
+                double* fo = a.fout + s * a.Fout + row * a.pitch;
+                fo[fold2_spos(k, H)] = o[0];
+                if (c != k) fo[fold2_spos(c, H)] = o[1];
+                fo[2 * H + k] = o[2];
+                if (k == H - 1) fo[2 * H - 1] = o[4];
+                else fo[3 * H + k] = o[3];
+            }
+        }
+    }
+    if constexpr (UF != UF_STORE) {
+        const int any_dom = __syncthreads_or(dom), any_bad = __syncthreads_or(bad);
+        if (threadIdx.x == 0) {
+            if (any_dom || any_bad) {
+                int kind = UF == UF_WHAT_SRC ? 2 : 3;
+                if (any_dom) kind = 5;
+                atomicCAS(&a.status->fail, 0, kind);
+            }
+            if (UF == UF_UPDATE && a.commit) {
+                __threadfence();
+                const unsigned prev = atomicAdd(&a.status->cta_done, 1u);
+                if (prev == gridDim.x - 1) {
+                    __threadfence();
+                    a.status->cta_done = 0;
+                    if (*reinterpret_cast<volatile int*>(&a.status->fail) == 0) {
+                        const long long nn = a.status->n + 1;
+                        a.status->n = nn;
+                        a.status->t = (double)nn * a.tau;
+                    }
+                }
             }
         }
     }

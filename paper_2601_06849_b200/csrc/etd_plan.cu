@@ -99,6 +99,19 @@ static KernelSpec pick(int mode, int S, int epi, bool pro, int sk = 0, int tile 
     return fold ? pick_fold(mode, S, epi, sk, tile, fold) : pick_dense(mode, S, epi, pro, sk, tile);
 }
 
+static const void* pick_unfold(int sk, int uf) {
+#define ETD_UF(K)                                                                                          \
+    case K:                                                                                                \
+        return uf == UF_WHAT_SRC ? reinterpret_cast<const void*>(etd_unfold2<K, UF_WHAT_SRC>)              \
+               : uf == UF_UPDATE ? reinterpret_cast<const void*>(etd_unfold2<K, UF_UPDATE>)                 \
+                                 : reinterpret_cast<const void*>(etd_unfold2<K, UF_STORE>);
+    switch (sk) {
+        ETD_UF(0) ETD_UF(1) ETD_UF(2) ETD_UF(3) ETD_UF(4) ETD_UF(5) ETD_UF(10) ETD_UF(11) ETD_UF(12) ETD_UF(13)
+    default: throw ConfigError("unknown source kind");
+    }
+#undef ETD_UF
+}
+
 static const void* pick_source(int sk) {
     switch (sk) {
     case 0: return reinterpret_cast<const void*>(etd_source<0>);
@@ -247,7 +260,7 @@ struct Piece {
 };
 
 struct Op {
-    enum Kind { KERNEL, SOURCE, COPY2D, EXCHANGE, FAILCODE, COMMIT, THOMAS, NOP, FOLD } kind = KERNEL;
+    enum Kind { KERNEL, SOURCE, COPY2D, EXCHANGE, FAILCODE, COMMIT, THOMAS, NOP, FOLD, UNFOLD } kind = KERNEL;
     // sharded steps: 1 = run on the communication stream; events (indices into
     // Plan::sev) waited on before / recorded after the op (ignored by virtual ranks)
     int strm = 0, wait_ev = -1, rec_ev = -1;
@@ -255,6 +268,7 @@ struct Op {
     SourceArgs sargs{};                          // SOURCE
     ThomasArgs targs{};                          // THOMAS
     Fold2Args fargs{};                           // FOLD (second-level split stack, etd_fold2)
+    Unfold2Args uargs{};                         // UNFOLD (second-level backward finish, etd_unfold2)
     int th_epi = 0;
     const void* src_fn = nullptr;                // SOURCE / THOMAS kernel
     unsigned src_blocks = 0;
@@ -445,6 +459,8 @@ struct Plan {
     bool fold2_all = false;          // every axis split twice: the step runs the level-2 schedule
     double* GA[3] = {nullptr, nullptr, nullptr};
     double* GB[3] = {nullptr, nullptr, nullptr};
+    double* GO[3] = {nullptr, nullptr, nullptr};     // level-2 backward: FOLD 4 over (sigma, delta)
+    double* GE[3] = {nullptr, nullptr, nullptr};     //   and FOLD 2 over the odd-mode group
     double* dvec = nullptr;          // [order 3][axis][slot 9][species 2][dmax]; order 1 = parity-major, 2 = level 2
     double* sintab[3] = {nullptr, nullptr, nullptr};  // sin(pi * coord) per axis (global extents)
     int dmax = 0;
@@ -478,7 +494,7 @@ struct Plan {
         for (double2* t : thfac) if (t) cudaFree(t);
         if (thscr) cudaFree(thscr);
         for (int a = 0; a < 3; ++a)
-            for (double* m : {PR[a], PTR[a], FF[a], FB[a], GA[a], GB[a]}) if (m) cudaFree(m);
+            for (double* m : {PR[a], PTR[a], FF[a], FB[a], GA[a], GB[a], GO[a], GE[a]}) if (m) cudaFree(m);
         if (status) cudaFree(status);
         if (status_host) cudaFreeHost(status_host);
         if (comm) Nccl::get().CommDestroy(comm);
@@ -575,7 +591,7 @@ struct Plan {
 
     // The per-step source pass f(t, U(,V)) into the f slots of the stack at `buf`,
     // or (fold_axis 1/2) the whole stack folded along that axis into `fold_out`.
-    Op source_op(const View& v, double* buf, double* fold_out = nullptr, int fold_axis = 0) const {
+    Op source_op(const View& v, double* buf, double* fold_out = nullptr, int fold_axis = 0, bool fold2 = false) const {
         Op o;
         o.kind = Op::SOURCE;
         o.name = "source";
@@ -612,6 +628,7 @@ struct Plan {
             a.fold = fold_axis;
             a.fh = fh[fold_axis];
             a.fold_out = fold_out;
+            a.fold2 = fold2 ? 1 : 0;
             o.L.bytes = pts * 8.0 * 3 * ns;  // read U(,V), write the folded [U,(V),fU,(fV)]
         }
         return o;
@@ -651,6 +668,55 @@ struct Plan {
         return o;
     }
 
+    // The second-level backward's finishing pass (etd_unfold2) of the intermediate
+    // stack `in` along `axis`, with the stage epilogue `uf` fused (UF_WHAT_SRC: What
+    // -> out, f's level-2 stack -> fout; UF_UPDATE: aux + g -> out, commit).
+    Op unfold_op(const View& v, const std::string& name, int axis, int uf, const double* in, double* out, int nf,
+                 const double* aux = nullptr, double* fout = nullptr) const {
+        Op o;
+        o.kind = Op::UNFOLD;
+        o.name = name;
+        o.L.name = name;
+        o.L.mode = axis == 0 ? 0 : 1;
+        o.L.epi = uf == UF_UPDATE ? EPI_UPDATE : uf == UF_WHAT_SRC ? EPI_WHAT_SRC : EPI_STORE;
+        o.L.args.out = out;  // the pipelined advance downloads U' from here
+        Unfold2Args& a = o.uargs;
+        a.in = in;
+        a.out = out;
+        a.Fin = a.Fout = a.Faux = v.F;
+        a.nf = nf;
+        a.axis = axis;
+        a.n = n_axis(v, axis);
+        a.H = fh[axis] / 2;
+        a.pitch = v.pitch;
+        a.plane = v.plane;
+        a.nx = v.nx;
+        a.ny = v.ny;
+        a.nz = v.nz;
+        a.x0 = 0;
+        a.x1 = v.nx;
+        a.r0 = 0;
+        a.r1 = (long long)v.ny * v.nz;
+        a.aux = aux;
+        a.fout = fout;
+        a.status = status;
+        a.tau = tau;
+        a.commit = (uf == UF_UPDATE && !sharded) ? 1 : 0;
+        for (int i = 0; i < 8; ++i) a.sp[i] = d.src_params[i];
+        a.sinx = sintab[0];
+        a.siny = sintab[1];
+        a.sinz = dim == 3 ? sintab[2] : nullptr;
+        a.ny_local = v.ny;
+        a.gj0 = v.gj0;
+        a.gz0 = v.gz0;
+        o.src_fn = pick_unfold(uf == UF_WHAT_SRC ? d.src_kind : 0, uf);
+        o.src_blocks = 148u * 16u;
+        const double pts = (double)v.nx * v.ny * v.nz;
+        o.L.flops = 0.0;
+        o.L.bytes = pts * 8.0 * nf * (uf == UF_STORE ? 2 : 3);
+        return o;
+    }
+
     // A transform along `axis` of `S` stacked operands at `in` (L loaded), M = P^T (fwd) or P.
     // Folded axes run the parity-split kernels unless `dense` (the dense n x n
     // contraction; kernel-level tests of a single direction use it).
@@ -665,8 +731,9 @@ struct Plan {
         int fold = (this->fold[axis] && !dense && !pro) ? (back ? 2 : 1) : 0;
         if (fold == 1 && prefolded) fold = 4;
         if (part) {
-            if (!fold2[axis] || back || pro || dense) throw ConfigError("second-level split needs a fold2 forward");
-            fold = part == 1 ? 5 : 4;
+            if (!fold2[axis] || back != (part >= 3) || pro || dense)
+                throw ConfigError("second-level split launch on an ineligible axis / direction");
+            fold = part == 1 ? 5 : part == 2 ? 4 : part == 3 ? 4 : 2;
         } else if (fold == 1 && axis == 0) {
             if (epi == EPI_CORR) fold = 4;
             else if (in_rev) fold = 3;
@@ -699,8 +766,9 @@ struct Plan {
             //  * S = 4 has one class (32x128, 8 warps)
             //  * 2 CTAs/SM when that fills two waves, except the S = 2 update (T=3 spills)
             //  * else the 8-warp tile down to ~2/3 of a wave (2D n = 1023 y stages), else 32x32
+            // (the FOLD 5 sigma/delta epilogue spills under the 2-CTA/SM register cap)
             if (S == 4) tile = 0;
-            else if (ctas(3) >= 2 * 148 && !(epi == EPI_UPDATE && S == 2)) tile = 3;
+            else if (ctas(3) >= 2 * 148 && !(epi == EPI_UPDATE && S == 2) && !(part == 1 && S == 2)) tile = 3;
             else if (ctas(0) >= 100) tile = 0;
             else tile = 2;
         } else if (kext <= 255) tile = 2;
@@ -716,7 +784,8 @@ struct Plan {
         L.tmA = mode == 0 ? mapA_x(v, in, loaded, L.k.bm) : mapA_yz(v, in, loaded, axis == 2, L.k.bm);
         L.tmA2 = fold == 3 ? mapA_x(v, in_rev, loaded, L.k.bm) : L.tmA;
         if (part) {
-            L.tmB = mapB_fold(part == 1 ? GA[axis] : GB[axis], axis, mode, L.k.bn, H2);
+            const double* M = part == 1 ? GA[axis] : part == 2 ? GB[axis] : part == 3 ? GO[axis] : GE[axis];
+            L.tmB = mapB_fold(M, axis, mode, L.k.bn, H2);
         } else if (fold) {
             L.tmB = mapB_fold(back ? FB[axis] : FF[axis], axis, mode, L.k.bn);
         } else {
@@ -731,7 +800,16 @@ struct Plan {
         if (part == 1) {
             L.args.n_axis = 2 * H2;  // the FOLD 2 mirror pairs (q, h-1-q) of the even-mode group
             L.args.fold_h = H2;
+            L.args.sd_out = 1;       // the level-2 backward reads (sigma, delta)
         } else if (part == 2) {
+            L.args.fold_h = H2;
+            L.args.kbase = 2 * H2;
+            L.args.nbase = 2 * H2;
+        } else if (part == 3) {
+            L.args.n_axis = 2 * H2;  // o at even i -> [0, H), odd i -> [H, 2H) of the intermediate stack
+            L.args.fold_h = H2;
+        } else if (part == 4) {
+            L.args.n_axis = 2 * H2 - 1;  // the DST-I of size h - 1: e_i and e_{2H-2-i} -> [2H, 4H - 1)
             L.args.fold_h = H2;
             L.args.kbase = 2 * H2;
             L.args.nbase = 2 * H2;
@@ -859,6 +937,10 @@ static void set_source(Plan& p, int kind, const double* params) {
                 op.L.args.src_kind = kind;
                 for (int i = 0; i < 8; ++i) op.L.args.sp[i] = p.d.src_params[i];
                 op.L.k = pick(op.L.mode, op.L.S, op.L.epi, op.L.pro, kind, op.L.tile, op.L.fold);
+            } else if (op.kind == Op::UNFOLD) {
+                for (int i = 0; i < 8; ++i) op.uargs.sp[i] = p.d.src_params[i];
+                const int uf = op.L.epi == EPI_WHAT_SRC ? UF_WHAT_SRC : op.L.epi == EPI_UPDATE ? UF_UPDATE : UF_STORE;
+                op.src_fn = pick_unfold(uf == UF_WHAT_SRC ? kind : 0, uf);
             }
     drop_graphs(p);
 }
@@ -982,9 +1064,13 @@ static int fold2_mode(int pos, int n) {
 //    Pm(i, q) = P(i, 2q+1), i, q < h-1 (fold_matrices on size 2H - 1).
 // FB (first-level backward, FOLD 2) with its odd-group columns in the level-2
 //    position order: FB[r][c] = P(q, fold2_mode(h + c)) for group 1.
-// Layouts as fold_matrices with H for h (GA, GB) and h (FB).
+// GO (FOLD 4, backward even modes over (sigma, delta)): row r = (b, t): group t/8,
+//    output i = 2q + group, q = 8b + t%8 < H; GO[r][c] = P(i, 2c).
+// GE (FOLD 2, backward odd modes) = the first-level backward matrix of Pm.
+// Layouts as fold_matrices with H for h (GA, GB, GO, GE) and h (FB).
 static void fold2_matrices(const std::vector<double>& Pc, int n, int mode, std::vector<double>& ga,
-                           std::vector<double>& gb, std::vector<double>& fb) {
+                           std::vector<double>& gb, std::vector<double>& fb, std::vector<double>* go = nullptr,
+                           std::vector<double>* ge = nullptr) {
     const int h = (n + 1) / 2, H = h / 2, m = h - 1;
     auto P = [&](int i, int k) { return Pc[(size_t)k * n + i]; };
     {
@@ -1004,7 +1090,19 @@ static void fold2_matrices(const std::vector<double>& Pc, int n, int mode, std::
         std::vector<double> Pm((size_t)m * m), unused;
         for (int q = 0; q < m; ++q)
             for (int i = 0; i < m; ++i) Pm[(size_t)q * m + i] = P(i, 2 * q + 1);
-        fold_matrices(Pm, m, mode, gb, unused);
+        fold_matrices(Pm, m, mode, gb, ge ? *ge : unused);
+    }
+    if (go) {
+        const int ld = mode == 0 ? (H + 15) / 16 * 16 : 2 * H;
+        go->assign(mode == 0 ? (size_t)2 * H * ld : (size_t)H * ld, 0.0);
+        auto at = [&](int r, int c) -> double& {
+            return mode == 0 ? (*go)[(size_t)r * ld + c] : (*go)[(size_t)c * ld + r];
+        };
+        for (int r = 0; r < 2 * H; ++r) {
+            const int grp = (r >> 3) & 1, q = (r >> 4) * 8 + (r & 7);
+            if (q >= H) continue;
+            for (int c = 0; c < H; ++c) at(r, c) = P(2 * q + grp, 2 * c);
+        }
     }
     {
         std::vector<double> ff;
@@ -1192,12 +1290,13 @@ static void build_plan(Plan& p, const etd_desc& d) {
         ETD_CK(cudaMemcpy(p.PR[a], pr.data(), pr.size() * 8, cudaMemcpyHostToDevice));
         ETD_CK(cudaMemcpy(p.PTR[a], ptr.data(), ptr.size() * 8, cudaMemcpyHostToDevice));
         if (p.fold2[a]) {
-            std::vector<double> ga, gb;
-            fold2_matrices(Pc, n, a == 0 ? 0 : 1, ga, gb, fb2_tmp);
-            ETD_CK(cudaMalloc(&p.GA[a], ga.size() * 8));
-            ETD_CK(cudaMalloc(&p.GB[a], gb.size() * 8));
-            ETD_CK(cudaMemcpy(p.GA[a], ga.data(), ga.size() * 8, cudaMemcpyHostToDevice));
-            ETD_CK(cudaMemcpy(p.GB[a], gb.data(), gb.size() * 8, cudaMemcpyHostToDevice));
+            std::vector<double> ga, gb, go, ge;
+            fold2_matrices(Pc, n, a == 0 ? 0 : 1, ga, gb, fb2_tmp, &go, &ge);
+            for (auto [dst, v] : {std::pair{&p.GA[a], &ga}, std::pair{&p.GB[a], &gb}, std::pair{&p.GO[a], &go},
+                                  std::pair{&p.GE[a], &ge}}) {
+                ETD_CK(cudaMalloc(dst, v->size() * 8));
+                ETD_CK(cudaMemcpy(*dst, v->data(), v->size() * 8, cudaMemcpyHostToDevice));
+            }
         }
         if (p.fold[a]) {
             std::vector<double> ff, fb;
@@ -1343,8 +1442,8 @@ static void build_plan(Plan& p, const etd_desc& d) {
         const bool f2 = p.fold2_all;
         auto fwd2 = [&](const View& vv, const std::string& nm, int axis, int S, int epi, const double* src,
                         double* tmp, double* dst, bool from1, const double* dA, const double* dB = nullptr,
-                        const double* aux = nullptr) {
-            L.push_back(p.fold_op(vv, "fold_" + nm, axis, src, tmp, S, from1));
+                        const double* aux = nullptr, bool stacked = false) {
+            if (!stacked) L.push_back(p.fold_op(vv, "fold_" + nm, axis, src, tmp, S, from1));
             for (int part = 1; part <= 2; ++part) {
                 L.push_back(kernel_op(p.transform(vv, nm + (part == 1 ? "_even" : "_odd"), axis, false, S, epi,
                                                   false, tmp, dst, false, nullptr, false, part)));
@@ -1353,11 +1452,21 @@ static void build_plan(Plan& p, const etd_desc& d) {
                 L.back().L.args.aux = aux;
             }
         };
+        // ... and every backward transform two launches into an intermediate stack
+        // (in -> tmp) finished by etd_unfold2 (tmp -> out) with the stage epilogue.
+        auto back2 = [&](const View& vv, const std::string& nm, int axis, int S, const double* src, double* tmp,
+                         double* dst, int uf, const double* aux = nullptr, double* fout = nullptr) {
+            for (int part = 3; part <= 4; ++part)
+                L.push_back(kernel_op(p.transform(vv, nm + (part == 3 ? "_o" : "_e"), axis, true, S, EPI_STORE,
+                                                  false, src, tmp, false, nullptr, false, part)));
+            L.push_back(p.unfold_op(vv, nm, axis, uf, tmp, dst, S, aux, fout));
+        };
         auto first_transform = [&](const View& vv, int axis, double* stack, double* dst, double* scratch) {
             if (f2) {
-                L.push_back(p.source_op(vv, stack));
+                // the source pass writes [U,(V),fU,(fV)]'s level-2 stack along the axis
+                L.push_back(p.source_op(vv, stack, scratch, axis, true));
                 fwd2(vv, axis == 2 ? "z_fwd" : "y_fwd", axis, 2 * ns, EPI_SCALE, stack, scratch, dst, false,
-                     p.dv(axis, 0));
+                     p.dv(axis, 0), nullptr, nullptr, true);
                 return;
             }
             const char* nm = axis == 2 ? (fused ? "z_fwd_src" : "z_fwd") : (fused ? "y_fwd_src" : "y_fwd");
@@ -1369,7 +1478,8 @@ static void build_plan(Plan& p, const etd_desc& d) {
         };
         if (p.dim == 3 && !p.sharded) {
             first_transform(V, 2, const_cast<double*>(in), p.Z, p.W);
-            L.push_back(kernel_op(p.transform(V, "z_back", 2, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
+            if (f2) back2(V, "z_back", 2, 2 * ns, p.Z, p.W, p.Z, UF_STORE);  // z-filtered stack in Z
+            else L.push_back(kernel_op(p.transform(V, "z_back", 2, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
         } else if (p.dim == 3) {
             // ---- z stage on y-row chunks: pack; forward exchanges (comm stream);
             // per chunk source + z transforms (compute stream) overlapping the next
@@ -1418,10 +1528,11 @@ static void build_plan(Plan& p, const etd_desc& d) {
                     double* zz_k = p.Zz + p.zbase[k];
                     double* wz_k = p.Wz + p.zbase[k];
                     first_transform(vk, 2, zin_k, zz_k, wz_k);
-                    L.push_back(kernel_op(p.transform(vk, "z_back", 2, true, 2 * ns, EPI_STORE, false, zz_k, wz_k)));
+                    if (f2) back2(vk, "z_back", 2, 2 * ns, zz_k, zin_k, wz_k, UF_STORE);
+                    else L.push_back(kernel_op(p.transform(vk, "z_back", 2, true, 2 * ns, EPI_STORE, false, zz_k, wz_k)));
                 } else {
                     // an empty chunk keeps the op list aligned across virtual ranks
-                    for (int i = 0; i < (fused ? 2 : f2 ? 5 : 3); ++i) {
+                    for (int i = 0; i < (fused ? 2 : f2 ? 6 : 3); ++i) {
                         Op o;
                         o.kind = Op::NOP;
                         o.name = "z_empty";
@@ -1438,23 +1549,31 @@ static void build_plan(Plan& p, const etd_desc& d) {
             L[copies(SP_UNPACK, "unpack")].wait_ev = EV_B;
         }
         if (f2) {
-            // y stage, then the x stage on (Xa = y_back's output, Xb = the other buffer)
-            double *Xa, *Xb;
+            // y stage on (B1, B2) with the z-filtered stack (3D) in B2, then the x stage
+            // on (Xa, Xb) = (B2, B1); the z stage left its output in Z (unsharded) or the
+            // unpack in W (sharded)
+            double *B1 = p.W, *B2 = p.Z;
             if (p.dim == 3) {
-                fwd2(V, "y_fwd", 1, 2 * ns, EPI_SCALE, p.W, p.Z, p.W, false, p.dv(1, 0));
-                L.push_back(kernel_op(p.transform(V, "y_back", 1, true, 2 * ns, EPI_STORE, false, p.W, p.Z)));
-                Xa = p.Z, Xb = p.W;
+                if (p.sharded) B1 = p.Z, B2 = p.W;
+                fwd2(V, "y_fwd", 1, 2 * ns, EPI_SCALE, B2, B1, B2, false, p.dv(1, 0));
             } else {
-                first_transform(V, 1, const_cast<double*>(in), p.Z, p.W);
-                L.push_back(kernel_op(p.transform(V, "y_back", 1, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
-                Xa = p.W, Xb = p.Z;
+                first_transform(V, 1, const_cast<double*>(in), B2, B1);
             }
+            back2(V, "y_back", 1, 2 * ns, B2, B1, B2, UF_STORE);
+            double *Xa = B2, *Xb = B1;
             const size_t Fs = (size_t)ns * V.F;
+            // x_fwd_mix: mix (sigma/delta) -> Xa[0, ns), w2b (mode positions) -> Xa[ns, 2ns)
             fwd2(V, "x_fwd_mix", 0, 2 * ns, EPI_MIX, Xa, Xb, Xa, false, p.dv(0, 0), p.dv(0, 1));
-            L.push_back(kernel_op(p.transform(V, "x_back_src", 0, true, ns, EPI_WHAT_SRC, false, Xa, Xb)));
-            fwd2(V, "x_fwd_corr", 0, ns, EPI_CORR, Xb + Fs, Xa, Xb + Fs, true, p.dv(0, 2), nullptr, Xa + Fs);
-            L.push_back(kernel_op(p.transform(V, "x_back_upd", 0, true, ns, EPI_UPDATE, false, Xb + Fs, out)));
-            L.back().L.args.aux = Xb;
+            // x_back_src: What -> Xa[0, ns), f(t + tau, What) as x_fwd_corr's level-2 stack -> Xb[ns, 2ns)
+            back2(V, "x_back_src", 0, ns, Xa, Xb, Xa, UF_WHAT_SRC, nullptr, Xb + Fs);
+            for (int part = 1; part <= 2; ++part) {
+                L.push_back(kernel_op(p.transform(V, part == 1 ? "x_fwd_corr_even" : "x_fwd_corr_odd", 0, false, ns,
+                                                  EPI_CORR, false, Xb + Fs, Xb, false, nullptr, false, part)));
+                L.back().L.args.dA = p.dv(0, 2);
+                L.back().L.args.aux = Xa + Fs;
+            }
+            // x_back_upd: U1 = What + tau Q3(fw) -> out (commits the step)
+            back2(V, "x_back_upd", 0, ns, Xb, Xb + Fs, out, UF_UPDATE, Xa);
         } else {
         if (p.dim == 3) {
             L.push_back(kernel_op(p.transform(V, "y_fwd", 1, false, 2 * ns, EPI_SCALE, false, p.W, p.Z)));
@@ -1507,7 +1626,8 @@ static void build_plan(Plan& p, const etd_desc& d) {
     }
     p.stats.clear();
     for (auto& op : p.steps[0])
-        if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS || op.kind == Op::FOLD)
+        if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS || op.kind == Op::FOLD ||
+            op.kind == Op::UNFOLD)
             p.stats.push_back({op.L.name, 0, 0, op.L.flops, op.L.bytes, op.L.dense_flops});
     ETD_CK(cudaStreamSynchronize(p.stream));
 }
@@ -1550,6 +1670,11 @@ static void run_op_body(Plan& p, const Op& op, cudaStream_t s) {
     case Op::FOLD: {
         void* args[1] = {const_cast<Fold2Args*>(&op.fargs)};
         ETD_CK(cudaLaunchKernel(reinterpret_cast<const void*>(etd_fold2), dim3(op.src_blocks), dim3(256), args, 0, s));
+        break;
+    }
+    case Op::UNFOLD: {
+        void* args[1] = {const_cast<Unfold2Args*>(&op.uargs)};
+        ETD_CK(cudaLaunchKernel(op.src_fn, dim3(op.src_blocks), dim3(256), args, 0, s));
         break;
     }
     case Op::FAILCODE: etd_fail_code<<<1, 1, 0, s>>>(p.status, p.codes + p.G); break;
@@ -1658,7 +1783,8 @@ static void do_steps(Plan& p, int nsteps) {
                 }
                 if (!p.profiling) continue;
                 const size_t e = rec();
-                if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS || op.kind == Op::FOLD)
+                if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS || op.kind == Op::FOLD ||
+                    op.kind == Op::UNFOLD)
                     spans.push_back({prev, kidx++});
                 prev = e;
             }
@@ -1758,7 +1884,7 @@ static constexpr int kXferChunks = 32;
 static int x_stage_index(const Plan& p) {
     const auto& ops = p.steps[0];
     for (size_t k = 0; k < ops.size(); ++k)
-        if ((ops[k].kind == Op::KERNEL && ops[k].L.mode == 0) || (ops[k].kind == Op::FOLD && ops[k].fargs.axis == 0))
+        if ((ops[k].kind == Op::KERNEL || ops[k].kind == Op::FOLD || ops[k].kind == Op::UNFOLD) && ops[k].L.mode == 0)
             return (int)k;
     return -1;
 }
@@ -1770,8 +1896,8 @@ static bool overlap_eligible(const Plan& p, int nsteps) {
     if (ix <= 0 || ops.back().L.name != "x_back_upd") return false;
     for (int k = 0; k < (int)ops.size(); ++k) {
         const Op& op = ops[k];
-        if (op.kind != Op::KERNEL && op.kind != Op::SOURCE && op.kind != Op::FOLD) return false;
-        if ((op.kind == Op::KERNEL || op.kind == Op::FOLD) && op.L.mode != (k < ix ? 1 : 0)) return false;
+        if (op.kind != Op::KERNEL && op.kind != Op::SOURCE && op.kind != Op::FOLD && op.kind != Op::UNFOLD) return false;
+        if (op.kind != Op::SOURCE && op.L.mode != (k < ix ? 1 : 0)) return false;
         if (op.kind == Op::SOURCE && k >= ix) return false;
     }
     return true;
@@ -1844,6 +1970,11 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
                         o.fargs.x0 = x0;
                         o.fargs.x1 = x1;
                         run_op(p, o, p.stream);
+                    } else if (ops[k].kind == Op::UNFOLD) {
+                        Op o = ops[k];
+                        o.uargs.x0 = x0;
+                        o.uargs.x1 = x1;
+                        run_op(p, o, p.stream);
                     } else {
                         Launch L = ops[k].L;
                         L.args.mtile0 = x0 / L.k.bm;
@@ -1869,6 +2000,14 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
                     Op o = ops[k];
                     o.fargs.r0 = r0;
                     o.fargs.r1 = r1;
+                    run_op(p, o, p.stream);
+                    continue;
+                }
+                if (ops[k].kind == Op::UNFOLD) {
+                    Op o = ops[k];
+                    o.uargs.r0 = r0;
+                    o.uargs.r1 = r1;
+                    o.uargs.commit = 0;
                     run_op(p, o, p.stream);
                     continue;
                 }
@@ -2042,7 +2181,10 @@ static void debug_transform(Plan& p, int species, int axis, int back, int ell, i
                 f.args.dA = p.dv(axis, 6 + ell - 1) + species * p.dmax;
                 launch(f, p.stream);
             }
-            launch(p.transform(v, "dbg_back", axis, true, 1, EPI_STORE, false, p.Z, p.W + v.F), p.stream);
+            for (int part = 3; part <= 4; ++part)
+                launch(p.transform(v, "dbg_back", axis, true, 1, EPI_STORE, false, p.Z, tmp, false, nullptr, false, part),
+                       p.stream);
+            run_op(p, p.unfold_op(v, "dbg_unfold", axis, UF_STORE, tmp, p.W + v.F, 1), p.stream);
             result = p.W + v.F;
         } else {
         if (axis == 0 && p.fold[0]) {
@@ -2328,17 +2470,19 @@ int etd_setup_fold_matrices(int n, int mode, double* ff, double* fb) {
     return ETD_OK;
 }
 
-int etd_setup_fold2_matrices(int n, int mode, double* ga, double* gb, double* fb) {
+int etd_setup_fold2_matrices(int n, int mode, double* ga, double* gb, double* fb, double* go, double* ge) {
     const int h = (n + 1) / 2;
     if (n < 2 || !(n & 1) || h % 16 != 0 || (mode != 0 && mode != 1) || !ga || !gb || !fb) return ETD_ERR_CONFIG;
     try {
         const etd::AxisOperator op = etd::axis_operator(n, 0.0, 1.0, 1, 1.0, 0.0);
-        std::vector<double> Pc, lam, a, b, c;
+        std::vector<double> Pc, lam, a, b, c, o, e;
         etd::eigensystem(op, Pc, lam);
-        etd::fold2_matrices(Pc, n, mode, a, b, c);
+        etd::fold2_matrices(Pc, n, mode, a, b, c, &o, &e);
         std::memcpy(ga, a.data(), a.size() * 8);
         std::memcpy(gb, b.data(), b.size() * 8);
         std::memcpy(fb, c.data(), c.size() * 8);
+        if (go) std::memcpy(go, o.data(), o.size() * 8);
+        if (ge) std::memcpy(ge, e.data(), e.size() * 8);
     } catch (...) {
         return ETD_ERR_CONFIG;
     }

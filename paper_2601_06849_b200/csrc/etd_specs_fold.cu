@@ -7,7 +7,8 @@ namespace etd {
 KernelSpec pick_fold(int mode, int S, int epi, int sk, int tile, int fold) {
     const bool pro = false;
     const bool fwd = epi == EPI_SCALE || epi == EPI_MIX || epi == EPI_CORR;
-    if (pro || fwd != (fold != 2) || (fold == 3 && mode != 0))
+    // FOLD 4 also runs the level-2 backward's (sigma, delta) launch (EPI_STORE)
+    if (pro || (fwd != (fold != 2) && !(fold == 4 && epi == EPI_STORE)) || (fold == 3 && mode != 0))
         throw ConfigError("no parity-split variant for this stage");
 #define ETD_FSPEC(M, SS, E, K, F)                                                                           \
     if (mode == M && S == SS && epi == E && sk == K && fold == F)                                           \

@@ -1,7 +1,7 @@
 // etd_specs_fold2.cu — second-level parity-split forward kernels:
 // FOLD 5 (even-mode group: DST-III halves, +/- epilogue) with every forward
-// epilogue, and the FOLD 4 (odd-mode group: DST-I sub-split) variants the
-// first-level schedule does not use.  A separate TU so nvcc builds it in parallel.
+// epilogue, and the FOLD 4 / FOLD 2 variants (odd-mode group forward, level-2
+// backward launches) the first-level schedule does not use.  A separate TU so nvcc builds it in parallel.
 #include "etd_registry.cuh"
 
 namespace etd {
@@ -20,6 +20,13 @@ KernelSpec pick_fold2(int mode, int S, int epi, int sk, int tile, int fold) {
     if (fold == 4) {
         ETD_FSPEC(1, 1, EPI_SCALE, 0, 4) ETD_FSPEC(0, 1, EPI_SCALE, 0, 4)
         ETD_FSPEC(0, 2, EPI_MIX, 0, 4) ETD_FSPEC(0, 4, EPI_MIX, 0, 4)
+        // level-2 backward, even modes: o from (sigma, delta) into the intermediate stack
+        ETD_FSPEC(1, 1, EPI_STORE, 0, 4) ETD_FSPEC(1, 2, EPI_STORE, 0, 4) ETD_FSPEC(1, 4, EPI_STORE, 0, 4)
+        ETD_FSPEC(0, 1, EPI_STORE, 0, 4) ETD_FSPEC(0, 2, EPI_STORE, 0, 4)
+    }
+    // level-2 backward, odd modes (x stage with two species)
+    if (fold == 2) {
+        ETD_FSPEC(0, 2, EPI_STORE, 0, 2)
     }
 #undef ETD_FSPEC
     throw ConfigError("no parity-split variant for this stage / source kind");

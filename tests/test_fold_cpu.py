@@ -114,13 +114,15 @@ def fold2_mats(n, mode):
     ldH = (H + 15) // 16 * 16 if mode == 0 else 2 * H
     ldh = (h + 15) // 16 * 16 if mode == 0 else 2 * h
     ga = np.zeros(2 * H * ldH if mode == 0 else H * ldH)
-    gb = np.zeros_like(ga)
+    gb, go, ge = np.zeros_like(ga), np.zeros_like(ga), np.zeros_like(ga)
     fb = np.zeros(2 * h * ldh if mode == 0 else h * ldh)
     vp = lambda a: a.ctypes.data_as(C.c_void_p)
-    assert etd.lib().etd_setup_fold2_matrices(n, mode, vp(ga), vp(gb), vp(fb)) == 0
+    assert etd.lib().etd_setup_fold2_matrices(n, mode, vp(ga), vp(gb), vp(fb), vp(go), vp(ge)) == 0
     if mode == 0:
-        return ga.reshape(2 * H, ldH)[:, :H], gb.reshape(2 * H, ldH)[:, :H], fb.reshape(2 * h, ldh)[:, :h]
-    return ga.reshape(H, 2 * H).T, gb.reshape(H, 2 * H).T, fb.reshape(h, 2 * h).T
+        small = lambda a: a.reshape(2 * H, ldH)[:, :H]
+        return small(ga), small(gb), fb.reshape(2 * h, ldh)[:, :h], small(go), small(ge)
+    small = lambda a: a.reshape(H, 2 * H).T
+    return small(ga), small(gb), fb.reshape(h, 2 * h).T, small(go), small(ge)
 
 
 def fold2_modes(n):
@@ -174,7 +176,7 @@ def fold2_forward(st, GA, GB, n):
 @pytest.mark.parametrize("n", [31, 63, 127, 255, 511])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_fold2_reproduces_dense_transform(n, mode):
-    GA, GB, FB2 = fold2_mats(n, mode)
+    GA, GB, FB2, GO, GE = fold2_mats(n, mode)
     P, _ = Oracle.spectral_factor(n, 2.0, -1.0)
     P = np.asarray(P).reshape(n, n).T if np.asarray(P).ndim == 1 else np.asarray(P)
     modes = fold2_modes(n)
@@ -199,5 +201,57 @@ def test_fold2_reproduces_dense_transform(n, mode):
 
 def test_fold2_matrices_reject_ineligible_sizes():
     p = C.c_void_p(0)
-    assert etd.lib().etd_setup_fold2_matrices(47, 0, p, p, p) != 0   # h = 24: H not a multiple of 8
-    assert etd.lib().etd_setup_fold2_matrices(64, 0, p, p, p) != 0   # even n
+    assert etd.lib().etd_setup_fold2_matrices(47, 0, p, p, p, p, p) != 0   # h = 24: H not a multiple of 8
+    assert etd.lib().etd_setup_fold2_matrices(64, 0, p, p, p, p, p) != 0   # even n
+
+
+def fold2_backward(gh, GO, GE, n):
+    """Level-2 backward restated: (sigma, delta) of the even-mode pairs (q, h-1-q) (the
+    FOLD 5 forward epilogue stores them, sd_out); FOLD 4 over them with GO -> o at even /
+    odd i; FOLD 2 over the odd-mode group with GE -> e, e mirrored about its centre;
+    etd_unfold2: g_i = o_i + e_i, g_{n-1-i} = o_i - e_i."""
+    h = (n + 1) // 2
+    H = h // 2
+    q = np.arange(H)
+    sig = gh[..., q] + gh[..., h - 1 - q]
+    dlt = gh[..., q] - gh[..., h - 1 - q]
+    mid = np.zeros(gh.shape[:-1] + (n,))               # [o even i | o odd i | e]
+    for r in range(2 * H):                           # FOLD 4 launch, kbase = nbase = 0
+        grp = (r >> 3) & 1
+        pos = (r >> 4) * 8 + (r & 7) + grp * H
+        if pos < 2 * H:
+            mid[..., pos] = (dlt if grp else sig) @ GO[r]
+    B0 = gh[..., 2 * H:3 * H]
+    B1 = np.concatenate([gh[..., 3 * H:], np.zeros(gh.shape[:-1] + (1,))], -1)
+    m = 2 * H - 1
+    for r in range(0, 2 * H, 16):                    # FOLD 2 launch, kbase = nbase = 2H, n_axis = 2H - 1
+        for t in range(8):
+            io = (r >> 4) * 8 + t
+            if io < H:
+                o, e = B0 @ GE[r + t], B1 @ GE[r + 8 + t]
+                mid[..., 2 * H + io] = o + e
+                mid[..., 2 * H + m - 1 - io] = o - e
+    spos = lambda i: H + i // 2 if i % 2 else i // 2
+    out = np.zeros_like(mid)
+    for i in range(h):
+        o = mid[..., spos(i)]
+        if i == h - 1:
+            out[..., i] = o
+        else:
+            e = mid[..., 2 * H + i]
+            out[..., i] = o + e
+            out[..., n - 1 - i] = o - e
+    return out
+
+
+@pytest.mark.parametrize("n", [31, 63, 127, 255, 511])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fold2_backward_reproduces_dense_transform(n, mode):
+    _, _, _, GO, GE = fold2_mats(n, mode)
+    P, _ = Oracle.spectral_factor(n, 2.0, -1.0)
+    P = np.asarray(P).reshape(n, n).T if np.asarray(P).ndim == 1 else np.asarray(P)
+    modes = fold2_modes(n)
+    gh = np.random.default_rng(n + 3).uniform(-1, 1, (5, n))   # level-2 positions
+    nat = np.zeros_like(gh)
+    nat[:, modes] = gh
+    assert np.max(np.abs(fold2_backward(gh, GO, GE, n) - nat @ P.T)) <= 1e-13 * n

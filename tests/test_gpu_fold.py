@@ -169,8 +169,13 @@ def test_fold_halves_the_transform_flops():
     st = {s["name"]: s for s in p.stage_stats()}
     pts = n ** 3
     h = (n + 1) // 2
-    assert st["z_back"]["flops_per_launch"] == pytest.approx(2.0 * 2 * h * h / n * pts * 2)
-    assert st["z_back"]["dense_flops_per_launch"] == pytest.approx(2.0 * n * pts * 2)
+    H = h // 2
+    # second level: each of the two launches 2 (2H) H / n per point
+    assert p.fold_level() == (2, 2, 2)
+    for nm in ("z_back_o", "z_back_e", "z_fwd_even", "z_fwd_odd"):
+        assert st[nm]["flops_per_launch"] == pytest.approx(2.0 * 2 * H * H / n * pts * 2)
+        assert st[nm]["dense_flops_per_launch"] == pytest.approx(0.5 * 2.0 * n * pts * 2)
+    assert st["z_back"]["flops_per_launch"] == 0   # the HBM-bound unfold pass
 
 
 @pytest.mark.parametrize("shape", [(127, 31, 47), (200, 41, 1), (255, 63, 1), (130, 20, 33)])
