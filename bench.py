@@ -240,7 +240,8 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
             # shape; the slowest of the pair flips run to run
             twin = {"y_fwd": "z_fwd", "z_fwd": "y_fwd", "y_back": "z_back", "z_back": "y_back",
                     "y_fwd_even": "z_fwd_even", "z_fwd_even": "y_fwd_even",
-                    "y_fwd_odd": "z_fwd_odd", "z_fwd_odd": "y_fwd_odd"}
+                    "y_fwd_odd": "z_fwd_odd", "z_fwd_odd": "y_fwd_odd",
+                    "y_back_o": "z_back_o", "z_back_o": "y_back_o", "y_back_e": "z_back_e", "z_back_e": "y_back_e"}
             for name in (dom["name"], twin.get(dom["name"])):
                 if name in tr:
                     traffic, traffic_stage = tr[name], name

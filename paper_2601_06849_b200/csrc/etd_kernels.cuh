@@ -1040,6 +1040,19 @@ struct Fold2Args {
 
 __device__ __forceinline__ int fold2_spos(int i, int H) { return (i & 1) ? H + (i >> 1) : (i >> 1); }
 
+// x-axis stack passes: `rpb` rows per block iteration, `tpr` threads per row
+struct RowLoop {
+    int rpb, tpr, sub, lane;
+};
+__device__ __forceinline__ RowLoop row_loop(int H) {
+    RowLoop r;
+    r.rpb = H >= (int)blockDim.x ? 1 : (int)blockDim.x / H;
+    r.tpr = (int)blockDim.x / r.rpb;
+    r.sub = threadIdx.x / r.tpr;
+    r.lane = threadIdx.x % r.tpr;
+    return r;
+}
+
 template <class T, class Get>
 __device__ __forceinline__ void fold2_orbit(int k, int H, bool from1, const Get& get, T (&o)[6]) {
     // o: s_k, s_c (c = 2H-2-k), dd_s, dd_d, s_centre (k = H-1 only)
@@ -1062,24 +1075,46 @@ static __global__ void __launch_bounds__(256) etd_fold2(const Fold2Args a) {
     const int H = a.H;
     const long long stride = (long long)gridDim.x * blockDim.x;
     if (a.axis == 0) {
-        const long long rows = a.r1 - a.r0, total = rows * H;
-        for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += stride) {
-            const int k = (int)(t % H);
-            const long long row = a.r0 + t / H;
-            for (int f = 0; f < a.nf; ++f) {
-                const double* src = a.in + f * a.Fin + row * a.pitch;
-                double* dst = a.out + f * a.Fout + row * a.pitch;
-                double o[6];
-                fold2_orbit(k, H, a.from1, [&](int i) { return src[i]; }, o);
+        // rows over blocks, orbits over threads (no 64-bit index division); every
+        // field's orbit is loaded before any store
+        const RowLoop rl = row_loop(H);
+        const int n = a.n;
+        for (long long row = a.r0 + (long long)blockIdx.x * rl.rpb + rl.sub; rl.sub < rl.rpb && row < a.r1;
+             row += (long long)gridDim.x * rl.rpb) {
+            for (int k = rl.lane; k < H; k += rl.tpr) {
                 const int c = 2 * H - 2 - k;
-                dst[fold2_spos(k, H)] = o[0];
-                if (c != k) dst[fold2_spos(c, H)] = o[1];
-                if (k == H - 1) {
-                    dst[2 * H + k] = o[2];  // c = k here: 2 d_{H-1}, and no difference term
-                    dst[2 * H - 1] = o[4];
-                } else {
-                    dst[2 * H + k] = o[2];
-                    dst[3 * H + k] = o[3];
+                const int i0 = k, i1 = a.from1 ? c : n - 1 - k, i2 = a.from1 ? 2 * H + k : c,
+                          i3 = a.from1 ? 2 * H + c : n - 1 - c;
+                double v[4][5];
+#pragma unroll
+                for (int f = 0; f < 4; ++f) {
+                    if (f >= a.nf) break;
+                    const double* __restrict__ src = a.in + f * a.Fin + row * a.pitch;
+                    v[f][0] = src[i0];
+                    v[f][1] = src[i1];
+                    v[f][2] = src[i2];
+                    v[f][3] = src[i3];
+                    v[f][4] = k == H - 1 ? src[2 * H - 1] : 0.0;
+                }
+#pragma unroll
+                for (int f = 0; f < 4; ++f) {
+                    if (f >= a.nf) break;
+                    double si, sc, di, dc;
+                    if (a.from1) {
+                        si = v[f][0]; sc = v[f][1]; di = v[f][2]; dc = v[f][3];
+                    } else {
+                        si = v[f][0] + v[f][1]; di = v[f][0] - v[f][1];
+                        sc = v[f][2] + v[f][3]; dc = v[f][2] - v[f][3];
+                    }
+                    double* __restrict__ dst = a.out + f * a.Fout + row * a.pitch;
+                    dst[fold2_spos(k, H)] = si;
+                    dst[2 * H + k] = di + dc;  // k = H-1: c = k, 2 d_{H-1}
+                    if (k == H - 1) {
+                        dst[2 * H - 1] = a.from1 ? v[f][4] : v[f][4] + v[f][4];
+                    } else {
+                        dst[fold2_spos(c, H)] = sc;
+                        dst[3 * H + k] = di - dc;
+                    }
                 }
             }
         }
@@ -1254,10 +1289,10 @@ static __global__ void __launch_bounds__(256) etd_unfold2(const Unfold2Args a) {
     }
     const double src_a = SK == 4 ? exp(-a.sp[0] * (a.status->t + a.tau)) : 0.0;
     constexpr int NS = UF == UF_STORE ? 4 : 2;  // register bound on the species loop
-    const long long rows = a.r1 - a.r0, total = rows * H;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += stride) {
-        const int k = (int)(t % H);
-        const long long row = a.r0 + t / H;
+    const RowLoop rl = row_loop(H);
+    for (long long row = a.r0 + (long long)blockIdx.x * rl.rpb + rl.sub; rl.sub < rl.rpb && row < a.r1;
+         row += (long long)gridDim.x * rl.rpb)
+    for (int k = rl.lane; k < H; k += rl.tpr) {
         const int c = 2 * H - 2 - k;
         // orbit points: 0: k, 1: n-1-k, 2: c, 3: n-1-c, 4: centre h-1 (k = H-1 only; then c = k)
         const int np = k == H - 1 ? 3 : 4;
@@ -1286,11 +1321,22 @@ static __global__ void __launch_bounds__(256) etd_unfold2(const Unfold2Args a) {
                 for (int p = 0; p < np; ++p) dst[pts[p]] = g[s][p];
             }
         } else if constexpr (UF == UF_UPDATE) {
-            for (int s = 0; s < nloop && s < NS; ++s) {
-                double* dst = a.out + s * a.Fout + row * a.pitch;
-                const double* au = a.aux + s * a.Faux + row * a.pitch;
-                for (int p = 0; p < np; ++p) {
-                    const double u = au[pts[p]] + g[s][p];
+            double w[NS][4];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                if (s >= nloop) break;
+                const double* __restrict__ au = a.aux + s * a.Faux + row * a.pitch;
+#pragma unroll
+                for (int p = 0; p < 4; ++p) w[s][p] = p < np ? au[pts[p]] : 0.0;
+            }
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                if (s >= nloop) break;
+                double* __restrict__ dst = a.out + s * a.Fout + row * a.pitch;
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    if (p >= np) break;
+                    const double u = w[s][p] + g[s][p];
                     bad |= !isfinite(u);
                     dst[pts[p]] = u;
                 }
