@@ -514,21 +514,21 @@ struct Plan {
 
     // ---- maps over stacked fields (one TMA box per stage per operand set) ----
     // MODE 0 view: dims {nx, R, count}, box {16, BM, count} -> smem [op][BM][16]
-    static CUtensorMap mapA_x(const View& v, const double* base, int count, int bm) {
+    static CUtensorMap mapA_x(const View& v, const double* base, int count, int bm, long long fs = 0) {
         const unsigned long long dims[3] = {(unsigned long long)v.nx, (unsigned long long)v.ny * v.nz,
                                             (unsigned long long)count};
-        const unsigned long long st[2] = {(unsigned long long)v.pitch, (unsigned long long)v.F};
+        const unsigned long long st[2] = {(unsigned long long)v.pitch, (unsigned long long)(fs ? fs : v.F)};
         const unsigned box[3] = {16, (unsigned)bm, (unsigned)count};
         return make_map(base, 3, dims, st, box);
     }
     // MODE 1 view: dims {x%16, k, x/16, outer, count}, box {16, 16, BM/16, 1, count}
     // -> smem [op][pb][k][16].  x columns past nx read the zero pad of the pitch.
-    static CUtensorMap mapA_yz(const View& v, const double* base, int count, bool zaxis, int bm) {
+    static CUtensorMap mapA_yz(const View& v, const double* base, int count, bool zaxis, int bm, long long fs = 0) {
         const unsigned long long nk = zaxis ? v.nz : v.ny, no = zaxis ? v.ny : v.nz;
         const unsigned long long sk = zaxis ? v.plane : v.pitch, so = zaxis ? v.pitch : v.plane;
         const unsigned long long dims[5] = {16, nk, (unsigned long long)((v.nx + 15) / 16), no,
                                             (unsigned long long)count};
-        const unsigned long long st[4] = {sk, 16, so, (unsigned long long)v.F};
+        const unsigned long long st[4] = {sk, 16, so, (unsigned long long)(fs ? fs : v.F)};
         const unsigned box[5] = {16, 16, (unsigned)(bm / 16), 1, (unsigned)count};
         return make_map(base, 5, dims, st, box);
     }
@@ -726,7 +726,7 @@ struct Plan {
     // transform (FOLD 5 / FOLD 4) of the etd_fold2 stack at `in`.
     Launch transform(const View& v, const std::string& name, int axis, bool back, int S, int epi, bool pro,
                      const double* in, double* out, bool dense = false, const double* in_rev = nullptr,
-                     bool prefolded = false, int part = 0) const {
+                     bool prefolded = false, int part = 0, long long fstride = 0) const {
         Launch L;
         int fold = (this->fold[axis] && !dense && !pro) ? (back ? 2 : 1) : 0;
         if (fold == 1 && prefolded) fold = 4;
@@ -768,7 +768,8 @@ struct Plan {
             //  * else the 8-warp tile down to ~2/3 of a wave (2D n = 1023 y stages), else 32x32
             // (the FOLD 5 sigma/delta epilogue spills under the 2-CTA/SM register cap)
             if (S == 4) tile = 0;
-            else if (ctas(3) >= 2 * 148 && !(epi == EPI_UPDATE && S == 2) && !(part == 1 && S == 2)) tile = 3;
+            else if (ctas(3) >= 2 * 148 && !(epi == EPI_UPDATE && S == 2) && !(part == 1 && S == 2 && epi == EPI_CORR))
+                tile = 3;
             else if (ctas(0) >= 100) tile = 0;
             else tile = 2;
         } else if (kext <= 255) tile = 2;
@@ -781,7 +782,7 @@ struct Plan {
         L.fold = fold;
         L.k = pick(mode, S, epi, pro, d.src_kind, tile, fold);
         const int loaded = pro ? S / 2 : S;
-        L.tmA = mode == 0 ? mapA_x(v, in, loaded, L.k.bm) : mapA_yz(v, in, loaded, axis == 2, L.k.bm);
+        L.tmA = mode == 0 ? mapA_x(v, in, loaded, L.k.bm, fstride) : mapA_yz(v, in, loaded, axis == 2, L.k.bm, fstride);
         L.tmA2 = fold == 3 ? mapA_x(v, in_rev, loaded, L.k.bm) : L.tmA;
         if (part) {
             const double* M = part == 1 ? GA[axis] : part == 2 ? GB[axis] : part == 3 ? GO[axis] : GE[axis];
@@ -795,6 +796,7 @@ struct Plan {
         }
         L.args = base_args(v, axis);
         L.args.out = out;
+        if (fstride) L.args.out_stride = fstride;
         L.args.kext = kext;
         L.args.fold_h = fh[axis];
         if (part == 1) {
@@ -1440,13 +1442,33 @@ static void build_plan(Plan& p, const etd_desc& d) {
         // Second-level split (p.fold2_all): every forward transform is
         // an etd_fold2 stack (src -> tmp) and its even/odd-mode launches (tmp -> dst).
         const bool f2 = p.fold2_all;
+        // S = 4 transform launches as two S = 2 launches (ETD_PAIRS=1)
+        const char* pe = std::getenv("ETD_PAIRS");
+        const bool pairs = pe && pe[0] == '1';
         auto fwd2 = [&](const View& vv, const std::string& nm, int axis, int S, int epi, const double* src,
                         double* tmp, double* dst, bool from1, const double* dA, const double* dB = nullptr,
                         const double* aux = nullptr, bool stacked = false) {
             if (!stacked) L.push_back(p.fold_op(vv, "fold_" + nm, axis, src, tmp, S, from1));
+            const long long F = vv.F;
             for (int part = 1; part <= 2; ++part) {
-                L.push_back(kernel_op(p.transform(vv, nm + (part == 1 ? "_even" : "_odd"), axis, false, S, epi,
-                                                  false, tmp, dst, false, nullptr, false, part)));
+                const std::string pn = nm + (part == 1 ? "_even" : "_odd");
+                if (pairs && S == 4) {
+                    // two S = 2 launches (2 CTAs/SM): fields (0,1), (2,3); the mix pairs
+                    // each species' (w1, w2) = fields (c, c + 2)
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const bool mix = epi == EPI_MIX;
+                        const long long off = mix ? h2 * F : 2 * h2 * F;
+                        L.push_back(kernel_op(p.transform(vv, pn + (h2 ? "_b" : "_a"), axis, false, 2, epi, false,
+                                                          tmp + off, dst + off, false, nullptr, false, part,
+                                                          mix ? 2 * F : 0)));
+                        L.back().L.args.dA = dA + (mix ? h2 * p.dmax : 0);
+                        L.back().L.args.dB = dB ? dB + (mix ? h2 * p.dmax : 0) : nullptr;
+                        L.back().L.args.aux = aux;
+                    }
+                    continue;
+                }
+                L.push_back(kernel_op(p.transform(vv, pn, axis, false, S, epi, false, tmp, dst, false, nullptr,
+                                                  false, part)));
                 L.back().L.args.dA = dA;
                 L.back().L.args.dB = dB;
                 L.back().L.args.aux = aux;
@@ -1456,9 +1478,18 @@ static void build_plan(Plan& p, const etd_desc& d) {
         // (in -> tmp) finished by etd_unfold2 (tmp -> out) with the stage epilogue.
         auto back2 = [&](const View& vv, const std::string& nm, int axis, int S, const double* src, double* tmp,
                          double* dst, int uf, const double* aux = nullptr, double* fout = nullptr) {
-            for (int part = 3; part <= 4; ++part)
-                L.push_back(kernel_op(p.transform(vv, nm + (part == 3 ? "_o" : "_e"), axis, true, S, EPI_STORE,
-                                                  false, src, tmp, false, nullptr, false, part)));
+            for (int part = 3; part <= 4; ++part) {
+                const std::string pn = nm + (part == 3 ? "_o" : "_e");
+                if (pairs && S == 4) {
+                    for (int h2 = 0; h2 < 2; ++h2)
+                        L.push_back(kernel_op(p.transform(vv, pn + (h2 ? "_b" : "_a"), axis, true, 2, EPI_STORE,
+                                                          false, src + 2 * h2 * vv.F, tmp + 2 * h2 * vv.F, false,
+                                                          nullptr, false, part)));
+                    continue;
+                }
+                L.push_back(kernel_op(p.transform(vv, pn, axis, true, S, EPI_STORE, false, src, tmp, false, nullptr,
+                                                  false, part)));
+            }
             L.push_back(p.unfold_op(vv, nm, axis, uf, tmp, dst, S, aux, fout));
         };
         auto first_transform = [&](const View& vv, int axis, double* stack, double* dst, double* scratch) {

@@ -146,3 +146,21 @@ def test_fold2_sharded_virtual_ranks_bitwise(G):
     (u, v), nn, _ = run_sharded(make, G, [u0, v0], 2, grid, f)
     assert nn == 2
     assert np.array_equal(u, want.U) and np.array_equal(v, want.V)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_fold2_pair_launches_bitwise_equal(dim, monkeypatch):
+    """ETD_PAIRS=1 issues every S = 4 transform launch as two S = 2 launches (fields
+    (0,1), (2,3); the mix pairs each species' (w1, w2)): the same per-element
+    contraction order, so the step is bitwise equal."""
+    n = 63
+    g = etd.unit_box_grid(dim, n + 1)
+    rng = np.random.default_rng(40 + dim)
+    u0, v0 = rng.uniform(-1, 1, n ** dim), rng.uniform(-0.5, 0.5, n ** dim)
+    st = etd.SystemState(0, 0.0, u0, v0)
+    a = etd.etd2rkds_step_system(etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0), st, etd.fhn_cubic(), nsteps=2)
+    monkeypatch.setenv("ETD_PAIRS", "1")
+    pp = etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0)
+    assert any(s["name"].endswith("_b") for s in pp.stage_stats())
+    b = etd.etd2rkds_step_system(pp, st, etd.fhn_cubic(), nsteps=2)
+    assert np.array_equal(a.U, b.U) and np.array_equal(a.V, b.V)
