@@ -1217,10 +1217,14 @@ static void build_plan(Plan& p, const etd_desc& d) {
         }
         // Second-level split where n = 4H - 1 with H a multiple of 8
         // (n = 32m - 1: every BASELINE config); the step uses it when every axis has
-        // it.  ETD_FOLD2=0 turns it off.
+        // it and the grid has >= 2^18 points (below, its extra stack-pass launches
+        // cost more than the halved contractions save: config 0, 127^2, runs
+        // 0.066 ms/step first-level vs 0.152 ms second-level; config 1, 1023^2,
+        // 0.405 vs 0.358).  ETD_FOLD2=0 turns it off, =1 forces it on any size.
         const char* f2 = std::getenv("ETD_FOLD2");
-        const bool f2_off = f2 && f2[0] == '0';
-        p.fold2_all = !f2_off && !fused0;
+        const bool f2_off = f2 && f2[0] == '0', f2_force = f2 && f2[0] == '1';
+        const double npts = (double)d.n[0] * d.n[1] * (d.dim == 3 ? d.n[2] : 1);
+        p.fold2_all = !f2_off && !fused0 && (f2_force || npts >= 262144.0);
         for (int a = 0; a < d.dim; ++a) {
             p.fold2[a] = p.fold[a] && !f2_off && (d.n[a] & 1) && p.fh[a] % 16 == 0;
             p.fold2_all = p.fold2_all && p.fold2[a];
@@ -1442,9 +1446,11 @@ static void build_plan(Plan& p, const etd_desc& d) {
         // Second-level split (p.fold2_all): every forward transform is
         // an etd_fold2 stack (src -> tmp) and its even/odd-mode launches (tmp -> dst).
         const bool f2 = p.fold2_all;
-        // S = 4 transform launches as two S = 2 launches (ETD_PAIRS=1)
+        // S = 4 transform launches as two S = 2 launches (2 CTAs/SM overlap one CTA's
+        // epilogue with the other's main loop; config 4 529.8 -> 521.1 ms/step,
+        // config 3 42.0 -> 40.0); ETD_PAIRS=0 keeps the S = 4 launches
         const char* pe = std::getenv("ETD_PAIRS");
-        const bool pairs = pe && pe[0] == '1';
+        const bool pairs = !(pe && pe[0] == '0');
         auto fwd2 = [&](const View& vv, const std::string& nm, int axis, int S, int epi, const double* src,
                         double* tmp, double* dst, bool from1, const double* dA, const double* dB = nullptr,
                         const double* aux = nullptr, bool stacked = false) {

@@ -13,9 +13,9 @@ from paper_2601_06849_b200 import configs
 pytestmark = pytest.mark.gpu
 
 STAGES_L1 = ["z_fwd", "z_back", "y_fwd", "y_back", "x_fwd_mix", "x_back_src", "x_fwd_corr", "x_back_upd"]
-STAGES_L2 = ["z_fwd_even", "z_fwd_odd", "z_back_o", "z_back_e", "y_fwd_even", "y_fwd_odd", "y_back_o", "y_back_e",
-             "x_fwd_mix_even", "x_fwd_mix_odd", "x_back_src_o", "x_back_src_e", "x_fwd_corr_even", "x_fwd_corr_odd",
-             "x_back_upd_o", "x_back_upd_e"]
+STAGES_L2 = [f"{s}_{h}" for s in ["z_fwd_even", "z_fwd_odd", "z_back_o", "z_back_e", "y_fwd_even", "y_fwd_odd",
+                                   "y_back_o", "y_back_e", "x_fwd_mix_even", "x_fwd_mix_odd"] for h in "ab"] + \
+            ["x_back_src_o", "x_back_src_e", "x_fwd_corr_even", "x_fwd_corr_odd", "x_back_upd_o", "x_back_upd_e"]
 
 
 @pytest.mark.parametrize("level", [1, 2])

@@ -160,9 +160,11 @@ def test_fold_sharded_equals_single_gpu(G):
     assert n == 3 and np.array_equal(u, ref.U) and np.array_equal(v, ref.V)
 
 
-def test_fold_halves_the_transform_flops():
+def test_fold_halves_the_transform_flops(monkeypatch):
     """Stage FLOPs reported per launch: the folded transform executes 2 (2h) h / n
     per point against 2 n dense."""
+    monkeypatch.setenv("ETD_FOLD2", "1")   # below the default size threshold
+    monkeypatch.setenv("ETD_PAIRS", "0")
     n = 63
     g = etd.unit_box_grid(3, n + 1)
     p = etd.make_plan(g, 0.01, 1.0, 1.0, source=etd.allen_cahn_cubic())

@@ -26,12 +26,18 @@ def R():
     return Ref if Ref.available() else Oracle
 
 
+@pytest.fixture(autouse=True)
+def force_level2(monkeypatch):
+    """The test grids are below the default size threshold (2^18 points): force it."""
+    monkeypatch.setenv("ETD_FOLD2", "1")
+
+
 def plans(make, monkeypatch):
     """(level-2, level-1, dense) plans of the same problem."""
     p2 = make()
     monkeypatch.setenv("ETD_FOLD2", "0")
     p1 = make()
-    monkeypatch.delenv("ETD_FOLD2")
+    monkeypatch.setenv("ETD_FOLD2", "1")
     monkeypatch.setenv("ETD_DENSE", "1")
     pd = make()
     monkeypatch.delenv("ETD_DENSE")
@@ -150,16 +156,17 @@ def test_fold2_sharded_virtual_ranks_bitwise(G):
 
 @pytest.mark.parametrize("dim", [2, 3])
 def test_fold2_pair_launches_bitwise_equal(dim, monkeypatch):
-    """ETD_PAIRS=1 issues every S = 4 transform launch as two S = 2 launches (fields
-    (0,1), (2,3); the mix pairs each species' (w1, w2)): the same per-element
-    contraction order, so the step is bitwise equal."""
+    """Every S = 4 transform launch runs as two S = 2 launches by default (fields
+    (0,1), (2,3); the mix pairs each species' (w1, w2)); ETD_PAIRS=0 keeps one S = 4
+    launch.  The same per-element contraction order, so the step is bitwise equal."""
     n = 63
     g = etd.unit_box_grid(dim, n + 1)
     rng = np.random.default_rng(40 + dim)
     u0, v0 = rng.uniform(-1, 1, n ** dim), rng.uniform(-0.5, 0.5, n ** dim)
     st = etd.SystemState(0, 0.0, u0, v0)
+    monkeypatch.setenv("ETD_PAIRS", "0")
     a = etd.etd2rkds_step_system(etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0), st, etd.fhn_cubic(), nsteps=2)
-    monkeypatch.setenv("ETD_PAIRS", "1")
+    monkeypatch.delenv("ETD_PAIRS")
     pp = etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0)
     assert any(s["name"].endswith("_b") for s in pp.stage_stats())
     b = etd.etd2rkds_step_system(pp, st, etd.fhn_cubic(), nsteps=2)
