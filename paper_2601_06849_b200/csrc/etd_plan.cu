@@ -2291,6 +2291,7 @@ int guarded(etd_handle* h, F&& f) {
         return ETD_ERR_MEMORY;
     } catch (const std::exception& e) {
         if (h) h->msg = e.what(); else g_create_error = e.what();
+        cudaGetLastError();  // a non-sticky launch/API error must not surface in the next call
         return ETD_ERR_CUDA;
     }
 }
@@ -2545,8 +2546,9 @@ int etd_debug_repeat_op(etd_handle* h, const char* name, int out, int reps, long
         for (const auto& o : p.steps[p.cur & 1])
             if ((o.kind == etd::Op::KERNEL || o.kind == etd::Op::SOURCE) && o.name == name) op = &o;
         if (!op || op->kind != etd::Op::KERNEL) throw etd::ConfigError("no such kernel op");
-        const long long F = op->L.args.out_stride;
-        const double* target = op->L.args.out + (size_t)out * F;
+        // outputs are out_stride apart (pair launches: 2 fields); each is one field
+        const long long F = p.slab.F;
+        const double* target = op->L.args.out + (size_t)out * op->L.args.out_stride;
         double* ref = nullptr;
         unsigned long long* cnt = nullptr;
         long long* dpos = nullptr;
