@@ -114,6 +114,8 @@ struct ContractArgs {
     double* out_rev;        // MODE 1 EPI_STORE: also store each output at x' = m_extent-1-x (FOLD 3 input)
     int kbase;              // FOLD 2/4/5: axis coordinate of the first A box (second-level split groups)
     int nbase;              // FOLD 2/4: first output position (second-level split groups)
+    int mix_w2;             // EPI_MIX: also store w2b (the first-level corrector's aux; the level-2
+                            // schedule subtracts w2 in physical space instead)
     int sd_out;             // FOLD 5: store the even-mode pairs as (sigma, delta) = (X_q + X_{h-1-q},
                             // X_q - X_{h-1-q}) at (q, H + q): the level-2 backward's input (EPI_MIX: the
                             // mix outputs only; w2b stays in mode positions for EPI_CORR)
@@ -618,7 +620,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                             if (c < NSD) {
                                 store(c, m, nb, vd[c][0] + vm[c][1], vd[c][1] + vm[c][0], true);
                                 store(c, m, args.fold_h + nb, vd[c][0] - vm[c][1], vd[c][1] - vm[c][0], true);
-                            } else {
+                            } else if (EPI != EPI_MIX || args.mix_w2) {
                                 store(c, m, nb, vd[c][0], vd[c][1], true);
                                 store(c, m, nm, vm[c][0], vm[c][1], true);
                             }
@@ -710,7 +712,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                         const double w10 = val(c, i, jp, 0), w11 = val(c, i, jp, 1);
                         const double w20 = val(S / 2 + c, i, jp, 0), w21 = val(S / 2 + c, i, jp, 1);
                         store(c, m, nb, da.x * w10 + db.x * w20, da.y * w11 + db.y * w21, two);
-                        store(S / 2 + c, m, nb, w20, w21, two);
+                        if (args.mix_w2) store(S / 2 + c, m, nb, w20, w21, two);
                     }
                 } else if constexpr (EPI == EPI_WHAT_SRC) {
                     double w[S][2];
@@ -1222,8 +1224,9 @@ __device__ void source_fold2_rows(const SourceArgs& a, double srcA, int nj, int&
 // pass finishes it: g_i = o_i + e_i, g_{n-1-i} = o_i - e_i (i < h - 1), g_{h-1} = o_{h-1},
 // with the stage's pointwise epilogue fused (x stage only):
 //   UF_STORE     g -> out (nf fields)
-//   UF_WHAT_SRC  What = g -> out; f(t + tau, What) with its checks (fail 2 / 5); f
-//                written as x_fwd_corr's level-2 stack into fout (etd_fold2 layout)
+//   UF_WHAT_SRC  What = g -> out; f(t + tau, What) with its checks (fail 2 / 5);
+//                f - w2 (aux: w2 in physical space) written as x_fwd_corr's level-2
+//                stack into fout (etd_fold2 layout)
 //   UF_UPDATE    U1 = aux + g -> out; check (fail 3); the last block commits the step
 // x: one thread per (row, orbit {k, n-1-k, 2H-2-k, 2H+k}); y/z (UF_STORE): 16-byte
 // x pairs per (outer, i).
@@ -1358,6 +1361,14 @@ static __global__ void __launch_bounds__(256) etd_unfold2(const Unfold2Args a) {
                 } else {
                     src2<SK>(a.sp, g[0][p], g[1][p], fv[0][p], fv[1][p]);
                     bad |= !(isfinite(fv[0][p]) && isfinite(fv[1][p]));
+                }
+            }
+            // fw - w2 in physical space (stepper.cpp:252; system_stepper.cpp:103): the
+            // corrector's operand, so x_fwd_corr is a plain scaled transform
+            if (a.aux) {
+                for (int s = 0; s < a.nf && s < 2; ++s) {
+                    const double* __restrict__ w2 = a.aux + s * a.Faux + row * a.pitch;
+                    for (int p = 0; p < np; ++p) fv[s][p] -= w2[pts[p]];
                 }
             }
             for (int s = 0; s < a.nf && s < 2; ++s) {

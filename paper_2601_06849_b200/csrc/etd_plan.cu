@@ -583,6 +583,7 @@ struct Plan {
         a.status = status;
         a.tau = tau;
         a.commit = sharded ? 0 : 1;
+        a.mix_w2 = 1;
         a.sinx = sintab[0];
         a.siny = sintab[1];
         a.sinz = dim == 3 ? sintab[2] : nullptr;
@@ -713,7 +714,7 @@ struct Plan {
         o.src_blocks = 148u * 16u;
         const double pts = (double)v.nx * v.ny * v.nz;
         o.L.flops = 0.0;
-        o.L.bytes = pts * 8.0 * nf * (uf == UF_STORE ? 2 : 3);
+        o.L.bytes = pts * 8.0 * nf * (uf == UF_STORE ? 2 : (uf == UF_WHAT_SRC && aux) ? 4 : 3);
         return o;
     }
 
@@ -1599,15 +1600,18 @@ static void build_plan(Plan& p, const etd_desc& d) {
             back2(V, "y_back", 1, 2 * ns, B2, B1, B2, UF_STORE);
             double *Xa = B2, *Xb = B1;
             const size_t Fs = (size_t)ns * V.F;
-            // x_fwd_mix: mix (sigma/delta) -> Xa[0, ns), w2b (mode positions) -> Xa[ns, 2ns)
+            // x_fwd_mix: mix (sigma/delta) -> Xa[0, ns); w2 stays in physical space at Xa[ns, 2ns)
+            const size_t mix0 = L.size();
             fwd2(V, "x_fwd_mix", 0, 2 * ns, EPI_MIX, Xa, Xb, Xa, false, p.dv(0, 0), p.dv(0, 1));
-            // x_back_src: What -> Xa[0, ns), f(t + tau, What) as x_fwd_corr's level-2 stack -> Xb[ns, 2ns)
-            back2(V, "x_back_src", 0, ns, Xa, Xb, Xa, UF_WHAT_SRC, nullptr, Xb + Fs);
+            for (size_t i = mix0; i < L.size(); ++i)
+                if (L[i].kind == Op::KERNEL) L[i].L.args.mix_w2 = 0;
+            // x_back_src: What -> Xa[0, ns); f(t + tau, What) - w2 (stepper.cpp:252) as
+            // x_fwd_corr's level-2 stack -> Xb[ns, 2ns)
+            back2(V, "x_back_src", 0, ns, Xa, Xb, Xa, UF_WHAT_SRC, Xa + Fs, Xb + Fs);
             for (int part = 1; part <= 2; ++part) {
                 L.push_back(kernel_op(p.transform(V, part == 1 ? "x_fwd_corr_even" : "x_fwd_corr_odd", 0, false, ns,
-                                                  EPI_CORR, false, Xb + Fs, Xb, false, nullptr, false, part)));
+                                                  EPI_SCALE, false, Xb + Fs, Xb, false, nullptr, false, part)));
                 L.back().L.args.dA = p.dv(0, 2);
-                L.back().L.args.aux = Xa + Fs;
             }
             // x_back_upd: U1 = What + tau Q3(fw) -> out (commits the step)
             back2(V, "x_back_upd", 0, ns, Xb, Xb + Fs, out, UF_UPDATE, Xa);

@@ -13,12 +13,12 @@ KernelSpec pick_fold2(int mode, int S, int epi, int sk, int tile, int fold) {
                : tile == 1 ? fold_spec<M, SS, E, K, 1, F>() : fold_spec<M, SS, E, K, 0, F>();
     if (fold == 5) {
         ETD_FSPEC(1, 1, EPI_SCALE, 0, 5) ETD_FSPEC(1, 2, EPI_SCALE, 0, 5) ETD_FSPEC(1, 4, EPI_SCALE, 0, 5)
-        ETD_FSPEC(0, 1, EPI_SCALE, 0, 5)
+        ETD_FSPEC(0, 1, EPI_SCALE, 0, 5) ETD_FSPEC(0, 2, EPI_SCALE, 0, 5)
         ETD_FSPEC(0, 2, EPI_MIX, 0, 5) ETD_FSPEC(0, 4, EPI_MIX, 0, 5)
         ETD_FSPEC(0, 1, EPI_CORR, 0, 5) ETD_FSPEC(0, 2, EPI_CORR, 0, 5)
     }
     if (fold == 4) {
-        ETD_FSPEC(1, 1, EPI_SCALE, 0, 4) ETD_FSPEC(0, 1, EPI_SCALE, 0, 4)
+        ETD_FSPEC(1, 1, EPI_SCALE, 0, 4) ETD_FSPEC(0, 1, EPI_SCALE, 0, 4) ETD_FSPEC(0, 2, EPI_SCALE, 0, 4)
         ETD_FSPEC(0, 2, EPI_MIX, 0, 4) ETD_FSPEC(0, 4, EPI_MIX, 0, 4)
         // level-2 backward, even modes: o from (sigma, delta) into the intermediate stack
         ETD_FSPEC(1, 1, EPI_STORE, 0, 4) ETD_FSPEC(1, 2, EPI_STORE, 0, 4) ETD_FSPEC(1, 4, EPI_STORE, 0, 4)
