@@ -1984,17 +1984,6 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
     ETD_CK(cudaStreamWaitEvent(p.cstream, ev_start, 0));
     auto rowb = [&](int c) { return c >= C ? R : R * c / C / 128 * 128; };  // x-stage row chunk bounds
     double* st_in = p.state[p.cur];
-    // ETD_TIMELINE=1: event timeline of the call on both streams (development aid)
-    const bool tl = std::getenv("ETD_TIMELINE") != nullptr;
-    std::vector<std::pair<std::string, cudaEvent_t>> tev;
-    auto mark = [&](const std::string& nm, cudaStream_t st) {
-        if (!tl) return;
-        cudaEvent_t e;
-        ETD_CK(cudaEventCreate(&e));
-        ETD_CK(cudaEventRecord(e, st));
-        tev.push_back({nm, e});
-    };
-    mark("start", p.stream);
     for (int c = 0; c < CX; ++c) {
         const int x0 = c * XW, x1 = std::min(V.nx, x0 + XW);
         for (int sp = 0; sp < p.ns; ++sp)
@@ -2002,7 +1991,6 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
                                      (size_t)V.nx * 8, (size_t)(x1 - x0) * 8, (size_t)R, cudaMemcpyHostToDevice,
                                      p.cstream));
         ETD_CK(cudaEventRecord(ev_in[c], p.cstream));
-        mark("h2d_" + std::to_string(c), p.cstream);
     }
     for (int s = 0; s < nsteps; ++s) {
         const auto& ops = p.steps[(p.cur + s) & 1];
@@ -2035,7 +2023,6 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
                         launch(L, p.stream);
                     }
                 }
-                mark("zy_" + std::to_string(c), p.stream);
             }
         } else {
             for (int k = 0; k < ix; ++k) run_op(p, ops[k], p.stream);
@@ -2072,7 +2059,6 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
                 launch(L, p.stream);
             }
             ETD_CK(cudaEventRecord(ev_out[c], p.stream));
-            mark("x_" + std::to_string(c), p.stream);
             ETD_CK(cudaStreamWaitEvent(p.cstream, ev_out[c], 0));
             for (int sp = 0; sp < p.ns; ++sp)
                 ETD_CK(cudaMemcpy2DAsync(hout[sp] + r0 * V.nx, (size_t)V.nx * 8,
@@ -2081,18 +2067,8 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
         }
         etd_commit<<<1, 1, 0, p.stream>>>(p.status, nullptr, 0, p.tau);
     }
-    mark("d2h_end", p.cstream);
     ETD_CK(cudaGetLastError());
     ETD_CK(cudaStreamSynchronize(p.cstream));
-    if (tl) {
-        ETD_CK(cudaStreamSynchronize(p.stream));
-        for (auto& [nm, e] : tev) {
-            float ms = 0;
-            ETD_CK(cudaEventElapsedTime(&ms, tev[0].second, e));
-            std::fprintf(stderr, "ETD_TIMELINE %s %.3f\n", nm.c_str(), ms);
-            cudaEventDestroy(e);
-        }
-    }
     finish_steps(p, n);
 }
 
