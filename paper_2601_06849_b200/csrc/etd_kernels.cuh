@@ -1345,7 +1345,18 @@ static __global__ void __launch_bounds__(256) etd_unfold2(const Unfold2Args a) {
                 }
             }
         } else {
-            // What, f(t + tau, What) at every orbit point, then f's level-2 stack
+            // What, f(t + tau, What) at every orbit point, then f's level-2 stack;
+            // w2 is loaded up front so its latency overlaps the o/e loads
+            double w2v[2][4] = {};
+            if (a.aux) {
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    if (s >= a.nf) break;
+                    const double* __restrict__ w2 = a.aux + s * a.Faux + row * a.pitch;
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) w2v[s][p] = p < np ? w2[pts[p]] : 0.0;
+                }
+            }
             double fv[2][5];
             const int jj = (int)(row % a.ny_local) + a.gj0, kz = (int)(row / a.ny_local) + a.gz0;
             for (int p = 0; p < np; ++p) {
@@ -1366,9 +1377,12 @@ static __global__ void __launch_bounds__(256) etd_unfold2(const Unfold2Args a) {
             // fw - w2 in physical space (stepper.cpp:252; system_stepper.cpp:103): the
             // corrector's operand, so x_fwd_corr is a plain scaled transform
             if (a.aux) {
-                for (int s = 0; s < a.nf && s < 2; ++s) {
-                    const double* __restrict__ w2 = a.aux + s * a.Faux + row * a.pitch;
-                    for (int p = 0; p < np; ++p) fv[s][p] -= w2[pts[p]];
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    if (s >= a.nf) break;
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+                        if (p < np) fv[s][p] -= w2v[s][p];
                 }
             }
             for (int s = 0; s < a.nf && s < 2; ++s) {
@@ -1410,6 +1424,73 @@ static __global__ void __launch_bounds__(256) etd_unfold2(const Unfold2Args a) {
                         a.status->t = (double)nn * a.tau;
                     }
                 }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------- fused z unfold + y stack
+// 3D second-level schedule, one GPU: z_back's finishing pass (etd_unfold2 along z)
+// and the y forward's stack pass (etd_fold2 along y) in one HBM pass.  A work item is
+// an x pair, a z pair (i, nz-1-i) and a y orbit {k, ny-1-k, 2Hy-2-k, 2Hy+k}: it reads
+// o, e at (z positions of i, 4 y points), forms g at 2 z x 4 y points and writes their
+// y butterflies.  Every element is read once and written once.
+struct ZYArgs {
+    const double* in;       // z_back's intermediate stack (z positions)
+    double* out;            // the y_fwd operand (y level-2 stack, z physical)
+    long long F, pitch, plane;
+    int nf, nx, ny, nz, Hz, Hy;
+    int x0, x1;
+};
+
+static __global__ void __launch_bounds__(256) etd_unfold_fold_zy(const ZYArgs a) {
+    const int Hz = a.Hz, Hy = a.Hy, hz = 2 * Hz, ny = a.ny, nz = a.nz;
+    const int items = (a.x1 - a.x0 + 1) / 2;
+    const long long total = (long long)hz * Hy * items;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int w = (int)(t % items);
+        const long long r = t / items;
+        const int k = (int)(r % Hy), i = (int)(r / Hy);
+        const int x = a.x0 + 2 * w;
+        const int c = 2 * Hy - 2 - k;
+        const int np = k == Hy - 1 ? 3 : 4;
+        const int ys[4] = {k, ny - 1 - k, k == Hy - 1 ? 2 * Hy - 1 : c, ny - 1 - c};
+        const bool zc = i == hz - 1;  // the z centre: one output plane
+        const int zo = fold2_spos(i, Hz), ze = 2 * Hz + i;
+        const int zs[2] = {i, nz - 1 - i};
+        for (int f = 0; f < a.nf; ++f) {
+            const double* src = a.in + f * a.F + x;
+            double* dst = a.out + f * a.F + x;
+            double2 g[2][4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                if (p >= np) break;
+                const double2 o = *reinterpret_cast<const double2*>(src + (long long)zo * a.plane + (long long)ys[p] * a.pitch);
+                if (zc) {
+                    g[0][p] = o;
+                } else {
+                    const double2 e = *reinterpret_cast<const double2*>(src + (long long)ze * a.plane + (long long)ys[p] * a.pitch);
+                    g[0][p] = o + e;
+                    g[1][p] = o - e;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (q == 1 && zc) break;
+                const double2* V = g[q];
+                auto get = [&](int yy) {
+                    return yy == k ? V[0] : yy == ny - 1 - k ? V[1] : (k == Hy - 1 ? V[2] : yy == c ? V[2] : V[3]);
+                };
+                double2 o[6];
+                fold2_orbit(k, Hy, false, get, o);
+                double* d = dst + (long long)zs[q] * a.plane;
+                auto put = [&](int yy, double2 v) { *reinterpret_cast<double2*>(d + (long long)yy * a.pitch) = v; };
+                put(fold2_spos(k, Hy), o[0]);
+                if (c != k) put(fold2_spos(c, Hy), o[1]);
+                put(2 * Hy + k, o[2]);
+                if (k == Hy - 1) put(2 * Hy - 1, o[4]);
+                else put(3 * Hy + k, o[3]);
             }
         }
     }

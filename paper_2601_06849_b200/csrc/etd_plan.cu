@@ -260,7 +260,7 @@ struct Piece {
 };
 
 struct Op {
-    enum Kind { KERNEL, SOURCE, COPY2D, EXCHANGE, FAILCODE, COMMIT, THOMAS, NOP, FOLD, UNFOLD } kind = KERNEL;
+    enum Kind { KERNEL, SOURCE, COPY2D, EXCHANGE, FAILCODE, COMMIT, THOMAS, NOP, FOLD, UNFOLD, ZYFOLD } kind = KERNEL;
     // sharded steps: 1 = run on the communication stream; events (indices into
     // Plan::sev) waited on before / recorded after the op (ignored by virtual ranks)
     int strm = 0, wait_ev = -1, rec_ev = -1;
@@ -269,6 +269,7 @@ struct Op {
     ThomasArgs targs{};                          // THOMAS
     Fold2Args fargs{};                           // FOLD (second-level split stack, etd_fold2)
     Unfold2Args uargs{};                         // UNFOLD (second-level backward finish, etd_unfold2)
+    ZYArgs zargs{};                              // ZYFOLD (z unfold + y stack, etd_unfold_fold_zy)
     int th_epi = 0;
     const void* src_fn = nullptr;                // SOURCE / THOMAS kernel
     unsigned src_blocks = 0;
@@ -1447,6 +1448,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
         // Second-level split (p.fold2_all): every forward transform is
         // an etd_fold2 stack (src -> tmp) and its even/odd-mode launches (tmp -> dst).
         const bool f2 = p.fold2_all;
+        bool zy_fused = false;  // unsharded 3D level 2: z_back's unfold + the y stack in one pass
         // S = 4 transform launches as two S = 2 launches (2 CTAs/SM overlap one CTA's
         // epilogue with the other's main loop; config 4 529.8 -> 521.1 ms/step,
         // config 3 42.0 -> 40.0); ETD_PAIRS=0 keeps the S = 4 launches
@@ -1516,8 +1518,30 @@ static void build_plan(Plan& p, const etd_desc& d) {
         };
         if (p.dim == 3 && !p.sharded) {
             first_transform(V, 2, const_cast<double*>(in), p.Z, p.W);
-            if (f2) back2(V, "z_back", 2, 2 * ns, p.Z, p.W, p.Z, UF_STORE);  // z-filtered stack in Z
-            else L.push_back(kernel_op(p.transform(V, "z_back", 2, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
+            if (f2) {
+                // z_back's launches (Z -> W), then its unfold fused with the y stack (W -> Z)
+                const bool pr = pairs && 2 * ns == 4;
+                for (int part = 3; part <= 4; ++part) {
+                    const std::string pn = std::string("z_back") + (part == 3 ? "_o" : "_e");
+                    for (int h2 = 0; h2 < (pr ? 2 : 1); ++h2)
+                        L.push_back(kernel_op(p.transform(V, pr ? pn + (h2 ? "_b" : "_a") : pn, 2, true,
+                                                          pr ? 2 : 2 * ns, EPI_STORE, false,
+                                                          p.Z + 2 * h2 * V.F, p.W + 2 * h2 * V.F, false, nullptr,
+                                                          false, part)));
+                }
+                Op zy;
+                zy.kind = Op::ZYFOLD;
+                zy.name = zy.L.name = "z_back_y_stack";
+                zy.L.mode = 1;
+                zy.zargs = ZYArgs{p.W, p.Z, (long long)V.F, V.pitch, V.plane, 2 * ns, V.nx, V.ny, V.nz,
+                                  p.fh[2] / 2, p.fh[1] / 2, 0, V.nx};
+                zy.src_blocks = 148u * 16u;
+                zy.L.bytes = (double)V.nx * V.ny * V.nz * 8.0 * 2 * 2 * ns;
+                L.push_back(zy);
+                zy_fused = true;
+            } else {
+                L.push_back(kernel_op(p.transform(V, "z_back", 2, true, 2 * ns, EPI_STORE, false, p.Z, p.W)));
+            }
         } else if (p.dim == 3) {
             // ---- z stage on y-row chunks: pack; forward exchanges (comm stream);
             // per chunk source + z transforms (compute stream) overlapping the next
@@ -1591,7 +1615,11 @@ static void build_plan(Plan& p, const etd_desc& d) {
             // on (Xa, Xb) = (B2, B1); the z stage left its output in Z (unsharded) or the
             // unpack in W (sharded)
             double *B1 = p.W, *B2 = p.Z;
-            if (p.dim == 3) {
+            if (zy_fused) {
+                // the y stack is already in Z: y_fwd Z -> W, y_back W -> (Z) -> W
+                B1 = p.Z, B2 = p.W;
+                fwd2(V, "y_fwd", 1, 2 * ns, EPI_SCALE, nullptr, B1, B2, false, p.dv(1, 0), nullptr, nullptr, true);
+            } else if (p.dim == 3) {
                 if (p.sharded) B1 = p.Z, B2 = p.W;
                 fwd2(V, "y_fwd", 1, 2 * ns, EPI_SCALE, B2, B1, B2, false, p.dv(1, 0));
             } else {
@@ -1668,7 +1696,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
     p.stats.clear();
     for (auto& op : p.steps[0])
         if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS || op.kind == Op::FOLD ||
-            op.kind == Op::UNFOLD)
+            op.kind == Op::UNFOLD || op.kind == Op::ZYFOLD)
             p.stats.push_back({op.L.name, 0, 0, op.L.flops, op.L.bytes, op.L.dense_flops});
     ETD_CK(cudaStreamSynchronize(p.stream));
 }
@@ -1711,6 +1739,12 @@ static void run_op_body(Plan& p, const Op& op, cudaStream_t s) {
     case Op::FOLD: {
         void* args[1] = {const_cast<Fold2Args*>(&op.fargs)};
         ETD_CK(cudaLaunchKernel(reinterpret_cast<const void*>(etd_fold2), dim3(op.src_blocks), dim3(256), args, 0, s));
+        break;
+    }
+    case Op::ZYFOLD: {
+        void* args[1] = {const_cast<ZYArgs*>(&op.zargs)};
+        ETD_CK(cudaLaunchKernel(reinterpret_cast<const void*>(etd_unfold_fold_zy), dim3(op.src_blocks), dim3(256),
+                                args, 0, s));
         break;
     }
     case Op::UNFOLD: {
@@ -1825,7 +1859,7 @@ static void do_steps(Plan& p, int nsteps) {
                 if (!p.profiling) continue;
                 const size_t e = rec();
                 if (op.kind == Op::KERNEL || op.kind == Op::SOURCE || op.kind == Op::THOMAS || op.kind == Op::FOLD ||
-                    op.kind == Op::UNFOLD)
+                    op.kind == Op::UNFOLD || op.kind == Op::ZYFOLD)
                     spans.push_back({prev, kidx++});
                 prev = e;
             }
@@ -1937,7 +1971,9 @@ static bool overlap_eligible(const Plan& p, int nsteps) {
     if (ix <= 0 || ops.back().L.name != "x_back_upd") return false;
     for (int k = 0; k < (int)ops.size(); ++k) {
         const Op& op = ops[k];
-        if (op.kind != Op::KERNEL && op.kind != Op::SOURCE && op.kind != Op::FOLD && op.kind != Op::UNFOLD) return false;
+        if (op.kind != Op::KERNEL && op.kind != Op::SOURCE && op.kind != Op::FOLD && op.kind != Op::UNFOLD &&
+            op.kind != Op::ZYFOLD)
+            return false;
         if (op.kind != Op::SOURCE && op.L.mode != (k < ix ? 1 : 0)) return false;
         if (op.kind == Op::SOURCE && k >= ix) return false;
     }
@@ -2015,6 +2051,11 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
                         Op o = ops[k];
                         o.uargs.x0 = x0;
                         o.uargs.x1 = x1;
+                        run_op(p, o, p.stream);
+                    } else if (ops[k].kind == Op::ZYFOLD) {
+                        Op o = ops[k];
+                        o.zargs.x0 = x0;
+                        o.zargs.x1 = x1;
                         run_op(p, o, p.stream);
                     } else {
                         Launch L = ops[k].L;
