@@ -5,4 +5,4 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; tail -2 gpurun_out/bench.err
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu --no-alt --e2e-steps 1 > gpurun_out/ncu_launch.log 2>&1; echo "ncu list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:etd_contract -s 23 -c 1 -o gpurun_out/xcorr_odd python tools/one_step.py 4 > gpurun_out/ncu_full6.log 2>&1; echo "ncu full6 rc=$?"; tail -2 gpurun_out/ncu_full6.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:etd_contract -s 24 -c 1 -o gpurun_out/xcorr_odd_final python tools/one_step.py 4 > gpurun_out/ncu_full6.log 2>&1; echo "ncu full6 rc=$?"; tail -2 gpurun_out/ncu_full6.log
