@@ -171,3 +171,42 @@ def test_fold2_pair_launches_bitwise_equal(dim, monkeypatch):
     assert any(s["name"].endswith("_b") for s in pp.stage_stats())
     b = etd.etd2rkds_step_system(pp, st, etd.fhn_cubic(), nsteps=2)
     assert np.array_equal(a.U, b.U) and np.array_equal(a.V, b.V)
+
+
+@pytest.mark.parametrize("shape", [(63, 95, 31), (95, 31, 63), (31, 63, 127)])
+def test_fold2_non_cubic_system_vs_dense(shape, monkeypatch):
+    """Different H per axis (8, 16, 24, 32): the fused z unfold + y stack pass and the
+    x / y stack passes index each axis with its own H.  Compared with the dense path
+    (itself pinned to the reference on non-cubic grids, test_gpu_parity.py)."""
+    g = etd.build_grid(3, [(0, 1)] * 3, [s + 1 for s in shape])
+    N = int(np.prod(shape))
+    rng = np.random.default_rng(sum(shape))
+    u0, v0 = rng.uniform(-1, 1, N), rng.uniform(-0.5, 0.5, N)
+    p = etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0)
+    assert p.fold_level() == (2, 2, 2)
+    assert any(s["name"] == "z_back_y_stack" for s in p.stage_stats())
+    got = etd.etd2rkds_step_system(p, etd.SystemState(0, 0.0, u0, v0), etd.fhn_cubic(), nsteps=3)
+    monkeypatch.setenv("ETD_DENSE", "1")
+    pd = etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0)
+    d = etd.etd2rkds_step_system(pd, etd.SystemState(0, 0.0, u0, v0), etd.fhn_cubic(), nsteps=3)
+    assert rel_gap(d.U, got.U) <= 1e-13 and rel_gap(d.V, got.V) <= 1e-13
+
+
+@pytest.mark.parametrize("shape", [(127, 95, 63), (95, 63, 1)])
+def test_fold2_pipelined_advance_ragged_chunks_bitwise(shape):
+    """etd_advance (column-chunked z / y stages, row-chunked x stage) on the level-2
+    schedule equals upload + etd_step + download bitwise, 3D and 2D."""
+    nx, ny, nz = shape
+    dim = 3 if nz > 1 else 2
+    g = etd.build_grid(dim, [(0, 1)] * dim, [s + 1 for s in shape[:dim]])
+    N = nx * ny * nz
+    rng = np.random.default_rng(N)
+    u0, v0 = rng.uniform(-1, 1, N), rng.uniform(-0.5, 0.5, N)
+    f = etd.fhn_cubic()
+    plan = etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0)
+    assert plan.fold_level() == (2,) * dim
+    st = etd.etd2rkds_step_system(plan, etd.SystemState(0, 0.0, u0, v0), f, nsteps=2)
+    plan.upload(0, u0)
+    plan.upload(1, v0)
+    plan.step(2)
+    assert np.array_equal(plan.download(0)[0], st.U) and np.array_equal(plan.download(1)[0], st.V)
