@@ -1301,7 +1301,7 @@ static __global__ void __launch_bounds__(256) etd_unfold2(const Unfold2Args a) {
         const int np = k == H - 1 ? 3 : 4;
         int pts[5] = {k, n - 1 - k, c, n - 1 - c, 2 * H - 1};
         if (k == H - 1) pts[2] = 2 * H - 1;  // slots 0, 1, 2 = k, n-1-k, centre
-        const int nloop = UF == UF_STORE ? a.nf : a.nf;
+        const int nloop = a.nf;
         double g[NS][5];
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
@@ -1459,26 +1459,31 @@ static __global__ void __launch_bounds__(256) etd_unfold_fold_zy(const ZYArgs a)
         const bool zc = i == hz - 1;  // the z centre: one output plane
         const int zo = fold2_spos(i, Hz), ze = 2 * Hz + i;
         const int zs[2] = {i, nz - 1 - i};
-        for (int f = 0; f < a.nf; ++f) {
-            const double* src = a.in + f * a.F + x;
-            double* dst = a.out + f * a.F + x;
-            double2 g[2][4];
+        // two fields per pass: all 16 loads are issued before any store
+        for (int f0 = 0; f0 < a.nf; f0 += 2) {
+            double2 g[2][2][4];
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                if (p >= np) break;
-                const double2 o = *reinterpret_cast<const double2*>(src + (long long)zo * a.plane + (long long)ys[p] * a.pitch);
-                if (zc) {
-                    g[0][p] = o;
-                } else {
-                    const double2 e = *reinterpret_cast<const double2*>(src + (long long)ze * a.plane + (long long)ys[p] * a.pitch);
-                    g[0][p] = o + e;
-                    g[1][p] = o - e;
+            for (int ff = 0; ff < 2; ++ff) {
+                const double* __restrict__ src = a.in + (f0 + ff) * a.F + x;
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    if (p >= np) break;
+                    const double2 o =
+                        *reinterpret_cast<const double2*>(src + (long long)zo * a.plane + (long long)ys[p] * a.pitch);
+                    const double2 e = zc ? make_double2(0.0, 0.0)
+                                         : *reinterpret_cast<const double2*>(src + (long long)ze * a.plane +
+                                                                             (long long)ys[p] * a.pitch);
+                    g[ff][0][p] = zc ? o : o + e;  // the centre plane is o itself (bitwise as etd_unfold2)
+                    g[ff][1][p] = o - e;
                 }
             }
 #pragma unroll
+            for (int ff = 0; ff < 2; ++ff)
+#pragma unroll
             for (int q = 0; q < 2; ++q) {
                 if (q == 1 && zc) break;
-                const double2* V = g[q];
+                double* __restrict__ dst = a.out + (f0 + ff) * a.F + x;
+                const double2* V = g[ff][q];
                 auto get = [&](int yy) {
                     return yy == k ? V[0] : yy == ny - 1 - k ? V[1] : (k == Hy - 1 ? V[2] : yy == c ? V[2] : V[3]);
                 };
