@@ -1952,7 +1952,15 @@ static void group_steps(std::vector<Plan*>& ps, int nsteps) {
 // host<->device copies pipelined against compute (advance_overlapped below); the
 // step commit moves to one etd_commit after the chunks.  Everything else takes
 // set_state / etd_step / get_state.
-static constexpr int kXferChunks = 32;
+// transfer chunks of the pipelined advance; config 4 e2e per chunk count (1 step):
+// 6: 745, 8: 727, 12: 713, 16: 714-716, 24: 709, 32: 754, 64: 783 ms
+static constexpr int kXferChunks = 16;
+static constexpr int kXferChunksMax = 128;
+static int xfer_chunks() {  // ETD_XFER_CHUNKS: A/B of the transfer chunk count (default 32)
+    const char* e = std::getenv("ETD_XFER_CHUNKS");
+    const int c = e ? std::atoi(e) : kXferChunks;
+    return std::max(1, std::min(kXferChunksMax, c));
+}
 
 // Index of the first x-stage op.  Everything before it (the source pass and the
 // z / y stages) treats x as a batch index, so it can run on x-column ranges.
@@ -1999,18 +2007,19 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
     int bm = 32;
     for (int k = 0; k < ix; ++k)
         if (p.steps[0][k].kind == Op::KERNEL) bm = std::max(bm, p.steps[0][k].L.k.bm);
-    const int XW = round_up((V.nx + kXferChunks - 1) / kXferChunks, bm);
+    const int NX = xfer_chunks();
+    const int XW = round_up((V.nx + NX - 1) / NX, bm);
     const int CX = (V.nx + XW - 1) / XW;
     const long long R = (long long)V.ny * V.nz;
-    const int C = (int)std::max(1LL, std::min<long long>(kXferChunks, R / 128));
+    const int C = (int)std::max(1LL, std::min<long long>(NX, R / 128));
     if (!p.cstream) {
         ETD_CK(cudaStreamCreateWithFlags(&p.cstream, cudaStreamNonBlocking));
-        p.xev.resize(2 * kXferChunks + 1);
+        p.xev.resize(2 * kXferChunksMax + 1);
         for (auto& e : p.xev) ETD_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     cudaEvent_t* ev_in = p.xev.data();
-    cudaEvent_t* ev_out = p.xev.data() + kXferChunks;
-    cudaEvent_t ev_start = p.xev[2 * kXferChunks];
+    cudaEvent_t* ev_out = p.xev.data() + kXferChunksMax;
+    cudaEvent_t ev_start = p.xev[2 * kXferChunksMax];
     p.status_host->n = n;
     p.status_host->t = t;
     p.status_host->fail = 0;
