@@ -1535,6 +1535,8 @@ static void build_plan(Plan& p, const etd_desc& d) {
                 zy.L.mode = 1;
                 zy.zargs = ZYArgs{p.W, p.Z, (long long)V.F, V.pitch, V.plane, 2 * ns, V.nx, V.ny, V.nz,
                                   p.fh[2] / 2, p.fh[1] / 2, 0, V.nx};
+                // etd_unfold_fold_zy moves two fields per work item (f0, f0 + 1)
+                if (zy.zargs.nf % 2 != 0) throw ConfigError("internal: z_back_y_stack needs an even field count");
                 zy.src_blocks = 148u * 16u;
                 zy.L.bytes = (double)V.nx * V.ny * V.nz * 8.0 * 2 * 2 * ns;
                 L.push_back(zy);
@@ -1582,6 +1584,11 @@ static void build_plan(Plan& p, const etd_desc& d) {
                 f.rec_ev = EV_F(k);
                 L.push_back(f);
             }
+            // ops a populated chunk emits: source (unless fused) + z_fwd launches + z_back
+            // launches (+ the level-2 unfold); an empty chunk pads with as many no-ops so
+            // every rank's op list stays aligned with rank 0's (group_steps, NCCL groups)
+            const int zl = (f2 && pairs && 2 * ns == 4) ? 2 : 1;  // launches per level-2 part
+            const int chunk_ops = fused ? 2 : f2 ? 1 + 2 * zl + 2 * zl + 1 : 3;
             for (int k = 0; k < C; ++k) {
                 const View& vk = p.zch[k];
                 const size_t first = L.size();
@@ -1592,9 +1599,12 @@ static void build_plan(Plan& p, const etd_desc& d) {
                     first_transform(vk, 2, zin_k, zz_k, wz_k);
                     if (f2) back2(vk, "z_back", 2, 2 * ns, zz_k, zin_k, wz_k, UF_STORE);
                     else L.push_back(kernel_op(p.transform(vk, "z_back", 2, true, 2 * ns, EPI_STORE, false, zz_k, wz_k)));
+                    if ((int)(L.size() - first) != chunk_ops)
+                        throw ConfigError("internal: z-chunk op count " + std::to_string(L.size() - first) +
+                                          " != " + std::to_string(chunk_ops));
                 } else {
                     // an empty chunk keeps the op list aligned across virtual ranks
-                    for (int i = 0; i < (fused ? 2 : f2 ? 6 : 3); ++i) {
+                    for (int i = 0; i < chunk_ops; ++i) {
                         Op o;
                         o.kind = Op::NOP;
                         o.name = "z_empty";
@@ -1896,6 +1906,12 @@ static void group_steps(std::vector<Plan*>& ps, int nsteps) {
     }
     if (nsteps < 0) throw ConfigError("nsteps must be >= 0");
     if (nsteps == 0) return;
+    for (int r = 1; r < G; ++r)
+        for (int par = 0; par < 2; ++par)
+            if (ps[r]->steps[par].size() != ps[0]->steps[par].size())
+                throw ConfigError("internal: virtual rank " + std::to_string(r) + " has " +
+                                  std::to_string(ps[r]->steps[par].size()) + " ops per step, rank 0 has " +
+                                  std::to_string(ps[0]->steps[par].size()));
     cudaStream_t s = ps[0]->stream;
     for (auto* p : ps) ETD_CK(cudaStreamSynchronize(p->stream));
     std::vector<long long> before(G);
@@ -1956,7 +1972,7 @@ static void group_steps(std::vector<Plan*>& ps, int nsteps) {
 // 6: 745, 8: 727, 12: 713, 16: 714-716, 24: 709, 32: 754, 64: 783 ms
 static constexpr int kXferChunks = 16;
 static constexpr int kXferChunksMax = 128;
-static int xfer_chunks() {  // ETD_XFER_CHUNKS: A/B of the transfer chunk count (default 32)
+static int xfer_chunks() {  // ETD_XFER_CHUNKS: A/B of the transfer chunk count (default kXferChunks)
     const char* e = std::getenv("ETD_XFER_CHUNKS");
     const int c = e ? std::atoi(e) : kXferChunks;
     return std::max(1, std::min(kXferChunksMax, c));
@@ -2216,18 +2232,24 @@ static void load_snapshot(Plan& p, int species, const char* path, long n) {
         (int)hdr[4] != (p.dim == 3 ? v.nz : 1))
         throw ConfigError(std::string(path) + ": snapshot shape does not match plan grid");
     if (std::fread(&t, 8, 1, fp) != 1) throw ConfigError(std::string(path) + ": truncated snapshot");
-    double* dst = p.state[p.cur] + (size_t)species * v.F;
+    // staged in the step scratch (free between steps; pads zero like the state's), so a
+    // truncated or non-finite file leaves the live state untouched (the reference's
+    // load_field has no side effects on failure, field.cpp:59-81)
+    double* stage = p.Z;
     const size_t rows = (size_t)v.ny * v.nz, per = std::max<size_t>(1, (32u << 20) / v.nx);
     PinnedBuf buf(per * v.nx);
+    ETD_CK(cudaMemsetAsync(stage, 0, (size_t)v.F * 8, p.stream));
     for (size_t r0 = 0; r0 < rows; r0 += per) {
         const size_t nr = std::min(per, rows - r0);
         if (std::fread(buf.ptr, 8, nr * v.nx, fp) != nr * v.nx)
             throw ConfigError(std::string(path) + ": truncated snapshot");
-        ETD_CK(cudaMemcpy2DAsync(dst + r0 * v.pitch, v.pitch * 8, buf.ptr, (size_t)v.nx * 8, (size_t)v.nx * 8, nr,
+        ETD_CK(cudaMemcpy2DAsync(stage + r0 * v.pitch, v.pitch * 8, buf.ptr, (size_t)v.nx * 8, (size_t)v.nx * 8, nr,
                                  cudaMemcpyHostToDevice, p.stream));
         ETD_CK(cudaStreamSynchronize(p.stream));
     }
-    if (!field_finite(p, dst)) throw NumericsError(std::string(path) + ": snapshot has non-finite entries");
+    if (!field_finite(p, stage)) throw NumericsError(std::string(path) + ": snapshot has non-finite entries");
+    double* dst = p.state[p.cur] + (size_t)species * v.F;
+    ETD_CK(cudaMemcpyAsync(dst, stage, (size_t)v.F * 8, cudaMemcpyDeviceToDevice, p.stream));
     // a snapshot carries t only; restart at n = round(t / tau) unless given
     p.status_host->n = n >= 0 ? n : (long long)std::llround(t / p.tau);
     p.status_host->t = t;

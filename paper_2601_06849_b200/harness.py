@@ -1,5 +1,4 @@
-"""Study-harness loops over the device stepper (reference harness.cpp:157-421,
-timing.cpp:140-211).
+"""Study-harness loops over the device stepper (reference harness.cpp:157-421).
 
 The reference's convergence study drives `advance` from host loops and copies a
 snapshot Field at every coarse time.  Here the state stays device-resident
@@ -484,49 +483,3 @@ def write_manifest(path: str, spec: ProblemSpec, rep: ConvergenceReport, coarse:
         lines.append(f"reference_N={spec.reference_N}")
     with open(path, "w") as f:
         f.write("\n".join(lines) + "\n" + extra)
-
-
-def run_timing_scaling(problem: str = "allen-cahn-2d", ms: Optional[List[int]] = None, tau: float = 1.0 / 32.0,
-                       repeats: int = 3, out: Optional[str] = None, params: Optional[ProblemParams] = None,
-                       T: Optional[float] = None) -> str:
-    """timing.cpp:140-211 on the device: median wall time of the N = T/tau steps
-    per grid size, Pade family and backend, as the CSV
-    "m,backend,scheme,seconds,per_step_seconds" (written to <out>/timing_<problem>.csv).
-    The state stays device resident for the N steps (one upload per repeat).  The
-    reference's non-sliced banded variant has no device implementation and is
-    not listed."""
-    p = params or ProblemParams()
-    if T is not None:
-        p = ProblemParams(**{**p.__dict__, "T": T})
-    spec = problem_by_name(problem, p)
-    if spec.system:
-        raise etd.ConfigError("the timing table covers scalar problems only")
-    N = int(round(spec.T / tau))
-    if N < 1 or abs(N * tau - spec.T) > 1e-9 * spec.T:
-        raise etd.ConfigError("tau must divide the final time")
-    ms = ms or ([16, 32, 64, 128, 256, 512] if spec.dim == 2 else [16, 32, 64, 128])
-    rows = ["m,backend,scheme,seconds,per_step_seconds"]
-    for m in ms:
-        grid = etd.unit_box_grid(spec.dim, m)
-        u0 = spec.initial(grid)
-        for fam in (etd.PadeFamily.P02, etd.PadeFamily.P04):
-            for label, backend in (("spectral", etd.BackendKind.Spectral), ("thomas", etd.BackendKind.Thomas)):
-                plan = _plan(spec, grid, tau, fam, backend)
-                try:
-                    plan.set_source(spec.source)
-                    samples = []
-                    for _ in range(max(1, repeats)):
-                        plan.upload(0, u0, 0, 0.0)
-                        t0 = time.perf_counter()
-                        plan.step(N)
-                        samples.append(time.perf_counter() - t0)
-                finally:
-                    plan.close()
-                sec = sorted(samples)[len(samples) // 2]
-                rows.append(f"{m},{label},{_family_name(fam)},{_g6(sec)},{_g6(sec / N)}")
-    text = "\n".join(rows) + "\n"
-    if out:
-        os.makedirs(out, exist_ok=True)
-        with open(os.path.join(out, f"timing_{spec.name}.csv"), "w") as f:
-            f.write(text)
-    return text

@@ -154,6 +154,29 @@ def test_fold2_sharded_virtual_ranks_bitwise(G):
     assert np.array_equal(u, want.U) and np.array_equal(v, want.V)
 
 
+@pytest.mark.parametrize("G,chunks", [(2, "40"), (3, "13")])
+def test_fold2_sharded_empty_chunks_bitwise(G, chunks, monkeypatch):
+    """More z-stage chunks than a rank has y rows (ETD_ZCHUNKS > rows per rank) with
+    the level-2 split forced and two species: empty chunks must pad the op list with
+    exactly as many no-ops as a populated chunk emits (source + 4 + 4 launches +
+    unfold with pair launches), or the virtual ranks' op lists misalign."""
+    from test_gpu_sharded import run_sharded
+    monkeypatch.setenv("ETD_FOLD2", "1")
+    monkeypatch.setenv("ETD_ZCHUNKS", chunks)
+    n = 31
+    grid = etd.unit_box_grid(3, n + 1)
+    rng = np.random.default_rng(10 + G)
+    u0, v0 = rng.uniform(-1, 1, n ** 3), rng.uniform(-0.5, 0.5, n ** 3)
+    f = etd.fhn_cubic()
+    make = lambda **kw: etd.SystemPlan(grid, 0.05, 1e-3, 5e-4, 0.0, source=f, **kw)
+    single = make()
+    assert single.fold_level() == (2, 2, 2)
+    want = etd.etd2rkds_step_system(single, etd.SystemState(0, 0.0, u0, v0), f, nsteps=2)
+    (u, v), nn, _ = run_sharded(make, G, [u0, v0], 2, grid, f)
+    assert nn == 2
+    assert np.array_equal(u, want.U) and np.array_equal(v, want.V)
+
+
 @pytest.mark.parametrize("dim", [2, 3])
 def test_fold2_pair_launches_bitwise_equal(dim, monkeypatch):
     """Every S = 4 transform launch runs as two S = 2 launches by default (fields

@@ -71,20 +71,3 @@ def test_cached_reference_trajectory_is_used(tmp_path):
     E_cached = harness.run_convergence(spec, 16, [16], coarse=16, out=out)[0].E
     E_fresh = harness.run_convergence(spec, 16, [16], coarse=16)[0].E
     assert abs(E_cached - E_fresh) > 5e-4
-
-
-def test_timing_table(tmp_path):
-    """timing.cpp:140-211: one row per (m, scheme, backend) with positive times."""
-    text = harness.run_timing_scaling("allen-cahn-2d", ms=[16, 32], repeats=2, out=str(tmp_path))
-    lines = text.strip().splitlines()
-    assert lines[0] == "m,backend,scheme,seconds,per_step_seconds"
-    rows = [l.split(",") for l in lines[1:]]
-    assert len(rows) == 2 * 2 * 2
-    assert {(r[0], r[1], r[2]) for r in rows} == {(m, b, s) for m in ("16", "32") for b in ("spectral", "thomas")
-                                                  for s in ("p02", "p04")}
-    assert all(float(r[3]) > 0 and abs(float(r[4]) * 32 - float(r[3])) <= 1e-3 * float(r[3]) + 1e-9 for r in rows)
-    assert open(tmp_path / "timing_allen-cahn-2d.csv").read() == text
-    with pytest.raises(etd.ConfigError):
-        harness.run_timing_scaling("fhn-2d")
-    with pytest.raises(etd.ConfigError):
-        harness.run_timing_scaling("allen-cahn-2d", tau=0.3)

@@ -58,3 +58,27 @@ def test_snapshot_guards(tmp_path):
     (tmp_path / "junk.etrd").write_bytes(b"NOPE" + b"\0" * 64)
     with pytest.raises(etd.ConfigError):
         plan.load_snapshot(0, str(tmp_path / "junk.etrd"))
+
+
+def test_failed_load_leaves_state_untouched(tmp_path):
+    """A truncated or non-finite snapshot raises and leaves the device state, n and
+    t as they were (the reference's load_field has no side effects on failure)."""
+    g = etd.unit_box_grid(3, 12)
+    plan = etd.make_plan(g, 0.01, 1.0, 1.0)
+    u0 = np.random.default_rng(3).uniform(-1, 1, 11 ** 3)
+    plan.upload(0, u0, 4, 0.04)
+    good = str(tmp_path / "good.etrd")
+    plan.save_snapshot(0, good)
+    raw = open(good, "rb").read()
+    trunc = str(tmp_path / "trunc.etrd")
+    open(trunc, "wb").write(raw[: len(raw) - 8 * 200])
+    nanf = str(tmp_path / "nan.etrd")
+    body = np.frombuffer(raw[32:], dtype=np.float64).copy()
+    body[-1] = np.nan
+    open(nanf, "wb").write(raw[:32] + body.tobytes())
+    plan.upload(0, 0.5 * u0, 9, 0.09)
+    for path, exc in ((trunc, etd.ConfigError), (nanf, etd.NumericsError)):
+        with pytest.raises(exc):
+            plan.load_snapshot(0, path)
+        u, n, t = plan.download(0)
+        assert np.array_equal(u, 0.5 * u0) and n == 9 and t == pytest.approx(0.09)
