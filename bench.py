@@ -8,7 +8,14 @@ transforms each).  Metric: grid-point updates per second
 (one species value advanced one step), FP64.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--config C] [--n N] [--no-cpu]
+                  [--config C] [--n N] [--no-cpu] [--dry-run]
+
+--gpus N > 1 without torchrun's WORLD_SIZE in the environment re-launches this
+script as N ranks (torch.distributed.run, one process per GPU, 127.0.0.1
+rendezvous); under torchrun each rank shards config 4's z-slabs over NCCL.
+--dry-run does no device work: the ranks rendezvous over gloo, check the
+per-rank device-memory budget of the sharded plan (etd_plan_device_bytes) and
+rank 0 prints the line it would measure with (n_gpus, parallelism, ranks seen).
 
 --impl reference times the reference's own CPU implementation (oracle/_ref,
 the unmodified etdrd core + OpenBLAS) on this host's cores, as a bounded
@@ -30,6 +37,19 @@ sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.19  # measured DMMA.8x8x4 peak, profiles/r01_fp64_peak.jsonl (MEASURED_PEAKS has no FP64)
 FP64_PEAK_NOTE = "measured: tools/fp64_peak.cu DMMA m8n8k4 sustained on this pool's B200 (profiles/r01_fp64_peak.jsonl)"
+
+
+def hbm_peak():
+    """HBM roofline denominator: MEASURED_PEAKS.json's hbm_gbs (driver-measured copy
+    bandwidth on this pool), else B200_PROFILING.md's stated fallback."""
+    try:
+        v = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"
+    except (OSError, ValueError, KeyError, TypeError):
+        return 6650.0, "of fallback: B200_PROFILING.md 6.65 TB/s (MEASURED_PEAKS.json absent)"
+
+
+HBM_PEAK_GBS, HBM_PEAK_NOTE = hbm_peak()
 
 
 def env_int(k, d):
@@ -180,6 +200,9 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
         dist.broadcast_object_list(obj, src=0)
         kw = {"world_size": world, "rank": rank, "nccl_id": obj[0]}
     plan = configs.make_plan(cfg, n, device=local_rank, **kw)
+    comm_ranks = plan.comm_ranks()  # ncclCommCount of the plan's communicator when sharded
+    from paper_2601_06849_b200 import etd as E
+    dev_bytes = E.plan_device_bytes(plan.grid, cfg.nspecies, world, rank)
     t0 = time.time()
     ics = configs.initial_state(cfg, n, z0=plan.slab[0], z1=plan.slab[1] if cfg.dim == 3 else None)
     t_ic = time.time() - t0
@@ -262,10 +285,18 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
                     "dense_equiv_tflops": round(st.get("dense_flops_per_launch", 0) / (a * 1e-3) * 1e-12, 2)}
         gbs = st["bytes_per_launch"] / (a * 1e-3) * 1e-9
         return {"name": st["name"], "ms": round(a, 3), "bound": "hbm", "gbs": round(gbs, 1),
-                "frac": round(gbs / 6552.0, 4)}
+                "frac": round(gbs / HBM_PEAK_GBS, 4)}
 
+    dense_ach = dom.get("dense_flops_per_launch", dom["flops_per_launch"]) / (dom_ms * 1e-3) * 1e-12
     roofline = {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic, "traffic_stage": traffic_stage,
+                "basis": "executed",
+                "basis_note": ("achieved = the FLOPs the launch executes (the DST-I parity split runs a quarter of "
+                               "the dense 2n per point per transform) / its event-timed duration; "
+                               "dense_equiv_achieved = SURVEY 8(d)'s dense count over the same time (exceeds the "
+                               "peak by construction); executed FLOP = 512 x DMMA.8x8x4 instructions "
+                               "(profiles/r02_ncu_dmma_counts_cfg3.md)"),
+                "dense_equiv_achieved": round(dense_ach, 3),
                 "kernel": dom["name"],
                 "peak_source": FP64_PEAK_NOTE,
                 "algorithmic_flops_per_launch": dom["flops_per_launch"],
@@ -284,7 +315,7 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
                                "fold_* stages are the HBM-bound stack passes of the second-level split"),
                 "stages": [stage_line(a, st) for a, st in per],
                 "non_kernel_ms_per_step": round(comm_ms, 3),
-                "hbm_peak_gbs": 6552.0}
+                "hbm_peak_gbs": HBM_PEAK_GBS, "hbm_peak_source": HBM_PEAK_NOTE}
 
     # ---- e2e through the public API: pinned host in -> step -> pinned host out ----
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
@@ -320,12 +351,42 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
            "d2h_bytes_per_step": bytes_io, "ms_per_step": e2e_ms,
            "api": "etd_advance(pinned host U,V in -> 1 step -> pinned host U,V out)"}
     finite = bool(np.all(np.isfinite(hout[0].numpy())))
+    del hin, hout
+
+    # ---- e2e through the reference-shaped value API on plain (pageable) numpy
+    # arrays: etd2rkds_step_system / advance allocate the output state per call,
+    # as the reference's advance returns a new Field (stepper.hpp:85-86) ----
+    e2e_pageable = None
+    if world == 1 and args.e2e_pageable:
+        from paper_2601_06849_b200 import etd as E
+        src = cfg.source
+
+        def pageable_step():
+            if cfg.nspecies == 1:
+                return E.advance(plan, E.StepperState(0, 0.0, ics[0]), src)
+            return E.etd2rkds_step_system(plan, E.SystemState(0, 0.0, ics[0], ics[1]), src)
+
+        r = pageable_step()  # warm: allocates the plan's pinned mirror once
+        del r
+        barrier()
+        w0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            r = pageable_step()
+            del r
+        barrier()
+        pg_ms = (time.perf_counter() - w0) / e2e_steps * 1e3
+        e2e_pageable = {"value": total_pts / (pg_ms * 1e-3), "unit": "grid-point updates/s", "ms_per_step": pg_ms,
+                        "h2d_bytes_per_step": bytes_io, "d2h_bytes_per_step": bytes_io,
+                        "api": ("etd2rkds_step_system(plan, SystemState(numpy U, V), f): pageable host arrays in, "
+                                "new pageable arrays out, 1 step per call; staged through the plan's pinned "
+                                "mirror by host copy threads (wall clock)")}
 
     line = {"metric": "grid-point updates/sec (FP64)", "value": value, "unit": "grid-point updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded counter-based RNG, DESIGN.md Inputs)",
-            "config": workload_config(cfg, n, world), "roofline": roofline, "e2e": e2e,
+            "config": dict(workload_config(cfg, n, world), comm_ranks=comm_ranks, device_bytes_per_rank=dev_bytes),
+            "roofline": roofline, "e2e": e2e, "e2e_pageable": e2e_pageable,
             "gpu_launches": plan.launches_per_step * args.steps, "clocks": clk, "finite": finite,
             "ic_seconds": round(t_ic, 2)}
 
@@ -401,7 +462,7 @@ def alt_plan(args, cfg, n, ics, local_rank, kind):
                 continue
             gbs = st["bytes_per_launch"] / (a * 1e-3) * 1e-9
             stages.append({"name": st["name"], "ms": round(a, 3), "bound": "hbm", "gbs": round(gbs, 1),
-                           "frac": round(gbs / 6552.0, 4)})
+                           "frac": round(gbs / HBM_PEAK_GBS, 4)})
         out = {"value": cfg.points(n) * cfg.nspecies / (ms * 1e-3), "unit": "grid-point updates/s",
                "ms_per_step": ms, "stages": stages}
         if kind == "dense":
@@ -416,6 +477,54 @@ def alt_plan(args, cfg, n, ics, local_rank, kind):
         tp.close()
 
 
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(n):
+    """One process per GPU: re-run this script under torch.distributed.run with N
+    ranks (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* set by the launcher).  Rank 0
+    prints the JSON line; the launcher's exit code is returned."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    env = dict(os.environ, ETD_BENCH_LAUNCHED="1", OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args, cfg, n, rank, world):
+    """Rendezvous + per-rank budget, no device work (CPU-testable N>1 path)."""
+    import torch.distributed as dist
+    from paper_2601_06849_b200 import etd as E
+    launched = "WORLD_SIZE" in os.environ
+    if launched:
+        dist.init_process_group("gloo")
+    grid = E.unit_box_grid(cfg.dim, n + 1)
+    mine = E.plan_device_bytes(grid, cfg.nspecies, world, rank) if cfg.dim == 3 or world == 1 else None
+    lo, hi = E.zslab_partition(n, world, rank) if cfg.dim == 3 else (0, 1)
+    me = {"rank": rank, "world_size": dist.get_world_size() if launched else 1, "slab": [lo, hi],
+          "device_bytes": mine}
+    got = [None] * world
+    if launched:
+        dist.all_gather_object(got, me)
+    else:
+        got = [me]
+    if rank == 0:
+        line = {"metric": "grid-point updates/sec (FP64)", "value": None, "unit": "grid-point updates/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "dry_run": True,
+                "ranks_seen": len(got), "world_sizes_seen": sorted({g["world_size"] for g in got}),
+                "slabs": [g["slab"] for g in got],
+                "per_rank_device_bytes": [g["device_bytes"] for g in got],
+                "config": workload_config(cfg, n, world)}
+        print(json.dumps(line), flush=True)
+    if launched:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=None)
@@ -425,17 +534,24 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--n", type=int, default=None, help="override the grid size (testing only)")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e-pageable", dest="e2e_pageable", action="store_false",
+                    help="skip the pageable-numpy e2e line")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the Thomas-backend line")
+    ap.add_argument("--dry-run", action="store_true", help="rendezvous and budget check only (no device work)")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus is not None and args.gpus > 1:
+        return launch_ranks(args.gpus)
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)
-    if args.gpus is not None and args.gpus != world and world != 1:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    if args.gpus is not None and args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     from paper_2601_06849_b200 import configs
     cfg = configs.CONFIGS[args.config]
     n = args.n or cfg.n
+    if args.dry_run:
+        return dry_run(args, cfg, n, rank, world)
     if args.impl == "reference":
         return reference_arm(args, cfg, n, rank, world)
     return b200_arm(args, cfg, n, rank, world, local_rank)

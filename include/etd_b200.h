@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define ETD_B200_ABI_VERSION 3
+#define ETD_B200_ABI_VERSION 4
 
 /* Status codes (0 = OK).  errors.hpp:8-30; CLI mapping cli.cpp:204-217. */
 enum etd_status {
@@ -86,6 +86,11 @@ typedef struct etd_desc {
     int world_size, rank;
     const void* nccl_unique_id; /* 128-byte ncclUniqueId (world_size > 1)          */
     int backend;             /* etd_backend (0 = spectral transforms)               */
+    /* make_plan's memory_cap_bytes (stepper.hpp:58-61; the reference guards its
+     * banded factorisation with it): here the cap on the plan's DEVICE memory
+     * on this rank.  0 = the device's free memory.  etd_create fails with
+     * ETD_ERR_MEMORY (MemoryGuardError) before allocating when the plan needs more. */
+    unsigned long long memory_cap_bytes;
 } etd_desc;
 
 typedef struct etd_handle etd_handle;
@@ -93,6 +98,10 @@ typedef struct etd_handle etd_handle;
 /* make_plan (stepper.cpp:118-177) / make_system_plan (system_stepper.cpp:31-70):
  * host setup (closed-form eigensystems, Pade d-vectors) + one upload.  */
 int etd_create(const etd_desc* desc, etd_handle** out);
+/* Device bytes etd_create would allocate for this desc on this rank (state ping-pong,
+ * step scratch, sharded exchange blocks, transform matrices).  Host only: the
+ * per-rank budget check behind ETD_ERR_MEMORY, callable without a GPU. */
+int etd_plan_device_bytes(const etd_desc* desc, unsigned long long* bytes);
 /* Plan destruction (plans are immutable values in the reference). */
 int etd_destroy(etd_handle* h);
 
@@ -153,6 +162,9 @@ int etd_last_error(const etd_handle* h, char* msg, size_t len, double* t, long* 
 /* ---- introspection / measurement (no reference equivalent) ---------------- */
 /* cudaStream_t the handle launches on (as an integer). */
 unsigned long long etd_stream(const etd_handle* h);
+/* Ranks of the plan's exchange group: ncclCommCount of its NCCL communicator
+ * (NCCL-sharded plans), else world_size (1 unsharded, G for virtual ranks). */
+int etd_comm_ranks(const etd_handle* h, int* out);
 /* Number of kernel launches one step issues (this rank). */
 int etd_launches_per_step(const etd_handle* h);
 /* Per-stage profiling: when enabled, etd_step records CUDA events around every

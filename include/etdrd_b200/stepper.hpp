@@ -15,6 +15,7 @@
 #pragma once
 
 #include <array>
+#include <complex>
 #include <cstddef>
 #include <memory>
 #include <span>
@@ -137,6 +138,40 @@ private:
 enum class PadeFamily { P02 = ETD_P02, P04 = ETD_P04 };
 enum class BackendKind { Spectral, Thomas, NonSplitBanded, ExactExpReference, CudaSpectral = 100, CudaThomas = 101 };
 
+inline std::string family_name(PadeFamily f) { return f == PadeFamily::P04 ? "p04" : "p02"; }
+
+// rational.hpp:15-47: upper-half-plane pole/residue terms of the three weight
+// functions (ell = 1..3), built by the same host setup the device plan uses
+// (rational.cpp:133-177; etd_setup_scheme).  A plan made from a RationalScheme
+// runs its family (the d-vectors are rebuilt from it on the host).
+struct PoleResiduePair {
+    std::complex<double> pole;
+    std::complex<double> residue;
+};
+struct RationalScheme {
+    PadeFamily name = PadeFamily::P02;
+    std::array<std::vector<PoleResiduePair>, 3> terms;  // index ell-1
+    const std::vector<PoleResiduePair>& for_ell(int ell) const {
+        if (ell < 1 || ell > 3) throw ConfigError("ell must be 1, 2, or 3");
+        return terms[ell - 1];
+    }
+};
+inline RationalScheme scheme_by_family(PadeFamily f) {
+    double buf[24];
+    int nt = 0;
+    if (etd_setup_scheme(static_cast<int>(f), buf, &nt) != ETD_OK) throw ConfigError("unknown Pade family");
+    RationalScheme s;
+    s.name = f;
+    for (int ell = 0; ell < 3; ++ell)
+        for (int t = 0; t < nt; ++t) {
+            const double* e = buf + 4 * (ell * nt + t);
+            s.terms[ell].push_back({{e[0], e[1]}, {e[2], e[3]}});
+        }
+    return s;
+}
+inline RationalScheme scheme_p02() { return scheme_by_family(PadeFamily::P02); }
+inline RationalScheme scheme_p04() { return scheme_by_family(PadeFamily::P04); }
+
 // Device stand-in for SourceFunction / SystemSource (stepper.hpp:18-29).
 struct DeviceSource {
     int kind = ETD_SRC_AC_CUBIC;
@@ -207,11 +242,13 @@ inline etd_desc make_desc(const Grid& g, double tau, PadeFamily fam, int ns, dou
     d.backend = ETD_SPECTRAL;
     return d;
 }
-// Spectral / CudaSpectral -> transforms, Thomas / CudaThomas -> tridiagonal solves
+// Spectral / CudaSpectral / ExactExpReference -> transforms, Thomas / CudaThomas ->
+// tridiagonal solves; NonSplitBanded (banded.cpp) has no device implementation
 inline int device_backend(BackendKind b) {
-    if (b == BackendKind::Spectral || b == BackendKind::CudaSpectral) return ETD_SPECTRAL;
+    if (b == BackendKind::Spectral || b == BackendKind::CudaSpectral || b == BackendKind::ExactExpReference)
+        return ETD_SPECTRAL;
     if (b == BackendKind::Thomas || b == BackendKind::CudaThomas) return ETD_THOMAS;
-    throw ConfigError("etdrd_b200 implements the Spectral and Thomas backends");
+    throw ConfigError("etdrd_b200 implements the Spectral, Thomas and ExactExpReference backends");
 }
 inline void set_source(etd_handle* h, const DeviceSource& s) {
     check(etd_set_source(h, s.kind, s.params.data()), h);
@@ -232,11 +269,13 @@ struct StepperState {
     Field U;
 };
 
-// stepper.hpp:59-61.  Spectral and Thomas backends on the device.
+// stepper.hpp:59-61.  Spectral, Thomas and ExactExpReference backends on the device.
+// memory_cap_bytes caps the plan's device memory on this GPU (0 = the free memory);
+// a plan above it throws MemoryGuardError before allocating (the reference guards
+// its banded factorisation the same way, stepper.cpp:57-70).
 inline StepperPlan make_plan(const Grid& grid, double tau, double kappa, double q, PadeFamily scheme,
                              BackendKind backend = BackendKind::CudaSpectral, std::size_t memory_cap_bytes = 0,
                              int device = 0) {
-    (void)memory_cap_bytes;
     const int bk = detail::device_backend(backend);
     StepperPlan p;
     p.backend = backend;
@@ -247,8 +286,17 @@ inline StepperPlan make_plan(const Grid& grid, double tau, double kappa, double 
     p.scheme = scheme;
     etd_desc d = detail::make_desc(grid, tau, scheme, 1, kappa, 0.0, q, DeviceSource::allen_cahn_cubic(), device);
     d.backend = bk;
+    // BackendKind::ExactExpReference (stepper.cpp:145-170, 259-295): the same step
+    // with exact e^{-tau lambda}, phi1, phi2 multipliers
+    if (backend == BackendKind::ExactExpReference) d.family = ETD_EXACT;
+    d.memory_cap_bytes = memory_cap_bytes;
     p.handle = PlanHandle(d);
     return p;
+}
+// The reference signature (stepper.hpp:59-61): scheme as a RationalScheme value.
+inline StepperPlan make_plan(const Grid& grid, double tau, double kappa, double q, const RationalScheme& scheme,
+                             BackendKind backend, std::size_t memory_cap_bytes = 0) {
+    return make_plan(grid, tau, kappa, q, scheme.name, backend, memory_cap_bytes);
 }
 
 // stepper.hpp:85-86 value semantics; nsteps > 1 keeps the state on the device
@@ -268,10 +316,21 @@ inline StepperState advance(const StepperPlan& plan, const StepperState& state, 
 // stepper.cpp:182-257: the split steps `advance` dispatches to (one step each).
 inline StepperState etd2rkds_step_2d(const StepperPlan& plan, const StepperState& state, const SourceFunction& f) {
     if (plan.grid.dim != 2) throw ConfigError("2D step on non-2D plan");
+    if (plan.backend == BackendKind::ExactExpReference)
+        throw ConfigError("2D split step requires the spectral or thomas backend");
     return advance(plan, state, f);
 }
 inline StepperState etd2rkds_step_3d(const StepperPlan& plan, const StepperState& state, const SourceFunction& f) {
     if (plan.grid.dim != 3) throw ConfigError("3D step on non-3D plan");
+    if (plan.backend == BackendKind::ExactExpReference)
+        throw ConfigError("3D split step requires the spectral or thomas backend");
+    return advance(plan, state, f);
+}
+// stepper.hpp:76-77 / stepper.cpp:259-295: the exact-exponential step, on plans made
+// with BackendKind::ExactExpReference (no 64-points-per-axis cap on the device).
+inline StepperState etd2rkds_reference_step(const StepperPlan& plan, const StepperState& state,
+                                            const SourceFunction& f) {
+    if (plan.backend != BackendKind::ExactExpReference) throw ConfigError("reference step requires the exact backend");
     return advance(plan, state, f);
 }
 
@@ -297,6 +356,8 @@ struct SystemState {
 inline SystemPlan make_system_plan(const Grid& grid, double tau, double kappa_u, double kappa_v, double q,
                                    PadeFamily scheme, BackendKind backend = BackendKind::CudaSpectral,
                                    int device = 0) {
+    if (backend == BackendKind::ExactExpReference)
+        throw ConfigError("system plans support the spectral and thomas backends only");
     const int bk = detail::device_backend(backend);
     SystemPlan p;
     p.backend = backend;
@@ -310,6 +371,14 @@ inline SystemPlan make_system_plan(const Grid& grid, double tau, double kappa_u,
     d.backend = bk;
     p.handle = PlanHandle(d);
     return p;
+}
+
+// The reference signature (stepper.hpp:107-108): scheme as a RationalScheme value.
+inline SystemPlan make_system_plan(const Grid& grid, double tau, double kappa_u, double kappa_v, double q,
+                                   const RationalScheme& scheme, BackendKind backend) {
+    if (backend == BackendKind::ExactExpReference || backend == BackendKind::NonSplitBanded)
+        throw ConfigError("system plans support the spectral and thomas backends only");
+    return make_system_plan(grid, tau, kappa_u, kappa_v, q, scheme.name, backend);
 }
 
 // system_stepper.cpp:74-114

@@ -10,7 +10,7 @@ from .etd import (BackendKind, ConfigError, DeviceError, DeviceSource, Grid, Mem
                   advance, etd2rkds_step_2d, etd2rkds_step_3d, etd2rkds_reference_step, etd2rk_nonsplit_step, phi1, phi2,
                   allen_cahn_cubic, allen_cahn_manufactured, singular, build_grid, etd2rkds_step_system, fhn_classic, fhn_cubic,
                   fill_config_ic, lib, make_plan, make_system_plan, poly3, setup_axis, setup_dvector,
-                  setup_scheme, unit_box_grid, zslab_partition, nccl_unique_id, group_step)
+                  setup_scheme, unit_box_grid, zslab_partition, nccl_unique_id, group_step, plan_device_bytes)
 from . import configs, harness
 
 __all__ = [n for n in dir() if not n.startswith("_")]

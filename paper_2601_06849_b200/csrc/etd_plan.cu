@@ -29,6 +29,7 @@
 #include <numbers>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/etd_b200.h"
@@ -204,6 +205,7 @@ struct Nccl {
     int (*GetUniqueId)(ncclUniqueId*) = nullptr;
     int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     int (*CommDestroy)(ncclComm_t) = nullptr;
+    int (*CommCount)(ncclComm_t, int*) = nullptr;
     int (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     int (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     int (*GroupStart)() = nullptr;
@@ -225,6 +227,7 @@ struct Nccl {
             n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(sym("ncclGetUniqueId"));
             n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(sym("ncclCommInitRank"));
             n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(sym("ncclCommDestroy"));
+            n.CommCount = reinterpret_cast<decltype(n.CommCount)>(sym("ncclCommCount"));
             n.Send = reinterpret_cast<decltype(n.Send)>(sym("ncclSend"));
             n.Recv = reinterpret_cast<decltype(n.Recv)>(sym("ncclRecv"));
             n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(sym("ncclGroupStart"));
@@ -475,6 +478,8 @@ struct Plan {
     void* comm = nullptr;            // ncclComm_t
     cudaStream_t cstream = nullptr;  // host<->device copy stream of the pipelined advance
     std::vector<cudaEvent_t> xev;    // its chunk events
+    double* mirror = nullptr;        // pinned host mirror of the state (pageable etd_advance buffers)
+    size_t mirror_elems = 0;
     // BackendKind::Thomas: per-axis factors [species][pole][mul, piv, 1/piv][n],
     // per-axis launch templates, forward-sweep scratch and pole partial sums
     bool thomas = false;
@@ -498,6 +503,7 @@ struct Plan {
             for (double* m : {PR[a], PTR[a], FF[a], FB[a], GA[a], GB[a], GO[a], GE[a]}) if (m) cudaFree(m);
         if (status) cudaFree(status);
         if (status_host) cudaFreeHost(status_host);
+        if (mirror) cudaFreeHost(mirror);
         if (comm) Nccl::get().CommDestroy(comm);
         for (auto e : xev) cudaEventDestroy(e);
         for (auto e : sev) cudaEventDestroy(e);
@@ -1124,6 +1130,49 @@ static void fold2_matrices(const std::vector<double>& Pc, int n, int mode, std::
     }
 }
 
+// Device bytes build_plan allocates (the memory guard and etd_plan_device_bytes):
+// state x2 + Z + W at 2 ns fields each; sharded: send blocks (ns fields), the
+// z-stage blocks zin/Zz/Wz (2 ns fields of this rank's y rows, full z) and the
+// receive blocks (2 ns fields); per axis P and P^T plus the split matrices
+// (<= 6 npad^2); Thomas factors and checkpoints; 64 MiB for descriptors,
+// d-vectors, tables and the allocator's rounding.
+static unsigned long long plan_device_bytes(const etd_desc& d) {
+    const int G = d.world_size < 1 ? 1 : d.world_size;
+    const int nz = d.dim == 3 ? d.n[2] : 1;
+    const unsigned long long pitch = (unsigned long long)round_up(d.n[0], 32);
+    int z0 = 0, z1 = nz, j0 = 0, j1 = d.n[1];
+    if (G > 1) {
+        partition(nz, G, d.rank, z0, z1);
+        partition(d.n[1], G, d.rank, j0, j1);
+    }
+    const unsigned long long F = pitch * d.n[1] * (z1 - z0), ns = d.nspecies;
+    unsigned long long b = 4ull * F * 2 * ns * 8;
+    if (G > 1) {
+        const unsigned long long Fz = pitch * (j1 - j0) * nz;
+        b += F * ns * 8 + 3ull * Fz * 2 * ns * 8 + F * 2 * ns * 8;
+    }
+    for (int a = 0; a < d.dim; ++a) {
+        const unsigned long long np = (unsigned long long)round_up(d.n[a], 32);
+        b += d.backend == ETD_THOMAS ? 2ull * 3 * ns * d.n[a] * 16 : 6ull * np * np * 8;
+    }
+    if (d.backend == ETD_THOMAS) b += F * ns * 2 * 16 / 4;  // checkpoint scratch (2/K complex per point)
+    return b + (64ull << 20);
+}
+
+static void memory_guard(const etd_desc& d) {
+    const unsigned long long need = plan_device_bytes(d);
+    if (d.memory_cap_bytes && need > d.memory_cap_bytes)
+        throw MemoryGuardError("device plan needs " + std::to_string(need >> 20) + " MiB, above the " +
+                               std::to_string(d.memory_cap_bytes >> 20) + " MiB cap");
+    size_t freeb = 0, total = 0;
+    ETD_CK(cudaMemGetInfo(&freeb, &total));
+    if (need > freeb)
+        throw MemoryGuardError("device plan needs " + std::to_string(need >> 20) + " MiB on rank " +
+                               std::to_string(d.world_size > 1 ? d.rank : 0) + ", " + std::to_string(freeb >> 20) +
+                               " MiB free on device " + std::to_string(d.device) +
+                               (d.dim == 3 ? " (shard the z-slabs over more GPUs: world_size)" : ""));
+}
+
 static void build_plan(Plan& p, const etd_desc& d) {
     validate(d);
     p.d = d;
@@ -1143,6 +1192,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
     ETD_CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d.device));
     if (major != 10) throw NoDevice("this build targets sm_100a (B200)");
     ETD_CK(cudaDeviceGetAttribute(&p.nsm, cudaDevAttrMultiProcessorCount, d.device));
+    memory_guard(d);
 
     p.nx = d.n[0];
     p.ny = d.n[1];
@@ -2015,6 +2065,52 @@ static bool overlap_eligible(const Plan& p, int nsteps) {
 //    a later chunk still has to produce, and x_back_upd's U' (written over the
 //    x-reversed W copy in the output state buffer) only lands on rows x_fwd_mix
 //    has already consumed.
+// Pageable host buffers (a plain std::vector / numpy array, the reference Field's
+// storage) cannot be DMA'd asynchronously: a device->host copy into pageable memory
+// returns only when it is done, which would serialise the pipeline.  They go
+// through a pinned host mirror of the state instead (allocated once per plan):
+// host threads copy each upload column range into the mirror just before its H2D
+// copy is queued, and copy each downloaded row chunk out of the mirror while the
+// next chunk computes.  Pinned (registered) buffers are DMA'd directly.
+static bool is_pageable(const void* ptr) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+static int copy_threads() {
+    if (const char* e = std::getenv("ETD_COPY_THREADS")) return std::max(1, std::atoi(e));
+    return (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+}
+
+// f(lo, hi) over [0, items) split across the host copy threads
+template <class F>
+static void parallel_rows(long long items, const F& f) {
+    const int T = (int)std::max(1LL, std::min<long long>(copy_threads(), items / 64));
+    if (T == 1) {
+        f(0, items);
+        return;
+    }
+    std::vector<std::thread> th;
+    th.reserve(T);
+    for (int i = 0; i < T; ++i) th.emplace_back([&, i] { f(items * i / T, items * (i + 1) / T); });
+    for (auto& x : th) x.join();
+}
+
+static double* ensure_mirror(Plan& p, size_t elems) {
+    if (p.mirror_elems < elems) {
+        if (p.mirror) ETD_CK(cudaFreeHost(p.mirror));
+        p.mirror = nullptr;
+        p.mirror_elems = 0;
+        ETD_CK(cudaHostAlloc(&p.mirror, elems * sizeof(double), cudaHostAllocDefault));
+        p.mirror_elems = elems;
+    }
+    return p.mirror;
+}
+
 static void advance_overlapped(Plan& p, const double* const* hin, double* const* hout, long n, double t,
                                int nsteps) {
     const View& V = p.slab;
@@ -2030,12 +2126,23 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
     const int C = (int)std::max(1LL, std::min<long long>(NX, R / 128));
     if (!p.cstream) {
         ETD_CK(cudaStreamCreateWithFlags(&p.cstream, cudaStreamNonBlocking));
-        p.xev.resize(2 * kXferChunksMax + 1);
+        p.xev.resize(3 * kXferChunksMax + 1);
         for (auto& e : p.xev) ETD_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     cudaEvent_t* ev_in = p.xev.data();
     cudaEvent_t* ev_out = p.xev.data() + kXferChunksMax;
-    cudaEvent_t ev_start = p.xev[2 * kXferChunksMax];
+    cudaEvent_t* ev_dl = p.xev.data() + 2 * kXferChunksMax;  // download of row chunk c landed
+    cudaEvent_t ev_start = p.xev[3 * kXferChunksMax];
+    // pageable buffers go through the pinned mirror [species][R][nx] (host layout)
+    const size_t cnt = (size_t)R * V.nx;
+    bool pg_in[2] = {false, false}, pg_out[2] = {false, false}, any_in = false, any_out = false;
+    for (int sp = 0; sp < p.ns; ++sp) {
+        pg_in[sp] = is_pageable(hin[sp]);
+        pg_out[sp] = is_pageable(hout[sp]);
+        any_in |= pg_in[sp];
+        any_out |= pg_out[sp];
+    }
+    double* mir = (any_in || any_out) ? ensure_mirror(p, cnt * p.ns) : nullptr;
     p.status_host->n = n;
     p.status_host->t = t;
     p.status_host->fail = 0;
@@ -2045,20 +2152,37 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
     ETD_CK(cudaStreamWaitEvent(p.cstream, ev_start, 0));
     auto rowb = [&](int c) { return c >= C ? R : R * c / C / 128 * 128; };  // x-stage row chunk bounds
     double* st_in = p.state[p.cur];
-    for (int c = 0; c < CX; ++c) {
+    auto upload = [&](int c) {
         const int x0 = c * XW, x1 = std::min(V.nx, x0 + XW);
-        for (int sp = 0; sp < p.ns; ++sp)
-            ETD_CK(cudaMemcpy2DAsync(st_in + (size_t)sp * V.F + x0, (size_t)V.pitch * 8, hin[sp] + x0,
+        for (int sp = 0; sp < p.ns; ++sp) {
+            const double* src = hin[sp];
+            if (pg_in[sp]) {
+                double* m = mir + (size_t)sp * cnt;
+                const double* h = hin[sp];
+                parallel_rows(R, [&](long long r0, long long r1) {
+                    for (long long r = r0; r < r1; ++r)
+                        std::memcpy(m + r * V.nx + x0, h + r * V.nx + x0, (size_t)(x1 - x0) * 8);
+                });
+                src = m;
+            }
+            ETD_CK(cudaMemcpy2DAsync(st_in + (size_t)sp * V.F + x0, (size_t)V.pitch * 8, src + x0,
                                      (size_t)V.nx * 8, (size_t)(x1 - x0) * 8, (size_t)R, cudaMemcpyHostToDevice,
                                      p.cstream));
+        }
         ETD_CK(cudaEventRecord(ev_in[c], p.cstream));
-    }
+    };
+    // pinned inputs: every column range is queued up front; pageable ones are
+    // staged range by range inside the first step's column loop, so each range's
+    // compute is queued right behind its copy while the host stages the next
+    if (!any_in)
+        for (int c = 0; c < CX; ++c) upload(c);
     for (int s = 0; s < nsteps; ++s) {
         const auto& ops = p.steps[(p.cur + s) & 1];
         const bool first = s == 0, last = s == nsteps - 1;
         // source + z / y stages: per x-column range in the first step
         if (first) {
             for (int c = 0; c < CX; ++c) {
+                if (any_in) upload(c);
                 ETD_CK(cudaStreamWaitEvent(p.stream, ev_in[c], 0));
                 const int x0 = c * XW, x1 = std::min(V.nx, x0 + XW);
                 for (int k = 0; k < ix; ++k) {
@@ -2099,6 +2223,21 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
             continue;
         }
         const Op& upd = ops.back();
+        // pageable outputs: copy row chunk c out of the mirror once its download landed
+        auto drain = [&](int c) {
+            const long long r0 = rowb(c), r1 = rowb(c + 1);
+            if (!any_out || r1 <= r0) return;
+            ETD_CK(cudaEventSynchronize(ev_dl[c]));
+            for (int sp = 0; sp < p.ns; ++sp) {
+                if (!pg_out[sp]) continue;
+                const double* m = mir + (size_t)sp * cnt + r0 * V.nx;
+                double* h = hout[sp] + r0 * V.nx;
+                parallel_rows(r1 - r0, [&](long long a, long long b) {
+                    std::memcpy(h + a * V.nx, m + a * V.nx, (size_t)(b - a) * V.nx * 8);
+                });
+            }
+        };
+        int prev = -1;  // last queued row chunk whose pageable copy-out is pending
         for (int c = 0; c < C; ++c) {
             const long long r0 = rowb(c), r1 = rowb(c + 1);
             if (r1 <= r0) continue;
@@ -2127,11 +2266,16 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
             ETD_CK(cudaEventRecord(ev_out[c], p.stream));
             ETD_CK(cudaStreamWaitEvent(p.cstream, ev_out[c], 0));
             for (int sp = 0; sp < p.ns; ++sp)
-                ETD_CK(cudaMemcpy2DAsync(hout[sp] + r0 * V.nx, (size_t)V.nx * 8,
-                                         upd.L.args.out + (size_t)sp * V.F + r0 * V.pitch, (size_t)V.pitch * 8,
-                                         (size_t)V.nx * 8, (size_t)(r1 - r0), cudaMemcpyDeviceToHost, p.cstream));
+                ETD_CK(cudaMemcpy2DAsync((pg_out[sp] ? mir + (size_t)sp * cnt : hout[sp]) + r0 * V.nx,
+                                         (size_t)V.nx * 8, upd.L.args.out + (size_t)sp * V.F + r0 * V.pitch,
+                                         (size_t)V.pitch * 8, (size_t)V.nx * 8, (size_t)(r1 - r0),
+                                         cudaMemcpyDeviceToHost, p.cstream));
+            ETD_CK(cudaEventRecord(ev_dl[c], p.cstream));
+            if (prev >= 0) drain(prev);
+            prev = c;
         }
         etd_commit<<<1, 1, 0, p.stream>>>(p.status, nullptr, 0, p.tau);
+        if (prev >= 0) drain(prev);
     }
     ETD_CK(cudaGetLastError());
     ETD_CK(cudaStreamSynchronize(p.cstream));
@@ -2362,6 +2506,9 @@ int guarded(etd_handle* h, F&& f) {
     } catch (const etd::NoDevice& e) {
         if (h) h->msg = e.what(); else g_create_error = e.what();
         return ETD_ERR_NODEVICE;
+    } catch (const etd::MemoryGuardError& e) {
+        if (h) h->msg = e.what(); else g_create_error = e.what();
+        return ETD_ERR_MEMORY;
     } catch (const std::bad_alloc& e) {
         if (h) h->msg = "host allocation failed"; else g_create_error = "host allocation failed";
         return ETD_ERR_MEMORY;
@@ -2394,6 +2541,14 @@ int etd_create(const etd_desc* desc, etd_handle** out) {
     }
     *out = h.release();
     return ETD_OK;
+}
+
+int etd_plan_device_bytes(const etd_desc* desc, unsigned long long* bytes) {
+    return guarded(nullptr, [&] {
+        if (!desc || !bytes) throw etd::ConfigError("null argument");
+        etd::validate(*desc);
+        *bytes = etd::plan_device_bytes(*desc);
+    });
 }
 
 int etd_destroy(etd_handle* h) {
@@ -2522,6 +2677,18 @@ int etd_last_error(const etd_handle* h, char* msg, size_t len, double* t, long* 
 
 unsigned long long etd_stream(const etd_handle* h) {
     return h ? reinterpret_cast<unsigned long long>(h->plan->stream) : 0ull;
+}
+
+int etd_comm_ranks(const etd_handle* h, int* out) {
+    return guarded(const_cast<etd_handle*>(h), [&] {
+        if (!h || !out) throw etd::ConfigError("null argument");
+        const etd::Plan& p = *h->plan;
+        *out = p.G;
+        if (p.sharded && !p.local_group) {
+            auto& nc = etd::Nccl::get();
+            nc.check(nc.CommCount(p.comm, out), "ncclCommCount");
+        }
+    });
 }
 
 int etd_launches_per_step(const etd_handle* h) {

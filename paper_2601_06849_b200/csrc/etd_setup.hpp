@@ -13,6 +13,8 @@ namespace etd {
 
 struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct NumericsError : std::runtime_error { using std::runtime_error::runtime_error; };
+// errors.hpp:28 MemoryGuardError: the plan's device memory does not fit the cap / the device
+struct MemoryGuardError : std::runtime_error { using std::runtime_error::runtime_error; };
 
 // Toeplitz tridiagonal factor of kappa*(-Laplacian) + q along one axis
 // (reference operators.cpp:11-34): diag = (2k + (q/dim) h^2)/h^2, off = -k/h^2.

@@ -202,6 +202,7 @@ class _Desc(C.Structure):
         ("tau", C.c_double), ("family", C.c_int), ("nspecies", C.c_int), ("kappa", C.c_double * 2),
         ("q", C.c_double), ("src_kind", C.c_int), ("src_params", C.c_double * 8), ("device", C.c_int),
         ("world_size", C.c_int), ("rank", C.c_int), ("nccl_unique_id", C.c_void_p), ("backend", C.c_int),
+        ("memory_cap_bytes", C.c_ulonglong),
     ]
 
 
@@ -219,6 +220,7 @@ def lib():
         i, d, l, vp, sz = C.c_int, C.c_double, C.c_long, C.c_void_p, C.c_size_t
         L.etd_create.argtypes = [C.POINTER(_Desc), C.POINTER(vp)]
         L.etd_destroy.argtypes = [vp]
+        L.etd_plan_device_bytes.argtypes = [C.POINTER(_Desc), C.POINTER(C.c_ulonglong)]
         L.etd_slab_range.argtypes = [vp, C.POINTER(i), C.POINTER(i)]
         L.etd_set_state.argtypes = [vp, i, vp, sz, l, d]
         L.etd_get_state.argtypes = [vp, i, vp, sz, C.POINTER(l), C.POINTER(d)]
@@ -229,6 +231,7 @@ def lib():
         L.etd_stream.argtypes = [vp]
         L.etd_stream.restype = C.c_ulonglong
         L.etd_launches_per_step.argtypes = [vp]
+        L.etd_comm_ranks.argtypes = [vp, C.POINTER(i)]
         L.etd_set_profiling.argtypes = [vp, i]
         L.etd_stage_count.argtypes = [vp]
         L.etd_stage_info.argtypes = [vp, i, C.c_char_p, sz, C.POINTER(d), C.POINTER(l), C.POINTER(d), C.POINTER(d)]
@@ -297,7 +300,7 @@ class _Handle:
 
 
 def _make_desc(grid: Grid, tau, family, nspecies, kappas, q, source: DeviceSource, device=0,
-               world_size=1, rank=0, nccl_id=None, backend=0) -> _Desc:
+               world_size=1, rank=0, nccl_id=None, backend=0, memory_cap_bytes=0) -> _Desc:
     d = _Desc()
     d.dim = grid.dim
     sh = grid.interior_shape()
@@ -318,6 +321,7 @@ def _make_desc(grid: Grid, tau, family, nspecies, kappas, q, source: DeviceSourc
     d.world_size = world_size
     d.rank = rank
     d.backend = int(backend)
+    d.memory_cap_bytes = int(memory_cap_bytes)
     d.nccl_unique_id = None
     if nccl_id is not None:
         d._id_buf = C.create_string_buffer(bytes(nccl_id), 128)  # kept alive with the desc
@@ -346,7 +350,7 @@ class _PlanBase:
     nspecies = 1
 
     def __init__(self, grid: Grid, tau: float, family, kappas, q, source: Optional[DeviceSource], device=0,
-                 world_size=1, rank=0, nccl_id=None, backend=BackendKind.CudaSpectral):
+                 world_size=1, rank=0, nccl_id=None, backend=BackendKind.CudaSpectral, memory_cap_bytes=0):
         if not tau > 0.0:
             raise ConfigError("tau must be positive")
         self.grid = grid
@@ -359,7 +363,7 @@ class _PlanBase:
         self.backend = BackendKind.CudaThomas if _DEVICE_BACKEND[backend] == 1 else BackendKind.CudaSpectral
         self._source = source or (allen_cahn_cubic() if self.nspecies == 1 else fhn_cubic())
         self._h = _Handle(_make_desc(grid, tau, self.family, self.nspecies, kappas, q, self._source, device,
-                                     world_size, rank, nccl_id, _DEVICE_BACKEND[backend]))
+                                     world_size, rank, nccl_id, _DEVICE_BACKEND[backend], memory_cap_bytes))
         z0, z1 = C.c_int(), C.c_int()
         lib().etd_slab_range(self._h.h, C.byref(z0), C.byref(z1))
         self.slab = (z0.value, z1.value)
@@ -432,6 +436,12 @@ class _PlanBase:
     def launches_per_step(self) -> int:
         return int(lib().etd_launches_per_step(self.handle))
 
+    def comm_ranks(self) -> int:
+        """Ranks of the exchange group (ncclCommCount of an NCCL-sharded plan)."""
+        out = C.c_int()
+        _raise(lib().etd_comm_ranks(self.handle, C.byref(out)), self.handle)
+        return out.value
+
     def set_profiling(self, on: bool):
         lib().etd_set_profiling(self.handle, int(bool(on)))
 
@@ -484,11 +494,12 @@ class StepperPlan(_PlanBase):
     nspecies = 1
 
     def __init__(self, grid, tau, kappa, q, family=PadeFamily.P02, source=None, device=0, world_size=1, rank=0,
-                 nccl_id=None, backend=BackendKind.CudaSpectral):
+                 nccl_id=None, backend=BackendKind.CudaSpectral, memory_cap_bytes=0):
         if not kappa > 0.0:
             raise ConfigError("diffusivity must be positive")
         self.kappa = float(kappa)
-        super().__init__(grid, tau, family, (kappa,), q, source, device, world_size, rank, nccl_id, backend)
+        super().__init__(grid, tau, family, (kappa,), q, source, device, world_size, rank, nccl_id, backend,
+                         memory_cap_bytes)
 
 
 class SystemPlan(_PlanBase):
@@ -496,12 +507,12 @@ class SystemPlan(_PlanBase):
     nspecies = 2
 
     def __init__(self, grid, tau, kappa_u, kappa_v, q, family=PadeFamily.P02, source=None, device=0,
-                 world_size=1, rank=0, nccl_id=None, backend=BackendKind.CudaSpectral):
+                 world_size=1, rank=0, nccl_id=None, backend=BackendKind.CudaSpectral, memory_cap_bytes=0):
         if not (kappa_u > 0.0 and kappa_v > 0.0):
             raise ConfigError("component diffusivities must be positive")
         self.kappa_u, self.kappa_v = float(kappa_u), float(kappa_v)
         super().__init__(grid, tau, family, (kappa_u, kappa_v), q, source, device, world_size, rank, nccl_id,
-                         backend)
+                         backend, memory_cap_bytes)
 
 
 def make_plan(grid: Grid, tau: float, kappa: float, q: float, scheme=PadeFamily.P02,
@@ -512,10 +523,11 @@ def make_plan(grid: Grid, tau: float, kappa: float, q: float, scheme=PadeFamily.
     (thomas.cpp); ExactExpReference: the reference's exact-exponential step
     (stepper.cpp:259-295) on the spectral transforms."""
     if backend == BackendKind.ExactExpReference:
-        return StepperPlan(grid, tau, kappa, q, EXACT_FAMILY, source, device)
+        return StepperPlan(grid, tau, kappa, q, EXACT_FAMILY, source, device, memory_cap_bytes=memory_cap_bytes)
     if backend not in _DEVICE_BACKEND:
         raise ConfigError("this package implements the Spectral, Thomas and ExactExpReference backends")
-    return StepperPlan(grid, tau, kappa, q, scheme, source, device, backend=backend)
+    return StepperPlan(grid, tau, kappa, q, scheme, source, device, backend=backend,
+                       memory_cap_bytes=memory_cap_bytes)
 
 
 def make_system_plan(grid: Grid, tau: float, kappa_u: float, kappa_v: float, q: float, scheme=PadeFamily.P02,
@@ -641,6 +653,18 @@ def setup_scheme(family: int) -> np.ndarray:
     nt = C.c_int()
     _raise(lib().etd_setup_scheme(int(family), _ptr(out), C.byref(nt)), None)
     return out[: 12 * nt.value].reshape(3, nt.value, 4)
+
+
+def plan_device_bytes(grid: Grid, nspecies: int = 1, world_size: int = 1, rank: int = 0,
+                      backend: BackendKind = BackendKind.CudaSpectral) -> int:
+    """Device bytes a plan allocates on `rank` (etd_plan_device_bytes; host only):
+    the per-rank budget etd_create checks before allocating (MemoryGuardError)."""
+    src = allen_cahn_cubic() if nspecies == 1 else fhn_cubic()
+    kap = (1.0,) if nspecies == 1 else (1.0, 1.0)
+    d = _make_desc(grid, 1.0, 0, nspecies, kap, 0.0, src, 0, world_size, rank, None, _DEVICE_BACKEND[backend])
+    out = C.c_ulonglong()
+    _raise(lib().etd_plan_device_bytes(C.byref(d), C.byref(out)), None)
+    return out.value
 
 
 def zslab_partition(n: int, world_size: int, rank: int):

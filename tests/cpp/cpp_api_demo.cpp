@@ -3,6 +3,7 @@
 //        cpp_api_demo errors
 // in.bin holds U (and V) as raw float64, x-fastest; out.bin receives the result.
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -40,8 +41,39 @@ int main(int argc, char** argv) {
         try {
             (void)advance(plan, bad, DeviceSource::allen_cahn_cubic());
         } catch (const ConfigError&) { ++ok; }
-        std::printf("errors ok=%d/4\n", ok);
-        return ok == 4 ? 0 : 1;
+        // make_plan's memory_cap_bytes: a plan above the cap is refused before allocating
+        try {
+            (void)make_plan(unit_box_grid(3, 64), 0.01, 1.0, 1.0, scheme_p02(), BackendKind::Spectral, 1 << 20);
+        } catch (const MemoryGuardError&) { ++ok; }
+        // RationalScheme values (rational.hpp:31-47): P02 one pole -1+i, P04 two
+        const RationalScheme s2 = scheme_p02(), s4 = scheme_by_family(PadeFamily::P04);
+        if (s2.for_ell(1).size() == 1 && s4.for_ell(3).size() == 2 && s2.terms[0][0].pole == std::complex<double>(-1, 1))
+            ++ok;
+        // ExactExpReference (stepper.cpp:259-295): a sine mode under f = 0 decays by
+        // exactly e^{-tau lambda}, lambda the discrete eigenvalue (operators.cpp:43-53)
+        {
+            const int m = 32;
+            const Grid ge = unit_box_grid(2, m);
+            const double tau = 0.01, kap = 0.7, qq = 0.4, pi = 3.14159265358979323846, h = 1.0 / m;
+            auto pe = make_plan(ge, tau, kap, qq, scheme_p02(), BackendKind::ExactExpReference);
+            StepperState s0{0, 0.0, Field::zeros(ge)};
+            for (int j = 0; j < m - 1; ++j)
+                for (int i = 0; i < m - 1; ++i) s0.U.at(i, j) = std::sin(pi * (i + 1) * h) * std::sin(pi * (j + 1) * h);
+            const StepperState s1 = etd2rkds_reference_step(pe, s0, DeviceSource{ETD_SRC_ZERO, {}, true});
+            const double lam = 2.0 * (kap * 2.0 * (1.0 - std::cos(pi * h)) / (h * h) + qq / 2.0);
+            double err = 0.0, mx = 0.0;
+            for (std::size_t k = 0; k < s0.U.size(); ++k) {
+                err = std::fmax(err, std::fabs(s1.U[k] - std::exp(-tau * lam) * s0.U[k]));
+                mx = std::fmax(mx, std::fabs(s0.U[k]));
+            }
+            if (s1.n == 1 && err / mx <= 1e-12) ++ok;
+            else std::printf("exact decay err %.3e\n", err / mx);
+            try {
+                (void)etd2rkds_step_2d(pe, s0, DeviceSource::allen_cahn_cubic());
+            } catch (const ConfigError&) { ++ok; }
+        }
+        std::printf("errors ok=%d/8\n", ok);
+        return ok == 8 ? 0 : 1;
     }
     if (argc != 12) {
         std::fprintf(stderr, "usage: see header\n");

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 20
     for s in syms:
         assert hasattr(L, s), s
-    assert L.etd_abi_version() == 3
+    assert L.etd_abi_version() == 4
 
 
 def test_header_is_plain_c_and_matches_ctypes_layout():

@@ -245,6 +245,38 @@ def test_pipelined_advance_equals_device_resident_steps():
         assert a.n == n == 2 + steps and a.t == pytest.approx(t)
 
 
+@pytest.mark.parametrize("pin_in,pin_out", [(True, True), (False, True), (True, False), (False, False)])
+def test_pipelined_advance_pinned_and_pageable_buffers(pin_in, pin_out, monkeypatch):
+    """The pipelined advance DMAs pinned host buffers directly and stages pageable
+    ones (plain numpy, the reference Field's std::vector) through the plan's pinned
+    mirror with host copy threads: every mix of the two is bitwise equal to the
+    device-resident steps, and the caller's input is left untouched."""
+    import torch
+    monkeypatch.setenv("ETD_COPY_THREADS", "3")
+    grid = etd.build_grid(3, [(0, 1)] * 3, [40, 34, 30])
+    nx, ny, nz = grid.interior_shape()
+    rng = np.random.default_rng(5)
+    u0, v0 = rng.uniform(-1, 1, nx * ny * nz), rng.uniform(-0.5, 0.5, nx * ny * nz)
+    f = etd.fhn_cubic()
+    ref = etd.make_system_plan(grid, 0.05, 1e-3, 5e-4, 0.0, source=f)
+    ref.upload(0, u0, 0, 0.0)
+    ref.upload(1, v0, 0, 0.0)
+    ref.step(2)
+    wu, wv = ref.download(0)[0], ref.download(1)[0]
+
+    def buf(a, pinned):
+        t = torch.from_numpy(a.copy())
+        return t.pin_memory() if pinned else t
+
+    hin = [buf(u0, pin_in), buf(v0, pin_in)]
+    hout = [buf(np.zeros_like(u0), pin_out), buf(np.zeros_like(v0), pin_out)]
+    plan = etd.make_system_plan(grid, 0.05, 1e-3, 5e-4, 0.0, source=f)
+    n, t = plan.advance_ptr(hin[0].data_ptr(), hin[1].data_ptr(), hout[0].data_ptr(), hout[1].data_ptr(), 0, 0.0, 2)
+    assert n == 2
+    assert np.array_equal(hout[0].numpy(), wu) and np.array_equal(hout[1].numpy(), wv)
+    assert np.array_equal(hin[0].numpy(), u0) and np.array_equal(hin[1].numpy(), v0)
+
+
 def test_pipelined_advance_abort_3d():
     g = etd.unit_box_grid(3, 14)
     plan = etd.make_plan(g, 0.01, 1.0, 1.0)
