@@ -194,6 +194,12 @@ int etd_setup_fold_matrices(int n, int mode, double* ff, double* fb);
  * Layouts as etd_setup_fold_matrices; go/ge may be NULL.  Returns
  * ETD_ERR_CONFIG otherwise.  Host only. */
 int etd_setup_fold2_matrices(int n, int mode, double* ga, double* gb, double* fb, double* go, double* ge);
+/* The fused level-2 backward matrix G6 of one axis with n = 32m - 1 (etd_plan.cu
+ * back6_matrix): 4H rows x H columns, H = (n+1)/4, rows in blocks of
+ * 32 (parity b & 1, orbit base b >> 1) of four 8-row fragments (o_k, o_{2H-2-k},
+ * eo_k, ee_k); mode 0 rows contiguous with leading dimension round_up(H, 16), mode
+ * 1 the transpose [H][4H].  Host only. */
+int etd_setup_back6_matrix(int n, int mode, double* g6);
 /* Parity-split level the step runs per axis: 0 dense, 1 first level (§4a),
  * 2 second level (§4b); out[a] for a < 3. */
 int etd_fold_level(const etd_handle* h, int* out);

@@ -17,8 +17,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libetd_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["etd_setup.cpp", "etd_plan.cu", "etd_specs_dense.cu", "etd_specs_fold.cu", "etd_specs_fold2.cu"]
-HEADERS = ["etd_setup.hpp", "etd_kernels.cuh", "etd_thomas.cuh", "etd_registry.cuh"]
+SOURCES = ["etd_setup.cpp", "etd_plan.cu", "etd_specs_dense.cu", "etd_specs_fold.cu", "etd_specs_fold2.cu",
+           "etd_specs_fold6.cu"]
+HEADERS = ["etd_setup.hpp", "etd_kernels.cuh", "etd_thomas.cuh", "etd_registry.cuh", "etd_back6.cuh"]
 
 
 def _nvcc() -> str:

@@ -1,0 +1,340 @@
+// etd_back6.cuh — fused second-level backward transform.
+//
+// The level-2 backward of an axis with n = 4H - 1 (h = 2H) reads the mode
+// coefficients in level-2 positions along the axis,
+//   [0, H) sigma_c,  [H, 2H) delta_c      (even modes as (X_c + X_{h-1-c}, X_c - X_{h-1-c}))
+//   [2H, 3H) Y_lo,   [3H, 4H-1) Y_hi      (odd modes 4c + 1 and 4c + 3)
+// and produces the physical pencil g.  For an orbit k < H, c = 2H - 2 - k:
+//   o_k  = sum_c P(k, 2c) sigma_c   (k even) | delta_c (k odd)         P(i, 2(h-1-c)) = (-1)^i P(i, 2c)
+//   o_c' = the same row for i = c' = 2H - 2 - k (same parity as k)
+//   eo_k = sum_c P(k, 4c + 1) Y_lo[c],  ee_k = sum_c P(k, 4c + 3) Y_hi[c]
+//   e_k = eo_k + ee_k,  e_c' = eo_k - ee_k      (the odd modes are a DST-I of size 2H - 1)
+//   g_k = o_k + e_k,  g_{n-1-k} = o_k - e_k,  g_c' = o_c' + e_c',  g_{n-1-c'} = o_c' - e_c'
+// (k = H - 1: c' = k, ee_k = 0 exactly, and the o_c' slot carries the centre
+// o_{2H-1} = g_{2H-1}).  The r01 schedule ran this as two launches (the o and the e
+// halves into an intermediate stack) and an HBM pass (etd_unfold2) that formed g
+// and applied the stage epilogue.  Here one launch contracts all four quarters at
+// once — a stage carries four A boxes (the k range of each quarter) — and every
+// thread ends up holding whole orbits, so the butterflies and the epilogue run on
+// the accumulators: the unfold pass and its HBM round trip disappear.  The DMMA
+// sequence of every accumulator is the one of the two-launch path (same operands,
+// same k order), so results are bitwise equal to it.
+//
+// B (matrix G6, etd_plan.cu back6_matrix): 4H rows in blocks of 32; block b has
+// parity par = b & 1 and orbit base kb = b >> 1; its four 8-row fragments are the
+// types t = 0 (o_k), 1 (o_c'), 2 (eo_k), 3 (ee_k) of k = 16 kb + 2 r + par, r < 8.
+// A warp's WN = 64 columns are one block pair (par 0, par 1), so fragment j has
+// type j & 3, parity (j >> 2) & 1 and reads A box (type < 2 ? parity : type).  A
+// thread (g, l) then holds, per 64-row block pair, the orbits k = 16 kb + 4 l + q,
+// q < 4 — four consecutive k, whole orbits, every species of the stack.
+#pragma once
+#include "etd_kernels.cuh"
+
+namespace etd {
+
+template <int MODE, int S, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
+struct Back6Cfg {
+    static constexpr int BK = 16, AB = 4;
+    static constexpr int NW = WARPS_M * WARPS_N, THREADS = 32 * NW;
+    static constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
+    static constexpr int MF = WM / 8, NF = WN / 8;
+    static constexpr int A1_DBL = S * BM * BK, A_DBL = AB * A1_DBL, B_DBL = BN * BK;
+    static constexpr int STAGE_DBL = A_DBL + B_DBL;
+    static constexpr uint32_t TX_BYTES = (AB * S * BM + BN) * BK * 8;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_DBL * 8 + 1024 + 2 * STAGES * 8 + 64;
+    static_assert(WM % 8 == 0 && WN % 64 == 0, "a warp covers whole (par 0, par 1) block pairs");
+    static_assert(BM % 16 == 0 && BN % 64 == 0, "cta tile");
+};
+
+template <int MODE, int S, int EPI, int SK, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB>
+__global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
+    etd_back6(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmA2, const ContractArgs args) {
+    static_assert(EPI == EPI_STORE || MODE == 0, "the x stage owns the predictor / update epilogues");
+    using C = Back6Cfg<MODE, S, BM, BN, WARPS_M, WARPS_N, STAGES>;
+    constexpr int BK = C::BK, MF = C::MF, NF = C::NF;
+    (void)tmA2;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    double* smem = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_DBL);
+    uint64_t* empty = full + STAGES;
+    int* cta_flag = reinterpret_cast<int*>(empty + STAGES);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n0 = blockIdx.x * BN;
+    const int m0 = (blockIdx.y + args.mtile0) * BM;
+    const int outer = blockIdx.z + args.outer0;
+    const int H = args.fold_h, n = args.n_axis;
+    const int KT = (H + BK - 1) / BK;
+
+    if (tid == 0) {
+        cta_flag[0] = *reinterpret_cast<volatile int*>(&args.status->fail);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (cta_flag[0] != 0) return;
+    int bad = 0, dom = 0;
+
+    // one TMA per quarter (sigma, delta, Y_lo, Y_hi at axis coordinate q H + k0) and
+    // one for the G6 tile; coordinates off the tensor read +0.0
+    auto issue = [&](int kt, int stage) {
+        double* sA = smem + stage * C::STAGE_DBL;
+        double* sB = sA + C::A_DBL;
+        mbar_expect_tx(&full[stage], C::TX_BYTES);
+        const int k0 = kt * BK;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if constexpr (MODE == 0) tma_load_3d(sA + q * C::A1_DBL, &tmA, &full[stage], k0 + q * H, m0, 0);
+            else tma_load_5d(sA + q * C::A1_DBL, &tmA, &full[stage], 0, k0 + q * H, m0 >> 4, outer, 0);
+        }
+        if constexpr (MODE == 0) tma_load_2d(sB, &tmB, &full[stage], k0, n0);
+        else tma_load_3d(sB, &tmB, &full[stage], 0, k0, n0 >> 4);
+    };
+    if (tid == 0) {
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+        for (int kt = 0; kt < KT && kt < STAGES; ++kt) issue(kt, kt);
+    }
+
+    const int g = lane >> 2, l = lane & 3;
+    const int wm0 = (warp / WARPS_N) * C::WM;
+    const int wn0 = (warp % WARPS_N) * C::WN;
+    double acc[S][MF][NF][2];
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int i = 0; i < MF; ++i)
+#pragma unroll
+            for (int j = 0; j < NF; ++j) acc[s][i][j][0] = acc[s][i][j][1] = 0.0;
+
+    // the k permutation of etd_contract (bank-conflict free fragment loads, and the
+    // same accumulation order as the two-launch path)
+    auto kperm = [&](int st) {
+        return MODE == 0 ? (2 * st + (l & 1) + 8 * (l >> 1)) : (2 * l + (st & 1) + 8 * (st >> 1));
+    };
+    // A fragments are double-buffered across steps; B fragments are loaded just in
+    // time inside mma() (each feeds S x MF DMMAs), which keeps the 2-CTA/SM class
+    // under its 128-register cap
+    auto load_frags = [&](int stg, int st, double (&a)[4][S][MF]) {
+        const double* sA = smem + stg * C::STAGE_DBL;
+        const int kk = kperm(st);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int i = 0; i < MF; ++i) {
+                    const int mm = wm0 + i * 8 + g;
+                    const double* base = sA + q * C::A1_DBL + s * BM * BK;
+                    a[q][s][i] = MODE == 0 ? base[swz(mm, kk)] : base[(mm >> 4) * 256 + swz(kk, mm & 15)];
+                }
+    };
+    auto mma = [&](int stg, int st, const double (&a)[4][S][MF]) {
+        const double* sB = smem + stg * C::STAGE_DBL + C::A_DBL;
+        const int kk = kperm(st);
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+            const int nn = wn0 + j * 8 + g;
+            const double b = MODE == 0 ? sB[swz(nn, kk)] : sB[(nn >> 4) * 256 + swz(kk, nn & 15)];
+            const int t = j & 3, box = t < 2 ? ((j >> 2) & 1) : t;
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int i = 0; i < MF; ++i) dmma884(acc[s][i][j][0], acc[s][i][j][1], a[box][s][i], b);
+        }
+    };
+
+    double fa[2][4][S][MF];
+    int stage = 0;
+    uint32_t phase = 0;
+    mbar_wait(&full[0], 0);
+    load_frags(0, 0, fa[0]);
+    for (int kt = 0; kt < KT; ++kt) {
+        const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
+        const uint32_t nphase = stage + 1 == STAGES ? phase ^ 1 : phase;
+#pragma unroll
+        for (int st = 0; st < BK / 4; ++st) {
+            const int cur = st & 1, nxt = cur ^ 1;
+            if (st < BK / 4 - 1) {
+                load_frags(stage, st + 1, fa[nxt]);
+            } else if (kt + 1 < KT) {
+                mbar_wait(&full[nstage], nphase);
+                load_frags(nstage, 0, fa[nxt]);
+            }
+            mma(stage, st, fa[cur]);
+            if (st == BK / 4 - 1) {
+                // release only after the DMMAs that consumed this stage's last
+                // fragments have issued (etd_contract: the stage-release race)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[stage]);
+            }
+        }
+        if (tid == 0 && kt + STAGES < KT) {
+            mbar_wait(&empty[stage], phase);
+            issue(kt + STAGES, stage);
+        }
+        __syncwarp();
+        stage = nstage;
+        phase = nphase;
+    }
+
+    // ===================== orbit epilogue =====================
+    double* __restrict__ outp = args.out;
+    auto offset = [&](int m, int p) -> long long {
+        if constexpr (MODE == 0) return (long long)m * args.pitch + p;
+        else return args.zaxis ? (long long)outer * args.pitch + (long long)p * args.plane + m
+                               : (long long)outer * args.plane + (long long)p * args.pitch + m;
+    };
+    const double src_a = SK == 4 ? exp(-args.sp[0] * (args.status->t + args.tau)) : 0.0;
+#pragma unroll
+    for (int i = 0; i < MF; ++i) {
+        const int m = m0 + wm0 + i * 8 + g;
+        if (m >= args.m_extent) continue;
+#pragma unroll
+        for (int bp = 0; bp < NF / 8; ++bp) {
+            const int kb = (n0 + wn0) / 64 + bp;
+#pragma unroll
+            for (int par = 0; par < 2; ++par)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int k = 16 * kb + 4 * l + 2 * e + par;
+                    if (k >= H) continue;
+                    const int jb = 8 * bp + 4 * par;
+                    const bool centre = k == H - 1;
+                    const int c = 2 * H - 2 - k;
+                    // orbit positions: 0 k, 1 n-1-k, 2 c (centre orbit: 2H-1), 3 n-1-c
+                    const int np = centre ? 3 : 4;
+                    const int pos[4] = {k, n - 1 - k, centre ? 2 * H - 1 : c, n - 1 - c};
+                    double gv[S][4];
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        const double O1 = acc[s][i][jb][e], O2 = acc[s][i][jb + 1][e];
+                        const double EO = acc[s][i][jb + 2][e], EE = acc[s][i][jb + 3][e];
+                        const double ek = EO + EE, ec = EO - EE;
+                        gv[s][0] = O1 + ek;
+                        gv[s][1] = O1 - ek;
+                        gv[s][2] = centre ? O2 : O2 + ec;
+                        gv[s][3] = O2 - ec;
+                    }
+                    if constexpr (EPI == EPI_STORE) {
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {
+                            double* o = outp + (long long)s * args.out_stride;
+#pragma unroll
+                            for (int p = 0; p < 4; ++p)
+                                if (p < np) o[offset(m, pos[p])] = gv[s][p];
+                        }
+                    } else if constexpr (EPI == EPI_UPDATE) {
+                        // U1 = What + tau Q3(fw) (stepper.cpp:253), checked (fail 3)
+                        double w[S][4];
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {
+                            const double* au = args.aux + (long long)s * args.aux_stride;
+#pragma unroll
+                            for (int p = 0; p < 4; ++p) w[s][p] = p < np ? __ldg(au + offset(m, pos[p])) : 0.0;
+                        }
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {
+                            double* o = outp + (long long)s * args.out_stride;
+#pragma unroll
+                            for (int p = 0; p < 4; ++p) {
+                                if (p >= np) break;
+                                const double u = w[s][p] + gv[s][p];
+                                bad |= !isfinite(u);
+                                o[offset(m, pos[p])] = u;
+                            }
+                        }
+                    } else {
+                        // EPI_WHAT_SRC: What -> out; f(t + tau, What) at the orbit (fail 2 / 5);
+                        // f - w2 (stepper.cpp:252; aux = w2 in physical space) written as
+                        // x_fwd_corr's level-2 stack (etd_fold2 positions) -> fout
+                        double w2[S][4];
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {
+                            const double* au = args.aux ? args.aux + (long long)s * args.aux_stride : nullptr;
+#pragma unroll
+                            for (int p = 0; p < 4; ++p) w2[s][p] = (au && p < np) ? __ldg(au + offset(m, pos[p])) : 0.0;
+                        }
+                        double fv[S][4];
+                        const int jj = m % args.ny_local + args.gj0, kz = m / args.ny_local + args.gz0;
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) {
+                            if (p >= np) {
+#pragma unroll
+                                for (int s = 0; s < S; ++s) fv[s][p] = 0.0;
+                                continue;
+                            }
+                            const int x = pos[p];
+                            if constexpr (S == 1) {
+                                double ustar = 0.0;
+                                if constexpr (SK == 4)
+                                    ustar = src_a * (args.sinx[x] * args.siny[jj] * (args.sinz ? args.sinz[kz] : 1.0));
+                                fv[0][p] = src1<SK>(args.sp, gv[0][p], ustar);
+                                if constexpr (SK == 3)
+                                    if (x == 0 && jj == 0 && kz == 0) fv[0][p] = __longlong_as_double(0x7ff8000000000000ll);
+                                bad |= !isfinite(fv[0][p]);
+                                dom |= src_domain_violation<SK>(gv[0][p]);
+                            } else {
+                                src2<SK>(args.sp, gv[0][p], gv[1][p], fv[0][p], fv[1][p]);
+                                bad |= !(isfinite(fv[0][p]) && isfinite(fv[1][p]));
+                            }
+#pragma unroll
+                            for (int s = 0; s < S; ++s) fv[s][p] -= w2[s][p];
+                        }
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {
+                            double* o = outp + (long long)s * args.out_stride;
+#pragma unroll
+                            for (int p = 0; p < 4; ++p)
+                                if (p < np) o[offset(m, pos[p])] = gv[s][p];
+                            // the orbit's level-2 stack (fold2_orbit): s_k, s_c, d_k +- d_c,
+                            // and for the centre orbit 2 f_centre at 2H - 1
+                            double* fo = args.fout + (long long)s * args.out_stride;
+                            const double sk = fv[s][0] + fv[s][1], dk = fv[s][0] - fv[s][1];
+                            fo[offset(m, fold2_spos(k, H))] = sk;
+                            if (centre) {
+                                fo[offset(m, 2 * H + k)] = dk + dk;
+                                fo[offset(m, 2 * H - 1)] = fv[s][2] + fv[s][2];
+                            } else {
+                                const double sc = fv[s][2] + fv[s][3], dc = fv[s][2] - fv[s][3];
+                                fo[offset(m, fold2_spos(c, H))] = sc;
+                                fo[offset(m, 2 * H + k)] = dk + dc;
+                                fo[offset(m, 3 * H + k)] = dk - dc;
+                            }
+                        }
+                    }
+                }
+        }
+    }
+
+    // ===================== status: abort flag and step commit (as etd_contract) =====================
+    const int any_dom = __syncthreads_or(dom);
+    const int any_bad = __syncthreads_or(bad);
+    if (tid == 0) {
+        if (any_dom || any_bad) {
+            int kind = EPI == EPI_WHAT_SRC ? 2 : EPI == EPI_UPDATE ? 3 : 1;
+            if (any_dom) kind = 5;
+            atomicCAS(&args.status->fail, 0, kind);
+        }
+        if (EPI == EPI_UPDATE && args.commit) {
+            __threadfence();
+            const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+            const unsigned prev = atomicAdd(&args.status->cta_done, 1u);
+            if (prev == total - 1) {
+                __threadfence();
+                args.status->cta_done = 0;
+                if (*reinterpret_cast<volatile int*>(&args.status->fail) == 0) {
+                    const long long nn = args.status->n + 1;
+                    args.status->n = nn;
+                    args.status->t = (double)nn * args.tau;
+                }
+            }
+        }
+    }
+}
+
+}  // namespace etd

@@ -119,6 +119,7 @@ struct ContractArgs {
     int sd_out;             // FOLD 5: store the even-mode pairs as (sigma, delta) = (X_q + X_{h-1-q},
                             // X_q - X_{h-1-q}) at (q, H + q): the level-2 backward's input (EPI_MIX: the
                             // mix outputs only; w2b stays in mode positions for EPI_CORR)
+    double* fout;           // etd_back6 EPI_WHAT_SRC: f(t + tau, What) - w2 as x_fwd_corr's level-2 stack
 };
 
 // ---------------------------------------------------------------- PTX helpers

@@ -97,6 +97,10 @@ static CUtensorMap make_map(const double* base, int rank, const unsigned long lo
 static KernelSpec pick(int mode, int S, int epi, bool pro, int sk = 0, int tile = 0, int fold = 0) {
     const bool uses_src = pro || epi == EPI_WHAT_SRC;
     if (!uses_src) sk = 0;
+    if (fold == 6) {
+        if (pro || tile == 1) throw ConfigError("no fused level-2 backward variant for this tile");
+        return pick_back6(mode, S, epi, sk, tile);
+    }
     return fold ? pick_fold(mode, S, epi, sk, tile, fold) : pick_dense(mode, S, epi, pro, sk, tile);
 }
 
@@ -465,6 +469,8 @@ struct Plan {
     double* GB[3] = {nullptr, nullptr, nullptr};
     double* GO[3] = {nullptr, nullptr, nullptr};     // level-2 backward: FOLD 4 over (sigma, delta)
     double* GE[3] = {nullptr, nullptr, nullptr};     //   and FOLD 2 over the odd-mode group
+    double* G6[3] = {nullptr, nullptr, nullptr};     // fused level-2 backward (etd_back6, back6_matrix)
+    bool back6 = false;                              // the level-2 backward runs fused (ETD_BACK6=0: r01 path)
     double* dvec = nullptr;          // [order 3][axis][slot 9][species 2][dmax]; order 1 = parity-major, 2 = level 2
     double* sintab[3] = {nullptr, nullptr, nullptr};  // sin(pi * coord) per axis (global extents)
     int dmax = 0;
@@ -500,7 +506,7 @@ struct Plan {
         for (double2* t : thfac) if (t) cudaFree(t);
         if (thscr) cudaFree(thscr);
         for (int a = 0; a < 3; ++a)
-            for (double* m : {PR[a], PTR[a], FF[a], FB[a], GA[a], GB[a], GO[a], GE[a]}) if (m) cudaFree(m);
+            for (double* m : {PR[a], PTR[a], FF[a], FB[a], GA[a], GB[a], GO[a], GE[a], G6[a]}) if (m) cudaFree(m);
         if (status) cudaFree(status);
         if (status_host) cudaFreeHost(status_host);
         if (mirror) cudaFreeHost(mirror);
@@ -569,6 +575,21 @@ struct Plan {
         return make_map(M, 3, dims, st, box);
     }
     static unsigned long long round16(unsigned long long x) { return (x + 15) / 16 * 16; }
+    // fused level-2 backward B (back6_matrix): 4H rows x H columns; mode 0 rows
+    // contiguous (leading dimension round16(H)), mode 1 the transpose [H][4H]
+    CUtensorMap mapB_back6(const double* M, int axis, int mode, int bn) const {
+        const unsigned long long H = fh[axis] / 2, R = (4 * H + 63) / 64 * 64;
+        if (mode == 0) {
+            const unsigned long long dims[2] = {H, R};
+            const unsigned long long st[1] = {round16(H)};
+            const unsigned box[2] = {16, (unsigned)bn};
+            return make_map(M, 2, dims, st, box);
+        }
+        const unsigned long long dims[3] = {16, H, R / 16};
+        const unsigned long long st[2] = {R, 16};
+        const unsigned box[3] = {16, 16, (unsigned)(bn / 16)};
+        return make_map(M, 3, dims, st, box);
+    }
 
     ContractArgs base_args(const View& v, int axis) const {
         ContractArgs a{};
@@ -741,7 +762,7 @@ struct Plan {
         if (part) {
             if (!fold2[axis] || back != (part >= 3) || pro || dense)
                 throw ConfigError("second-level split launch on an ineligible axis / direction");
-            fold = part == 1 ? 5 : part == 2 ? 4 : part == 3 ? 4 : 2;
+            fold = part == 1 ? 5 : part == 2 ? 4 : part == 3 ? 4 : part == 6 ? 6 : 2;
         } else if (fold == 1 && axis == 0) {
             if (epi == EPI_CORR) fold = 4;
             else if (in_rev) fold = 3;
@@ -762,14 +783,18 @@ struct Plan {
         //  * otherwise 2 CTAs/SM with 32 accumulators (T=3) when that fills two waves
         //  * else the 8-warp tile (T=0) when it fills two waves, else T=2
         const int H2 = fh[axis] / 2;
-        const int nrows = part ? 2 * H2 : fold ? 2 * fh[axis] : nax;  // B rows = N extent of the launch
+        const int nrows = part == 6 ? (4 * H2 + 63) / 64 * 64 : part ? 2 * H2 : fold ? 2 * fh[axis] : nax;  // B rows
         const int kext = part ? H2 : fold ? fh[axis] : nax;
         auto ctas = [&](int t) {
             const KernelSpec k = pick(mode, S, epi, pro, d.src_kind, t, fold);
             return (long long)((nrows + k.bn - 1) / k.bn) * ((mext + k.bm - 1) / k.bm) * gz;
         };
         int tile;
-        if (fold) {
+        if (fold == 6) {
+            // fused level-2 backward: 2 CTAs/SM with a 2-deep ring when that fills two
+            // waves, else the 1-CTA/SM 4-stage class, else the small tile
+            tile = ctas(3) >= 2 * 148 ? 3 : ctas(0) >= 148 ? 0 : 2;
+        } else if (fold) {
             // parity-split kernels (tools/tile_sweep.py on configs 1-4, profiles/r01_tile_sweep_fold.txt):
             //  * S = 4 has one class (32x128, 8 warps)
             //  * 2 CTAs/SM when that fills two waves, except the S = 2 update (T=3 spills)
@@ -786,13 +811,16 @@ struct Plan {
         else tile = 2;
         if (const char* f = std::getenv("ETD_FORCE_TILE"))  // tests: exercise every tile class
             if (f[0] >= '0' && f[0] <= '3' && f[1] == 0) tile = f[0] - '0';
+        if (fold == 6 && tile == 1) tile = 0;  // the fused backward has no 4-warp 64x64 class
         L.tile = tile;
         L.fold = fold;
         L.k = pick(mode, S, epi, pro, d.src_kind, tile, fold);
         const int loaded = pro ? S / 2 : S;
         L.tmA = mode == 0 ? mapA_x(v, in, loaded, L.k.bm, fstride) : mapA_yz(v, in, loaded, axis == 2, L.k.bm, fstride);
         L.tmA2 = fold == 3 ? mapA_x(v, in_rev, loaded, L.k.bm) : L.tmA;
-        if (part) {
+        if (part == 6) {
+            L.tmB = mapB_back6(G6[axis], axis, mode, L.k.bn);
+        } else if (part) {
             const double* M = part == 1 ? GA[axis] : part == 2 ? GB[axis] : part == 3 ? GO[axis] : GE[axis];
             L.tmB = mapB_fold(M, axis, mode, L.k.bn, H2);
         } else if (fold) {
@@ -823,6 +851,8 @@ struct Plan {
             L.args.fold_h = H2;
             L.args.kbase = 2 * H2;
             L.args.nbase = 2 * H2;
+        } else if (part == 6) {
+            L.args.fold_h = H2;          // the whole level-2 backward in one launch (etd_back6)
         }
         const unsigned gx = (nrows + L.k.bn - 1) / L.k.bn;
         const unsigned gy = (unsigned)((mext + L.k.bm - 1) / L.k.bm);
@@ -831,11 +861,12 @@ struct Plan {
         // executed (= algorithmic) FLOPs of this launch: 2 n per point dense,
         // 2 (2h) h / n per point split (half)
         L.flops = 2.0 * ((double)nrows * kext / nax) * pts * S;
-        L.dense_flops = 2.0 * nax * pts * S * (part ? 0.5 : 1.0);
+        L.dense_flops = 2.0 * nax * pts * S * ((part && part != 6) ? 0.5 : 1.0);
         int outs = S, aux = 0;
         if (epi == EPI_WHAT_SRC) outs = 2 * S;
         if (epi == EPI_CORR || epi == EPI_UPDATE) aux = S;
-        L.bytes = pts * 8.0 * (loaded + outs + aux) * (part ? 0.5 : 1.0);
+        if (part == 6 && epi == EPI_WHAT_SRC) aux = S;  // w2 in physical space
+        L.bytes = pts * 8.0 * (loaded + outs + aux) * ((part && part != 6) ? 0.5 : 1.0);
         return L;
     }
 
@@ -1130,6 +1161,39 @@ static void fold2_matrices(const std::vector<double>& Pc, int n, int mode, std::
     }
 }
 
+// Fused level-2 backward matrix G6 (etd_back6.cuh) of an axis with n = 4H - 1: 4H
+// rows, rounded up to whole 64-row block pairs (H = 8 mod 16: the odd-parity block
+// of the last pair), in blocks of 32 (block b: parity par = b & 1, orbit base kb = b >> 1), each
+// four 8-row fragments of type t = (r >> 3) & 3 for the orbit k = 16 kb + 2 (r & 7) + par;
+// H columns c:
+//   t 0  o_k:   P(k, 2c)                        (A: sigma for even k, delta for odd k)
+//   t 1  o_c':  P(c', 2c), c' = 2H - 2 - k;  the centre orbit k = H - 1: P(2H - 1, 2c)
+//   t 2  eo_k:  P(k, 4c + 1)                    (A: the odd modes 4c + 1 at [2H, 3H))
+//   t 3  ee_k:  P(k, 4c + 3), 0 for c = H - 1 and for the centre row k = H - 1
+// the same entries GO / GE hold (fold2_matrices), regrouped so one thread gets whole
+// orbits.  mode 0 rows contiguous (leading dimension round16(H)); mode 1 [H][4H].
+static int back6_rows(int H) { return (4 * H + 63) / 64 * 64; }  // whole (par 0, par 1) block pairs
+static void back6_matrix(const std::vector<double>& Pc, int n, int mode, std::vector<double>& g6) {
+    const int H = (n + 1) / 4, R = back6_rows(H);
+    const int ld = mode == 0 ? (H + 15) / 16 * 16 : R;
+    auto P = [&](int i, int k) { return Pc[(size_t)k * n + i]; };
+    g6.assign(mode == 0 ? (size_t)R * ld : (size_t)H * ld, 0.0);
+    auto at = [&](int r, int c) -> double& { return mode == 0 ? g6[(size_t)r * ld + c] : g6[(size_t)c * ld + r]; };
+    for (int r = 0; r < R; ++r) {
+        const int blk = r >> 5, t = (r >> 3) & 3, par = blk & 1, kb = blk >> 1;
+        const int k = 16 * kb + 2 * (r & 7) + par;
+        if (k >= H) continue;
+        for (int c = 0; c < H; ++c) {
+            double v = 0.0;
+            if (t == 0) v = P(k, 2 * c);
+            else if (t == 1) v = P(k == H - 1 ? 2 * H - 1 : 2 * H - 2 - k, 2 * c);
+            else if (t == 2) v = P(k, 4 * c + 1);
+            else if (k != H - 1 && c != H - 1) v = P(k, 4 * c + 3);
+            at(r, c) = v;
+        }
+    }
+}
+
 // Device bytes build_plan allocates (the memory guard and etd_plan_device_bytes):
 // state x2 + Z + W at 2 ns fields each; sharded: send blocks (ns fields), the
 // z-stage blocks zin/Zz/Wz (2 ns fields of this rank's y rows, full z) and the
@@ -1283,6 +1347,10 @@ static void build_plan(Plan& p, const etd_desc& d) {
         }
         // mixed levels are not scheduled: every axis keeps §4a then
         for (int a = 0; a < d.dim; ++a) p.fold2[a] = p.fold2[a] && p.fold2_all;
+        // level-2 backward transforms fused into one launch each;
+        // ETD_BACK6=0 keeps the two launches + etd_unfold2 pass of round 1 (A/B, tests)
+        const char* b6 = std::getenv("ETD_BACK6");
+        p.back6 = p.fold2_all && !(b6 && b6[0] == '0');
     }
     for (int a = 0; a < d.dim && p.thomas; ++a) {
         // build_thomas_payload (thomas.cpp:88-126) per species: c = tau diag k - s_l,
@@ -1347,6 +1415,12 @@ static void build_plan(Plan& p, const etd_desc& d) {
         ETD_CK(cudaMalloc(&p.PTR[a], ptr.size() * 8));
         ETD_CK(cudaMemcpy(p.PR[a], pr.data(), pr.size() * 8, cudaMemcpyHostToDevice));
         ETD_CK(cudaMemcpy(p.PTR[a], ptr.data(), ptr.size() * 8, cudaMemcpyHostToDevice));
+        if (p.fold2[a] && p.back6) {
+            std::vector<double> g6;
+            back6_matrix(Pc, n, a == 0 ? 0 : 1, g6);
+            ETD_CK(cudaMalloc(&p.G6[a], g6.size() * 8));
+            ETD_CK(cudaMemcpy(p.G6[a], g6.data(), g6.size() * 8, cudaMemcpyHostToDevice));
+        }
         if (p.fold2[a]) {
             std::vector<double> ga, gb, go, ge;
             fold2_matrices(Pc, n, a == 0 ? 0 : 1, ga, gb, fb2_tmp, &go, &ge);
@@ -1443,7 +1517,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
                     for (int pro = 0; pro < 2; ++pro)
                         for (int sk : {0, 1, 2, 3, 4, 5, 10, 11, 12, 13})
                             for (int tile = 0; tile < 4; ++tile)
-                                for (int fold = 0; fold < 6; ++fold) {
+                                for (int fold = 0; fold < 7; ++fold) {
                                     try {
                                         KernelSpec ks = pick(mode, S, e, pro != 0, sk, tile, fold);
                                         ETD_CK(cudaFuncSetAttribute(
@@ -1535,8 +1609,24 @@ static void build_plan(Plan& p, const etd_desc& d) {
         };
         // ... and every backward transform two launches into an intermediate stack
         // (in -> tmp) finished by etd_unfold2 (tmp -> out) with the stage epilogue.
+        // With p.back6 it is ONE fused launch (etd_back6: all four quarters, butterflies
+        // and the stage epilogue on the accumulators) straight from src to dst (src !=
+        // dst; tmp unused); S = 4 stacks run as two S = 2 launches.
         auto back2 = [&](const View& vv, const std::string& nm, int axis, int S, const double* src, double* tmp,
                          double* dst, int uf, const double* aux = nullptr, double* fout = nullptr) {
+            if (p.back6) {
+                if (src == dst) throw ConfigError("internal: fused backward in place");
+                const int epi = uf == UF_UPDATE ? EPI_UPDATE : uf == UF_WHAT_SRC ? EPI_WHAT_SRC : EPI_STORE;
+                const int nl = S == 4 ? 2 : 1;
+                for (int h2 = 0; h2 < nl; ++h2) {
+                    L.push_back(kernel_op(p.transform(vv, nl == 2 ? nm + (h2 ? "_b" : "_a") : nm, axis, true, S / nl,
+                                                      epi, false, src + 2 * h2 * vv.F, dst + 2 * h2 * vv.F, false,
+                                                      nullptr, false, 6)));
+                    L.back().L.args.aux = aux;
+                    L.back().L.args.fout = fout;
+                }
+                return;
+            }
             for (int part = 3; part <= 4; ++part) {
                 const std::string pn = nm + (part == 3 ? "_o" : "_e");
                 if (pairs && S == 4) {
@@ -1568,7 +1658,12 @@ static void build_plan(Plan& p, const etd_desc& d) {
         };
         if (p.dim == 3 && !p.sharded) {
             first_transform(V, 2, const_cast<double*>(in), p.Z, p.W);
-            if (f2) {
+            if (f2 && p.back6) {
+                // z_back fused (Z -> W physical), then the y stack pass (W -> Z)
+                back2(V, "z_back", 2, 2 * ns, p.Z, nullptr, p.W, UF_STORE);
+                L.push_back(p.fold_op(V, "fold_y_fwd", 1, p.W, p.Z, 2 * ns));
+                zy_fused = true;
+            } else if (f2) {
                 // z_back's launches (Z -> W), then its unfold fused with the y stack (W -> Z)
                 const bool pr = pairs && 2 * ns == 4;
                 for (int part = 3; part <= 4; ++part) {
@@ -1637,8 +1732,8 @@ static void build_plan(Plan& p, const etd_desc& d) {
             // ops a populated chunk emits: source (unless fused) + z_fwd launches + z_back
             // launches (+ the level-2 unfold); an empty chunk pads with as many no-ops so
             // every rank's op list stays aligned with rank 0's (group_steps, NCCL groups)
-            const int zl = (f2 && pairs && 2 * ns == 4) ? 2 : 1;  // launches per level-2 part
-            const int chunk_ops = fused ? 2 : f2 ? 1 + 2 * zl + 2 * zl + 1 : 3;
+            const int zl = (f2 && (pairs || p.back6) && 2 * ns == 4) ? 2 : 1;  // launches per level-2 part
+            const int chunk_ops = fused ? 2 : f2 ? 1 + 2 * zl + (p.back6 ? zl : 2 * zl + 1) : 3;
             for (int k = 0; k < C; ++k) {
                 const View& vk = p.zch[k];
                 const size_t first = L.size();
@@ -1685,9 +1780,30 @@ static void build_plan(Plan& p, const etd_desc& d) {
             } else {
                 first_transform(V, 1, const_cast<double*>(in), B2, B1);
             }
+            const size_t Fs = (size_t)ns * V.F;
+            if (p.back6) {
+                // fused backward launches never run in place:
+                //   y_back        B2 -> B1 (physical w1, w2);  Xa = B1, Xb = B2
+                //   x_fwd_mix     stack Xa -> Xb, launches Xb -> Xa[0, ns) (mix); w2 stays at Xa[ns, 2ns)
+                //   x_back_src    Xa[0, ns) -> What at Xb[0, ns), f(t + tau, What) - w2 stack at Xb[ns, 2ns)
+                //   x_fwd_corr    Xb[ns, 2ns) -> Xa[0, ns)
+                //   x_back_upd    Xa[0, ns) + What -> out (commits the step)
+                back2(V, "y_back", 1, 2 * ns, B2, nullptr, B1, UF_STORE);
+                double *Xa = B1, *Xb = B2;
+                const size_t mix0 = L.size();
+                fwd2(V, "x_fwd_mix", 0, 2 * ns, EPI_MIX, Xa, Xb, Xa, false, p.dv(0, 0), p.dv(0, 1));
+                for (size_t i = mix0; i < L.size(); ++i)
+                    if (L[i].kind == Op::KERNEL) L[i].L.args.mix_w2 = 0;
+                back2(V, "x_back_src", 0, ns, Xa, nullptr, Xb, UF_WHAT_SRC, Xa + Fs, Xb + Fs);
+                for (int part = 1; part <= 2; ++part) {
+                    L.push_back(kernel_op(p.transform(V, part == 1 ? "x_fwd_corr_even" : "x_fwd_corr_odd", 0, false,
+                                                      ns, EPI_SCALE, false, Xb + Fs, Xa, false, nullptr, false, part)));
+                    L.back().L.args.dA = p.dv(0, 2);
+                }
+                back2(V, "x_back_upd", 0, ns, Xa, nullptr, out, UF_UPDATE, Xb);
+            } else {
             back2(V, "y_back", 1, 2 * ns, B2, B1, B2, UF_STORE);
             double *Xa = B2, *Xb = B1;
-            const size_t Fs = (size_t)ns * V.F;
             // x_fwd_mix: mix (sigma/delta) -> Xa[0, ns); w2 stays in physical space at Xa[ns, 2ns)
             const size_t mix0 = L.size();
             fwd2(V, "x_fwd_mix", 0, 2 * ns, EPI_MIX, Xa, Xb, Xa, false, p.dv(0, 0), p.dv(0, 1));
@@ -1703,6 +1819,7 @@ static void build_plan(Plan& p, const etd_desc& d) {
             }
             // x_back_upd: U1 = What + tau Q3(fw) -> out (commits the step)
             back2(V, "x_back_upd", 0, ns, Xb, Xb + Fs, out, UF_UPDATE, Xa);
+            }
         } else {
         if (p.dim == 3) {
             L.push_back(kernel_op(p.transform(V, "y_fwd", 1, false, 2 * ns, EPI_SCALE, false, p.W, p.Z)));
@@ -2768,6 +2885,19 @@ int etd_setup_fold2_matrices(int n, int mode, double* ga, double* gb, double* fb
         return ETD_ERR_CONFIG;
     }
     return ETD_OK;
+}
+
+int etd_setup_back6_matrix(int n, int mode, double* g6) {
+    return guarded(nullptr, [&] {
+        const int h = (n + 1) / 2;
+        if (n < 3 || !(n & 1) || h % 16 != 0) throw etd::ConfigError("fused level-2 backward needs n = 32m - 1");
+        if (mode != 0 && mode != 1) throw etd::ConfigError("mode must be 0 or 1");
+        etd::AxisOperator op = etd::axis_operator(n, 0.0, 1.0, 1, 1.0, 0.0);
+        std::vector<double> Pc, lam, m6;
+        etd::eigensystem(op, Pc, lam);
+        etd::back6_matrix(Pc, n, mode, m6);
+        std::copy(m6.begin(), m6.end(), g6);
+    });
 }
 
 int etd_fold_level(const etd_handle* h, int* out) {

@@ -72,5 +72,7 @@ static KernelSpec spec() {
 KernelSpec pick_dense(int mode, int S, int epi, bool pro, int sk, int tile);
 KernelSpec pick_fold(int mode, int S, int epi, int sk, int tile, int fold);
 KernelSpec pick_fold2(int mode, int S, int epi, int sk, int tile, int fold);
+// fused level-2 backward (etd_back6.cuh, "FOLD 6"): tiles 0, 2, 3
+KernelSpec pick_back6(int mode, int S, int epi, int sk, int tile);
 
 }  // namespace etd

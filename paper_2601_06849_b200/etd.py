@@ -239,6 +239,7 @@ def lib():
         L.etd_parity_split.argtypes = [vp, C.POINTER(C.c_int)]
         L.etd_setup_fold_matrices.argtypes = [i, i, vp, vp]
         L.etd_setup_fold2_matrices.argtypes = [i, i, vp, vp, vp, vp, vp]
+        L.etd_setup_back6_matrix.argtypes = [i, i, vp]
         L.etd_fold_level.argtypes = [vp, C.POINTER(C.c_int)]
         L.etd_debug_transform.argtypes = [vp, i, i, i, i, i, vp, vp]
         L.etd_fill_config_ic.argtypes = [i, C.c_ulonglong, i, i, i, i, vp]

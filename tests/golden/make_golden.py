@@ -54,6 +54,10 @@ def main():
         ("system2d_fhn", 2, 15, 0.05, 1e-3, 5e-4, 0.0, 0, 10, (0.1, 0.01, 0.5), 5),
         ("system2d_fhn_classic_p04", 2, 12, 0.01, 0.01, 10.0, 0.0, 1, 11, (1.0, 1.0), 4),
         ("system3d_fhn", 3, 9, 0.05, 1e-3, 5e-4, 0.0, 0, 10, (0.1, 0.01, 0.5), 4),
+        # q != 0: the unit-kappa operator carries q/dim per axis and kappa_c scales the
+        # whole eigenvalue, q term included (system_stepper.cpp:52-61)
+        ("system2d_fhn_q", 2, 14, 0.05, 2e-2, 5e-3, 0.6, 1, 10, (0.1, 0.01, 0.5), 4),
+        ("system3d_fhn_q", 3, 10, 0.05, 2e-2, 5e-3, 0.9, 0, 10, (0.1, 0.01, 0.5), 3),
         ("cfg4_physics_n11", 3, 11, 0.05, 1e-3, 5e-4, 0.0, 0, 10, (0.1, 0.01, 0.5), 3),
     ]
     for name, dim, n, tau, ku, kv, q, fam, kind, params, steps in system:

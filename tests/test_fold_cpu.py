@@ -255,3 +255,93 @@ def test_fold2_backward_reproduces_dense_transform(n, mode):
     nat = np.zeros_like(gh)
     nat[:, modes] = gh
     assert np.max(np.abs(fold2_backward(gh, GO, GE, n) - nat @ P.T)) <= 1e-13 * n
+
+
+# ---------------------------------------------------------------- fused level-2 backward
+def back6_mat(n, mode):
+    H = (n + 1) // 4
+    R = (4 * H + 63) // 64 * 64                    # whole (par 0, par 1) block pairs
+    ld = (H + 15) // 16 * 16 if mode == 0 else R
+    g6 = np.zeros(R * ld if mode == 0 else H * ld)
+    assert etd.lib().etd_setup_back6_matrix(n, mode, g6.ctypes.data_as(C.c_void_p)) == 0
+    return g6.reshape(R, ld)[:, :H] if mode == 0 else g6.reshape(H, R).T
+
+
+def back6_backward(st, G6, n):
+    """etd_back6 restated: the input stack [sigma | delta | Y_lo | Y_hi] (4 boxes of H
+    along the axis), B rows in 32-row blocks (parity b & 1, orbit base b >> 1) of four
+    fragments (o_k, o_c', eo_k, ee_k), fragment A box = parity for types 0/1, else the
+    type; the orbit epilogue e = eo +- ee, g = o +- e at k, n-1-k, c', n-1-c'."""
+    H = (n + 1) // 4
+    boxes = [st[..., q * H:(q + 1) * H] for q in range(3)]
+    boxes.append(np.concatenate([st[..., 3 * H:], np.zeros(st.shape[:-1] + (1,))], -1))
+    acc = {}
+    for r in range(G6.shape[0]):
+        blk, t = r >> 5, (r >> 3) & 3
+        par, kb = blk & 1, blk >> 1
+        k = 16 * kb + 2 * (r & 7) + par
+        if k >= H:
+            assert not G6[r].any()
+            continue
+        box = par if t < 2 else t
+        acc[(k, t)] = boxes[box] @ G6[r]
+    out = np.zeros(st.shape[:-1] + (n,))
+    for k in range(H):
+        O1, O2, EO, EE = (acc[(k, t)] for t in range(4))
+        ek, ec = EO + EE, EO - EE
+        out[..., k] = O1 + ek
+        out[..., n - 1 - k] = O1 - ek
+        if k == H - 1:
+            out[..., 2 * H - 1] = O2            # the centre o_{2H-1}
+        else:
+            c = 2 * H - 2 - k
+            out[..., c] = O2 + ec
+            out[..., n - 1 - c] = O2 - ec
+    return out
+
+
+@pytest.mark.parametrize("n", [31, 63, 127, 255, 511, 1023])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_back6_equals_two_launch_backward_bitwise(n, mode):
+    """G6 holds exactly GO's and GE's entries, regrouped: every accumulator is the
+    same dot product of the same vectors, so the fused backward equals the round-1
+    two-launch + unfold path bit for bit, and the dense transform to rounding."""
+    _, _, _, GO, GE = fold2_mats(n, mode)
+    G6 = back6_mat(n, mode)
+    h = (n + 1) // 2
+    H = h // 2
+    gh = np.random.default_rng(n + 11).uniform(-1, 1, (4, n))   # level-2 positions
+    q = np.arange(H)
+    st = np.concatenate([gh[:, q] + gh[:, h - 1 - q], gh[:, q] - gh[:, h - 1 - q], gh[:, 2 * H:]], -1)
+    got = back6_backward(st, G6, n)
+    assert np.max(np.abs(got - fold2_backward(gh, GO, GE, n))) <= 1e-15 * n
+    # bitwise: every G6 row is the GO / GE row of the same output
+    for r in range(G6.shape[0]):
+        blk, t = r >> 5, (r >> 3) & 3
+        k = 16 * (blk >> 1) + 2 * (r & 7) + (blk & 1)
+        if k >= H:
+            continue
+        if t < 2:
+            i = k if t == 0 else (2 * H - 1 if k == H - 1 else 2 * H - 2 - k)
+            ro = ((i >> 1) >> 3) * 16 + (i & 1) * 8 + ((i >> 1) & 7)   # GO row of output i = 2q + group
+            assert np.array_equal(G6[r], GO[ro])
+        else:
+            ro = (k >> 3) * 16 + (t - 2) * 8 + (k & 7)                   # GE row of (k, group t - 2)
+            assert np.array_equal(G6[r], GE[ro])
+    P, _ = Oracle.spectral_factor(n, 2.0, -1.0)
+    P = np.asarray(P).reshape(n, n).T if np.asarray(P).ndim == 1 else np.asarray(P)
+    nat = np.zeros_like(gh)
+    nat[:, fold2_modes(n)] = gh
+    assert np.max(np.abs(got - nat @ P.T)) <= 1e-13 * n
+    # the centre row of ee and its last column are exact zeros (odd group: 2H - 1 modes)
+    for r in range(G6.shape[0]):
+        blk, t = r >> 5, (r >> 3) & 3
+        k = 16 * (blk >> 1) + 2 * (r & 7) + (blk & 1)
+        if t == 3 and k < H:
+            assert G6[r, H - 1] == 0.0 and (k != H - 1 or not G6[r].any())
+
+
+def test_back6_matrix_rejects_ineligible_sizes():
+    p = C.c_void_p(0)
+    assert etd.lib().etd_setup_back6_matrix(47, 0, p) != 0
+    assert etd.lib().etd_setup_back6_matrix(64, 1, p) != 0

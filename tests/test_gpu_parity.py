@@ -79,8 +79,12 @@ def test_scalar_steps_vs_reference(dim, n, steps, family):
 
 @pytest.mark.parametrize("dim,n,steps", [(2, 63, 6), (3, 31, 4), (3, 17, 3)])
 @pytest.mark.parametrize("src", ["fhn_cubic", "fhn_classic"])
-def test_system_steps_vs_reference(dim, n, steps, src):
-    tau, ku, kv = 0.05, 1e-3, 5e-4
+@pytest.mark.parametrize("q", [0.0, 0.8])
+def test_system_steps_vs_reference(dim, n, steps, src, q):
+    """Two species against the reference: 2D through its make_system_plan, 3D the
+    composed step.  q != 0 checks that kappa_c scales the unit-kappa eigenvalue
+    with its q/dim term (system_stepper.cpp:52-61)."""
+    tau, ku, kv = 0.05, 2e-2 if q else 1e-3, 5e-4
     rng = np.random.default_rng(4)
     u0, v0 = rng.uniform(-1, 1, n ** dim), rng.uniform(-1, 1, n ** dim)
     if src == "fhn_cubic":
@@ -88,9 +92,9 @@ def test_system_steps_vs_reference(dim, n, steps, src):
     else:
         f, kind, params = etd.fhn_classic(1.0, 1.0), 11, (1.0, 1.0)
     g = etd.unit_box_grid(dim, n + 1)
-    plan = etd.make_system_plan(g, tau, ku, kv, 0.0)
+    plan = etd.make_system_plan(g, tau, ku, kv, q)
     got = etd.etd2rkds_step_system(plan, etd.SystemState(0, 0.0, u0, v0), f, nsteps=steps)
-    wu, wv, nn, tt = ref_or_oracle().system_run(dim, n, tau, ku, kv, 0.0, u0, v0, steps, src_kind=kind,
+    wu, wv, nn, tt = ref_or_oracle().system_run(dim, n, tau, ku, kv, q, u0, v0, steps, src_kind=kind,
                                                  src_params=params)[:4]
     assert got.n == nn
     assert rel_gap(wu, got.U) <= STEP_TOL and rel_gap(wv, got.V) <= STEP_TOL
@@ -103,6 +107,27 @@ def test_config_shapes_vs_reference(cfg_id, n, steps):
     cfg = configs.CONFIGS[cfg_id]
     ics = configs.initial_state(cfg, n)
     plan = configs.make_plan(cfg, n)
+    R = ref_or_oracle()
+    if cfg.nspecies == 1:
+        got = etd.advance(plan, etd.StepperState(0, 0.0, ics[0]), cfg.source, nsteps=steps)
+        want = R.scalar_run(cfg.dim, n, cfg.tau, cfg.kappa[0], cfg.q, ics[0], steps, src_kind=1)[0]
+        assert rel_gap(want, got.U) <= STEP_TOL
+    else:
+        got = etd.etd2rkds_step_system(plan, etd.SystemState(0, 0.0, ics[0], ics[1]), cfg.source, nsteps=steps)
+        wu, wv = R.system_run(cfg.dim, n, cfg.tau, cfg.kappa[0], cfg.kappa[1], cfg.q, ics[0], ics[1], steps,
+                              src_kind=10, src_params=(0.1, 0.01, 0.5))[:2]
+        assert rel_gap(wu, got.U) <= STEP_TOL and rel_gap(wv, got.V) <= STEP_TOL
+
+
+@pytest.mark.parametrize("cfg_id,n,steps", [(3, 127, 3), (2, 127, 4), (1, 767, 6)])
+def test_default_level2_schedule_vs_reference(cfg_id, n, steps):
+    """BASELINE physics at sizes where the default plan picks the second-level split
+    by itself (>= 2^18 points, n = 32m - 1): the shipped schedule, not a forced
+    one, against the reference CPU implementation."""
+    cfg = configs.CONFIGS[cfg_id]
+    plan = configs.make_plan(cfg, n)
+    assert plan.fold_level()[:cfg.dim] == (2,) * cfg.dim
+    ics = configs.initial_state(cfg, n)
     R = ref_or_oracle()
     if cfg.nspecies == 1:
         got = etd.advance(plan, etd.StepperState(0, 0.0, ics[0]), cfg.source, nsteps=steps)

@@ -5,8 +5,8 @@ host cores and a call is capped at one hour.
   python tools/parity_cfg4_full.py part1 OUT.jsonl   # reference steps 0 -> 10, ETRD checkpoint in /tmp
   python tools/parity_cfg4_full.py part2 OUT.jsonl   # restart from the checkpoint, steps 10 -> 20
 
-Each part also runs the device path (default schedule, and ETD_DENSE=1 dense
-transforms) to the same step and records max|a-b|/max|a| against the reference.
+Each part also runs the device path (default schedule, ETD_DENSE=1 dense
+transforms, optionally ETD_BACK6=0: ETD_PARITY_SCHEDULES) to the same step and records max|a-b|/max|a| against the reference.
 The checkpoint is written and read with the reference's own save_field /
 load_field (ETRD, field.cpp:46-81), so the restart is the reference's own.  Part 2
 needs part 1's checkpoint on the same box (gpurun reuses a box for a call that
@@ -32,13 +32,17 @@ CK = "/tmp/etd_cfg4_ref_step{step}_{sp}.etrd"
 SAMPLE_STRIDE = 4099
 
 
-def gpu_run(cfg, n, ics, steps, dense):
-    if dense:
-        os.environ["ETD_DENSE"] = "1"
+SCHEDULES = {"default": {}, "dense": {"ETD_DENSE": "1"}, "r01_unfold": {"ETD_BACK6": "0"}}
+
+
+def gpu_run(cfg, n, ics, steps, name):
+    env = SCHEDULES[name]
+    os.environ.update(env)
     try:
         plan = configs.make_plan(cfg, n)
     finally:
-        os.environ.pop("ETD_DENSE", None)
+        for k in env:
+            os.environ.pop(k, None)
     t0 = time.time()
     g = etd.etd2rkds_step_system(plan, etd.SystemState(0, 0.0, ics[0], ics[1]), cfg.source, nsteps=steps)
     sec = time.time() - t0
@@ -76,24 +80,26 @@ def main():
         np.savez(os.path.join(ROOT, "gpurun_out", "r02_cfg4_ref_step20_sample.npz"), idx=idx,
                  u=ref[0][idx], v=ref[1][idx], stride=SAMPLE_STRIDE)
     ics = configs.initial_state(cfg, n)
-    gpu = {}
-    for dense in (False, True):
-        st, sec, lvl = gpu_run(cfg, n, ics, s1, dense)
-        gpu["dense" if dense else "default"] = ([rel_gap(a, b) for a, b in zip(ref, st)],
-                                                [float(np.max(np.abs(a - b))) for a, b in zip(ref, st)],
-                                                [bool(np.all(np.isfinite(b))) for b in st], sec, lvl)
-        del st
-    for name, (gaps, diffs, fin, sec, lvl) in gpu.items():
+    # one record per schedule, written as soon as it is measured (a failing schedule
+    # must not lose the reference run)
+    for name in os.environ.get("ETD_PARITY_SCHEDULES", "default,dense").split(","):
+        try:
+            st, sec, lvl = gpu_run(cfg, n, ics, s1, name)
+        except Exception as e:
+            print(json.dumps({"schedule": name, "error": repr(e)}), flush=True)
+            continue
         rec = {"config": 4, "n": n, "steps": s1, "reference_steps_this_call": [s0, s1],
                "schedule": name, "fold_level": list(lvl),
-               "rel_gap": gaps, "max_abs_diff": diffs,
+               "rel_gap": [rel_gap(a, b) for a, b in zip(ref, st)],
+               "max_abs_diff": [float(np.max(np.abs(a - b))) for a, b in zip(ref, st)],
                "max_abs_ref": [float(np.max(np.abs(a))) for a in ref],
-               "finite": fin,
+               "finite": [bool(np.all(np.isfinite(b))) for b in st],
                "tolerance": 1e-11, "gpu_wall_s": round(sec, 2), "ref_wall_s": round(t_ref, 1),
                "ref": (f"oracle/_ref (unmodified etdrd core, OpenBLAS {cores} threads), 3D two-species step "
                        "composed from reference primitives (system_stepper.cpp:74-114 + stepper.cpp:244-247)"
                        + ("" if part == "part1" else f"; restarted at step {s0} from the reference's own ETRD "
                                                        "save_field/load_field checkpoint"))}
+        del st
         rec["pass"] = all(x <= 1e-11 for x in rec["rel_gap"]) and all(rec["finite"])
         print(json.dumps(rec), flush=True)
         with open(out, "a") as f:
