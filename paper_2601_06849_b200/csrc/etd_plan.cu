@@ -484,6 +484,7 @@ struct Plan {
     void* comm = nullptr;            // ncclComm_t
     cudaStream_t cstream = nullptr;  // host<->device copy stream of the pipelined advance
     std::vector<cudaEvent_t> xev;    // its chunk events
+    int state_fields = 0;            // fields per state buffer (ns on the level-2 schedule, else 2 ns)
     double* mirror = nullptr;        // pinned host mirror of the state (pageable etd_advance buffers)
     size_t mirror_elems = 0;
     // BackendKind::Thomas: per-axis factors [species][pole][mul, piv, 1/piv][n],
@@ -1195,11 +1196,30 @@ static void back6_matrix(const std::vector<double>& Pc, int n, int mode, std::ve
 }
 
 // Device bytes build_plan allocates (the memory guard and etd_plan_device_bytes):
-// state x2 + Z + W at 2 ns fields each; sharded: send blocks (ns fields), the
+// state x2 (ns fields on the level-2 schedule, else 2 ns) + Z + W at 2 ns fields each; sharded: send blocks (ns fields), the
 // z-stage blocks zin/Zz/Wz (2 ns fields of this rank's y rows, full z) and the
 // receive blocks (2 ns fields); per axis P and P^T plus the split matrices
 // (<= 6 npad^2); Thomas factors and checkpoints; 64 MiB for descriptors,
 // d-vectors, tables and the allocator's rounding.
+// Whether a plan runs the second-level split schedule on every axis (the decision
+// build_plan makes, restated from the desc and the A/B environment switches): its
+// source pass writes the first transform's stack into scratch, so the state
+// buffers need no f slots (ns fields instead of [U,(V),fU,(fV)]).
+static bool level2_schedule(const etd_desc& d) {
+    if (d.backend == ETD_THOMAS) return false;
+    auto env_is = [](const char* k, char c) { const char* e = std::getenv(k); return e && e[0] == c; };
+    if (env_is("ETD_DENSE", '1') || env_is("ETD_FUSED_SOURCE", '1') || env_is("ETD_FOLD2", '0')) return false;
+    const char* fa = std::getenv("ETD_FOLD_AXES");
+    const int axes = fa ? std::atoi(fa) : 7;
+    const double npts = (double)d.n[0] * d.n[1] * (d.dim == 3 ? d.n[2] : 1);
+    if (!(env_is("ETD_FOLD2", '1') || npts >= 262144.0)) return false;
+    for (int a = 0; a < d.dim; ++a) {
+        const int h = (d.n[a] + 1) / 2;
+        if (!(h % 16 == 0 && (d.n[a] & 1) && (axes >> a & 1))) return false;
+    }
+    return true;
+}
+
 static unsigned long long plan_device_bytes(const etd_desc& d) {
     const int G = d.world_size < 1 ? 1 : d.world_size;
     const int nz = d.dim == 3 ? d.n[2] : 1;
@@ -1210,7 +1230,8 @@ static unsigned long long plan_device_bytes(const etd_desc& d) {
         partition(d.n[1], G, d.rank, j0, j1);
     }
     const unsigned long long F = pitch * d.n[1] * (z1 - z0), ns = d.nspecies;
-    unsigned long long b = 4ull * F * 2 * ns * 8;
+    const unsigned long long sf = level2_schedule(d) ? ns : 2 * ns;  // fields per state buffer
+    unsigned long long b = (2ull * sf + 2ull * 2 * ns) * F * 8;
     if (G > 1) {
         const unsigned long long Fz = pitch * (j1 - j0) * nz;
         b += F * ns * 8 + 3ull * Fz * 2 * ns * 8 + F * 2 * ns * 8;
@@ -1295,7 +1316,10 @@ static void build_plan(Plan& p, const etd_desc& d) {
         ETD_CK(cudaMemsetAsync(ptr, 0, elems * sizeof(double), p.stream));  // pads stay +0.0 forever
     };
     const size_t F = (size_t)p.slab.F;
-    for (int s = 0; s < 2; ++s) alloc(p.state[s], F * 2 * p.ns);  // [U,(V),fU,(fV)]
+    // [U,(V),fU,(fV)]; the level-2 schedule's source pass writes f into the first
+    // transform's stack in scratch, so its state buffers hold only U(,V)
+    p.state_fields = level2_schedule(d) ? p.ns : 2 * p.ns;
+    for (int s = 0; s < 2; ++s) alloc(p.state[s], F * p.state_fields);
     alloc(p.Z, F * 2 * p.ns);
     alloc(p.W, F * 2 * p.ns);
     if (p.sharded) {
@@ -1347,6 +1371,8 @@ static void build_plan(Plan& p, const etd_desc& d) {
         }
         // mixed levels are not scheduled: every axis keeps §4a then
         for (int a = 0; a < d.dim; ++a) p.fold2[a] = p.fold2[a] && p.fold2_all;
+        if (p.fold2_all != level2_schedule(d))
+            throw ConfigError("internal: level-2 schedule decision differs from the state allocation");
         // level-2 backward transforms fused into one launch each;
         // ETD_BACK6=0 keeps the two launches + etd_unfold2 pass of round 1 (A/B, tests)
         const char* b6 = std::getenv("ETD_BACK6");
@@ -2555,10 +2581,17 @@ static void debug_transform(Plan& p, int species, int axis, int back, int ell, i
                 f.args.dA = p.dv(axis, 6 + ell - 1) + species * p.dmax;
                 launch(f, p.stream);
             }
-            for (int part = 3; part <= 4; ++part)
-                launch(p.transform(v, "dbg_back", axis, true, 1, EPI_STORE, false, p.Z, tmp, false, nullptr, false, part),
+            if (p.back6) {
+                launch(p.transform(v, "dbg_back", axis, true, 1, EPI_STORE, false, p.Z, p.W + v.F, false, nullptr,
+                                   false, 6),
                        p.stream);
-            run_op(p, p.unfold_op(v, "dbg_unfold", axis, UF_STORE, tmp, p.W + v.F, 1), p.stream);
+            } else {
+                for (int part = 3; part <= 4; ++part)
+                    launch(p.transform(v, "dbg_back", axis, true, 1, EPI_STORE, false, p.Z, tmp, false, nullptr, false,
+                                       part),
+                           p.stream);
+                run_op(p, p.unfold_op(v, "dbg_unfold", axis, UF_STORE, tmp, p.W + v.F, 1), p.stream);
+            }
             result = p.W + v.F;
         } else {
         if (axis == 0 && p.fold[0]) {

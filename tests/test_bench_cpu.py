@@ -31,8 +31,8 @@ def test_self_launch_two_ranks_dry_run():
     b0, b1 = line["per_rank_device_bytes"]
     assert 0 < b1 <= b0 < 170e9
     single = run_bench("--dry-run")["per_rank_device_bytes"][0]
-    # config 4 on one GPU: 8 fields per species (state x2, Z, W at [U,V,fU,fV]) at pitch 1024
-    assert 8 * 2 * 1024 * 1023 * 1023 * 8 <= single < 170e9
+    # config 4 on one GPU, level-2 schedule: 12 fields (state x2 [U,V], Z and W [U,V,fU,fV]) at pitch 1024
+    assert 12 * 1024 * 1023 * 1023 * 8 <= single < 12 * 1024 * 1023 * 1023 * 8 + 3e8  # + matrices, tables
 
 
 def test_gpus_mismatch_is_refused():
@@ -46,8 +46,8 @@ def test_plan_device_bytes_and_memory_cap():
     import paper_2601_06849_b200 as etd
     g = etd.unit_box_grid(3, 1024)
     one = etd.plan_device_bytes(g, 2)
-    assert one > 130e9  # config 4 does not fit one GPU twice over
+    assert 100e9 < one < 110e9  # config 4 on one GPU: 12 fields of 8.57 GB + matrices
     per = [etd.plan_device_bytes(g, 2, 8, r) for r in range(8)]
-    assert max(per) < one / 3  # 17 slab-fields per rank (state x2, Z, W, exchange blocks) of 8 at G = 8
+    assert max(per) < one / 3  # 15 slab-fields per rank (state x2, Z, W, exchange blocks) of 8 at G = 8
     with pytest.raises(etd.ConfigError):
         etd.plan_device_bytes(g, 2, 2000, 0)  # more ranks than z planes

@@ -13,20 +13,27 @@ from paper_2601_06849_b200 import configs
 pytestmark = pytest.mark.gpu
 
 STAGES_L1 = ["z_fwd", "z_back", "y_fwd", "y_back", "x_fwd_mix", "x_back_src", "x_fwd_corr", "x_back_upd"]
-STAGES_L2 = [f"{s}_{h}" for s in ["z_fwd_even", "z_fwd_odd", "z_back_o", "z_back_e", "y_fwd_even", "y_fwd_odd",
-                                   "y_back_o", "y_back_e", "x_fwd_mix_even", "x_fwd_mix_odd"] for h in "ab"] + \
-            ["x_back_src_o", "x_back_src_e", "x_fwd_corr_even", "x_fwd_corr_odd", "x_back_upd_o", "x_back_upd_e"]
+STAGES_L2_R01 = [f"{s}_{h}" for s in ["z_fwd_even", "z_fwd_odd", "z_back_o", "z_back_e", "y_fwd_even", "y_fwd_odd",
+                                       "y_back_o", "y_back_e", "x_fwd_mix_even", "x_fwd_mix_odd"] for h in "ab"] + \
+                ["x_back_src_o", "x_back_src_e", "x_fwd_corr_even", "x_fwd_corr_odd", "x_back_upd_o", "x_back_upd_e"]
+# default level 2: every backward transform is one fused launch (etd_back6)
+STAGES_L2 = ["z_fwd_even_a", "z_fwd_even_b", "z_fwd_odd_a", "z_fwd_odd_b", "z_back_a", "z_back_b",
+             "y_fwd_even_a", "y_fwd_even_b", "y_fwd_odd_a", "y_fwd_odd_b", "y_back_a", "y_back_b",
+             "x_fwd_mix_even_a", "x_fwd_mix_even_b", "x_fwd_mix_odd_a", "x_fwd_mix_odd_b", "x_back_src",
+             "x_fwd_corr_even", "x_fwd_corr_odd", "x_back_upd"]
 
 
-@pytest.mark.parametrize("level", [1, 2])
+@pytest.mark.parametrize("level", ["1", "2", "2-r01"])
 def test_stage_kernels_are_deterministic(level, monkeypatch):
-    if level == 1:
+    if level == "1":
         monkeypatch.setenv("ETD_FOLD2", "0")
+    if level == "2-r01":
+        monkeypatch.setenv("ETD_BACK6", "0")
     cfg = configs.CONFIGS[4]
     n = 383
     plan = configs.make_plan(cfg, n)
-    assert plan.fold_level() == (level,) * 3
-    stages = STAGES_L2 if level == 2 else STAGES_L1
+    assert plan.fold_level() == (int(level[0]),) * 3
+    stages = {"1": STAGES_L1, "2": STAGES_L2, "2-r01": STAGES_L2_R01}[level]
     assert [s["name"] for s in plan.stage_stats() if s["flops_per_launch"] > 0] == stages
     for s, a in enumerate(configs.initial_state(cfg, n)):
         plan.upload(s, a)
