@@ -167,10 +167,9 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
             }
             mma(stage, st, fa[cur]);
             if (st == BK / 4 - 1) {
-                // release only after the DMMAs that consumed this stage's last
-                // fragments have issued (etd_contract: the stage-release race)
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[stage]);
+                // every LDS of this stage is ordered before the TMA refill
+                // (consumer_release: generic -> async proxy fence, then arrive)
+                consumer_release(&empty[stage], lane);
             }
         }
         if (tid == 0 && kt + STAGES < KT) {

@@ -137,6 +137,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Consumer release of a ring slot that TMA (the async proxy) refills after the
+// empty barrier completes.  The slot was read with generic-proxy LDS; without a
+// proxy fence ptxas may issue the arrive while those loads are still in flight
+// (observed: SYNCS.ARRIVE right after the last LDS.64 of the stage, ahead of the
+// DMMAs that consume them), and the refill then races them.  Every lane orders
+// its own shared reads before the async proxy's writes, then lane 0 arrives.
+__device__ __forceinline__ void consumer_release(uint64_t* bar, int lane) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -465,8 +476,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                     // LDS of this stage is still in flight when the producer's TMA
                     // refills the slot (releasing right after *issuing* the last
                     // loads was a WAR race on the slot).
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[stage]);
+                    consumer_release(&empty[stage], lane);
                 }
                 if (st < BK / 4 - 1 || kt + 1 < KT) combine(fa[nxt], fa2[nxt]);
                 if (st < BK / 4 - 1) apply_src(kt, st + 1, fa[nxt]);

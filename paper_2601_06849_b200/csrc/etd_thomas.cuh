@@ -196,8 +196,7 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
     };
     auto release = [&]() {
         const int slot = q % S;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
+        consumer_release(&empty[slot], lane);
         ++q;
         // refill the slot of the stage before last (every warp is normally past it)
         if (t == 0)

@@ -207,7 +207,8 @@ def test_fold2_non_cubic_system_vs_dense(shape, monkeypatch):
     u0, v0 = rng.uniform(-1, 1, N), rng.uniform(-0.5, 0.5, N)
     p = etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0)
     assert p.fold_level() == (2, 2, 2)
-    assert any(s["name"] == "z_back_y_stack" for s in p.stage_stats())
+    # fused backward (default): z_back then the y stack pass; r01 path: z unfold + y stack in one pass
+    assert any(s["name"] in ("fold_y_fwd", "z_back_y_stack") for s in p.stage_stats())
     got = etd.etd2rkds_step_system(p, etd.SystemState(0, 0.0, u0, v0), etd.fhn_cubic(), nsteps=3)
     monkeypatch.setenv("ETD_DENSE", "1")
     pd = etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0)
@@ -215,10 +216,13 @@ def test_fold2_non_cubic_system_vs_dense(shape, monkeypatch):
     assert rel_gap(d.U, got.U) <= 1e-13 and rel_gap(d.V, got.V) <= 1e-13
 
 
+@pytest.mark.parametrize("back6", ["1", "0"])
 @pytest.mark.parametrize("shape", [(127, 95, 63), (95, 63, 1)])
-def test_fold2_pipelined_advance_ragged_chunks_bitwise(shape):
+def test_fold2_pipelined_advance_ragged_chunks_bitwise(shape, back6, monkeypatch):
     """etd_advance (column-chunked z / y stages, row-chunked x stage) on the level-2
-    schedule equals upload + etd_step + download bitwise, 3D and 2D."""
+    schedule equals upload + etd_step + download bitwise, 3D and 2D; fused backward
+    launches (default) and the round-1 two-launch + unfold path (ETD_BACK6=0)."""
+    monkeypatch.setenv("ETD_BACK6", back6)
     nx, ny, nz = shape
     dim = 3 if nz > 1 else 2
     g = etd.build_grid(dim, [(0, 1)] * dim, [s + 1 for s in shape[:dim]])
@@ -233,3 +237,26 @@ def test_fold2_pipelined_advance_ragged_chunks_bitwise(shape):
     plan.upload(1, v0)
     plan.step(2)
     assert np.array_equal(plan.download(0)[0], st.U) and np.array_equal(plan.download(1)[0], st.V)
+
+
+@pytest.mark.parametrize("dim,n", [(3, 255), (2, 1023)])
+def test_fused_backward_bitwise_equals_two_launch_path(dim, n, monkeypatch):
+    """The fused level-2 backward (etd_back6) accumulates every output with the same
+    DMMA sequence as the two launches + unfold pass it replaces (G6 holds GO / GE's
+    rows, tests/test_fold_cpu.py), so whole steps are bitwise equal; at n = 255 the
+    k loop refills the 2-stage ring (the proxy-fenced release, etd_kernels.cuh)."""
+    g = etd.unit_box_grid(dim, n + 1)
+    rng = np.random.default_rng(n + dim)
+    N = n ** dim
+    u0, v0 = rng.uniform(-1, 1, N), rng.uniform(-0.5, 0.5, N)
+    out = []
+    for b6 in ("1", "0"):
+        monkeypatch.setenv("ETD_BACK6", b6)
+        p = etd.make_system_plan(g, 0.05, 1e-3, 5e-4, 0.0, source=etd.fhn_cubic())
+        assert p.fold_level() == (2,) * dim
+        p.upload(0, u0)
+        p.upload(1, v0)
+        p.step(3)
+        out.append((p.download(0)[0], p.download(1)[0]))
+        p.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
