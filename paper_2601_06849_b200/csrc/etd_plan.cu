@@ -812,6 +812,9 @@ struct Plan {
         else tile = 2;
         if (const char* f = std::getenv("ETD_FORCE_TILE"))  // tests: exercise every tile class
             if (f[0] >= '0' && f[0] <= '3' && f[1] == 0) tile = f[0] - '0';
+        if (fold == 6)
+            if (const char* f = std::getenv(mode == 0 ? "ETD_BACK6_TILE_X" : "ETD_BACK6_TILE_YZ"))  // A/B
+                if (f[0] >= '0' && f[0] <= '3' && f[1] == 0) tile = f[0] - '0';
         if (fold == 6 && tile == 1) tile = 0;  // the fused backward has no 4-warp 64x64 class
         L.tile = tile;
         L.fold = fold;
