@@ -172,12 +172,22 @@ def test_fold_halves_the_transform_flops(monkeypatch):
     pts = n ** 3
     h = (n + 1) // 2
     H = h // 2
-    # second level: each of the two launches 2 (2H) H / n per point
+    # second level: each of the two forward launches 2 (2H) H / n per point
     assert p.fold_level() == (2, 2, 2)
-    for nm in ("z_back_o", "z_back_e", "z_fwd_even", "z_fwd_odd"):
+    for nm in ("z_fwd_even", "z_fwd_odd"):
         assert st[nm]["flops_per_launch"] == pytest.approx(2.0 * 2 * H * H / n * pts * 2)
         assert st[nm]["dense_flops_per_launch"] == pytest.approx(0.5 * 2.0 * n * pts * 2)
-    # z_back's unfold runs fused with the y stack (one HBM-bound pass, no FLOPs counted)
+    # the fused backward (§4c): one launch of all four quarters, 2 (4H) H / n per point
+    # (n = 63: 4H = 64 rows, already whole 64-row block pairs)
+    assert st["z_back"]["flops_per_launch"] == pytest.approx(2.0 * 4 * H * H / n * pts * 2)
+    assert st["z_back"]["dense_flops_per_launch"] == pytest.approx(2.0 * n * pts * 2)
+    # the y stack pass (HBM-bound, no FLOPs counted)
+    assert st["fold_y_fwd"]["flops_per_launch"] == 0
+    # the round-1 backward: two launches + the fused z unfold / y stack pass
+    monkeypatch.setenv("ETD_BACK6", "0")
+    st = {s["name"]: s for s in etd.make_plan(g, 0.01, 1.0, 1.0, source=etd.allen_cahn_cubic()).stage_stats()}
+    for nm in ("z_back_o", "z_back_e"):
+        assert st[nm]["flops_per_launch"] == pytest.approx(2.0 * 2 * H * H / n * pts * 2)
     assert st["z_back_y_stack"]["flops_per_launch"] == 0 and st["y_back"]["flops_per_launch"] == 0
 
 
