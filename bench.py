@@ -252,20 +252,32 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
         t = torch.tensor([p[0] for p in per], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         per = [(float(a), s) for a, (_, s) in zip(t.tolist(), per)]
-    dom_ms, dom = max((x for x in per if x[1]["flops_per_launch"] > 0), key=lambda x: x[0])
-    achieved = dom["flops_per_launch"] / (dom_ms * 1e-3) * 1e-12
+    # The dominant kernel is the transform family with the largest share of the step:
+    # the forward contractions (etd_contract, FOLD 5 / 4 launches of equal FLOPs) or the
+    # fused backward launches (etd_back6); achieved = its executed FLOPs per launch over
+    # its average launch time.  The slowest single launch is reported next to it.
+    fams = {}
+    for a, st in per:
+        if st["flops_per_launch"] <= 0:
+            continue
+        fam = "forward contractions (etd_contract)" if "_fwd" in st["name"] else "backward contractions (etd_back6)"
+        f = fams.setdefault(fam, {"ms": 0.0, "flops": 0.0, "dense": 0.0, "launches": 0, "names": []})
+        f["ms"] += a
+        f["flops"] += st["flops_per_launch"]
+        f["dense"] += st.get("dense_flops_per_launch", st["flops_per_launch"])
+        f["launches"] += 1
+        f["names"].append(st["name"])
+    dom_fam, domf = max(fams.items(), key=lambda kv: kv[1]["ms"])
+    dom_ms = domf["ms"] / domf["launches"]
+    achieved = domf["flops"] / (domf["ms"] * 1e-3) * 1e-12
+    slow_ms, slow = max((x for x in per if x[1]["flops_per_launch"] > 0), key=lambda x: x[0])
     traffic, traffic_stage = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
             tr = json.load(open(tpath)).get(f"cfg{cfg.id}_n{n}", {})
-            # z_fwd and y_fwd (z_back and y_back) are the same kernel on the same
-            # shape; the slowest of the pair flips run to run
-            twin = {"y_fwd": "z_fwd", "z_fwd": "y_fwd", "y_back": "z_back", "z_back": "y_back",
-                    "y_fwd_even": "z_fwd_even", "z_fwd_even": "y_fwd_even",
-                    "y_fwd_odd": "z_fwd_odd", "z_fwd_odd": "y_fwd_odd",
-                    "y_back_o": "z_back_o", "z_back_o": "y_back_o", "y_back_e": "z_back_e", "z_back_e": "y_back_e"}
-            for name in (dom["name"], twin.get(dom["name"])):
+            # per-launch DRAM bytes of one ncu-captured launch of the family
+            for name in domf["names"] + [k for k in tr if ("_fwd" in k) == ("forward" in dom_fam)]:
                 if name in tr:
                     traffic, traffic_stage = tr[name], name
                     break
@@ -287,20 +299,26 @@ def b200_arm(args, cfg, n, rank, world, local_rank):
         return {"name": st["name"], "ms": round(a, 3), "bound": "hbm", "gbs": round(gbs, 1),
                 "frac": round(gbs / HBM_PEAK_GBS, 4)}
 
-    dense_ach = dom.get("dense_flops_per_launch", dom["flops_per_launch"]) / (dom_ms * 1e-3) * 1e-12
+    dense_ach = domf["dense"] / (domf["ms"] * 1e-3) * 1e-12
     roofline = {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic, "traffic_stage": traffic_stage,
+                "kernel_share_of_step": round(domf["ms"] / ms, 4), "launches_per_step": domf["launches"],
+                "avg_launch_ms": round(dom_ms, 3),
+                "slowest_launch": {"name": slow["name"], "ms": round(slow_ms, 3),
+                                   "tflops": round(slow["flops_per_launch"] / (slow_ms * 1e-3) * 1e-12, 3),
+                                   "frac": round(slow["flops_per_launch"] / (slow_ms * 1e-3) * 1e-12
+                                                 / FP64_PEAK_TFLOPS, 4)},
                 "basis": "executed",
                 "basis_note": ("achieved = the FLOPs the launch executes (the DST-I parity split runs a quarter of "
                                "the dense 2n per point per transform) / its event-timed duration; "
                                "dense_equiv_achieved = SURVEY 8(d)'s dense count over the same time (exceeds the "
                                "peak by construction); executed FLOP = 512 x DMMA.8x8x4 instructions "
-                               "(profiles/r02_ncu_dmma_counts_cfg3.md)"),
+                               "(sm__inst_executed_pipe_tensor_subpipe_dmma.sum, profiles/r02_ncu_full_cfg3_contract.md)"),
                 "dense_equiv_achieved": round(dense_ach, 3),
-                "kernel": dom["name"],
+                "kernel": dom_fam,
                 "peak_source": FP64_PEAK_NOTE,
-                "algorithmic_flops_per_launch": dom["flops_per_launch"],
-                "dense_flops_per_launch": dom.get("dense_flops_per_launch"),
+                "algorithmic_flops_per_launch": domf["flops"] / domf["launches"],
+                "dense_flops_per_launch": domf["dense"] / domf["launches"],
                 "all_transforms": {"tflops": round(transform_flops / (transform_ms * 1e-3) * 1e-12, 3),
                                    "frac": round(transform_flops / (transform_ms * 1e-3) * 1e-12 / FP64_PEAK_TFLOPS, 4),
                                    "ms_per_step": round(transform_ms, 3),
