@@ -2265,11 +2265,34 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
     int bm = 32;
     for (int k = 0; k < ix; ++k)
         if (p.steps[0][k].kind == Op::KERNEL) bm = std::max(bm, p.steps[0][k].L.k.bm);
+    // Column ranges of the upload.  The column phase ends at about max(upload,
+    // first range's upload + column compute) + the last range's compute, and wider
+    // ranges upload faster (2D copies of (x1-x0)*8-byte row pieces, config 4 with
+    // compute running: 48.4 GB/s at 512 B, 51.7 at 1 KB, 53.5 at 2 KB,
+    // tools/e2e_timeline.py).  So: one narrow range first (compute starts early),
+    // wide ranges in the middle, narrowing ranges at the end (short tail).
+    // ETD_XFER_CHUNKS=N restores N uniform ranges (A/B).
+    std::vector<int> colb{0};
     const int NX = xfer_chunks();
-    const int XW = round_up((V.nx + NX - 1) / NX, bm);
-    const int CX = (V.nx + XW - 1) / XW;
+    if (std::getenv("ETD_XFER_CHUNKS") || V.nx < 16 * bm) {
+        const int XW = round_up((V.nx + NX - 1) / NX, bm);
+        for (int x = XW; x < V.nx; x += XW) colb.push_back(x);
+    } else {
+        const int base = round_up((V.nx + 7) / 8, bm);
+        const int tail[3] = {3 * bm, 2 * bm, bm};
+        int x = bm;
+        colb.push_back(x);
+        const int mid_end = (V.nx - (tail[0] + tail[1] + tail[2])) / bm * bm;  // range starts stay tile aligned
+        while (x + base < mid_end) colb.push_back(x += base);
+        if (mid_end > x) colb.push_back(x = mid_end);
+        for (int t : tail)
+            if (x + t < V.nx) colb.push_back(x += t);
+    }
+    colb.push_back(V.nx);
+    const int CX = (int)colb.size() - 1;
     const long long R = (long long)V.ny * V.nz;
     const int C = (int)std::max(1LL, std::min<long long>(NX, R / 128));
+    if (CX > kXferChunksMax) throw ConfigError("internal: too many upload ranges");
     if (!p.cstream) {
         ETD_CK(cudaStreamCreateWithFlags(&p.cstream, cudaStreamNonBlocking));
         p.xev.resize(3 * kXferChunksMax + 1);
@@ -2296,10 +2319,18 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
     ETD_CK(cudaMemcpyAsync(p.status, p.status_host, sizeof(StepStatus), cudaMemcpyHostToDevice, p.stream));
     ETD_CK(cudaEventRecord(ev_start, p.stream));
     ETD_CK(cudaStreamWaitEvent(p.cstream, ev_start, 0));
-    auto rowb = [&](int c) { return c >= C ? R : R * c / C / 128 * 128; };  // x-stage row chunk bounds
+    // x-stage row chunks (multiples of 128 rows): a small first chunk so the
+    // download starts early, then uniform chunks (the download, not the x stage,
+    // paces the rest)
+    const long long R1 = C > 1 ? std::max<long long>(128, R / (4LL * C) / 128 * 128) : R;
+    auto rowb = [&](int c) -> long long {
+        if (c <= 0) return 0;
+        if (c >= C) return R;
+        return R1 + (R - R1) * (c - 1) / (C - 1) / 128 * 128;
+    };
     double* st_in = p.state[p.cur];
     auto upload = [&](int c) {
-        const int x0 = c * XW, x1 = std::min(V.nx, x0 + XW);
+        const int x0 = colb[c], x1 = colb[c + 1];
         for (int sp = 0; sp < p.ns; ++sp) {
             const double* src = hin[sp];
             if (pg_in[sp]) {
@@ -2322,6 +2353,23 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
     // compute is queued right behind its copy while the host stages the next
     if (!any_in)
         for (int c = 0; c < CX; ++c) upload(c);
+    // ETD_TIMELINE: device timestamps of the pipeline (uploads, column chunks, x
+    // chunks, downloads) printed to stderr after the call (measurement aid)
+    const bool tl = std::getenv("ETD_TIMELINE") != nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> tev;
+    auto mark = [&](const std::string& what, cudaStream_t st) {
+        if (!tl) return;
+        cudaEvent_t e;
+        ETD_CK(cudaEventCreate(&e));
+        ETD_CK(cudaEventRecord(e, st));
+        tev.push_back({what, e});
+    };
+    mark("start", p.stream);
+    if (tl && !any_in)
+        for (int c = 0; c < CX; ++c) {
+            ETD_CK(cudaStreamWaitEvent(p.cstream, ev_in[c], 0));
+            mark("up" + std::to_string(c), p.cstream);
+        }
     for (int s = 0; s < nsteps; ++s) {
         const auto& ops = p.steps[(p.cur + s) & 1];
         const bool first = s == 0, last = s == nsteps - 1;
@@ -2329,8 +2377,9 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
         if (first) {
             for (int c = 0; c < CX; ++c) {
                 if (any_in) upload(c);
+                if (c > 0) mark("col" + std::to_string(c - 1), p.stream);
                 ETD_CK(cudaStreamWaitEvent(p.stream, ev_in[c], 0));
-                const int x0 = c * XW, x1 = std::min(V.nx, x0 + XW);
+                const int x0 = colb[c], x1 = colb[c + 1];
                 for (int k = 0; k < ix; ++k) {
                     if (ops[k].kind == Op::SOURCE) {
                         Op o = ops[k];
@@ -2363,6 +2412,7 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
         } else {
             for (int k = 0; k < ix; ++k) run_op(p, ops[k], p.stream);
         }
+        if (first) mark("col" + std::to_string(CX - 1), p.stream);
         // x stage
         if (!last) {
             for (size_t k = ix; k < ops.size(); ++k) run_op(p, ops[k], p.stream);
@@ -2410,6 +2460,7 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
                 launch(L, p.stream);
             }
             ETD_CK(cudaEventRecord(ev_out[c], p.stream));
+            mark("x" + std::to_string(c), p.stream);
             ETD_CK(cudaStreamWaitEvent(p.cstream, ev_out[c], 0));
             for (int sp = 0; sp < p.ns; ++sp)
                 ETD_CK(cudaMemcpy2DAsync((pg_out[sp] ? mir + (size_t)sp * cnt : hout[sp]) + r0 * V.nx,
@@ -2417,6 +2468,7 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
                                          (size_t)V.pitch * 8, (size_t)V.nx * 8, (size_t)(r1 - r0),
                                          cudaMemcpyDeviceToHost, p.cstream));
             ETD_CK(cudaEventRecord(ev_dl[c], p.cstream));
+            mark("down" + std::to_string(c), p.cstream);
             if (prev >= 0) drain(prev);
             prev = c;
         }
@@ -2425,6 +2477,15 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
     }
     ETD_CK(cudaGetLastError());
     ETD_CK(cudaStreamSynchronize(p.cstream));
+    if (tl) {
+        ETD_CK(cudaDeviceSynchronize());
+        for (auto& [what, e] : tev) {
+            float ms = 0;
+            ETD_CK(cudaEventElapsedTime(&ms, tev[0].second, e));
+            std::fprintf(stderr, "ETD_TIMELINE %s %.3f\n", what.c_str(), ms);
+        }
+        for (auto& te : tev) cudaEventDestroy(te.second);
+    }
     finish_steps(p, n);
 }
 
