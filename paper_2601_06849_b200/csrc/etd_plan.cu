@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/mman.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -2312,6 +2313,14 @@ static void advance_overlapped(Plan& p, const double* const* hin, double* const*
         any_out |= pg_out[sp];
     }
     double* mir = (any_in || any_out) ? ensure_mirror(p, cnt * p.ns) : nullptr;
+    // pageable outputs are typically fresh allocations (a new Field / numpy array per
+    // call): ask for transparent huge pages before the copy threads first-touch them
+    for (int sp = 0; sp < p.ns && any_out; ++sp) {
+        if (!pg_out[sp]) continue;
+        const uintptr_t a = reinterpret_cast<uintptr_t>(hout[sp]), pg = 2u << 20;
+        const uintptr_t lo = (a + pg - 1) / pg * pg, hi = (a + cnt * 8) / pg * pg;
+        if (hi > lo) madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+    }
     p.status_host->n = n;
     p.status_host->t = t;
     p.status_host->fail = 0;

@@ -14,10 +14,19 @@ cfg = configs.CONFIGS[4]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else cfg.n
 ics = configs.initial_state(cfg, n)
 plan = configs.make_plan(cfg, n)
-hin = [torch.from_numpy(a).pin_memory() for a in ics]
-hout = [torch.empty_like(h).pin_memory() for h in hin]
+pageable = len(sys.argv) > 2 and sys.argv[2] == "pageable"
+if pageable:  # plain numpy (the reference Field's storage): staged through the plan's pinned mirror
+    hin = [torch.from_numpy(a) for a in ics]
+    hout = [torch.empty_like(h) for h in hin]
+else:
+    hin = [torch.from_numpy(a).pin_memory() for a in ics]
+    hout = [torch.empty_like(h).pin_memory() for h in hin]
+import time  # noqa: E402
 for rep in range(2):
     if rep == 1:
         os.environ["ETD_TIMELINE"] = "1"
+        if pageable:
+            hout = [torch.empty_like(h) for h in hin]  # fresh pages, as a new Field per call
+    t0 = time.perf_counter()
     r = plan.advance_ptr(hin[0].data_ptr(), hin[1].data_ptr(), hout[0].data_ptr(), hout[1].data_ptr(), 0, 0.0, 1)
-    print("call", rep, r, flush=True)
+    print("call", rep, r, "wall ms", round((time.perf_counter() - t0) * 1e3, 1), flush=True)
