@@ -1049,6 +1049,10 @@ struct Fold2Args {
     int nx, ny, nz;
     int x0, x1;             // y/z: x-column range (x0 even)
     long long r0, r1;       // x: row range (row = y + ny z)
+    // y axis of a sharded step, input straight from the backward exchange's receive
+    // blocks (the unpack fused in): row j of field f, plane z is at
+    // in + rows[3j] + f rows[3j+1] + z rows[3j+2]  (element offsets)
+    const long long* rows;
 };
 
 __device__ __forceinline__ int fold2_spos(int i, int H) { return (i & 1) ? H + (i >> 1) : (i >> 1); }
@@ -1146,7 +1150,12 @@ static __global__ void __launch_bounds__(256) etd_fold2(const Fold2Args a) {
         for (int f = 0; f < a.nf; ++f) {
             const double* src = a.in + f * a.Fin + outer * so + x;
             double* dst = a.out + f * a.Fout + outer * so + x;
-            auto get = [&](int i) { return *reinterpret_cast<const double2*>(src + i * sk); };
+            auto get = [&](int i) {
+                if (a.rows)  // sharded y stack: row i of the slab from its receive block
+                    return *reinterpret_cast<const double2*>(a.in + a.rows[3 * i] + f * a.rows[3 * i + 1] +
+                                                             outer * a.rows[3 * i + 2] + x);
+                return *reinterpret_cast<const double2*>(src + i * sk);
+            };
             double2 o[6];
             fold2_orbit(k, H, a.from1, get, o);
             auto put = [&](int i, double2 v) { *reinterpret_cast<double2*>(dst + i * sk) = v; };

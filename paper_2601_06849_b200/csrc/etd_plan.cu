@@ -427,6 +427,30 @@ static std::vector<SchedRec> sharded_schedule(int nx, int ny, int nz, int ns, in
     return out;
 }
 
+// Where each y row of this rank's slab lands in the receive blocks of the backward
+// exchange (sharded_schedule's layout: block (s, k) = [c < 2 ns][my z][rows of (s,k)][x]):
+// {element offset, field stride, z stride} per global y row.  The sharded level-2
+// y stack pass reads the slab straight from there (no unpack copy).
+static std::vector<long long> recv_row_table(int ny, int nz, int ns, int G, int r, long long pitch, int C) {
+    const ZChunks zc = zchunks(ny, nz, ns, G, pitch, C);
+    const long long nzr = zc.zh[r] - zc.zl[r];
+    std::vector<long long> t(3 * (size_t)ny, 0);
+    long long ro = 0;
+    for (int s = 0; s < G; ++s)
+        for (int k = 0; k < C; ++k) {
+            int a, b;
+            zc.rows(s, k, a, b);
+            const long long nk = b - a;
+            for (int j = zc.jl[s] + a; j < zc.jl[s] + b; ++j) {
+                t[3 * j] = ro + (j - zc.jl[s] - a) * pitch;
+                t[3 * j + 1] = nzr * nk * pitch;
+                t[3 * j + 2] = nk * pitch;
+            }
+            ro += 2 * ns * nzr * nk * pitch;
+        }
+    return t;
+}
+
 struct Plan {
     etd_desc d{};
     int dim = 2, ns = 1;
@@ -486,6 +510,7 @@ struct Plan {
     cudaStream_t cstream = nullptr;  // host<->device copy stream of the pipelined advance
     std::vector<cudaEvent_t> xev;    // its chunk events
     int state_fields = 0;            // fields per state buffer (ns on the level-2 schedule, else 2 ns)
+    long long* recv_rows = nullptr;  // sharded level 2: per slab y row, {offset, field stride, z stride} in recvb
     double* mirror = nullptr;        // pinned host mirror of the state (pageable etd_advance buffers)
     size_t mirror_elems = 0;
     // BackendKind::Thomas: per-axis factors [species][pole][mul, piv, 1/piv][n],
@@ -504,6 +529,7 @@ struct Plan {
             if (g) cudaGraphExecDestroy(g);
         for (double* p : {state[0], state[1], Z, W, dvec, sendbuf, zin, Zz, Wz, recvb}) if (p) cudaFree(p);
         if (codes) cudaFree(codes);
+        if (recv_rows) cudaFree(recv_rows);
         for (double* t : sintab) if (t) cudaFree(t);
         for (double2* t : thfac) if (t) cudaFree(t);
         if (thscr) cudaFree(thscr);
@@ -692,6 +718,7 @@ struct Plan {
         a.x1 = v.nx;
         a.r0 = 0;
         a.r1 = (long long)v.ny * v.nz;
+        a.rows = nullptr;
         const double pts = (double)v.nx * v.ny * v.nz;
         o.L.flops = 0.0;
         o.L.bytes = pts * 8.0 * 2 * nf;
@@ -1793,7 +1820,24 @@ static void build_plan(Plan& p, const etd_desc& d) {
                 b.rec_ev = EV_B;
                 L.push_back(b);
             }
-            L[copies(SP_UNPACK, "unpack")].wait_ev = EV_B;
+            if (f2 && p.back6) {
+                // the unpack fused into the y stack pass: it reads the slab's y rows
+                // straight from the receive blocks (recv_row_table) and writes the y
+                // stack into Z, as the unsharded z_back + fold_y_fwd do
+                if (!p.recv_rows) {  // (both step parities share it)
+                    const auto tab = recv_row_table(p.ny, p.nz, ns, p.G, p.rank, p.pitch, C);
+                    ETD_CK(cudaMalloc(&p.recv_rows, tab.size() * sizeof(long long)));
+                    ETD_CK(cudaMemcpy(p.recv_rows, tab.data(), tab.size() * sizeof(long long),
+                                      cudaMemcpyHostToDevice));
+                }
+                Op fy = p.fold_op(V, "fold_y_fwd", 1, p.recvb, p.Z, 2 * ns);
+                fy.fargs.rows = p.recv_rows;
+                fy.wait_ev = EV_B;
+                L.push_back(fy);
+                zy_fused = true;
+            } else {
+                L[copies(SP_UNPACK, "unpack")].wait_ev = EV_B;
+            }
         }
         if (f2) {
             // y stage on (B1, B2) with the z-filtered stack (3D) in B2, then the x stage
