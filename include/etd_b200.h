@@ -119,6 +119,12 @@ int etd_zslab_partition(int n, int world_size, int rank, int* lo, int* hi);
  * out may be NULL to query *count. */
 int etd_sharded_schedule(int nx, int ny, int nz, int nspecies, int world_size, int rank, long long pitch,
                          int chunks, long long* out, int capacity, int* count);
+/* Where the sharded level-2 step's y stack pass reads each y row of this rank's slab
+ * from the backward exchange's receive blocks (buffer 4 above; the unpack copies are
+ * fused into that pass): out[3 j .. 3 j + 2] = {element offset, field stride, z stride}
+ * for global y row j < ny.  Host only. */
+int etd_sharded_recv_rows(int ny, int nz, int nspecies, int world_size, int rank, long long pitch, int chunks,
+                          long long* out);
 /* 128-byte ncclUniqueId for etd_desc.nccl_unique_id (rank 0 creates, all ranks
  * receive it out of band, e.g. over torch.distributed). */
 int etd_nccl_unique_id(void* out128);

@@ -189,6 +189,71 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                                : (long long)outer * args.plane + (long long)p * args.pitch + m;
     };
     const double src_a = SK == 4 ? exp(-args.sp[0] * (args.status->t + args.tau)) : 0.0;
+    if constexpr (MODE == 0 && EPI == EPI_UPDATE) {
+        // x stage, U1 = What + tau Q3(fw): a thread's four orbits k0 + q (q < 4) are
+        // four consecutive positions in each range, so What is read and U1 written in
+        // 16-byte pieces where the range is even-aligned (R0 k, R3 2H + k) and as one
+        // pair plus two singles where it runs backwards from an odd start (R1 n-1-k,
+        // R2 2H-2-k): 10 accesses per species and row instead of 16
+#pragma unroll
+        for (int i = 0; i < MF; ++i) {
+            const int m = m0 + wm0 + i * 8 + g;
+            if (m >= args.m_extent) continue;
+#pragma unroll
+            for (int bp = 0; bp < NF / 8; ++bp) {
+                const int k0 = 16 * ((n0 + wn0) / 64 + bp) + 4 * l;
+                if (k0 >= H) continue;
+                const bool cen = k0 + 3 == H - 1;  // orbit q = 3 is the centre
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    double gq[4][4];  // [q][range]
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int par = q & 1, e = q >> 1, jb = 8 * bp + 4 * par;
+                        const double O1 = acc[s][i][jb][e], O2 = acc[s][i][jb + 1][e];
+                        const double EO = acc[s][i][jb + 2][e], EE = acc[s][i][jb + 3][e];
+                        const double ek = EO + EE, ec = EO - EE;
+                        gq[q][0] = O1 + ek;
+                        gq[q][1] = O1 - ek;
+                        gq[q][2] = (cen && q == 3) ? O2 : O2 + ec;
+                        gq[q][3] = O2 - ec;
+                    }
+                    const double* au = args.aux + (long long)s * args.aux_stride + (long long)m * args.pitch;
+                    double* o = outp + (long long)s * args.out_stride + (long long)m * args.pitch;
+                    auto ld2 = [&](int p) { return __ldg(reinterpret_cast<const double2*>(au + p)); };
+                    auto st2 = [&](int p, double a, double b) { *reinterpret_cast<double2*>(o + p) = make_double2(a, b); };
+                    const int p1 = n - 1 - k0, p2 = 2 * H - 2 - k0, p3 = 2 * H + k0;
+                    const double2 r0a = ld2(k0), r0b = ld2(k0 + 2);
+                    const double2 r3a = ld2(p3);
+                    const double r3c = __ldg(au + p3 + 2), r3d = cen ? 0.0 : __ldg(au + p3 + 3);
+                    const double r1q0 = __ldg(au + p1), r1q3 = __ldg(au + p1 - 3);
+                    const double2 r1m = ld2(p1 - 2);  // (q2, q1)
+                    const double r2q0 = __ldg(au + p2), r2q3 = __ldg(au + (cen ? 2 * H - 1 : p2 - 3));
+                    const double2 r2m = ld2(p2 - 2);  // (q2, q1)
+                    const double u[4][4] = {{r0a.x + gq[0][0], r1q0 + gq[0][1], r2q0 + gq[0][2], r3a.x + gq[0][3]},
+                                            {r0a.y + gq[1][0], r1m.y + gq[1][1], r2m.y + gq[1][2], r3a.y + gq[1][3]},
+                                            {r0b.x + gq[2][0], r1m.x + gq[2][1], r2m.x + gq[2][2], r3c + gq[2][3]},
+                                            {r0b.y + gq[3][0], r1q3 + gq[3][1], r2q3 + gq[3][2], r3d + gq[3][3]}};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+#pragma unroll
+                        for (int R = 0; R < 4; ++R)
+                            if (!(cen && q == 3 && R == 3)) bad |= !isfinite(u[q][R]);
+                    st2(k0, u[0][0], u[1][0]);
+                    st2(k0 + 2, u[2][0], u[3][0]);
+                    st2(p1 - 2, u[2][1], u[1][1]);
+                    o[p1] = u[0][1];
+                    o[p1 - 3] = u[3][1];
+                    st2(p2 - 2, u[2][2], u[1][2]);
+                    o[p2] = u[0][2];
+                    o[cen ? 2 * H - 1 : p2 - 3] = u[3][2];
+                    st2(p3, u[0][3], u[1][3]);
+                    o[p3 + 2] = u[2][3];
+                    if (!cen) o[p3 + 3] = u[3][3];
+                }
+            }
+        }
+    } else {
 #pragma unroll
     for (int i = 0; i < MF; ++i) {
         const int m = m0 + wm0 + i * 8 + g;
@@ -309,6 +374,8 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                 }
         }
     }
+
+    }  // generic orbit epilogue
 
     // ===================== status: abort flag and step commit (as etd_contract) =====================
     const int any_dom = __syncthreads_or(dom);

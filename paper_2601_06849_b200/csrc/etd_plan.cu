@@ -2852,6 +2852,16 @@ int etd_sharded_schedule(int nx, int ny, int nz, int nspecies, int world_size, i
     return ETD_OK;
 }
 
+int etd_sharded_recv_rows(int ny, int nz, int nspecies, int world_size, int rank, long long pitch, int chunks,
+                          long long* out) {
+    if (!out || world_size < 1 || rank < 0 || rank >= world_size || world_size > nz || world_size > ny ||
+        nspecies < 1 || nspecies > 2 || chunks < 1)
+        return ETD_ERR_CONFIG;
+    const auto t = etd::recv_row_table(ny, nz, nspecies, world_size, rank, pitch, chunks);
+    std::memcpy(out, t.data(), t.size() * sizeof(long long));
+    return ETD_OK;
+}
+
 int etd_nccl_unique_id(void* out) {
     if (!out) return ETD_ERR_CONFIG;
     return guarded(nullptr, [&] {

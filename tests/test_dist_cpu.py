@@ -135,6 +135,18 @@ def _worker(rank, world, port, shape, ns, chunks, result_q):
         c_, z_, j_, x_ = np.meshgrid(np.arange(2 * ns), np.arange(z0, z1), np.arange(ny), np.arange(pitch),
                                      indexing="ij")
         ok_back = np.array_equal(w, c_ * 1e6 + z_ * 1e4 + j_ * 1e2 + x_)
+        # the level-2 y stack pass reads the slab straight from the receive blocks
+        # (etd_sharded_recv_rows): the same values as the unpacked slab
+        L.etd_sharded_recv_rows.argtypes = [C.c_int] * 5 + [C.c_longlong, C.c_int, C.c_void_p]
+        tab = np.zeros(3 * ny, dtype=np.int64)
+        assert L.etd_sharded_recv_rows(ny, nz, ns, world, rank, pitch, chunks, tab.ctypes.data_as(C.c_void_p)) == 0
+        via = np.empty_like(w)
+        for c in range(2 * ns):
+            for zl in range(nzr):
+                for j in range(ny):
+                    o = tab[3 * j] + c * tab[3 * j + 1] + zl * tab[3 * j + 2]
+                    via[c, zl, j] = bufs[4][o:o + pitch]
+        ok_back = ok_back and np.array_equal(via, w)
         # NCCL unique-id bootstrap (bench.py): rank 0 creates, everyone receives
         obj = [etd.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
