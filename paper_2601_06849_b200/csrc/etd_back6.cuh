@@ -189,7 +189,170 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                                : (long long)outer * args.plane + (long long)p * args.pitch + m;
     };
     const double src_a = SK == 4 ? exp(-args.sp[0] * (args.status->t + args.tau)) : 0.0;
-    if constexpr (MODE == 0 && EPI == EPI_UPDATE) {
+    if constexpr (MODE == 0 && EPI == EPI_WHAT_SRC) {
+        // x stage, the predictor: What, f(t + tau, What) with its checks and f - w2's
+        // level-2 stack, with the orbit ranges read / written in 16-byte pieces where
+        // aligned (as the EPI_UPDATE path below); half A = ranges R0 (k), R1 (n-1-k)
+        // from O1 +- e_k, half B = R2 (c), R3 (n-1-c) from O2 +- e_c
+#pragma unroll
+        for (int i = 0; i < MF; ++i) {
+            const int m = m0 + wm0 + i * 8 + g;
+            if (m >= args.m_extent) continue;
+            const int jj = m % args.ny_local + args.gj0, kz = m / args.ny_local + args.gz0;
+#pragma unroll
+            for (int bp = 0; bp < NF / 8; ++bp) {
+                const int k0 = 16 * ((n0 + wn0) / 64 + bp) + 4 * l;
+                if (k0 >= H) continue;
+                const bool cen = k0 + 3 == H - 1;
+                const long long row = (long long)m * args.pitch;
+                const int p1 = n - 1 - k0, p2 = 2 * H - 2 - k0, p3 = 2 * H + k0;
+                // w2 at the four ranges, 16-byte where aligned: [s][q]
+                auto ldr = [&](const double* a, int R, double (&w)[4]) {
+                    if (R == 0) {
+                        const double2 x = __ldg(reinterpret_cast<const double2*>(a + k0)),
+                                      y = __ldg(reinterpret_cast<const double2*>(a + k0 + 2));
+                        w[0] = x.x; w[1] = x.y; w[2] = y.x; w[3] = y.y;
+                    } else if (R == 3) {
+                        const double2 x = __ldg(reinterpret_cast<const double2*>(a + p3));
+                        w[0] = x.x; w[1] = x.y;
+                        if (cen) { w[2] = __ldg(a + p3 + 2); w[3] = 0.0; }
+                        else {
+                            const double2 y = __ldg(reinterpret_cast<const double2*>(a + p3 + 2));
+                            w[2] = y.x; w[3] = y.y;
+                        }
+                    } else {
+                        const int p = R == 1 ? p1 : p2;
+                        const double2 x = __ldg(reinterpret_cast<const double2*>(a + p - 2));  // (q2, q1)
+                        w[0] = __ldg(a + p);
+                        w[1] = x.y;
+                        w[2] = x.x;
+                        w[3] = __ldg(a + (R == 2 && cen ? 2 * H - 1 : p - 3));
+                    }
+                };
+                auto str = [&](double* o, int R, const double (&v)[4]) {
+                    auto st2 = [&](int p, double a, double b) {
+                        *reinterpret_cast<double2*>(o + p) = make_double2(a, b);
+                    };
+                    if (R == 0) { st2(k0, v[0], v[1]); st2(k0 + 2, v[2], v[3]); }
+                    else if (R == 3) {
+                        st2(p3, v[0], v[1]);
+                        if (cen) o[p3 + 2] = v[2];
+                        else st2(p3 + 2, v[2], v[3]);
+                    } else {
+                        const int p = R == 1 ? p1 : p2;
+                        st2(p - 2, v[2], v[1]);
+                        o[p] = v[0];
+                        o[R == 2 && cen ? 2 * H - 1 : p - 3] = v[3];
+                    }
+                };
+                auto fpoint = [&](int x, const double (&gs)[S], double (&fs)[S], bool in) {
+                    if constexpr (S == 1) {
+                        double ustar = 0.0;
+                        if constexpr (SK == 4)
+                            ustar = src_a * (args.sinx[x] * args.siny[jj] * (args.sinz ? args.sinz[kz] : 1.0));
+                        fs[0] = src1<SK>(args.sp, gs[0], ustar);
+                        if constexpr (SK == 3)
+                            if (x == 0 && jj == 0 && kz == 0) fs[0] = __longlong_as_double(0x7ff8000000000000ll);
+                        bad |= (int)in & (int)!isfinite(fs[0]);
+                        dom |= (int)in & src_domain_violation<SK>(gs[0]);
+                    } else {
+                        src2<SK>(args.sp, gs[0], gs[1], fs[0], fs[1]);
+                        bad |= (int)in & (int)!(isfinite(fs[0]) && isfinite(fs[1]));
+                    }
+                };
+                double dk[S][4];
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const int Ra = 2 * half, Rb = Ra + 1;
+                    double ga[S][4], gb[S][4], wa[S][4], wb[S][4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int par = q & 1, e = q >> 1, jb = 8 * bp + 4 * par;
+#pragma unroll
+                        for (int sp = 0; sp < S; ++sp) {
+                            const double EO = acc[sp][i][jb + 2][e], EE = acc[sp][i][jb + 3][e];
+                            if (half == 0) {
+                                const double O1 = acc[sp][i][jb][e], ek = EO + EE;
+                                ga[sp][q] = O1 + ek;
+                                gb[sp][q] = O1 - ek;
+                            } else {
+                                const double O2 = acc[sp][i][jb + 1][e], ec = EO - EE;
+                                ga[sp][q] = (cen && q == 3) ? O2 : O2 + ec;
+                                gb[sp][q] = O2 - ec;
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int sp = 0; sp < S; ++sp) {
+                        if (args.aux) {
+                            const double* a = args.aux + (long long)sp * args.aux_stride + row;
+                            ldr(a, Ra, wa[sp]);
+                            ldr(a, Rb, wb[sp]);
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) wa[sp][q] = wb[sp][q] = 0.0;
+                        }
+                        double* o = outp + (long long)sp * args.out_stride + row;
+                        str(o, Ra, ga[sp]);
+                        str(o, Rb, gb[sp]);
+                    }
+                    // f - w2 at both ranges; stack values of the half
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int k = k0 + q;
+                        const bool qc = cen && q == 3;
+                        const int xa = half == 0 ? k : (qc ? 2 * H - 1 : 2 * H - 2 - k);
+                        const int xb = half == 0 ? n - 1 - k : 2 * H + k;
+                        double gsa[S], gsb[S], fa[S], fb[S];
+#pragma unroll
+                        for (int sp = 0; sp < S; ++sp) { gsa[sp] = ga[sp][q]; gsb[sp] = gb[sp][q]; }
+                        fpoint(xa, gsa, fa, true);
+                        fpoint(xb, gsb, fb, !(half == 1 && qc));
+#pragma unroll
+                        for (int sp = 0; sp < S; ++sp) {
+                            fa[sp] -= wa[sp][q];
+                            fb[sp] -= wb[sp][q];
+                            if (half == 0) {
+                                ga[sp][q] = fa[sp] + fb[sp];  // s_k (reuses ga)
+                                dk[sp][q] = fa[sp] - fb[sp];
+                            } else if (qc) {
+                                ga[sp][q] = fa[sp] + fa[sp];  // 2 f(2H - 1), the centre of s
+                                gb[sp][q] = dk[sp][q] + dk[sp][q];
+                            } else {
+                                const double sc = fa[sp] + fb[sp], dc = fa[sp] - fb[sp];
+                                ga[sp][q] = sc;
+                                gb[sp][q] = dk[sp][q] + dc;
+                                dk[sp][q] = dk[sp][q] - dc;
+                            }
+                        }
+                    }
+                    // level-2 stack positions (fold2_orbit): spos(k) = k/2 (even) | H + k/2 (odd),
+                    // spos(c) likewise, 2H + k: d_k + d_c, 3H + k: d_k - d_c
+#pragma unroll
+                    for (int sp = 0; sp < S; ++sp) {
+                        double* fo = args.fout + (long long)sp * args.out_stride + row;
+                        auto st2 = [&](int p, double a, double b) {
+                            *reinterpret_cast<double2*>(fo + p) = make_double2(a, b);
+                        };
+                        if (half == 0) {
+                            st2(k0 / 2, ga[sp][0], ga[sp][2]);
+                            st2(H + k0 / 2, ga[sp][1], ga[sp][3]);
+                        } else {
+                            st2(H - 2 - k0 / 2, ga[sp][2], ga[sp][0]);           // s_c, c even
+                            fo[2 * H - 2 - k0 / 2] = ga[sp][1];                   // s_c, c odd (q = 1)
+                            if (cen) fo[2 * H - 1] = ga[sp][3];                   // the centre of s
+                            else fo[2 * H - 3 - k0 / 2] = ga[sp][3];              // s_c, c odd (q = 3)
+                            st2(2 * H + k0, gb[sp][0], gb[sp][1]);
+                            st2(2 * H + k0 + 2, gb[sp][2], gb[sp][3]);
+                            st2(3 * H + k0, dk[sp][0], dk[sp][1]);
+                            if (cen) fo[3 * H + k0 + 2] = dk[sp][2];
+                            else st2(3 * H + k0 + 2, dk[sp][2], dk[sp][3]);
+                        }
+                    }
+                }
+            }
+        }
+    } else if constexpr (MODE == 0 && EPI == EPI_UPDATE) {
         // x stage, U1 = What + tau Q3(fw): a thread's four orbits k0 + q (q < 4) are
         // four consecutive positions in each range, so What is read and U1 written in
         // 16-byte pieces where the range is even-aligned (R0 k, R3 2H + k) and as one
@@ -225,7 +388,8 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                     const int p1 = n - 1 - k0, p2 = 2 * H - 2 - k0, p3 = 2 * H + k0;
                     const double2 r0a = ld2(k0), r0b = ld2(k0 + 2);
                     const double2 r3a = ld2(p3);
-                    const double r3c = __ldg(au + p3 + 2), r3d = cen ? 0.0 : __ldg(au + p3 + 3);
+                    const double2 r3b = cen ? make_double2(__ldg(au + p3 + 2), 0.0) : ld2(p3 + 2);
+                    const double r3c = r3b.x, r3d = r3b.y;
                     const double r1q0 = __ldg(au + p1), r1q3 = __ldg(au + p1 - 3);
                     const double2 r1m = ld2(p1 - 2);  // (q2, q1)
                     const double r2q0 = __ldg(au + p2), r2q3 = __ldg(au + (cen ? 2 * H - 1 : p2 - 3));
@@ -248,8 +412,8 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                     o[p2] = u[0][2];
                     o[cen ? 2 * H - 1 : p2 - 3] = u[3][2];
                     st2(p3, u[0][3], u[1][3]);
-                    o[p3 + 2] = u[2][3];
-                    if (!cen) o[p3 + 3] = u[3][3];
+                    if (cen) o[p3 + 2] = u[2][3];
+                    else st2(p3 + 2, u[2][3], u[3][3]);
                 }
             }
         }
