@@ -112,34 +112,26 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
             for (int j = 0; j < NF; ++j) acc[s][i][j][0] = acc[s][i][j][1] = 0.0;
 
     // the k permutation of etd_contract (bank-conflict free fragment loads, and the
-    // same accumulation order as the two-launch path)
-    auto kperm = [&](int st) {
-        return MODE == 0 ? (2 * st + (l & 1) + 8 * (l >> 1)) : (2 * l + (st & 1) + 8 * (st >> 1));
-    };
+    // same accumulation order as the two-launch path): FragOffsets below
     // A fragments are double-buffered across steps; B fragments are loaded just in
     // time inside mma() (each feeds S x MF DMMAs), which keeps the 2-CTA/SM class
     // under its 128-register cap
+    // (fragment offsets pinned in registers once: FragOffsets, etd_kernels.cuh)
+    const FragOffsets<MODE, 0, MF> fo(wm0, wn0, g, l, C::A1_DBL, C::A_DBL);
     auto load_frags = [&](int stg, int st, double (&a)[4][S][MF]) {
         const double* sA = smem + stg * C::STAGE_DBL;
-        const int kk = kperm(st);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
             for (int s = 0; s < S; ++s)
 #pragma unroll
-                for (int i = 0; i < MF; ++i) {
-                    const int mm = wm0 + i * 8 + g;
-                    const double* base = sA + q * C::A1_DBL + s * BM * BK;
-                    a[q][s][i] = MODE == 0 ? base[swz(mm, kk)] : base[(mm >> 4) * 256 + swz(kk, mm & 15)];
-                }
+                for (int i = 0; i < MF; ++i) a[q][s][i] = sA[q * C::A1_DBL + s * BM * BK + fo.a(st, i)];
     };
     auto mma = [&](int stg, int st, const double (&a)[4][S][MF]) {
-        const double* sB = smem + stg * C::STAGE_DBL + C::A_DBL;
-        const int kk = kperm(st);
+        const double* sA = smem + stg * C::STAGE_DBL;
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
-            const int nn = wn0 + j * 8 + g;
-            const double b = MODE == 0 ? sB[swz(nn, kk)] : sB[(nn >> 4) * 256 + swz(kk, nn & 15)];
+            const double b = sA[fo.b(st, j)];
             const int t = j & 3, box = t < 2 ? ((j >> 2) & 1) : t;
 #pragma unroll
             for (int s = 0; s < S; ++s)

@@ -250,6 +250,7 @@ struct ContractCfg {
     static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile");
     static_assert(BM % 16 == 0 && BN % 16 == 0, "cta tile");
     static_assert(FOLD == 0 || (WN % 16 == 0 && !PRO), "FOLD pairs 8-row fragments; no source prologue");
+    static_assert(WN % 16 == 0, "FragOffsets: warp column blocks start on a 16-row swizzle group");
     static_assert(FOLD != 3 || MODE == 0, "FOLD 3 is an x-axis variant");
 };
 
@@ -257,6 +258,70 @@ struct ContractCfg {
 __device__ __forceinline__ int swz(int row, int col) {
     return row * 16 + ((((col >> 1) ^ (row & 7)) << 1) | (col & 1));
 }
+
+// keeps v in a register: the compiler may not re-derive it (from the thread
+// index) inside the main loop
+__device__ __forceinline__ int pin(int v) {
+    asm volatile("" : "+r"(v));
+    return v;
+}
+
+// Per-thread fragment offsets (doubles from the stage base) of etd_contract and
+// etd_back6 for the kperm k order, A row m = wm0 + 8i + g, B row n = wn0 + 8j + g
+// (the B tile follows the A boxes at a_dbl; a1 = one A box).
+//   MODE 1, tile [m/16][16 k][16 m]: k = 2l + (st&1) + 8(st>>1).  The 128B
+//     swizzle XORs with k & 7 = 2l + (st&1), so step st reads the st&1 entry plus
+//     128 (st>>1); the FOLD 1 mirror box (k' = 15 - k) the st&1 entry minus
+//     128 (st>>1).  B (wn0 % 16 == 0): one entry per (st&1, j&1), plus 256 (j>>1).
+//   MODE 0, tile [m][16 k]: k = 2st + (l&1) + 8(l>>1).  The swizzle XORs the k pair
+//     st + 4(l>>1) with m & 7 = g, so A and B share x[st] = 16 g + X(st):
+//     A = 16 wm0 + 128 i + x[st], B = a_dbl + 16 wn0 + 128 j + x[st]; the second A
+//     box adds a1 (FOLD 1 mirror: x2[st], k' = 15 - k).
+template <int MODE, int FOLD, int MF>
+struct FragOffsets {
+    int ea[2][MF], ea2[2][MF], eb[2][2];  // MODE 1
+    int x[4], x2[4], wa, wa2, wb;         // MODE 0
+    __device__ __forceinline__ FragOffsets(int wm0, int wn0, int g, int l, int a1, int a_dbl) {
+        if constexpr (MODE == 1) {
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const int kk = 2 * l + p;
+#pragma unroll
+                for (int i = 0; i < MF; ++i) {
+                    const int mm = wm0 + i * 8 + g;
+                    ea[p][i] = pin((mm >> 4) * 256 + swz(kk, mm & 15));
+                    ea2[p][i] = pin(a1 + (mm >> 4) * 256 + swz(FOLD == 1 ? 15 - kk : kk, mm & 15));
+                }
+#pragma unroll
+                for (int jo = 0; jo < 2; ++jo) {
+                    const int nn = wn0 + jo * 8 + g;
+                    eb[p][jo] = pin(a_dbl + (nn >> 4) * 256 + swz(kk, nn & 15));
+                }
+            }
+        } else {
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+                x[st] = pin(16 * g + ((((st + 4 * (l >> 1)) ^ g) << 1) | (l & 1)));
+                x2[st] = pin(16 * g + ((((7 - st - 4 * (l >> 1)) ^ g) << 1) | (1 - (l & 1))));
+            }
+            wa = 16 * wm0;
+            wa2 = a1 + 16 * wm0;
+            wb = a_dbl + 16 * wn0;
+        }
+    }
+    __device__ __forceinline__ int a(int st, int i) const {
+        if constexpr (MODE == 1) return ea[st & 1][i] + 128 * (st >> 1);
+        else return wa + 128 * i + x[st];
+    }
+    __device__ __forceinline__ int a2(int st, int i) const {
+        if constexpr (MODE == 1) return ea2[st & 1][i] + (FOLD == 1 ? -128 : 128) * (st >> 1);
+        else return wa2 + 128 * i + (FOLD == 1 ? x2[st] : x[st]);
+    }
+    __device__ __forceinline__ int b(int st, int j) const {
+        if constexpr (MODE == 1) return eb[st & 1][j & 1] + 256 * (j >> 1) + 128 * (st >> 1);
+        else return wb + 128 * j + x[st];
+    }
+};
 
 // ------------------------------------------------------------- the kernel
 template <int MODE, int S, int EPI, bool PRO, int SK, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES,
@@ -353,28 +418,26 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
         };
         // a2: the second A box (FOLD).  The mirror box is read at 15 - k: the swizzle
         // slot maps by an XOR, so the reversed reads stay bank-conflict free.
+        //
+        // Fragment offsets.  The swizzled index of a fragment depends on the lane
+        // and on the step st only through a few per-thread constants (FragOffsets
+        // below), computed once and pinned in registers; every fragment load of the
+        // main loop is then one LDS at [stage base + constant + immediate].  (Left to
+        // itself the compiler re-derived the swizzle from the thread index every step:
+        // ~4 integer instructions per DMMA and spills in the MODE 1 loop.)
+        const FragOffsets<MODE, FOLD, C::MF> fo(wm0, wn0, g, l, C::A1_DBL, C::A_DBL);
         auto load_frags = [&](int stg, int st, double (&a)[S][C::MF], double (&a2)[S][C::MF],
                               double (&b)[C::NF]) {
             const double* sA = smem + stg * C::STAGE_DBL;
-            const double* sB = sA + C::A_DBL;
-            const int kk = kperm(st);
 #pragma unroll
-            for (int j = 0; j < C::NF; ++j) {
-                const int nn = wn0 + j * 8 + g;
-                b[j] = MODE == 0 ? sB[swz(nn, kk)] : sB[(nn >> 4) * 256 + swz(kk, nn & 15)];
-            }
+            for (int j = 0; j < C::NF; ++j) b[j] = sA[fo.b(st, j)];
 #pragma unroll
             for (int s = 0; s < C::L; ++s)
 #pragma unroll
                 for (int i = 0; i < C::MF; ++i) {
-                    const int mm = wm0 + i * 8 + g;
                     const double* base = sA + s * BM * BK;
-                    a[s][i] = MODE == 0 ? base[swz(mm, kk)] : base[(mm >> 4) * 256 + swz(kk, mm & 15)];
-                    if constexpr (FOLD != 0) {
-                        const double* b2 = base + C::A1_DBL;
-                        const int k2 = FOLD == 1 ? BK - 1 - kk : kk;
-                        a2[s][i] = MODE == 0 ? b2[swz(mm, k2)] : b2[(mm >> 4) * 256 + swz(k2, mm & 15)];
-                    }
+                    a[s][i] = base[fo.a(st, i)];
+                    if constexpr (FOLD != 0) a2[s][i] = base[fo.a2(st, i)];
                 }
         };
         // FOLD 1/3: (a, a2) = (g_k, g_mirror) -> (s, d).  Issued after the current
