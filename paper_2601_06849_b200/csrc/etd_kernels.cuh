@@ -1116,6 +1116,7 @@ struct Fold2Args {
     // blocks (the unpack fused in): row j of field f, plane z is at
     // in + rows[3j] + f rows[3j+1] + z rows[3j+2]  (element offsets)
     const long long* rows;
+    int x4;                 // x axis, !from1: four orbits per thread, 16-byte accesses (fold2_x_rows4)
 };
 
 __device__ __forceinline__ int fold2_spos(int i, int H) { return (i & 1) ? H + (i >> 1) : (i >> 1); }
@@ -1151,9 +1152,75 @@ __device__ __forceinline__ void fold2_orbit(int k, int H, bool from1, const Get&
 __device__ __forceinline__ double2 operator+(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 operator-(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 
+// x-axis stack pass, four consecutive orbits k0 + q (q < 4, k0 = 4 * item) per thread:
+// the orbit's ranges R0 [k0, k0+4), R3 [2H+k0, +4) are two aligned 16-byte pieces, the
+// reversed ranges R1 (n-1-k) and R2 (2H-2-k) one aligned pair and two singles; the
+// stack positions likewise (the layout of etd_back6's EPI_WHAT_SRC stores).  One field
+// at a time: its 10 loads, the butterflies, its 9 stores.  8-byte accesses run this
+// HBM-bound pass at 0.78 of the copy bandwidth (r02_experiments.md), 16-byte ones higher.
+// Values are etd_fold2's (same additions).
+__device__ __forceinline__ void fold2_x_rows4(const Fold2Args& a) {
+    const int H = a.H, n = a.n, W = H / 4;
+    const int tpr = W >= (int)blockDim.x ? (int)blockDim.x : W;
+    const int rpb = (int)blockDim.x / tpr, sub = threadIdx.x / tpr, lane = threadIdx.x % tpr;
+    if (sub >= rpb) return;
+    for (long long row = a.r0 + (long long)blockIdx.x * rpb + sub; row < a.r1; row += (long long)gridDim.x * rpb) {
+        for (int it = lane; it < W; it += tpr) {
+            const int k0 = 4 * it;
+            const bool cen = k0 + 3 == H - 1;
+            const int p1 = n - 1 - k0, p2 = 2 * H - 2 - k0, p3 = 2 * H + k0;
+            for (int f = 0; f < a.nf; ++f) {
+                const double* __restrict__ src = a.in + f * a.Fin + row * a.pitch;
+                double* __restrict__ dst = a.out + f * a.Fout + row * a.pitch;
+                auto ld2 = [&](int p) { return *reinterpret_cast<const double2*>(src + p); };
+                auto st2 = [&](int p, double x, double y) { *reinterpret_cast<double2*>(dst + p) = make_double2(x, y); };
+                const double2 r0a = ld2(k0), r0b = ld2(k0 + 2);
+                const double2 r3a = ld2(p3);
+                const double2 r3b = cen ? make_double2(src[p3 + 2], 0.0) : ld2(p3 + 2);
+                const double2 r1m = ld2(p1 - 2), r2m = ld2(p2 - 2);  // (q2, q1)
+                const double r1q0 = src[p1], r1q3 = src[p1 - 3];
+                const double r2q0 = src[p2], r2q3 = src[cen ? 2 * H - 1 : p2 - 3];
+                // [q]: g_k, g_{n-1-k}, g_c, g_{n-1-c}
+                const double ga[4] = {r0a.x, r0a.y, r0b.x, r0b.y};
+                const double gb[4] = {r1q0, r1m.y, r1m.x, r1q3};
+                const double gc[4] = {r2q0, r2m.y, r2m.x, r2q3};
+                const double ge[4] = {r3a.x, r3a.y, r3b.x, r3b.y};
+                double si[4], sc[4], o2[4], o3[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double di = ga[q] - gb[q], dc = gc[q] - ge[q];
+                    si[q] = ga[q] + gb[q];
+                    sc[q] = gc[q] + ge[q];
+                    o2[q] = di + dc;
+                    o3[q] = di - dc;
+                }
+                if (cen) {  // orbit q = 3 is the centre: c = k, the s_c slot carries 2 g_{2H-1}
+                    const double di = ga[3] - gb[3];
+                    sc[3] = gc[3] + gc[3];
+                    o2[3] = di + di;
+                }
+                st2(k0 / 2, si[0], si[2]);
+                st2(H + k0 / 2, si[1], si[3]);
+                st2(H - 2 - k0 / 2, sc[2], sc[0]);
+                dst[2 * H - 2 - k0 / 2] = sc[1];
+                dst[cen ? 2 * H - 1 : 2 * H - 3 - k0 / 2] = sc[3];
+                st2(p3, o2[0], o2[1]);
+                st2(p3 + 2, o2[2], o2[3]);
+                st2(3 * H + k0, o3[0], o3[1]);
+                if (cen) dst[3 * H + k0 + 2] = o3[2];
+                else st2(3 * H + k0 + 2, o3[2], o3[3]);
+            }
+        }
+    }
+}
+
 static __global__ void __launch_bounds__(256) etd_fold2(const Fold2Args a) {
     const int H = a.H;
     const long long stride = (long long)gridDim.x * blockDim.x;
+    if (a.axis == 0 && a.x4) {
+        fold2_x_rows4(a);
+        return;
+    }
     if (a.axis == 0) {
         // rows over blocks, orbits over threads (no 64-bit index division); every
         // field's orbit is loaded before any store
@@ -1298,6 +1365,132 @@ __device__ void source_fold2_rows(const SourceArgs& a, double srcA, int nj, int&
             else put(3 * H + k, o[3]);
         }
     }
+}
+
+// The same pass as a kernel of its own (the default on the level-2 schedule): one
+// field is finished (source, butterflies, stores) before the next starts, so a thread
+// holds the orbit's U(,V) and ONE field of f at a time -- under the register cap of
+// MINB blocks per SM, where etd_source's all-paths body needs 124 registers (2 blocks,
+// 25% occupancy, 0.76 of the copy bandwidth).  XW = x values per thread (2: 16-byte
+// accesses).  Values and fail kinds are etd_source's, bit for bit.
+template <int XW>
+struct XVec;
+template <>
+struct XVec<1> {
+    using T = double;
+    static __device__ __forceinline__ double get(const T& v, int) { return v; }
+    static __device__ __forceinline__ void set(T& v, int, double x) { v = x; }
+};
+template <>
+struct XVec<2> {
+    using T = double2;
+    static __device__ __forceinline__ double get(const T& v, int e) { return e ? v.y : v.x; }
+    static __device__ __forceinline__ void set(T& v, int e, double x) {
+        if (e) v.y = x;
+        else v.x = x;
+    }
+};
+
+template <int SK, int NS, int XW, int MINB, bool OUTER_FAST>
+__global__ void __launch_bounds__(256, MINB) etd_source_l2(const SourceArgs a) {
+    using XV = XVec<XW>;
+    using T = typename XV::T;
+    __shared__ int stop;
+    if (threadIdx.x == 0) stop = *reinterpret_cast<volatile int*>(&a.status->fail);
+    __syncthreads();
+    if (stop) return;
+    const double srcA = SK == 4 ? exp(-a.sp[0] * a.status->t) : 0.0;
+    const int nj = a.j1 - a.j0;
+    int bad = 0, dom = 0;
+    const bool zf = a.fold == 2;
+    const int n = zf ? a.nz : a.ny, H = a.fh / 2;
+    const long long sk = zf ? a.plane : a.pitch;
+    const int nouter = zf ? nj : a.nz;
+    const int items = (a.x1 - a.x0 + XW - 1) / XW;
+    const long long total = (long long)nouter * H * items;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int w = (int)(t % items);
+        const long long r = t / items;
+        // OUTER_FAST: concurrent blocks share the orbit's planes (few 2 MB pages live)
+        const int k = OUTER_FAST ? (int)(r / nouter) : (int)(r % H);
+        const int outer = OUTER_FAST ? (int)(r % nouter) : (int)(r / H);
+        const int x = a.x0 + XW * w;
+        const int j0 = zf ? a.j0 + outer : 0, kz0 = zf ? 0 : outer;
+        const long long base = zf ? (long long)j0 * a.pitch + x : (long long)kz0 * a.plane + x;
+        const int c = 2 * H - 2 - k;
+        const bool cen = k == H - 1;
+        const int pts[4] = {k, n - 1 - k, cen ? 2 * H - 1 : c, n - 1 - c};
+        T u[NS][4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+                u[s][p] = (p < 3 || !cen) ? *reinterpret_cast<const T*>(a.buf + s * a.F + base + pts[p] * sk) : T{};
+        // etd_fold2's butterflies of one field's orbit values, stored at the stack positions
+        auto finish = [&](int fld, const T (&V)[4]) {
+            double* dst = a.fold_out + fld * a.F + base;
+            auto put = [&](int i, const T& v) { *reinterpret_cast<T*>(dst + i * sk) = v; };
+            T si, di, sc, dc, o2, o3;
+#pragma unroll
+            for (int e = 0; e < XW; ++e) {
+                const double ga = XV::get(V[0], e), gb = XV::get(V[1], e), gc = XV::get(V[2], e), ge = XV::get(V[3], e);
+                XV::set(si, e, ga + gb);
+                XV::set(di, e, ga - gb);
+                XV::set(sc, e, cen ? gc + gc : gc + ge);   // centre orbit: 2 g_{2H-1}
+                XV::set(dc, e, cen ? ga - gb : gc - ge);   // centre orbit: c = k, d_c = d_k
+            }
+#pragma unroll
+            for (int e = 0; e < XW; ++e) {
+                XV::set(o2, e, XV::get(di, e) + XV::get(dc, e));
+                XV::set(o3, e, XV::get(di, e) - XV::get(dc, e));
+            }
+            put(fold2_spos(k, H), si);
+            put(2 * H + k, o2);
+            if (cen) put(2 * H - 1, sc);
+            else {
+                put(fold2_spos(c, H), sc);
+                put(3 * H + k, o3);
+            }
+        };
+#pragma unroll
+        for (int fs = 0; fs < NS; ++fs) {
+            T f[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                f[p] = T{};
+                if (p == 3 && cen) continue;
+                const int jj = zf ? j0 : pts[p], kk = zf ? pts[p] : kz0;
+#pragma unroll
+                for (int e = 0; e < XW; ++e) {
+                    double uv[2] = {0.0, 0.0}, fv[2] = {0.0, 0.0};
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) uv[s] = XV::get(u[s][p], e);
+                    if (x + e < a.nx) {
+                        if constexpr (NS == 1) {
+                            double ustar = 0.0;
+                            if constexpr (SK == 4)
+                                ustar = srcA * (a.sinx[x + e] * a.siny[jj + a.gj0] * (a.sinz ? a.sinz[kk + a.gz0] : 1.0));
+                            fv[0] = src1<SK>(a.sp, uv[0], ustar);
+                            if constexpr (SK == 3)
+                                if (x + e == 0 && jj + a.gj0 == 0 && kk + a.gz0 == 0)
+                                    fv[0] = __longlong_as_double(0x7ff8000000000000ll);
+                            dom |= src_domain_violation<SK>(uv[0]);
+                        } else {
+                            src2<SK>(a.sp, uv[0], uv[1], fv[0], fv[1]);
+                        }
+                        bad |= !isfinite(fv[fs]);
+                    }
+                    XV::set(f[p], e, fv[fs]);
+                }
+            }
+            finish(NS + fs, f);
+        }
+#pragma unroll
+        for (int s = 0; s < NS; ++s) finish(s, u[s]);
+    }
+    const int any_dom = __syncthreads_or(dom), any_bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0 && (any_dom || any_bad)) atomicCAS(&a.status->fail, 0, any_dom ? 4 : 1);
 }
 
 // ------------------------------------------------------------- second-level unfold pass

@@ -118,7 +118,43 @@ static const void* pick_unfold(int sk, int uf) {
 #undef ETD_UF
 }
 
-static const void* pick_source(int sk) {
+// level-2 source pass (etd_source_l2): variant v = 1 (16-byte x pairs, 3 blocks/SM),
+// 2 (one x per thread, 4 blocks/SM); 3 / 4 the same with the outer index fastest;
+// 5 x pairs, 2 blocks, outer fastest
+template <int SK>
+static const void* pick_source_l2_sk(int ns, int v) {
+#define ETD_SL2(NS)                                                                                   \
+    (v == 1   ? reinterpret_cast<const void*>(etd_source_l2<SK, NS, 2, 3, false>)                      \
+     : v == 2 ? reinterpret_cast<const void*>(etd_source_l2<SK, NS, 1, 4, false>)                      \
+     : v == 3 ? reinterpret_cast<const void*>(etd_source_l2<SK, NS, 2, 3, true>)                       \
+     : v == 4 ? reinterpret_cast<const void*>(etd_source_l2<SK, NS, 1, 4, true>)                       \
+              : reinterpret_cast<const void*>(etd_source_l2<SK, NS, 2, 2, true>))
+    return ns == 1 ? ETD_SL2(1) : ETD_SL2(2);
+#undef ETD_SL2
+}
+
+static int source_l2_variant() {
+    const char* e = getenv("ETD_SRC_L2");
+    return e ? atoi(e) : 3;
+}
+
+static const void* pick_source(int sk, int ns = 0, bool fold2 = false) {
+    const int v = source_l2_variant();
+    if (fold2 && v > 0) {
+        switch (sk) {
+        case 0: return pick_source_l2_sk<0>(ns, v);
+        case 1: return pick_source_l2_sk<1>(ns, v);
+        case 2: return pick_source_l2_sk<2>(ns, v);
+        case 3: return pick_source_l2_sk<3>(ns, v);
+        case 4: return pick_source_l2_sk<4>(ns, v);
+        case 5: return pick_source_l2_sk<5>(ns, v);
+        case 10: return pick_source_l2_sk<10>(ns, v);
+        case 11: return pick_source_l2_sk<11>(ns, v);
+        case 12: return pick_source_l2_sk<12>(ns, v);
+        case 13: return pick_source_l2_sk<13>(ns, v);
+        default: throw ConfigError("unknown source kind");
+        }
+    }
     switch (sk) {
     case 0: return reinterpret_cast<const void*>(etd_source<0>);
     case 1: return reinterpret_cast<const void*>(etd_source<1>);
@@ -676,7 +712,7 @@ struct Plan {
         a.siny = sintab[1];
         a.sinz = dim == 3 ? sintab[2] : nullptr;
         a.status = status;
-        o.src_fn = pick_source(d.src_kind);
+        o.src_fn = pick_source(d.src_kind, ns, fold_axis && fold2);
         o.src_blocks = (unsigned)std::min<long long>((long long)v.ny * v.nz, 148LL * 16);
         const double pts = (double)v.nx * v.ny * v.nz;
         o.L.flops = 0.0;
@@ -719,6 +755,10 @@ struct Plan {
         a.r0 = 0;
         a.r1 = (long long)v.ny * v.nz;
         a.rows = nullptr;
+        {
+            const char* e = getenv("ETD_FOLDX4");  // A/B: 0 = one orbit per thread, 8-byte accesses
+            a.x4 = (axis == 0 && !from1 && a.H % 4 == 0 && !(e && atoi(e) == 0)) ? 1 : 0;
+        }
         const double pts = (double)v.nx * v.ny * v.nz;
         o.L.flops = 0.0;
         o.L.bytes = pts * 8.0 * 2 * nf;
@@ -1002,7 +1042,7 @@ static void set_source(Plan& p, int kind, const double* params) {
         for (auto& op : p.steps[par])
             if (op.kind == Op::SOURCE) {
                 for (int i = 0; i < 8; ++i) op.sargs.sp[i] = p.d.src_params[i];
-                op.src_fn = pick_source(kind);
+                op.src_fn = pick_source(kind, p.ns, op.sargs.fold && op.sargs.fold2);
             } else if (op.kind == Op::THOMAS) {
                 for (int i = 0; i < 8; ++i) op.targs.sp[i] = p.d.src_params[i];
                 op.src_fn = pick_thomas(op.L.mode, op.th_epi, p.ns, kind, op.targs.npoles).fn;
