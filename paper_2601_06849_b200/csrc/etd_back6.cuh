@@ -41,7 +41,7 @@ struct Back6Cfg {
     static constexpr int A1_DBL = S * BM * BK, A_DBL = AB * A1_DBL, B_DBL = BN * BK;
     static constexpr int STAGE_DBL = A_DBL + B_DBL;
     static constexpr uint32_t TX_BYTES = (AB * S * BM + BN) * BK * 8;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_DBL * 8 + 1024 + 2 * STAGES * 8 + 64;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_DBL * 8 + 1024 + 2 * STAGES * 8 + 64 + 192;  // + CTA trace scratch
     static_assert(WM % 8 == 0 && WN % 64 == 0, "a warp covers whole (par 0, par 1) block pairs");
     static_assert(BM % 16 == 0 && BN % 64 == 0, "cta tile");
 };
@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     const int outer = blockIdx.z + args.outer0;
     const int H = args.fold_h, n = args.n_axis;
     const int KT = (H + BK - 1) / BK;
+    unsigned long long* tr = reinterpret_cast<unsigned long long*>(cta_flag + 2);
+    trace_stamp(args, tr, 0);
 
     if (tid == 0) {
         cta_flag[0] = *reinterpret_cast<volatile int*>(&args.status->fail);
@@ -144,6 +146,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     int stage = 0;
     uint32_t phase = 0;
     mbar_wait(&full[0], 0);
+    trace_stamp(args, tr, 1);
     load_frags(0, 0, fa[0]);
     for (int kt = 0; kt < KT; ++kt) {
         const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
@@ -169,11 +172,13 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
             issue(kt + STAGES, stage);
         }
         __syncwarp();
+        if (kt < 16) trace_stamp(args, tr, 4 + kt);
         stage = nstage;
         phase = nphase;
     }
 
     // ===================== orbit epilogue =====================
+    trace_stamp(args, tr, 2);
     double* __restrict__ outp = args.out;
     auto offset = [&](int m, int p) -> long long {
         if constexpr (MODE == 0) return (long long)m * args.pitch + p;
@@ -375,16 +380,21 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                     }
                     const double* au = args.aux + (long long)s * args.aux_stride + (long long)m * args.pitch;
                     double* o = outp + (long long)s * args.out_stride + (long long)m * args.pitch;
-                    auto ld2 = [&](int p) { return __ldg(reinterpret_cast<const double2*>(au + p)); };
+                    // plain loads (not ld.global.nc): they stay behind the previous species'
+                    // stores, so one species is finished -- loads, adds, stores -- before the
+                    // next starts; with all 20 loads hoisted ahead of all 20 stores the
+                    // launch is 4% slower (r02_experiments.md)
+                    auto ld1 = [&](int p) { return au[p]; };
+                    auto ld2 = [&](int p) { return *reinterpret_cast<const double2*>(au + p); };
                     auto st2 = [&](int p, double a, double b) { *reinterpret_cast<double2*>(o + p) = make_double2(a, b); };
                     const int p1 = n - 1 - k0, p2 = 2 * H - 2 - k0, p3 = 2 * H + k0;
                     const double2 r0a = ld2(k0), r0b = ld2(k0 + 2);
                     const double2 r3a = ld2(p3);
-                    const double2 r3b = cen ? make_double2(__ldg(au + p3 + 2), 0.0) : ld2(p3 + 2);
+                    const double2 r3b = cen ? make_double2(ld1(p3 + 2), 0.0) : ld2(p3 + 2);
                     const double r3c = r3b.x, r3d = r3b.y;
-                    const double r1q0 = __ldg(au + p1), r1q3 = __ldg(au + p1 - 3);
+                    const double r1q0 = ld1(p1), r1q3 = ld1(p1 - 3);
                     const double2 r1m = ld2(p1 - 2);  // (q2, q1)
-                    const double r2q0 = __ldg(au + p2), r2q3 = __ldg(au + (cen ? 2 * H - 1 : p2 - 3));
+                    const double r2q0 = ld1(p2), r2q3 = ld1(cen ? 2 * H - 1 : p2 - 3);
                     const double2 r2m = ld2(p2 - 2);  // (q2, q1)
                     const double u[4][4] = {{r0a.x + gq[0][0], r1q0 + gq[0][1], r2q0 + gq[0][2], r3a.x + gq[0][3]},
                                             {r0a.y + gq[1][0], r1m.y + gq[1][1], r2m.y + gq[1][2], r3a.y + gq[1][3]},
@@ -536,6 +546,8 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     // ===================== status: abort flag and step commit (as etd_contract) =====================
     const int any_dom = __syncthreads_or(dom);
     const int any_bad = __syncthreads_or(bad);
+    trace_stamp(args, tr, 3);
+    trace_flush(args, tr);
     if (tid == 0) {
         if (any_dom || any_bad) {
             int kind = EPI == EPI_WHAT_SRC ? 2 : EPI == EPI_UPDATE ? 3 : 1;

@@ -120,6 +120,7 @@ struct ContractArgs {
                             // X_q - X_{h-1-q}) at (q, H + q): the level-2 backward's input (EPI_MIX: the
                             // mix outputs only; w2b stays in mode positions for EPI_CORR)
     double* fout;           // etd_back6 EPI_WHAT_SRC: f(t + tau, What) - w2 as x_fwd_corr's level-2 stack
+    unsigned long long* trace;  // diagnostic (ETD_CTA_TRACE): per-CTA phase clocks of SMs 0-3, else null
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -137,6 +138,24 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// CTA phase trace (diagnostic): thread 0 stamps clock64 into a shared scratch slot at
+// each phase boundary; at exit the CTAs of SMs 0-3 append {smid, block, t0..t3}.
+__device__ __forceinline__ void trace_stamp(const ContractArgs& args, unsigned long long* scratch, int i) {
+    if (args.trace && threadIdx.x == 0) scratch[i] = (unsigned long long)clock64();
+}
+__device__ __forceinline__ void trace_flush(const ContractArgs& args, const unsigned long long* scratch) {
+    if (!args.trace || threadIdx.x != 0) return;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (smid >= 4) return;
+    const unsigned long long idx = atomicAdd(args.trace, 1ull);
+    if (idx >= 8192ull) return;
+    unsigned long long* r = args.trace + 8 + idx * 24;
+    r[0] = smid;
+    r[1] = blockIdx.x + gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z);
+    for (int i = 0; i < 20; ++i) r[2 + i] = scratch[i];  // t0..t3, then the end of k-tiles 0..15
+}
+
 // Consumer release of a ring slot that TMA (the async proxy) refills after the
 // empty barrier completes.  The slot was read with generic-proxy LDS; without a
 // proxy fence ptxas may issue the arrive while those loads are still in flight

@@ -537,6 +537,7 @@ struct Plan {
     int dmax = 0;
     StepStatus* status = nullptr;
     StepStatus* status_host = nullptr;
+    mutable unsigned long long* trace = nullptr;  // ETD_CTA_TRACE=<stage name part>: CTA phase clocks (diagnostic)
     int cur = 0;
     std::vector<Op> steps[2];
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
@@ -571,6 +572,18 @@ struct Plan {
         if (thscr) cudaFree(thscr);
         for (int a = 0; a < 3; ++a)
             for (double* m : {PR[a], PTR[a], FF[a], FB[a], GA[a], GB[a], GO[a], GE[a], G6[a]}) if (m) cudaFree(m);
+        if (trace) {
+            // dump {count, records of smid, block, t0..t3} for tools/cta_trace.py
+            std::vector<unsigned long long> h(8 + 8192 * 24);
+            if (cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
+                const char* path = std::getenv("ETD_CTA_TRACE_OUT");
+                if (FILE* f = std::fopen(path ? path : "cta_trace.bin", "wb")) {
+                    std::fwrite(h.data(), 8, h.size(), f);
+                    std::fclose(f);
+                }
+            }
+            cudaFree(trace);
+        }
         if (status) cudaFree(status);
         if (status_host) cudaFreeHost(status_host);
         if (mirror) cudaFreeHost(mirror);
@@ -929,6 +942,14 @@ struct Plan {
         const unsigned gx = (nrows + L.k.bn - 1) / L.k.bn;
         const unsigned gy = (unsigned)((mext + L.k.bm - 1) / L.k.bm);
         L.grid = dim3(gx, gy, gz);
+        if (const char* e = std::getenv("ETD_CTA_TRACE"))
+            if (fold == 6 && name.find(e) != std::string::npos) {
+                if (!trace) {
+                    ETD_CK(cudaMalloc(&trace, (8 + 8192 * 24) * 8));
+                    ETD_CK(cudaMemset(trace, 0, (8 + 8192 * 24) * 8));
+                }
+                L.args.trace = trace;
+            }
         const double pts = (double)v.nx * v.ny * v.nz;
         // executed (= algorithmic) FLOPs of this launch: 2 n per point dense,
         // 2 (2h) h / n per point split (half)
@@ -1618,7 +1639,8 @@ static void build_plan(Plan& p, const etd_desc& d) {
                                     try {
                                         KernelSpec ks = pick(mode, S, e, pro != 0, sk, tile, fold);
                                         ETD_CK(cudaFuncSetAttribute(
-                                            ks.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ks.smem));
+                                            ks.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            std::getenv("ETD_ONE_CTA") ? std::max(ks.smem, 120000) : ks.smem));
                                     } catch (const ConfigError&) {
                                     }
                                 }
@@ -1995,7 +2017,8 @@ static void build_plan(Plan& p, const etd_desc& d) {
 static void launch(const Launch& L, cudaStream_t s) {
     void* args[4] = {const_cast<CUtensorMap*>(&L.tmA), const_cast<CUtensorMap*>(&L.tmB),
                      const_cast<CUtensorMap*>(&L.tmA2), const_cast<ContractArgs*>(&L.args)};
-    ETD_CK(cudaLaunchKernel(L.k.fn, L.grid, dim3(L.k.threads), args, L.k.smem, s));
+    static const bool one_cta = std::getenv("ETD_ONE_CTA") != nullptr;  // diagnostic: one CTA per SM
+    ETD_CK(cudaLaunchKernel(L.k.fn, L.grid, dim3(L.k.threads), args, one_cta ? std::max(L.k.smem, 120000) : L.k.smem, s));
 }
 
 // One op of one rank.  EXCHANGE over NCCL here; virtual-rank groups route
