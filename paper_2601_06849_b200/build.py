@@ -44,6 +44,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
     objdir = os.path.join(CSRC, "_obj")
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++20", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
+    common += os.environ.get("ETD_BUILD_DEFS", "").split()  # diagnostics, e.g. -DETD_CTA_TRACE_BUILD
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")

@@ -66,8 +66,8 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     const int outer = blockIdx.z + args.outer0;
     const int H = args.fold_h, n = args.n_axis;
     const int KT = (H + BK - 1) / BK;
-    unsigned long long* tr = reinterpret_cast<unsigned long long*>(cta_flag + 2);
-    trace_stamp(args, tr, 0);
+    [[maybe_unused]] unsigned long long* tr = reinterpret_cast<unsigned long long*>(cta_flag + 2);
+    ETD_TRACE_STAMP(args, tr, 0);
 
     if (tid == 0) {
         cta_flag[0] = *reinterpret_cast<volatile int*>(&args.status->fail);
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     int stage = 0;
     uint32_t phase = 0;
     mbar_wait(&full[0], 0);
-    trace_stamp(args, tr, 1);
+    ETD_TRACE_STAMP(args, tr, 1);
     load_frags(0, 0, fa[0]);
     for (int kt = 0; kt < KT; ++kt) {
         const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
@@ -172,13 +172,13 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
             issue(kt + STAGES, stage);
         }
         __syncwarp();
-        if (kt < 16) trace_stamp(args, tr, 4 + kt);
+        if (kt < 16) ETD_TRACE_STAMP(args, tr, 4 + kt);
         stage = nstage;
         phase = nphase;
     }
 
     // ===================== orbit epilogue =====================
-    trace_stamp(args, tr, 2);
+    ETD_TRACE_STAMP(args, tr, 2);
     double* __restrict__ outp = args.out;
     auto offset = [&](int m, int p) -> long long {
         if constexpr (MODE == 0) return (long long)m * args.pitch + p;
@@ -546,8 +546,8 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     // ===================== status: abort flag and step commit (as etd_contract) =====================
     const int any_dom = __syncthreads_or(dom);
     const int any_bad = __syncthreads_or(bad);
-    trace_stamp(args, tr, 3);
-    trace_flush(args, tr);
+    ETD_TRACE_STAMP(args, tr, 3);
+    ETD_TRACE_FLUSH(args, tr);
     if (tid == 0) {
         if (any_dom || any_bad) {
             int kind = EPI == EPI_WHAT_SRC ? 2 : EPI == EPI_UPDATE ? 3 : 1;

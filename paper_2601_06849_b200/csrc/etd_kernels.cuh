@@ -138,8 +138,18 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// CTA phase trace (diagnostic): thread 0 stamps clock64 into a shared scratch slot at
-// each phase boundary; at exit the CTAs of SMs 0-3 append {smid, block, t0..t3}.
+// CTA phase trace (diagnostic, compiled in only with -DETD_CTA_TRACE_BUILD:
+// ETD_BUILD_DEFS="-DETD_CTA_TRACE_BUILD" python -m paper_2601_06849_b200.build -f;
+// even as dead branches the stamps cost the 128-register fused backward ~0.7 ms per
+// launch): thread 0 stamps clock64 into a shared scratch slot at each phase boundary;
+// at exit the CTAs of SMs 0-3 append {smid, block, t0..t3, k-tile ends}.
+#ifdef ETD_CTA_TRACE_BUILD
+#define ETD_TRACE_STAMP(args, scratch, i) trace_stamp(args, scratch, i)
+#define ETD_TRACE_FLUSH(args, scratch) trace_flush(args, scratch)
+#else
+#define ETD_TRACE_STAMP(args, scratch, i) ((void)0)
+#define ETD_TRACE_FLUSH(args, scratch) ((void)0)
+#endif
 __device__ __forceinline__ void trace_stamp(const ContractArgs& args, unsigned long long* scratch, int i) {
     if (args.trace && threadIdx.x == 0) scratch[i] = (unsigned long long)clock64();
 }
