@@ -1084,31 +1084,47 @@ __global__ void __launch_bounds__(256) etd_source(const SourceArgs a) {
         if (threadIdx.x == 0 && (any_dom || any_bad)) atomicCAS(&a.status->fail, 0, any_dom ? 4 : 1);
         return;
     }
+    // plain pass (dense / Thomas / unsplit schedules): x pairs, 16-byte accesses (x0 is
+    // even and rows are pitch aligned; the pad column past an odd nx is written as +0.0)
     const long long rows = (long long)a.nz * nj;
-    const RowMap rm = row_map(a.x1 - a.x0);
+    const int items = (a.x1 - a.x0 + 1) / 2;
+    const RowMap rm = row_map(items);
     for (long long r = (long long)blockIdx.x * rm.rpb + rm.sub; rm.sub < rm.rpb && r < rows;
          r += (long long)gridDim.x * rm.rpb) {
         const int kz = (int)(r / nj), j = a.j0 + (int)(r % nj);
         const long long base = kz * a.plane + (long long)j * a.pitch;
-        for (int i = a.x0 + rm.lane; i < a.x1; i += rm.span) {
+        for (int w = rm.lane; w < items; w += rm.span) {
+            const int i = a.x0 + 2 * w;
             const long long o = base + i;
             if (a.nspecies == 1) {
-                const double u = a.buf[o];
-                double ustar = 0.0;
-                if constexpr (SK == 4)
-                    ustar = srcA * (a.sinx[i] * a.siny[j + a.gj0] * (a.sinz ? a.sinz[kz + a.gz0] : 1.0));
-                double f = src1<SK>(a.sp, u, ustar);
-                if constexpr (SK == 3)
-                    if (i == 0 && j + a.gj0 == 0 && kz + a.gz0 == 0) f = __longlong_as_double(0x7ff8000000000000ll);
-                a.buf[a.F + o] = f;
-                bad |= !isfinite(f);
-                dom |= src_domain_violation<SK>(u);
+                const double2 u = *reinterpret_cast<const double2*>(a.buf + o);
+                double f[2] = {0.0, 0.0};
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    if (i + e >= a.x1 || i + e >= a.nx) continue;
+                    const double ue = e ? u.y : u.x;
+                    double ustar = 0.0;
+                    if constexpr (SK == 4)
+                        ustar = srcA * (a.sinx[i + e] * a.siny[j + a.gj0] * (a.sinz ? a.sinz[kz + a.gz0] : 1.0));
+                    f[e] = src1<SK>(a.sp, ue, ustar);
+                    if constexpr (SK == 3)
+                        if (i + e == 0 && j + a.gj0 == 0 && kz + a.gz0 == 0) f[e] = __longlong_as_double(0x7ff8000000000000ll);
+                    bad |= !isfinite(f[e]);
+                    dom |= src_domain_violation<SK>(ue);
+                }
+                *reinterpret_cast<double2*>(a.buf + a.F + o) = make_double2(f[0], f[1]);
             } else {
-                double fu, fv;
-                src2<SK>(a.sp, a.buf[o], a.buf[a.F + o], fu, fv);
-                a.buf[2 * a.F + o] = fu;
-                a.buf[3 * a.F + o] = fv;
-                bad |= !(isfinite(fu) && isfinite(fv));
+                const double2 u = *reinterpret_cast<const double2*>(a.buf + o);
+                const double2 v = *reinterpret_cast<const double2*>(a.buf + a.F + o);
+                double fu[2] = {0.0, 0.0}, fv[2] = {0.0, 0.0};
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    if (i + e >= a.x1 || i + e >= a.nx) continue;
+                    src2<SK>(a.sp, e ? u.y : u.x, e ? v.y : v.x, fu[e], fv[e]);
+                    bad |= !(isfinite(fu[e]) && isfinite(fv[e]));
+                }
+                *reinterpret_cast<double2*>(a.buf + 2 * a.F + o) = make_double2(fu[0], fu[1]);
+                *reinterpret_cast<double2*>(a.buf + 3 * a.F + o) = make_double2(fv[0], fv[1]);
             }
         }
     }
