@@ -2203,7 +2203,12 @@ static void do_steps(Plan& p, int nsteps) {
 static void group_steps(std::vector<Plan*>& ps, int nsteps) {
     const int G = (int)ps.size();
     if (G < 1) throw ConfigError("empty group");
+    // ETD_SOLO_RANK (timing diagnostic, tools/solo_rank.py): one virtual rank of a G-rank
+    // plan runs its own ops with the exchanges skipped (peer data reads as the buffers'
+    // zero fill), to time a rank's compute at a G that does not fit one device G times
+    const bool solo = G == 1 && ps[0]->local_group && ps[0]->G > 1 && std::getenv("ETD_SOLO_RANK");
     for (int r = 0; r < G; ++r) {
+        if (solo) break;
         if (!ps[r]->local_group || ps[r]->G != G || ps[r]->rank != r)
             throw ConfigError("group handles must be virtual ranks 0..G-1 of one sharded plan");
         if (ps[r]->d.device != ps[0]->d.device) throw ConfigError("virtual ranks must share a device");
@@ -2232,6 +2237,14 @@ static void group_steps(std::vector<Plan*>& ps, int nsteps) {
                 const Op& op = p.steps[(p.cur + st) & 1][k];
                 if (op.kind != Op::EXCHANGE) {
                     run_op(p, op, s);
+                    continue;
+                }
+                if (solo) {
+                    // every peer "reports" this rank's own fail code; the data exchanges are skipped
+                    if (op.name == "gather_codes")
+                        for (size_t i = 0; i < op.sends.size() && i < op.recvs.size(); ++i)
+                            ETD_CK(cudaMemcpyAsync(op.recvs[i].ptr, op.sends[i].ptr, op.sends[i].bytes,
+                                                   cudaMemcpyDeviceToDevice, s));
                     continue;
                 }
                 // push this rank's sends into the peers' receive pieces (matched in order)
