@@ -120,14 +120,35 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     // under its 128-register cap
     // (fragment offsets pinned in registers once: FragOffsets, etd_kernels.cuh)
     const FragOffsets<MODE, 0, MF> fo(wm0, wn0, g, l, C::A1_DBL, C::A_DBL);
+    // XPAIR (y/z, 16 x per warp): the warp's two M fragments interleave, fragment i row g
+    // is x = wm0 + 2 g + i.  Both fragments' A values are then ONE 16-byte LDS (the pair
+    // is a swizzle chunk of the [k][16 x] tile: conflict free, a quarter warp reads a whole
+    // 128-byte row), and each thread owns two adjacent x of every output: 16-byte stores.
+    constexpr bool XPAIR = MODE == 1 && MF == 2;
+    int eap[2] = {0, 0};
+    if constexpr (XPAIR) {
+#pragma unroll
+        for (int pp = 0; pp < 2; ++pp) {
+            const int kk = 2 * l + pp;
+            eap[pp] = pin((wm0 >> 4) * 256 + kk * 16 + ((g ^ (kk & 7)) << 1));
+        }
+    }
     auto load_frags = [&](int stg, int st, double (&a)[4][S][MF]) {
         const double* sA = smem + stg * C::STAGE_DBL;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int s = 0; s < S; ++s)
+            for (int s = 0; s < S; ++s) {
+                if constexpr (XPAIR) {
+                    const double2 v = *reinterpret_cast<const double2*>(sA + q * C::A1_DBL + s * BM * BK +
+                                                                        eap[st & 1] + 128 * (st >> 1));
+                    a[q][s][0] = v.x;
+                    a[q][s][MF - 1] = v.y;
+                } else {
 #pragma unroll
-                for (int i = 0; i < MF; ++i) a[q][s][i] = sA[q * C::A1_DBL + s * BM * BK + fo.a(st, i)];
+                    for (int i = 0; i < MF; ++i) a[q][s][i] = sA[q * C::A1_DBL + s * BM * BK + fo.a(st, i)];
+                }
+            }
     };
     auto mma = [&](int stg, int st, const double (&a)[4][S][MF]) {
         const double* sA = smem + stg * C::STAGE_DBL;
@@ -417,6 +438,47 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                     if (cen) o[p3 + 2] = u[2][3];
                     else st2(p3 + 2, u[2][3], u[3][3]);
                 }
+            }
+        }
+    } else if constexpr (XPAIR) {
+        // y/z store epilogue, two adjacent x per thread (m even; an odd extent's pad
+        // column receives the +0.0 its zero A rows produce)
+        const int m = m0 + wm0 + 2 * g;
+        if (m < args.m_extent) {
+#pragma unroll
+            for (int bp = 0; bp < NF / 8; ++bp) {
+                const int kb = (n0 + wn0) / 64 + bp;
+#pragma unroll
+                for (int par = 0; par < 2; ++par)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int k = 16 * kb + 4 * l + 2 * e + par;
+                        if (k >= H) continue;
+                        const int jb = 8 * bp + 4 * par;
+                        const bool centre = k == H - 1;
+                        const int c = 2 * H - 2 - k;
+                        const int np = centre ? 3 : 4;
+                        const int pos[4] = {k, n - 1 - k, centre ? 2 * H - 1 : c, n - 1 - c};
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {
+                            double gv[2][4];
+#pragma unroll
+                            for (int i = 0; i < 2; ++i) {
+                                const double O1 = acc[s][i][jb][e], O2 = acc[s][i][jb + 1][e];
+                                const double EO = acc[s][i][jb + 2][e], EE = acc[s][i][jb + 3][e];
+                                const double ek = EO + EE, ec = EO - EE;
+                                gv[i][0] = O1 + ek;
+                                gv[i][1] = O1 - ek;
+                                gv[i][2] = centre ? O2 : O2 + ec;
+                                gv[i][3] = O2 - ec;
+                            }
+                            double* o = outp + (long long)s * args.out_stride;
+#pragma unroll
+                            for (int p = 0; p < 4; ++p)
+                                if (p < np)
+                                    *reinterpret_cast<double2*>(o + offset(m, pos[p])) = make_double2(gv[0][p], gv[1][p]);
+                        }
+                    }
             }
         }
     } else {

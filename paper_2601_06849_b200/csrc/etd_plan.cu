@@ -133,6 +133,13 @@ static const void* pick_source_l2_sk(int ns, int v) {
 #undef ETD_SL2
 }
 
+// y/z fused backward launches: one field per launch (S = 1 tiles, XPAIR fragment interleave,
+// etd_back6.cuh) unless ETD_BACK6_XPAIR=0 (S = 4 stacks as two S = 2 launches; A/B)
+static bool back6_xpair() {
+    const char* e = std::getenv("ETD_BACK6_XPAIR");
+    return !(e && atoi(e) == 0);
+}
+
 static int source_l2_variant() {
     const char* e = getenv("ETD_SRC_L2");
     return e ? atoi(e) : 3;
@@ -1736,10 +1743,16 @@ static void build_plan(Plan& p, const etd_desc& d) {
             if (p.back6) {
                 if (src == dst) throw ConfigError("internal: fused backward in place");
                 const int epi = uf == UF_UPDATE ? EPI_UPDATE : uf == UF_WHAT_SRC ? EPI_WHAT_SRC : EPI_STORE;
-                const int nl = S == 4 ? 2 : 1;
+                // y/z: one launch per field (S = 1 tiles are 64 x wide, so a warp holds 16 x and
+                // the XPAIR fragment interleave gives 16-byte LDS / stores); ETD_BACK6_XPAIR=0:
+                // S = 4 stacks as two S = 2 launches (A/B)
+                const int nl = (back6_xpair() && axis != 0) ? S : (S == 4 ? 2 : 1);
+                const int per = S / nl;
                 for (int h2 = 0; h2 < nl; ++h2) {
-                    L.push_back(kernel_op(p.transform(vv, nl == 2 ? nm + (h2 ? "_b" : "_a") : nm, axis, true, S / nl,
-                                                      epi, false, src + 2 * h2 * vv.F, dst + 2 * h2 * vv.F, false,
+                    const std::string sfx(1, (char)('a' + h2));
+                    L.push_back(kernel_op(p.transform(vv, nl >= 2 ? nm + "_" + sfx : nm, axis, true, per,
+                                                      epi, false, src + (size_t)per * h2 * vv.F,
+                                                      dst + (size_t)per * h2 * vv.F, false,
                                                       nullptr, false, 6)));
                     L.back().L.args.aux = aux;
                     L.back().L.args.fout = fout;
@@ -1852,7 +1865,8 @@ static void build_plan(Plan& p, const etd_desc& d) {
             // launches (+ the level-2 unfold); an empty chunk pads with as many no-ops so
             // every rank's op list stays aligned with rank 0's (group_steps, NCCL groups)
             const int zl = (f2 && (pairs || p.back6) && 2 * ns == 4) ? 2 : 1;  // launches per level-2 part
-            const int chunk_ops = fused ? 2 : f2 ? 1 + 2 * zl + (p.back6 ? zl : 2 * zl + 1) : 3;
+            const int zb6 = back6_xpair() ? 2 * ns : zl;  // fused backward launches of a chunk
+            const int chunk_ops = fused ? 2 : f2 ? 1 + 2 * zl + (p.back6 ? zb6 : 2 * zl + 1) : 3;
             for (int k = 0; k < C; ++k) {
                 const View& vk = p.zch[k];
                 const size_t first = L.size();
@@ -3155,6 +3169,7 @@ int etd_debug_repeat_op(etd_handle* h, const char* name, int out, int reps, long
         for (const auto& o : p.steps[p.cur & 1])
             if ((o.kind == etd::Op::KERNEL || o.kind == etd::Op::SOURCE) && o.name == name) op = &o;
         if (!op || op->kind != etd::Op::KERNEL) throw etd::ConfigError("no such kernel op");
+        if (out < 0 || out >= std::max(1, op->L.S)) throw etd::ConfigError("output index beyond the launch's stack");
         // outputs are out_stride apart (pair launches: 2 fields); each is one field
         const long long F = p.slab.F;
         const double* target = op->L.args.out + (size_t)out * op->L.args.out_stride;

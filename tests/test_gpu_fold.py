@@ -179,8 +179,10 @@ def test_fold_halves_the_transform_flops(monkeypatch):
         assert st[nm]["dense_flops_per_launch"] == pytest.approx(0.5 * 2.0 * n * pts * 2)
     # the fused backward (§4c): one launch of all four quarters, 2 (4H) H / n per point
     # (n = 63: 4H = 64 rows, already whole 64-row block pairs)
-    assert st["z_back"]["flops_per_launch"] == pytest.approx(2.0 * 4 * H * H / n * pts * 2)
-    assert st["z_back"]["dense_flops_per_launch"] == pytest.approx(2.0 * n * pts * 2)
+    # (y/z: one launch per field of the [U, fU] stack)
+    for nm in ("z_back_a", "z_back_b"):
+        assert st[nm]["flops_per_launch"] == pytest.approx(2.0 * 4 * H * H / n * pts)
+        assert st[nm]["dense_flops_per_launch"] == pytest.approx(2.0 * n * pts)
     # the y stack pass (HBM-bound, no FLOPs counted)
     assert st["fold_y_fwd"]["flops_per_launch"] == 0
     # the round-1 backward: two launches + the fused z unfold / y stack pass
