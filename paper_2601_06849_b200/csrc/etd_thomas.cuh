@@ -39,6 +39,10 @@
 namespace etd {
 
 enum ThomasEpi { TH_STORE = 0, TH_WHAT = 1, TH_UPDATE = 2 };
+// ring depth of the x-axis kernels (their stages are L operands wide: 32 KB)
+#ifndef ETD_THOMAS_XSTAGES
+#define ETD_THOMAS_XSTAGES 3
+#endif
 
 struct ThomasArgs {
     double* out;              // output stack, stride F
@@ -87,7 +91,7 @@ struct ThomasCfg {
     static constexpr int P = SPLIT ? 64 : 128;             // pencils per tile
     static constexpr int J = 16;                           // axis points per stage
     static constexpr int L = MODE == 0 ? (EPI == TH_WHAT ? 2 * NS : EPI == TH_UPDATE ? 2 : 1) : 1;
-    static constexpr int STAGES = 3;
+    static constexpr int STAGES = MODE == 0 ? ETD_THOMAS_XSTAGES : 3;
     static constexpr int OP_DBL = P * J;
     static constexpr int STAGE_DBL = L * OP_DBL;
     static constexpr int NSU = EPI == TH_WHAT ? NS : 1;    // species whose factors a stage carries
@@ -198,9 +202,10 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
         const int slot = q % S;
         consumer_release(&empty[slot], lane);
         ++q;
-        // refill the slot of the stage before last (every warp is normally past it)
+        // refill the slot of the stage before last (every warp is normally past it);
+        // a 2-deep ring refills the slot just released
         if (t == 0)
-            for (; issued < total && issued <= q + S - 2; ++issued) {
+            for (; issued < total && issued <= q + (S > 2 ? S - 2 : S - 1); ++issued) {
                 mbar_wait(&empty[issued % S], (uint32_t)((issued / S - 1) & 1));
                 issue(issued);
             }
@@ -302,12 +307,28 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
         // (thomas.cpp:40-46, 65-84), chunk by chunk from the end of the axis: the
         // chunk's forward values are recomputed from its checkpoint (same bits)
         double2 wn[R][NP];
-        for (int jt = nt - 1; jt >= 0; --jt) {
-            const double* st = acquire();
-#pragma unroll 1
-            for (int cc = J / K - 1; cc >= 0; --cc) {
+        // Each chunk starts from its checkpoint, an L2 / HBM round trip the recurrence
+        // waits for (ncu, config 3: 45% of a pass's stall samples sat on the first use
+        // of that load).  PREF: the chunk loop is unrolled over a stage's J / K chunks
+        // and chunk cc's checkpoint registers pf[cc] are reloaded, right after their
+        // use, with the checkpoint of the same chunk of the next (lower) stage: one
+        // stage of lead, no register shuffling (a shifted ring waits on every load it
+        // moves: measured slower).  The coupled predictor (TH_WHAT) keeps the plain
+        // loop: its stalls move to the shared-memory operand loads and the unrolled
+        // body outgrows the instruction cache (x_what 48.2 -> 52.4 ms at config 4).
+        constexpr bool PREF = EPI != TH_WHAT;
+        constexpr int NCH = J / K;
+        auto cp_load = [&](int c, double2 (&dst)[R][NP]) {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int l = 0; l < NP; ++l)
+                    dst[r][l] = (c > 0 && c < nc) ? cpt[((long long)(r * NP + l) * nc + c) * cstr]
+                                                  : make_double2(0.0, 0.0);
+        };
+        auto chunk = [&](const double* st, int jt, int cc, const double2 (&cp0)[R][NP]) {
                 const int j0 = jt * J + cc * K, c = j0 / K;
-                if (j0 >= n) continue;
+                if (j0 >= n) return;
                 const bool edge = c == 0 || j0 + K >= n;  // first chunk, or holds j = n - 1
                 double v[R][K];
 #pragma unroll
@@ -315,7 +336,7 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                     double2 wv[R][K];
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        double2 prev = c > 0 ? cpt[((long long)(r * NP + l) * nc + c) * cstr] : make_double2(0.0, 0.0);
+                        double2 prev = cp0[r][l];
 #pragma unroll
                         for (int k = 0; k < K; ++k) {
                             const int j = j0 + k;
@@ -369,9 +390,9 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                         a.out[(long long)sl * a.F + o] = Wm;
                         a.out[(long long)(NS + sl) * a.F + o] = __dsub_rn(fm, rd(st, NS + sl, cc * K + k));
                     }
-                    continue;
+                    return;
                 }
-                if (!valid) continue;
+                if (!valid) return;
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const int j = j0 + k;
@@ -410,6 +431,31 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                             a.out[(long long)(NS + s) * a.F + o] = __dsub_rn(fv[s], rd(st, NS + s, cc * K + k));
                         }
                     }
+                }
+        };
+        double2 pf[PREF ? NCH : 1][R][NP];
+        if constexpr (PREF) {
+#pragma unroll
+            for (int cc = 0; cc < NCH; ++cc) cp_load((nt - 1) * NCH + cc, pf[cc]);
+        }
+        for (int jt = nt - 1; jt >= 0; --jt) {
+            const double* st = acquire();
+            if constexpr (PREF) {
+#pragma unroll
+                for (int cc = NCH - 1; cc >= 0; --cc) {
+                    double2 cp0[R][NP];
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+#pragma unroll
+                        for (int l = 0; l < NP; ++l) cp0[r][l] = pf[cc][r][l];
+                    cp_load(jt * NCH + cc - NCH, pf[cc]);
+                    chunk(st, jt, cc, cp0);
+                }
+            } else {
+#pragma unroll 1
+                for (int cc = NCH - 1; cc >= 0; --cc) {
+                    cp_load(jt * NCH + cc, pf[0]);
+                    chunk(st, jt, cc, pf[0]);
                 }
             }
             release();
