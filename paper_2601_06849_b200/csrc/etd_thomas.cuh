@@ -217,6 +217,26 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
         if constexpr (MODE == 1) return st[(tp >> 4) * (J * 16) + swz(jj, tp & 15)];
         else return st[op * C::OP_DBL + swz(tp, jj)];
     };
+    // N consecutive axis points (jj0 even) of an operand.  MODE 0: a thread's points are
+    // consecutive columns of its own row, read as 16-byte pairs -- a pair is one swizzle
+    // chunk, so the four rows that share a chunk position fill a 128-byte wavefront
+    // (8-byte reads leave half of every wavefront unused: ncu counted as many bank
+    // conflicts as useful wavefronts on the x passes)
+    auto rdn = [&](const double* st, int op, int jj0, auto& dst) {
+        constexpr int N = sizeof(dst) / sizeof(double);
+        if constexpr (MODE == 0) {
+#pragma unroll
+            for (int k2 = 0; k2 < N / 2; ++k2) {
+                const double2 pr = *reinterpret_cast<const double2*>(
+                    st + op * C::OP_DBL + tp * 16 + ((((jj0 >> 1) + k2) ^ (tp & 7)) << 1));
+                dst[2 * k2] = pr.x;
+                dst[2 * k2 + 1] = pr.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < N; ++k) dst[k] = rd(st, op, jj0 + k);
+        }
+    };
     // operand (= global rhs index for TH_WHAT) of this thread's rhs r
     auto opr = [&](int r) { return EPI == TH_WHAT ? (SPLIT ? r * NS + sl : r) : 0; };
     // checkpoints of this thread: (r, l, c) at cpt[((r * NP + l) * nc + c) * G * P]
@@ -260,10 +280,11 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
         // ---- forward elimination w_i = b_i - mul_i w_{i-1} (thomas.cpp:38-39, 56-64),
         // checkpointing w_{cK-1} before every chunk c
         double2 wp[R][NP];
-        auto fwd_point = [&](const double* st, int jj, int j) {
+        constexpr int JP = MODE == 0 ? J : 1;  // the x passes preload a stage's operand values
+        auto fwd_point = [&](const double* st, int jj, int j, const double (&bq)[R][JP]) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const double b = rd(st, opr(r), jj);
+                const double b = MODE == 0 ? bq[r][jj % JP] : rd(st, opr(r), jj);
 #pragma unroll
                 for (int l = 0; l < NP; ++l) {
                     if (j == 0) {
@@ -284,11 +305,17 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
         for (int jt = 0; jt < nt; ++jt) {
             const double* st = acquire();
             const int j0 = jt * J;
+            // the stage's operand values (a tile always holds J columns: TMA zero-fills past n)
+            double bq[R][JP];
+            if constexpr (MODE == 0) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) rdn(st, opr(r), 0, bq[r]);
+            }
             if (jt > 0 && j0 + J <= n) {  // interior stage: no guards
 #pragma unroll
                 for (int jj = 0; jj < J; ++jj) {
                     if (jj % K == 0) checkpoint((j0 + jj) / K);
-                    fwd_point(st, jj, j0 + jj);
+                    fwd_point(st, jj, j0 + jj, bq);
                 }
             } else {
 #pragma unroll
@@ -296,7 +323,7 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                     const int j = j0 + jj;
                     if (j < n) {
                         if (jj % K == 0 && j > 0) checkpoint(j / K);
-                        fwd_point(st, jj, j);
+                        fwd_point(st, jj, j, bq);
                     }
                 }
             }
@@ -326,10 +353,37 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                     dst[r][l] = (c > 0 && c < nc) ? cpt[((long long)(r * NP + l) * nc + c) * cstr]
                                                   : make_double2(0.0, 0.0);
         };
+        // a chunk's K outputs of one field: 16-byte pairs along an x pencil (the chunk
+        // start is even and rows are 16-byte aligned), guarded singles on edge chunks
+        auto put = [&](long long fld, int j0, bool edge, const double (&x)[K]) {
+            double* o = a.out + fld * a.F + base;
+            if constexpr (MODE == 0) {
+                if (!edge) {
+#pragma unroll
+                    for (int k2 = 0; k2 < K / 2; ++k2)
+                        *reinterpret_cast<double2*>(o + j0 + 2 * k2) = make_double2(x[2 * k2], x[2 * k2 + 1]);
+                    return;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int j = j0 + k;
+                if (edge && j >= n) continue;
+                o[MODE == 0 ? (long long)j : j * a.es] = x[k];
+            }
+        };
         auto chunk = [&](const double* st, int jt, int cc, const double2 (&cp0)[R][NP]) {
                 const int j0 = jt * J + cc * K, c = j0 / K;
                 if (j0 >= n) return;
                 const bool edge = c == 0 || j0 + K >= n;  // first chunk, or holds j = n - 1
+                constexpr int KP = MODE == 0 ? K : 1;
+                double bq[R][KP];
+                if constexpr (MODE == 0) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) rdn(st, opr(r), cc * K, bq[r]);
+                }
+                [[maybe_unused]] double aq[K];  // TH_UPDATE: What
+                if constexpr (EPI == TH_UPDATE) rdn(st, 1, cc * K, aq);
                 double v[R][K];
 #pragma unroll
                 for (int l = 0; l < NP; ++l) {
@@ -341,7 +395,7 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                         for (int k = 0; k < K; ++k) {
                             const int j = j0 + k;
                             if (edge && j >= n) break;
-                            const double b = rd(st, opr(r), cc * K + k);
+                            const double b = MODE == 0 ? bq[r][k % KP] : rd(st, opr(r), cc * K + k);
                             if (edge && j == 0) {
                                 prev = make_double2(b, 0.0);
                             } else {
@@ -374,9 +428,11 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                 if constexpr (SPLIT) {
                     // What of this lane's species; the pair swaps them for f(t + tau, What)
                     // (all lanes of the warp take this path: same chunk, same guards)
+                    double o0[K], o1[K];
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         const int j = j0 + k;
+                        o0[k] = o1[k] = 0.0;
                         if (edge && j >= n) continue;
                         const double Wm = __dadd_rn(v[0][k], __dmul_rn(a.tau, v[1][k]));
                         const double Wo = __shfl_xor_sync(0xffffffffu, Wm, 1);
@@ -386,27 +442,37 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                         src2<SK>(a.sp, Wu, Wv, fu, fv);
                         const double fm = sl == 0 ? fu : fv;
                         bad |= !isfinite(fm);
-                        const long long o = base + j;
-                        a.out[(long long)sl * a.F + o] = Wm;
-                        a.out[(long long)(NS + sl) * a.F + o] = __dsub_rn(fm, rd(st, NS + sl, cc * K + k));
+                        o0[k] = Wm;
+                        o1[k] = __dsub_rn(fm, MODE == 0 ? bq[1][k % KP] : 0.0);  // rhs 1 = w2 of this species
                     }
+                    if (!valid) return;
+                    put(sl, j0, edge, o0);
+                    put(NS + sl, j0, edge, o1);
                     return;
                 }
                 if (!valid) return;
+                if constexpr (EPI == TH_STORE) {
+                    put(f, j0, edge, v[0]);
+                } else if constexpr (EPI == TH_UPDATE) {
+                    // U1 = What + tau Q3(fw) (stepper.cpp:225, 252)
+                    double u1[K];
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const int j = j0 + k;
-                    if (edge && j >= n) continue;
-                    const long long o = base + (MODE == 0 ? (long long)j : j * a.es);
-                    if constexpr (EPI == TH_STORE) {
-                        a.out[(long long)f * a.F + o] = v[0][k];
-                    } else if constexpr (EPI == TH_UPDATE) {
-                        // U1 = What + tau Q3(fw) (stepper.cpp:225, 252)
-                        const double u1 = __dadd_rn(rd(st, 1, cc * K + k), __dmul_rn(a.tau, v[0][k]));
-                        a.out[(long long)f * a.F + o] = u1;
-                        bad |= !isfinite(u1);
-                    } else if constexpr (!SPLIT) {
-                        // What = Q1(w1) + tau Q2(w2); fw = f(t + tau, What) - w2
+                    for (int k = 0; k < K; ++k) {
+                        u1[k] = 0.0;
+                        if (edge && j0 + k >= n) continue;
+                        u1[k] = __dadd_rn(aq[k], __dmul_rn(a.tau, v[0][k]));
+                        bad |= !isfinite(u1[k]);
+                    }
+                    put(f, j0, edge, u1);
+                } else if constexpr (!SPLIT) {
+                    // What = Q1(w1) + tau Q2(w2); fw = f(t + tau, What) - w2
+                    double Wk[NS][K], gk[NS][K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const int j = j0 + k;
+#pragma unroll
+                        for (int s = 0; s < NS; ++s) Wk[s][k] = gk[s][k] = 0.0;
+                        if (edge && j >= n) continue;
                         double W[NS], fv[NS];
 #pragma unroll
                         for (int s = 0; s < NS; ++s) W[s] = __dadd_rn(v[s][k], __dmul_rn(a.tau, v[NS + s][k]));
@@ -427,9 +493,14 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
 #pragma unroll
                         for (int s = 0; s < NS; ++s) {
                             bad |= !isfinite(fv[s]);
-                            a.out[(long long)s * a.F + o] = W[s];
-                            a.out[(long long)(NS + s) * a.F + o] = __dsub_rn(fv[s], rd(st, NS + s, cc * K + k));
+                            Wk[s][k] = W[s];
+                            gk[s][k] = __dsub_rn(fv[s], MODE == 0 ? bq[NS + s][k % KP] : 0.0);  // rhs NS + s = w2
                         }
+                    }
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) {
+                        put(s, j0, edge, Wk[s]);
+                        put(NS + s, j0, edge, gk[s]);
                     }
                 }
         };
