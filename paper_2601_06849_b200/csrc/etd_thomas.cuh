@@ -211,7 +211,11 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
             }
     };
     // this thread's pencil within the tile, and (SPLIT) its species
-    const int tp = SPLIT ? t >> 1 : t, sl = SPLIT ? t & 1 : 0;
+    // SPLIT: a warp owns 16 pencils, lanes 0-15 their first species and lanes 16-31 the
+    // second, so the 8 lanes of a shared-memory wavefront read 8 consecutive rows of ONE
+    // operand tile (8 distinct swizzle chunks).  With the species on adjacent lanes every
+    // LDS.128 took 8 wavefronts instead of 4: the two tiles' rows share their banks.
+    const int tp = SPLIT ? (t >> 5) * 16 + (lane & 15) : t, sl = SPLIT ? lane >> 4 : 0;
     // operand `op` at axis offset jj of this thread's pencil
     auto rd = [&](const double* st, int op, int jj) -> double {
         if constexpr (MODE == 1) return st[(tp >> 4) * (J * 16) + swz(jj, tp & 15)];
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                         o0[k] = o1[k] = 0.0;
                         if (edge && j >= n) continue;
                         const double Wm = __dadd_rn(v[0][k], __dmul_rn(a.tau, v[1][k]));
-                        const double Wo = __shfl_xor_sync(0xffffffffu, Wm, 1);
+                        const double Wo = __shfl_xor_sync(0xffffffffu, Wm, 16);
                         if (!valid) continue;
                         const double Wu = sl == 0 ? Wm : Wo, Wv = sl == 0 ? Wo : Wm;
                         double fu, fv;
