@@ -993,6 +993,7 @@ struct Plan {
         a.f_first = f0;
         a.fin_off = fin_off;
         a.commit = epi == TH_UPDATE;
+        a.aux = stack;
         const int nfl = epi == TH_WHAT ? 1 : nfields;
         const unsigned long long nst = 2ull * ns;
         const ThomasSpec k = pick_thomas(mode, epi, ns, d.src_kind, a.npoles);

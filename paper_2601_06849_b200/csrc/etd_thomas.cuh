@@ -64,6 +64,7 @@ struct ThomasArgs {
     double2 res[2][3][2];     // [species][ell-1][pole]
     double tau;
     double2* scratch;         // checkpoints [rhs][pole][chunk][CTA][128]
+    const double* aux;        // TH_UPDATE: the What fields (the input stack's fields [0, ns))
     // TH_WHAT source evaluation (x pencils: row r -> y = r % ny, z = r / ny)
     int ny;
     int gj0, gz0;
@@ -90,7 +91,9 @@ struct ThomasCfg {
     static constexpr int T = 128;                          // threads per CTA
     static constexpr int P = SPLIT ? 64 : 128;             // pencils per tile
     static constexpr int J = 16;                           // axis points per stage
-    static constexpr int L = MODE == 0 ? (EPI == TH_WHAT ? 2 * NS : EPI == TH_UPDATE ? 2 : 1) : 1;
+    // operands a stage carries (TH_UPDATE reads What straight from global memory in the
+    // chunk epilogue: staging it would double the stage and halve the resident CTAs)
+    static constexpr int L = MODE == 0 && EPI == TH_WHAT ? 2 * NS : 1;
     static constexpr int STAGES = MODE == 0 ? ETD_THOMAS_XSTAGES : 3;
     static constexpr int OP_DBL = P * J;
     static constexpr int STAGE_DBL = L * OP_DBL;
@@ -156,9 +159,9 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
         const int jt = s < nt ? s : per_tile - 1 - s;
         const long long w = blockIdx.x + (long long)i * G;
         double* dst = smem + slot * C::STAGE_DBL;
-        // the forward sweep needs neither the 1/piv rows nor (TH_UPDATE) the What operand
+        // the forward sweep does not need the 1/piv rows
         const bool fwd = s < nt;
-        const int nops = (EPI == TH_UPDATE && fwd) ? 1 : L, nrows = fwd ? 1 : 2;
+        const int nops = L, nrows = fwd ? 1 : 2;
         mbar_expect_tx(&full[slot], (uint32_t)(nops * C::OP_DBL * 8 + C::NSU * NP * nrows * C::FAC_BYTES));
         const int pb = (int)(w % a.ptiles);
         const int rest = (int)(w / a.ptiles);
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
         } else {
             const int f = a.f_first + rest;
             for (int op = 0; op < nops; ++op) {
-                const int fld = EPI == TH_WHAT ? op : (op == 0 ? a.fin_off + f : f);
+                const int fld = EPI == TH_WHAT ? op : a.fin_off + f;
                 tma_load_3d(dst + op * C::OP_DBL, &tm, &full[slot], jt * J, pb * P, fld);
             }
         }
@@ -387,7 +390,22 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                     for (int r = 0; r < R; ++r) rdn(st, opr(r), cc * K, bq[r]);
                 }
                 [[maybe_unused]] double aq[K];  // TH_UPDATE: What
-                if constexpr (EPI == TH_UPDATE) rdn(st, 1, cc * K, aq);
+                if constexpr (EPI == TH_UPDATE) {
+                    // issued here, used after the chunk's recurrences
+                    const double* w = a.aux + (long long)f * a.F + base + (MODE == 0 ? (long long)j0 : j0 * a.es);
+                    if (MODE == 0 && !edge && valid) {
+#pragma unroll
+                        for (int k2 = 0; k2 < K / 2; ++k2) {
+                            const double2 pr = __ldg(reinterpret_cast<const double2*>(w) + k2);
+                            aq[2 * k2] = pr.x;
+                            aq[2 * k2 + 1] = pr.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < K; ++k)
+                            aq[k] = (valid && j0 + k < n) ? __ldg(w + (MODE == 0 ? (long long)k : k * a.es)) : 0.0;
+                    }
+                }
                 double v[R][K];
 #pragma unroll
                 for (int l = 0; l < NP; ++l) {
