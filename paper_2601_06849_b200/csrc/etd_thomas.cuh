@@ -39,6 +39,10 @@
 namespace etd {
 
 enum ThomasEpi { TH_STORE = 0, TH_WHAT = 1, TH_UPDATE = 2 };
+// right-hand sides per thread from which the back-substitution chunk is 4 points (else 8)
+#ifndef ETD_THOMAS_K4_RHS
+#define ETD_THOMAS_K4_RHS 3
+#endif
 // ring depth of the x-axis kernels (their stages are L operands wide: 32 KB)
 #ifndef ETD_THOMAS_XSTAGES
 #define ETD_THOMAS_XSTAGES 3
@@ -77,7 +81,7 @@ struct ThomasArgs {
 };
 
 __host__ __device__ constexpr int thomas_rhs(int epi, int ns) { return epi == TH_WHAT ? 2 * ns : 1; }
-__host__ __device__ constexpr int thomas_chunk(int rhs) { return rhs >= 2 ? 4 : 8; }
+__host__ __device__ constexpr int thomas_chunk(int rhs) { return rhs >= ETD_THOMAS_K4_RHS ? 4 : 8; }
 
 template <int MODE, int EPI, int NS>
 struct ThomasCfg {
