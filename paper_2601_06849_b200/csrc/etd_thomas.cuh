@@ -43,6 +43,10 @@ enum ThomasEpi { TH_STORE = 0, TH_WHAT = 1, TH_UPDATE = 2 };
 #ifndef ETD_THOMAS_K4_RHS
 #define ETD_THOMAS_K4_RHS 3
 #endif
+// checkpoint prefetch (unrolled chunk loop) in the coupled predictor too
+#ifndef ETD_THOMAS_PREF_WHAT
+#define ETD_THOMAS_PREF_WHAT 1
+#endif
 // ring depth of the x-axis kernels (their stages are L operands wide: 32 KB)
 #ifndef ETD_THOMAS_XSTAGES
 #define ETD_THOMAS_XSTAGES 3
@@ -354,7 +358,7 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
         // moves: measured slower).  The coupled predictor (TH_WHAT) keeps the plain
         // loop: its stalls move to the shared-memory operand loads and the unrolled
         // body outgrows the instruction cache (x_what 48.2 -> 52.4 ms at config 4).
-        constexpr bool PREF = EPI != TH_WHAT;
+        constexpr bool PREF = ETD_THOMAS_PREF_WHAT || EPI != TH_WHAT;
         constexpr int NCH = J / K;
         auto cp_load = [&](int c, double2 (&dst)[R][NP]) {
 #pragma unroll
