@@ -374,9 +374,13 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
             double* o = a.out + fld * a.F + base;
             if constexpr (MODE == 0) {
                 if (!edge) {
+                    // 32-byte stores (st.global.v4.f64, sm_100): one whole sector each
+                    static_assert(K % 4 == 0, "chunks are whole 32-byte pieces");
 #pragma unroll
-                    for (int k2 = 0; k2 < K / 2; ++k2)
-                        *reinterpret_cast<double2*>(o + j0 + 2 * k2) = make_double2(x[2 * k2], x[2 * k2 + 1]);
+                    for (int k4 = 0; k4 < K / 4; ++k4)
+                        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o + j0 + 4 * k4), "d"(x[4 * k4]),
+                                     "d"(x[4 * k4 + 1]), "d"(x[4 * k4 + 2]), "d"(x[4 * k4 + 3])
+                                     : "memory");
                     return;
                 }
             }
@@ -403,11 +407,10 @@ __global__ void __launch_bounds__(128) etd_thomas(const __grid_constant__ CUtens
                     const double* w = a.aux + (long long)f * a.F + base + (MODE == 0 ? (long long)j0 : j0 * a.es);
                     if (MODE == 0 && !edge && valid) {
 #pragma unroll
-                        for (int k2 = 0; k2 < K / 2; ++k2) {
-                            const double2 pr = __ldg(reinterpret_cast<const double2*>(w) + k2);
-                            aq[2 * k2] = pr.x;
-                            aq[2 * k2 + 1] = pr.y;
-                        }
+                        for (int k4 = 0; k4 < K / 4; ++k4)
+                            asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                                         : "=d"(aq[4 * k4]), "=d"(aq[4 * k4 + 1]), "=d"(aq[4 * k4 + 2]), "=d"(aq[4 * k4 + 3])
+                                         : "l"(w + 4 * k4));
                     } else {
 #pragma unroll
                         for (int k = 0; k < K; ++k)
