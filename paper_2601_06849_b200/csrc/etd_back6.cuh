@@ -32,6 +32,23 @@
 
 namespace etd {
 
+// 32-byte global accesses (sm_100: LDG / STG .ENL2.256), p 32-byte aligned.  A whole
+// sector per access; the x-stage epilogues use them where an orbit range is four
+// consecutive, aligned positions (R0 at k0, R3 at 2H + k0, the stack's 2H + k0 / 3H + k0).
+#ifndef ETD_BACK6_V4
+#define ETD_BACK6_V4 1
+#endif
+__device__ __forceinline__ void ldg_v4(const double* p, double (&w)[4]) {
+    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(w[0]), "=d"(w[1]), "=d"(w[2]), "=d"(w[3]) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void ldg_nc_v4(const double* p, double (&w)[4]) {
+    // not volatile: read-only data, free to move above earlier stores (as __ldg is)
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(w[0]), "=d"(w[1]), "=d"(w[2]), "=d"(w[3]) : "l"(p));
+}
+__device__ __forceinline__ void stg_v4(double* p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 template <int MODE, int S, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
 struct Back6Cfg {
     static constexpr int BK = 16, AB = 4;
@@ -227,9 +244,15 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                 // w2 at the four ranges, 16-byte where aligned: [s][q]
                 auto ldr = [&](const double* a, int R, double (&w)[4]) {
                     if (R == 0) {
-                        const double2 x = __ldg(reinterpret_cast<const double2*>(a + k0)),
-                                      y = __ldg(reinterpret_cast<const double2*>(a + k0 + 2));
-                        w[0] = x.x; w[1] = x.y; w[2] = y.x; w[3] = y.y;
+                        if constexpr (ETD_BACK6_V4) {
+                            ldg_nc_v4(a + k0, w);
+                        } else {
+                            const double2 x = __ldg(reinterpret_cast<const double2*>(a + k0)),
+                                          y = __ldg(reinterpret_cast<const double2*>(a + k0 + 2));
+                            w[0] = x.x; w[1] = x.y; w[2] = y.x; w[3] = y.y;
+                        }
+                    } else if (R == 3 && ETD_BACK6_V4 && !cen) {
+                        ldg_nc_v4(a + p3, w);
                     } else if (R == 3) {
                         const double2 x = __ldg(reinterpret_cast<const double2*>(a + p3));
                         w[0] = x.x; w[1] = x.y;
@@ -251,8 +274,12 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                     auto st2 = [&](int p, double a, double b) {
                         *reinterpret_cast<double2*>(o + p) = make_double2(a, b);
                     };
-                    if (R == 0) { st2(k0, v[0], v[1]); st2(k0 + 2, v[2], v[3]); }
-                    else if (R == 3) {
+                    if (R == 0) {
+                        if constexpr (ETD_BACK6_V4) stg_v4(o + k0, v[0], v[1], v[2], v[3]);
+                        else { st2(k0, v[0], v[1]); st2(k0 + 2, v[2], v[3]); }
+                    } else if (R == 3 && ETD_BACK6_V4 && !cen) {
+                        stg_v4(o + p3, v[0], v[1], v[2], v[3]);
+                    } else if (R == 3) {
                         st2(p3, v[0], v[1]);
                         if (cen) o[p3 + 2] = v[2];
                         else st2(p3 + 2, v[2], v[3]);
@@ -360,11 +387,19 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                             fo[2 * H - 2 - k0 / 2] = ga[sp][1];                   // s_c, c odd (q = 1)
                             if (cen) fo[2 * H - 1] = ga[sp][3];                   // the centre of s
                             else fo[2 * H - 3 - k0 / 2] = ga[sp][3];              // s_c, c odd (q = 3)
-                            st2(2 * H + k0, gb[sp][0], gb[sp][1]);
-                            st2(2 * H + k0 + 2, gb[sp][2], gb[sp][3]);
-                            st2(3 * H + k0, dk[sp][0], dk[sp][1]);
-                            if (cen) fo[3 * H + k0 + 2] = dk[sp][2];
-                            else st2(3 * H + k0 + 2, dk[sp][2], dk[sp][3]);
+                            if constexpr (ETD_BACK6_V4) {
+                                stg_v4(fo + 2 * H + k0, gb[sp][0], gb[sp][1], gb[sp][2], gb[sp][3]);
+                            } else {
+                                st2(2 * H + k0, gb[sp][0], gb[sp][1]);
+                                st2(2 * H + k0 + 2, gb[sp][2], gb[sp][3]);
+                            }
+                            if (ETD_BACK6_V4 && !cen) {
+                                stg_v4(fo + 3 * H + k0, dk[sp][0], dk[sp][1], dk[sp][2], dk[sp][3]);
+                            } else {
+                                st2(3 * H + k0, dk[sp][0], dk[sp][1]);
+                                if (cen) fo[3 * H + k0 + 2] = dk[sp][2];
+                                else st2(3 * H + k0 + 2, dk[sp][2], dk[sp][3]);
+                            }
                         }
                     }
                 }
@@ -409,9 +444,26 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                     auto ld2 = [&](int p) { return *reinterpret_cast<const double2*>(au + p); };
                     auto st2 = [&](int p, double a, double b) { *reinterpret_cast<double2*>(o + p) = make_double2(a, b); };
                     const int p1 = n - 1 - k0, p2 = 2 * H - 2 - k0, p3 = 2 * H + k0;
-                    const double2 r0a = ld2(k0), r0b = ld2(k0 + 2);
-                    const double2 r3a = ld2(p3);
-                    const double2 r3b = cen ? make_double2(ld1(p3 + 2), 0.0) : ld2(p3 + 2);
+                    double2 r0a, r0b, r3a, r3b;
+                    if constexpr (ETD_BACK6_V4) {
+                        double w0[4];
+                        ldg_v4(au + k0, w0);
+                        r0a = make_double2(w0[0], w0[1]);
+                        r0b = make_double2(w0[2], w0[3]);
+                        if (!cen) {
+                            double w3[4];
+                            ldg_v4(au + p3, w3);
+                            r3a = make_double2(w3[0], w3[1]);
+                            r3b = make_double2(w3[2], w3[3]);
+                        } else {
+                            r3a = ld2(p3);
+                            r3b = make_double2(ld1(p3 + 2), 0.0);
+                        }
+                    } else {
+                        r0a = ld2(k0), r0b = ld2(k0 + 2);
+                        r3a = ld2(p3);
+                        r3b = cen ? make_double2(ld1(p3 + 2), 0.0) : ld2(p3 + 2);
+                    }
                     const double r3c = r3b.x, r3d = r3b.y;
                     const double r1q0 = ld1(p1), r1q3 = ld1(p1 - 3);
                     const double2 r1m = ld2(p1 - 2);  // (q2, q1)
@@ -426,17 +478,25 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
 #pragma unroll
                         for (int R = 0; R < 4; ++R)
                             if (!(cen && q == 3 && R == 3)) bad |= !isfinite(u[q][R]);
-                    st2(k0, u[0][0], u[1][0]);
-                    st2(k0 + 2, u[2][0], u[3][0]);
+                    if constexpr (ETD_BACK6_V4) {
+                        stg_v4(o + k0, u[0][0], u[1][0], u[2][0], u[3][0]);
+                    } else {
+                        st2(k0, u[0][0], u[1][0]);
+                        st2(k0 + 2, u[2][0], u[3][0]);
+                    }
                     st2(p1 - 2, u[2][1], u[1][1]);
                     o[p1] = u[0][1];
                     o[p1 - 3] = u[3][1];
                     st2(p2 - 2, u[2][2], u[1][2]);
                     o[p2] = u[0][2];
                     o[cen ? 2 * H - 1 : p2 - 3] = u[3][2];
-                    st2(p3, u[0][3], u[1][3]);
-                    if (cen) o[p3 + 2] = u[2][3];
-                    else st2(p3 + 2, u[2][3], u[3][3]);
+                    if (ETD_BACK6_V4 && !cen) {
+                        stg_v4(o + p3, u[0][3], u[1][3], u[2][3], u[3][3]);
+                    } else {
+                        st2(p3, u[0][3], u[1][3]);
+                        if (cen) o[p3 + 2] = u[2][3];
+                        else st2(p3 + 2, u[2][3], u[3][3]);
+                    }
                 }
             }
         }
