@@ -32,23 +32,6 @@
 
 namespace etd {
 
-// 32-byte global accesses (sm_100: LDG / STG .ENL2.256), p 32-byte aligned.  A whole
-// sector per access; the x-stage epilogues use them where an orbit range is four
-// consecutive, aligned positions (R0 at k0, R3 at 2H + k0, the stack's 2H + k0 / 3H + k0).
-#ifndef ETD_BACK6_V4
-#define ETD_BACK6_V4 1
-#endif
-__device__ __forceinline__ void ldg_v4(const double* p, double (&w)[4]) {
-    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(w[0]), "=d"(w[1]), "=d"(w[2]), "=d"(w[3]) : "l"(p) : "memory");
-}
-__device__ __forceinline__ void ldg_nc_v4(const double* p, double (&w)[4]) {
-    // not volatile: read-only data, free to move above earlier stores (as __ldg is)
-    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(w[0]), "=d"(w[1]), "=d"(w[2]), "=d"(w[3]) : "l"(p));
-}
-__device__ __forceinline__ void stg_v4(double* p, double a, double b, double c, double d) {
-    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
-}
-
 template <int MODE, int S, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
 struct Back6Cfg {
     static constexpr int BK = 16, AB = 4;

@@ -288,6 +288,24 @@ __device__ __forceinline__ int swz(int row, int col) {
     return row * 16 + ((((col >> 1) ^ (row & 7)) << 1) | (col & 1));
 }
 
+// 32-byte global accesses (sm_100: LDG / STG .ENL2.256), p 32-byte aligned.  A whole
+// sector per access; the x-stage epilogues of etd_back6 and the x-axis stack pass
+// use them where an orbit range is four consecutive, aligned positions (R0 at k0, R3 at
+// 2H + k0, the stack's 2H + k0 / 3H + k0).
+#ifndef ETD_BACK6_V4
+#define ETD_BACK6_V4 1
+#endif
+__device__ __forceinline__ void ldg_v4(const double* p, double (&w)[4]) {
+    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(w[0]), "=d"(w[1]), "=d"(w[2]), "=d"(w[3]) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void ldg_nc_v4(const double* p, double (&w)[4]) {
+    // not volatile: read-only data, free to move above earlier stores (as __ldg is)
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(w[0]), "=d"(w[1]), "=d"(w[2]), "=d"(w[3]) : "l"(p));
+}
+__device__ __forceinline__ void stg_v4(double* p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 // keeps v in a register: the compiler may not re-derive it (from the thread
 // index) inside the main loop
 __device__ __forceinline__ int pin(int v) {
@@ -1245,9 +1263,26 @@ __device__ __forceinline__ void fold2_x_rows4(const Fold2Args& a) {
                 double* __restrict__ dst = a.out + f * a.Fout + row * a.pitch;
                 auto ld2 = [&](int p) { return *reinterpret_cast<const double2*>(src + p); };
                 auto st2 = [&](int p, double x, double y) { *reinterpret_cast<double2*>(dst + p) = make_double2(x, y); };
-                const double2 r0a = ld2(k0), r0b = ld2(k0 + 2);
-                const double2 r3a = ld2(p3);
-                const double2 r3b = cen ? make_double2(src[p3 + 2], 0.0) : ld2(p3 + 2);
+                double2 r0a, r0b, r3a, r3b;
+                if constexpr (ETD_BACK6_V4) {
+                    double w0[4];
+                    ldg_v4(src + k0, w0);
+                    r0a = make_double2(w0[0], w0[1]);
+                    r0b = make_double2(w0[2], w0[3]);
+                    if (!cen) {
+                        double w3[4];
+                        ldg_v4(src + p3, w3);
+                        r3a = make_double2(w3[0], w3[1]);
+                        r3b = make_double2(w3[2], w3[3]);
+                    } else {
+                        r3a = ld2(p3);
+                        r3b = make_double2(src[p3 + 2], 0.0);
+                    }
+                } else {
+                    r0a = ld2(k0), r0b = ld2(k0 + 2);
+                    r3a = ld2(p3);
+                    r3b = cen ? make_double2(src[p3 + 2], 0.0) : ld2(p3 + 2);
+                }
                 const double2 r1m = ld2(p1 - 2), r2m = ld2(p2 - 2);  // (q2, q1)
                 const double r1q0 = src[p1], r1q3 = src[p1 - 3];
                 const double r2q0 = src[p2], r2q3 = src[cen ? 2 * H - 1 : p2 - 3];
@@ -1275,11 +1310,19 @@ __device__ __forceinline__ void fold2_x_rows4(const Fold2Args& a) {
                 st2(H - 2 - k0 / 2, sc[2], sc[0]);
                 dst[2 * H - 2 - k0 / 2] = sc[1];
                 dst[cen ? 2 * H - 1 : 2 * H - 3 - k0 / 2] = sc[3];
-                st2(p3, o2[0], o2[1]);
-                st2(p3 + 2, o2[2], o2[3]);
-                st2(3 * H + k0, o3[0], o3[1]);
-                if (cen) dst[3 * H + k0 + 2] = o3[2];
-                else st2(3 * H + k0 + 2, o3[2], o3[3]);
+                if constexpr (ETD_BACK6_V4) {
+                    stg_v4(dst + p3, o2[0], o2[1], o2[2], o2[3]);
+                } else {
+                    st2(p3, o2[0], o2[1]);
+                    st2(p3 + 2, o2[2], o2[3]);
+                }
+                if (ETD_BACK6_V4 && !cen) {
+                    stg_v4(dst + 3 * H + k0, o3[0], o3[1], o3[2], o3[3]);
+                } else {
+                    st2(3 * H + k0, o3[0], o3[1]);
+                    if (cen) dst[3 * H + k0 + 2] = o3[2];
+                    else st2(3 * H + k0 + 2, o3[2], o3[3]);
+                }
             }
         }
     }
